@@ -1,0 +1,981 @@
+// api.cu -- the C ABI of libleggedrl.so (include/lg.h): validation, buffer binding, TMA descriptor
+// construction and the orchestration of one PPO iteration. Host code only enqueues work.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace lg;
+
+namespace {
+
+template <typename T>
+T* at(void* base, size_t off) { return reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(base) + off); }
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Dims {
+  int N, T, E, K, H0, H1, H2, D, Dp, nx, ny, L, C, R_hf, C_hf, B, Mmb, R;
+  long long P;
+};
+
+bool dims_of(const lg_config* c, Dims& d) {
+  d.N = c->n_envs; d.T = c->n_steps; d.E = c->n_epochs; d.K = c->n_minibatches;
+  d.H0 = c->hidden[0]; d.H1 = c->hidden[1]; d.H2 = c->hidden[2];
+  d.nx = c->scan_nx; d.ny = c->scan_ny;
+  d.D = 48 + d.nx * d.ny;
+  d.Dp = (d.D + 7) / 8 * 8;
+  d.L = c->n_levels; d.C = c->n_cols;
+  d.R_hf = 80 * d.L; d.C_hf = 80 * d.C;
+  d.B = d.N * d.T;
+  d.Mmb = d.K > 0 ? d.B / d.K : 0;
+  d.R = std::max(d.N, d.Mmb);
+  long long P = 0;
+  for (int z = 0; z < 2; ++z) {
+    int A = z == 0 ? 12 : 1;
+    P += (long long)d.H0 * d.D + d.H0 + (long long)d.H1 * d.H0 + d.H1 + (long long)d.H2 * d.H1 + d.H2 + (long long)A * d.H2 + A;
+  }
+  d.P = P + 12;
+  return true;
+}
+
+// canonical offsets
+struct Canon {
+  long long W1[2], b1[2], W2[2], b2[2], W3[2], b3[2], W4[2], b4[2], logstd;
+};
+Canon canon_of(const Dims& d) {
+  Canon c;
+  long long o = 0;
+  for (int z = 0; z < 2; ++z) {
+    int A = z == 0 ? 12 : 1;
+    c.W1[z] = o; o += (long long)d.H0 * d.D;
+    c.b1[z] = o; o += d.H0;
+    c.W2[z] = o; o += (long long)d.H1 * d.H0;
+    c.b2[z] = o; o += d.H1;
+    c.W3[z] = o; o += (long long)d.H2 * d.H1;
+    c.b3[z] = o; o += d.H2;
+    c.W4[z] = o; o += (long long)A * d.H2;
+    c.b4[z] = o; o += A;
+  }
+  c.logstd = o;
+  return c;
+}
+
+int bn_for(int n) { return n >= 256 ? 256 : (n > 64 ? 128 : (n > 32 ? 64 : 32)); }
+
+struct DwPlan {
+  int rows, N, bn, n_tiles, m_tiles, kb_total, kb_per_split, S, ld, rows_pad, nz;
+  size_t bytes;
+};
+DwPlan dw_plan(int rows, int N, int K, int nz) {
+  DwPlan p;
+  p.rows = rows; p.N = N; p.nz = nz;
+  p.bn = bn_for(N);
+  p.n_tiles = (N + p.bn - 1) / p.bn;
+  p.m_tiles = (rows + 127) / 128;
+  p.kb_total = (K + 63) / 64;
+  int tiles = p.n_tiles * p.m_tiles * nz;
+  int S = std::max(1, std::min(p.kb_total, 148 / std::max(1, tiles)));
+  p.kb_per_split = (p.kb_total + S - 1) / S;
+  p.S = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.ld = p.n_tiles * p.bn + 16;
+  p.rows_pad = p.m_tiles * 128;
+  p.bytes = (size_t)nz * p.S * p.rows_pad * p.ld * 4;
+  return p;
+}
+
+struct Layout {
+  size_t bytes[LG_NUM_BUFFERS];
+  // WEIGHTS
+  size_t w_W1, w_W2, w_W3, w_b1, w_b2, w_b3, w_W4a, w_b4a, w_W4c, w_b4c, w_ls, w_lso;
+  // ACTIV
+  size_t a_X, a_H1, a_H2, a_H3, a_dZ1, a_dZ2, a_dZ3, a_act, a_mu, a_logp, a_V, a_adv, a_ret, a_omu, a_oV;
+  // WORK
+  size_t k_sc, k_gae, k_var, k_tot, k_lpart, k_spart, k_dw1, k_dw2, k_dw3, k_perm, k_tobs, k_tidx, k_step, k_stats,
+      k_ctrl;
+  int HP, nblk_loss, nblk_gae, nblk_var;
+  DwPlan dw1, dw2, dw3;
+};
+
+Layout layout_of(const Dims& d) {
+  Layout L;
+  memset(&L, 0, sizeof(L));
+  L.bytes[LG_BUF_HEIGHTFIELD] = al((size_t)d.R_hf * d.C_hf * 4);
+  L.bytes[LG_BUF_STATE] = al((size_t)NW * d.N * 4);
+  L.bytes[LG_BUF_OBS] = al((size_t)(d.T + 1) * d.N * d.Dp * 2);
+  L.bytes[LG_BUF_ACT] = L.bytes[LG_BUF_MU] = al((size_t)d.B * 12 * 4);
+  for (int b : {LG_BUF_LOGP, LG_BUF_VALUE, LG_BUF_REWARD, LG_BUF_BOOT, LG_BUF_ADV, LG_BUF_RET}) L.bytes[b] = al((size_t)d.B * 4);
+  L.bytes[LG_BUF_FLAGS] = al((size_t)d.B);
+  L.bytes[LG_BUF_VALUE_T] = al((size_t)d.N * 4);
+  L.bytes[LG_BUF_THETA] = L.bytes[LG_BUF_ADAM_M] = L.bytes[LG_BUF_ADAM_V] = al((size_t)d.P * 4);
+  L.bytes[LG_BUF_GRAD] = al((size_t)(d.P + 16) * 4);
+  size_t o = 0;
+  L.w_W1 = o; o = al(o + (size_t)2 * d.H0 * d.Dp * 2);
+  L.w_W2 = o; o = al(o + (size_t)2 * d.H1 * d.H0 * 2);
+  L.w_W3 = o; o = al(o + (size_t)2 * d.H2 * d.H1 * 2);
+  L.w_b1 = o; o = al(o + (size_t)2 * d.H0 * 4);
+  L.w_b2 = o; o = al(o + (size_t)2 * d.H1 * 4);
+  L.w_b3 = o; o = al(o + (size_t)2 * d.H2 * 4);
+  L.w_W4a = o; o = al(o + (size_t)12 * d.H2 * 4);
+  L.w_b4a = o; o = al(o + 12 * 4);
+  L.w_W4c = o; o = al(o + (size_t)d.H2 * 4);
+  L.w_b4c = o; o = al(o + 4);
+  L.w_ls = o; o = al(o + 12 * 4);
+  L.w_lso = o; o = al(o + 12 * 4);
+  L.bytes[LG_BUF_WEIGHTS] = o;
+  o = 0;
+  const size_t R = (size_t)d.R;
+  L.a_X = o; o = al(o + R * d.Dp * 2);
+  L.a_H1 = o; o = al(o + R * 2 * d.H0 * 2);
+  L.a_H2 = o; o = al(o + R * 2 * d.H1 * 2);
+  L.a_H3 = o; o = al(o + R * 2 * d.H2 * 2);
+  L.a_dZ1 = o; o = al(o + R * 2 * d.H0 * 2);
+  L.a_dZ2 = o; o = al(o + R * 2 * d.H1 * 2);
+  L.a_dZ3 = o; o = al(o + R * 2 * d.H2 * 2);
+  L.a_act = o; o = al(o + R * 12 * 4);
+  L.a_mu = o; o = al(o + R * 12 * 4);
+  L.a_logp = o; o = al(o + R * 4);
+  L.a_V = o; o = al(o + R * 4);
+  L.a_adv = o; o = al(o + R * 4);
+  L.a_ret = o; o = al(o + R * 4);
+  L.a_omu = o; o = al(o + R * 12 * 4);
+  L.a_oV = o; o = al(o + R * 4);
+  L.bytes[LG_BUF_ACTIV] = o;
+  L.HP = loss_head_partial_floats(d.H2);
+  L.nblk_loss = loss_blocks(d.R);
+  L.nblk_gae = gae_blocks(d.N);
+  L.nblk_var = var_blocks(d.B);
+  L.dw1 = dw_plan(2 * d.H0, d.Dp, d.Mmb, 1);
+  L.dw2 = dw_plan(d.H1, d.H0, d.Mmb, 2);
+  L.dw3 = dw_plan(d.H2, d.H1, d.Mmb, 2);
+  o = 0;
+  L.k_sc = o; o = al(o + sizeof(DevScalars));
+  L.k_gae = o; o = al(o + (size_t)L.nblk_gae * 8);
+  L.k_var = o; o = al(o + (size_t)L.nblk_var * 8);
+  L.k_tot = o; o = al(o + 8 * 8);
+  L.k_lpart = o; o = al(o + (size_t)L.nblk_loss * L.HP * 4);
+  L.k_spart = o; o = al(o + (size_t)L.nblk_loss * 8 * 8);
+  L.k_dw1 = o; o = al(o + L.dw1.bytes);
+  L.k_dw2 = o; o = al(o + L.dw2.bytes);
+  L.k_dw3 = o; o = al(o + L.dw3.bytes);
+  L.k_perm = o; o = al(o + (size_t)d.B * 4);
+  L.k_tobs = o; o = al(o + (size_t)d.N * d.Dp * 2);
+  L.k_tidx = o; o = al(o + (size_t)d.N * 4);
+  L.k_step = o; o = al(o + 16 * 4);
+  L.k_stats = o; o = al(o + sizeof(lg_update_stats));
+  L.k_ctrl = o; o = al(o + 64);
+  L.bytes[LG_BUF_WORK] = o;
+  return L;
+}
+
+}  // namespace
+
+struct lg_ctx {
+  lg_config cfg;
+  Dims d;
+  Layout L;
+  Canon cn;
+  void* buf[LG_NUM_BUFFERS];
+  cudaStream_t st;
+  lg_status err = LG_OK;
+  std::string msg;
+  int world = 1;
+  ncclComm_t comm = nullptr;
+  bool reset_done = false;
+  // prebuilt launch descriptors
+  std::vector<GemmArgs> l1_roll;  // per OBS slot 0..T
+  GemmArgs l1_upd, l2, l3, l1_boot, l2_boot, l3_boot, l1_vt, dx3, dx2, dw3, dw2, dw1;
+  EnvParams ep;
+  ShadowArgs shadow;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  // pointers
+  DevScalars* sc;
+  float* payload;
+  float* step_f;
+};
+
+namespace {
+
+lg_status fail(lg_ctx* c, lg_status s, const char* fmt, ...) {
+  if (c && c->err == LG_OK) {
+    char b[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(b, sizeof(b), fmt, ap);
+    va_end(ap);
+    c->err = s;
+    c->msg = b;
+  }
+  return s;
+}
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define CKL()                                                                                                  \
+  do {                                                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "launch (%s:%d): %s", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+  } while (0)
+#define CKN(call)                                                                                  \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess) return fail(ctx, LG_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+#define GUARD()                          \
+  do {                                   \
+    if (!ctx) return LG_ERR_INVALID_ARG; \
+    if (ctx->err != LG_OK) return ctx->err; \
+  } while (0)
+
+lg_status validate(const lg_config* c) {
+  if (!c || c->struct_size != sizeof(lg_config)) return LG_ERR_INVALID_ARG;
+  if (c->n_envs < 1 || c->n_steps < 1 || c->n_epochs < 1 || c->n_minibatches < 1) return LG_ERR_INVALID_ARG;
+  if (((long long)c->n_envs * c->n_steps) % c->n_minibatches != 0) return LG_ERR_INVALID_ARG;
+  if ((long long)c->n_envs * c->n_steps >= (1LL << 30)) return LG_ERR_RANGE;
+  for (int k = 0; k < 3; ++k)
+    if (c->hidden[k] < 32 || c->hidden[k] > 512 || c->hidden[k] % 32 != 0) return LG_ERR_SHAPE;
+  if (c->hidden[0] % 64 != 0 || c->hidden[1] % 64 != 0) return LG_ERR_SHAPE;  // K of the next layer in 64-blocks
+  if (c->scan_nx < 0 || c->scan_ny < 0 || (c->scan_nx == 0) != (c->scan_ny == 0)) return LG_ERR_SHAPE;
+  if (c->n_levels < 1 || c->n_cols < 1) return LG_ERR_RANGE;
+  if (!(c->gamma > 0.f && c->gamma <= 1.f) || !(c->lam >= 0.f && c->lam <= 1.f)) return LG_ERR_RANGE;
+  if (!(c->clip > 0.f) || !(c->vclip > 0.f) || !(c->kl_target > 0.f)) return LG_ERR_RANGE;
+  if (!(c->lr_init >= 1e-5f && c->lr_init <= 1e-2f)) return LG_ERR_RANGE;
+  if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) return LG_ERR_RANGE;
+  if (!(c->inv_cell > 0.f)) return LG_ERR_RANGE;
+  return LG_OK;
+}
+
+void set_fwd_common(GemmArgs& g, int M, int N, int K, int bn, int nz) {
+  g.M = M; g.N = N; g.M_dev = nullptr;
+  g.kb_total = (K + 63) / 64;
+  g.kb_per_split = g.kb_total;
+  g.n_tiles = (N + bn - 1) / bn;
+  g.n_splits = 1;
+  (void)nz;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t lg_num_params(const lg_config* c) {
+  if (validate(c) != LG_OK) return -1;
+  Dims d;
+  dims_of(c, d);
+  return d.P;
+}
+int32_t lg_obs_dim(const lg_config* c) { return c ? 48 + c->scan_nx * c->scan_ny : -1; }
+int32_t lg_obs_stride(const lg_config* c) { return c ? (48 + c->scan_nx * c->scan_ny + 7) / 8 * 8 : -1; }
+
+lg_status lg_required_sizes(const lg_config* c, size_t bytes_h[LG_NUM_BUFFERS]) {
+  lg_status s = validate(c);
+  if (s != LG_OK) return s;
+  if (!bytes_h) return LG_ERR_INVALID_ARG;
+  Dims d;
+  dims_of(c, d);
+  Layout L = layout_of(d);
+  for (int i = 0; i < LG_NUM_BUFFERS; ++i) bytes_h[i] = L.bytes[i];
+  return LG_OK;
+}
+
+const char* lg_last_error(const lg_ctx* ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
+
+lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS], void* stream, lg_ctx** out_h) {
+  lg_status s = validate(cfg);
+  if (s != LG_OK) return s;
+  if (!buffers_h || !out_h) return LG_ERR_INVALID_ARG;
+  for (int i = 0; i < LG_NUM_BUFFERS; ++i)
+    if (!buffers_h[i] || (reinterpret_cast<uintptr_t>(buffers_h[i]) & 255)) return LG_ERR_INVALID_ARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return LG_ERR_UNSUPPORTED;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10) return LG_ERR_UNSUPPORTED;
+  lg_ctx* ctx = new lg_ctx();
+  ctx->cfg = *cfg;
+  dims_of(cfg, ctx->d);
+  ctx->L = layout_of(ctx->d);
+  ctx->cn = canon_of(ctx->d);
+  for (int i = 0; i < LG_NUM_BUFFERS; ++i) ctx->buf[i] = buffers_h[i];
+  ctx->st = reinterpret_cast<cudaStream_t>(stream);
+  ctx->world = cfg->world_size;
+  const Dims& d = ctx->d;
+  const Layout& L = ctx->L;
+  void* W = ctx->buf[LG_BUF_WEIGHTS];
+  void* A = ctx->buf[LG_BUF_ACTIV];
+  void* K = ctx->buf[LG_BUF_WORK];
+  ctx->sc = at<DevScalars>(K, L.k_sc);
+  ctx->payload = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]) + d.P;
+  ctx->step_f = at<float>(K, L.k_step);
+
+  auto bf = [](void* p, size_t off) { return at<__nv_bfloat16>(p, off); };
+  __nv_bfloat16* W1 = bf(W, L.w_W1);
+  __nv_bfloat16* W2 = bf(W, L.w_W2);
+  __nv_bfloat16* W3 = bf(W, L.w_W3);
+  __nv_bfloat16* X = bf(A, L.a_X);
+  __nv_bfloat16* H1 = bf(A, L.a_H1);
+  __nv_bfloat16* H2 = bf(A, L.a_H2);
+  __nv_bfloat16* H3 = bf(A, L.a_H3);
+  __nv_bfloat16* dZ1 = bf(A, L.a_dZ1);
+  __nv_bfloat16* dZ2 = bf(A, L.a_dZ2);
+  __nv_bfloat16* dZ3 = bf(A, L.a_dZ3);
+  __nv_bfloat16* OBS = reinterpret_cast<__nv_bfloat16*>(ctx->buf[LG_BUF_OBS]);
+  __nv_bfloat16* TOBS = bf(K, L.k_tobs);
+  float* b1 = at<float>(W, L.w_b1);
+  float* b2 = at<float>(W, L.w_b2);
+  float* b3 = at<float>(W, L.w_b3);
+  bool ok = true;
+  const int bn1 = bn_for(2 * d.H0), bn1c = bn_for(d.H0), bn2 = bn_for(d.H1), bn3 = bn_for(d.H2);
+  const uint64_t R = d.R;
+
+  // ---- forward, layer 1 (both nets concatenated: N = 2*H0)
+  ctx->l1_roll.resize(d.T + 1);
+  for (int t = 0; t <= d.T; ++t) {
+    GemmArgs& g = ctx->l1_roll[t];
+    memset(&g, 0, sizeof(g));
+    ok &= make_tmap_bf16(&g.tmA[0], OBS + (size_t)t * d.N * d.Dp, d.N, d.Dp, d.Dp, 128);
+    ok &= make_tmap_bf16(&g.tmB[0], W1, 2 * d.H0, d.Dp, d.Dp, bn1);
+    set_fwd_common(g, d.N, 2 * d.H0, d.Dp, bn1, 1);
+    g.out[0] = H1; g.ldo = 2 * d.H0; g.bias[0] = b1;
+  }
+  GemmArgs& u1 = ctx->l1_upd;
+  memset(&u1, 0, sizeof(u1));
+  ok &= make_tmap_bf16(&u1.tmA[0], X, R, d.Dp, d.Dp, 128);
+  ok &= make_tmap_bf16(&u1.tmB[0], W1, 2 * d.H0, d.Dp, d.Dp, bn1);
+  set_fwd_common(u1, d.Mmb, 2 * d.H0, d.Dp, bn1, 1);
+  u1.out[0] = H1; u1.ldo = 2 * d.H0; u1.bias[0] = b1;
+  // ---- forward, layers 2, 3 (z = net)
+  GemmArgs& g2 = ctx->l2;
+  memset(&g2, 0, sizeof(g2));
+  GemmArgs& g3 = ctx->l3;
+  memset(&g3, 0, sizeof(g3));
+  for (int z = 0; z < 2; ++z) {
+    ok &= make_tmap_bf16(&g2.tmA[z], H1 + z * d.H0, R, d.H0, 2 * d.H0, 128);
+    ok &= make_tmap_bf16(&g2.tmB[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, bn2);
+    g2.out[z] = H2 + z * d.H1; g2.bias[z] = b2 + z * d.H1;
+    ok &= make_tmap_bf16(&g3.tmA[z], H2 + z * d.H1, R, d.H1, 2 * d.H1, 128);
+    ok &= make_tmap_bf16(&g3.tmB[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, bn3);
+    g3.out[z] = H3 + z * d.H2; g3.bias[z] = b3 + z * d.H2;
+  }
+  set_fwd_common(g2, d.Mmb, d.H1, d.H0, bn2, 2); g2.ldo = 2 * d.H1;
+  set_fwd_common(g3, d.Mmb, d.H2, d.H1, bn3, 2); g3.ldo = 2 * d.H2;
+  // ---- critic-only chains (time-out bootstrap on compacted rows; V(o_T) on OBS slot T)
+  GemmArgs& c1 = ctx->l1_boot;
+  memset(&c1, 0, sizeof(c1));
+  ok &= make_tmap_bf16(&c1.tmA[0], TOBS, d.N, d.Dp, d.Dp, 128);
+  ok &= make_tmap_bf16(&c1.tmB[0], W1 + (size_t)d.H0 * d.Dp, d.H0, d.Dp, d.Dp, bn1c);
+  set_fwd_common(c1, d.N, d.H0, d.Dp, bn1c, 1);
+  c1.M_dev = &ctx->sc->n_to;
+  c1.out[0] = H1 + d.H0; c1.ldo = 2 * d.H0; c1.bias[0] = b1 + d.H0;
+  GemmArgs& cv = ctx->l1_vt;
+  cv = c1;
+  ok &= make_tmap_bf16(&cv.tmA[0], OBS + (size_t)d.T * d.N * d.Dp, d.N, d.Dp, d.Dp, 128);
+  cv.M_dev = nullptr;
+  GemmArgs& c2 = ctx->l2_boot;
+  memset(&c2, 0, sizeof(c2));
+  c2.tmA[0] = g2.tmA[1]; c2.tmB[0] = g2.tmB[1];
+  set_fwd_common(c2, d.N, d.H1, d.H0, bn2, 1);
+  c2.out[0] = g2.out[1]; c2.bias[0] = g2.bias[1]; c2.ldo = 2 * d.H1;
+  GemmArgs& c3 = ctx->l3_boot;
+  memset(&c3, 0, sizeof(c3));
+  c3.tmA[0] = g3.tmA[1]; c3.tmB[0] = g3.tmB[1];
+  set_fwd_common(c3, d.N, d.H2, d.H1, bn3, 1);
+  c3.out[0] = g3.out[1]; c3.bias[0] = g3.bias[1]; c3.ldo = 2 * d.H2;
+  // ---- backward dX (A = dZ K-major, B = W MN-major), epilogue * ELU'(H)
+  GemmArgs& x3 = ctx->dx3;
+  memset(&x3, 0, sizeof(x3));
+  GemmArgs& x2 = ctx->dx2;
+  memset(&x2, 0, sizeof(x2));
+  for (int z = 0; z < 2; ++z) {
+    ok &= make_tmap_bf16(&x3.tmA[z], dZ3 + z * d.H2, R, d.H2, 2 * d.H2, 128);
+    ok &= make_tmap_bf16(&x3.tmB[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, 64);
+    x3.out[z] = dZ2 + z * d.H1; x3.aux[z] = H2 + z * d.H1;
+    ok &= make_tmap_bf16(&x2.tmA[z], dZ2 + z * d.H1, R, d.H1, 2 * d.H1, 128);
+    ok &= make_tmap_bf16(&x2.tmB[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, 64);
+    x2.out[z] = dZ1 + z * d.H0; x2.aux[z] = H1 + z * d.H0;
+  }
+  set_fwd_common(x3, d.Mmb, d.H1, d.H2, bn_for(d.H1), 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
+  set_fwd_common(x2, d.Mmb, d.H0, d.H1, bn_for(d.H0), 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
+  // ---- backward dW (A = dZ MN-major, B = activations MN-major), split-K over the minibatch
+  auto dw_setup = [&](GemmArgs& g, const DwPlan& p, size_t part_off) {
+    g.M = p.rows; g.N = p.N; g.M_dev = nullptr;
+    g.kb_total = p.kb_total; g.kb_per_split = p.kb_per_split; g.n_tiles = p.n_tiles; g.n_splits = p.S;
+    g.part = at<float>(K, part_off);
+    g.part_sstride = (long long)p.rows_pad * p.ld;
+    g.part_zstride = (long long)p.S * g.part_sstride;
+    g.part_ld = p.ld; g.part_bias_col = p.n_tiles * p.bn; g.bias_col = 1;
+  };
+  GemmArgs& w3 = ctx->dw3;
+  memset(&w3, 0, sizeof(w3));
+  GemmArgs& w2 = ctx->dw2;
+  memset(&w2, 0, sizeof(w2));
+  GemmArgs& w1 = ctx->dw1;
+  memset(&w1, 0, sizeof(w1));
+  const uint64_t Mr = d.Mmb;
+  for (int z = 0; z < 2; ++z) {
+    ok &= make_tmap_bf16(&w3.tmA[z], dZ3 + z * d.H2, Mr, d.H2, 2 * d.H2, 64);
+    ok &= make_tmap_bf16(&w3.tmB[z], H2 + z * d.H1, Mr, d.H1, 2 * d.H1, 64);
+    ok &= make_tmap_bf16(&w2.tmA[z], dZ2 + z * d.H1, Mr, d.H1, 2 * d.H1, 64);
+    ok &= make_tmap_bf16(&w2.tmB[z], H1 + z * d.H0, Mr, d.H0, 2 * d.H0, 64);
+  }
+  ok &= make_tmap_bf16(&w1.tmA[0], dZ1, Mr, 2 * d.H0, 2 * d.H0, 64);
+  ok &= make_tmap_bf16(&w1.tmB[0], X, Mr, d.Dp, d.Dp, 64);
+  dw_setup(w3, L.dw3, L.k_dw3);
+  dw_setup(w2, L.dw2, L.k_dw2);
+  dw_setup(w1, L.dw1, L.k_dw1);
+  if (!ok) {
+    delete ctx;
+    return LG_ERR_CUDA;
+  }
+  // ---- env params
+  EnvParams& ep = ctx->ep;
+  ep.hf = reinterpret_cast<const float*>(ctx->buf[LG_BUF_HEIGHTFIELD]);
+  ep.R = d.R_hf; ep.C = d.C_hf; ep.inv_cell = cfg->inv_cell;
+  ep.N = d.N; ep.rank = cfg->rank; ep.n_levels = d.L; ep.n_cols = d.C; ep.scan_nx = d.nx; ep.scan_ny = d.ny;
+  ep.obs_dim = d.D; ep.obs_stride = d.Dp; ep.flags = cfg->flags;
+  ep.seed_lo = (uint32_t)(cfg->seed & 0xFFFFFFFFu); ep.seed_hi = (uint32_t)(cfg->seed >> 32);
+  ep.state = reinterpret_cast<uint32_t*>(ctx->buf[LG_BUF_STATE]);
+  ep.scalars = ctx->sc;
+  ep.obs_out = OBS;
+  ep.reward = reinterpret_cast<float*>(ctx->buf[LG_BUF_REWARD]);
+  ep.flags_out = reinterpret_cast<uint8_t*>(ctx->buf[LG_BUF_FLAGS]);
+  ep.boot = reinterpret_cast<float*>(ctx->buf[LG_BUF_BOOT]);
+  ep.term_obs = TOBS;
+  ep.term_idx = at<int32_t>(K, L.k_tidx);
+  // ---- shadow segments (canonical θ -> GEMM layouts)
+  ShadowArgs& sh = ctx->shadow;
+  memset(&sh, 0, sizeof(sh));
+  sh.P = d.P;
+  auto seg = [&](long long off, int rows, int cols, int kind, void* dst, int ld) {
+    Segment& s = sh.seg[sh.nseg++];
+    s.off = off; s.rows = rows; s.cols = cols; s.kind = kind; s.dst = dst; s.dst_ld = ld;
+  };
+  const Canon& cn = ctx->cn;
+  for (int z = 0; z < 2; ++z) {
+    seg(cn.W1[z], d.H0, d.D, 0, W1 + (size_t)z * d.H0 * d.Dp, d.Dp);
+    seg(cn.b1[z], 1, d.H0, 1, b1 + z * d.H0, d.H0);
+    seg(cn.W2[z], d.H1, d.H0, 0, W2 + (size_t)z * d.H1 * d.H0, d.H0);
+    seg(cn.b2[z], 1, d.H1, 1, b2 + z * d.H1, d.H1);
+    seg(cn.W3[z], d.H2, d.H1, 0, W3 + (size_t)z * d.H2 * d.H1, d.H1);
+    seg(cn.b3[z], 1, d.H2, 1, b3 + z * d.H2, d.H2);
+  }
+  seg(cn.W4[0], 12, d.H2, 1, at<float>(W, L.w_W4a), d.H2);
+  seg(cn.b4[0], 1, 12, 1, at<float>(W, L.w_b4a), 12);
+  seg(cn.W4[1], 1, d.H2, 1, at<float>(W, L.w_W4c), d.H2);
+  seg(cn.b4[1], 1, 1, 1, at<float>(W, L.w_b4c), 1);
+  seg(cn.logstd, 1, 12, 1, at<float>(W, L.w_ls), 12);
+  // zero the padded weight columns and the work buffer once (no kernels launched by the caller yet)
+  cudaError_t e = cudaMemsetAsync(W, 0, L.bytes[LG_BUF_WEIGHTS], ctx->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(K, 0, L.bytes[LG_BUF_WORK], ctx->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->buf[LG_BUF_OBS], 0, L.bytes[LG_BUF_OBS], ctx->st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->buf[LG_BUF_GRAD], 0, L.bytes[LG_BUF_GRAD], ctx->st);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return LG_ERR_CUDA;
+  }
+  *out_h = ctx;
+  return LG_OK;
+}
+
+lg_status lg_destroy(lg_ctx* ctx) {
+  if (!ctx) return LG_ERR_INVALID_ARG;
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  delete ctx;
+  return LG_OK;
+}
+
+static lg_status set_alpha(lg_ctx* ctx) {
+  DevScalars tmp;
+  memset(&tmp, 0, sizeof(tmp));
+  // alpha/adam_t are device fields: write them with small memcpys (no host read)
+  float a = ctx->cfg.lr_init;
+  int32_t z = 0;
+  CK(cudaMemcpyAsync(&ctx->sc->alpha, &a, 4, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(&ctx->sc->adam_t, &z, 4, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));  // host values above live on the stack
+  return LG_OK;
+}
+
+lg_status lg_params_set(lg_ctx* ctx, const float* theta) {
+  GUARD();
+  if (!theta) return fail(ctx, LG_ERR_INVALID_ARG, "params_set: null theta");
+  const size_t bytes = (size_t)ctx->d.P * 4;
+  CK(cudaMemcpyAsync(ctx->buf[LG_BUF_THETA], theta, bytes, cudaMemcpyDeviceToDevice, ctx->st));
+  CK(cudaMemsetAsync(ctx->buf[LG_BUF_ADAM_M], 0, bytes, ctx->st));
+  CK(cudaMemsetAsync(ctx->buf[LG_BUF_ADAM_V], 0, bytes, ctx->st));
+  launch_sync_shadow(ctx->shadow, reinterpret_cast<const float*>(ctx->buf[LG_BUF_THETA]), ctx->st);
+  CKL();
+  return set_alpha(ctx);
+}
+
+lg_status lg_params_sync(lg_ctx* ctx) {
+  GUARD();
+  launch_sync_shadow(ctx->shadow, reinterpret_cast<const float*>(ctx->buf[LG_BUF_THETA]), ctx->st);
+  CKL();
+  return LG_OK;
+}
+
+// ------------------------------------------------------------------ MLP helpers
+static lg_status gemm(lg_ctx* ctx, GemmKind kind, const GemmArgs& g, int bn, int nz) {
+  int m_tiles = (g.M + 127) / 128;
+  cudaError_t e = launch_gemm(kind, bn, g, m_tiles, nz, ctx->st);
+  if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm(kind %d, bn %d): %s", (int)kind, bn, cudaGetErrorString(e));
+  return LG_OK;
+}
+
+static HeadArgs head_args(lg_ctx* ctx, int M) {
+  HeadArgs h;
+  memset(&h, 0, sizeof(h));
+  const Dims& d = ctx->d;
+  void* W = ctx->buf[LG_BUF_WEIGHTS];
+  h.nd = NetDims{d.D, d.Dp, d.H0, d.H1, d.H2};
+  h.H3 = at<__nv_bfloat16>(ctx->buf[LG_BUF_ACTIV], ctx->L.a_H3);
+  h.W4a = at<float>(W, ctx->L.w_W4a); h.b4a = at<float>(W, ctx->L.w_b4a);
+  h.W4c = at<float>(W, ctx->L.w_W4c); h.b4c = at<float>(W, ctx->L.w_b4c);
+  h.logstd = at<float>(W, ctx->L.w_ls);
+  h.M = M;
+  h.N = d.N; h.rank = ctx->cfg.rank;
+  h.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); h.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
+  h.scalars = ctx->sc;
+  return h;
+}
+
+static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int M) {
+  const Dims& d = ctx->d;
+  l1.M = M;
+  GemmArgs g2 = ctx->l2, g3 = ctx->l3;
+  g2.M = M; g3.M = M;
+  lg_status s;
+  if ((s = gemm(ctx, GEMM_FWD, l1, bn_for(2 * d.H0), 1)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, g2, bn_for(d.H1), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, g3, bn_for(d.H2), 2)) != LG_OK) return s;
+  return LG_OK;
+}
+
+static lg_status critic_rows(lg_ctx* ctx, GemmArgs& c1, const int* M_dev, int M) {
+  const Dims& d = ctx->d;
+  GemmArgs a = c1, b = ctx->l2_boot, c = ctx->l3_boot;
+  a.M = b.M = c.M = M;
+  a.M_dev = b.M_dev = c.M_dev = M_dev;
+  lg_status s;
+  if ((s = gemm(ctx, GEMM_FWD, a, bn_for(d.H0), 1)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, b, bn_for(d.H1), 1)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, c, bn_for(d.H2), 1)) != LG_OK) return s;
+  return LG_OK;
+}
+
+// ------------------------------------------------------------------ env
+lg_status env_reset(lg_ctx* ctx, const uint8_t* mask, int32_t init, float* obs) {
+  GUARD();
+  launch_env_reset(ctx->ep, mask, init, obs, ctx->st);
+  CKL();
+  ctx->reset_done = true;
+  return LG_OK;
+}
+
+lg_status env_step_obs_reward(lg_ctx* ctx, int32_t t, const float* actions, float* obs, float* reward,
+                              uint8_t* terminated, uint8_t* timeout, float* terms) {
+  GUARD();
+  const Dims& d = ctx->d;
+  if (t < 0 || t >= d.T) return fail(ctx, LG_ERR_RANGE, "env_step: t=%d out of [0,%d)", t, d.T);
+  if (!ctx->reset_done) return fail(ctx, LG_ERR_STATE, "env_step before env_reset");
+  float* act_slot = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
+  if (actions && actions != act_slot)
+    CK(cudaMemcpyAsync(act_slot, actions, (size_t)d.N * 12 * 4, cudaMemcpyDeviceToDevice, ctx->st));
+  CK(cudaMemsetAsync(&ctx->sc->n_to, 0, 4, ctx->st));
+  launch_env_step(ctx->ep, t, act_slot, obs, reward, terminated, timeout, terms, ctx->st);
+  CKL();
+  if (ctx->cfg.flags & LG_F_BOOTSTRAP) {  // V(o_term) of the time-out envs, compacted rows
+    lg_status s = critic_rows(ctx, ctx->l1_boot, &ctx->sc->n_to, d.N);
+    if (s != LG_OK) return s;
+    HeadArgs h = head_args(ctx, d.N);
+    h.M_dev = &ctx->sc->n_to;
+    h.mode = 1;
+    h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_BOOT]) + (size_t)t * d.N;
+    h.idx = ctx->ep.term_idx;
+    launch_heads(h, ctx->st);
+    CKL();
+  }
+  return LG_OK;
+}
+
+lg_status curriculum_update(lg_ctx* ctx, int32_t n, const uint8_t* crossed, const float* disp, const float* cmd,
+                            const int32_t* ep, const uint32_t* words, int32_t* level) {
+  GUARD();
+  if (n < 0 || (n > 0 && (!crossed || !disp || !cmd || !ep || !words || !level)))
+    return fail(ctx, LG_ERR_INVALID_ARG, "curriculum_update: bad arguments");
+  if (n == 0) return LG_OK;
+  launch_curriculum(n, ctx->d.L, crossed, disp, cmd, ep, words, level, ctx->st);
+  CKL();
+  return LG_OK;
+}
+
+// ------------------------------------------------------------------ policy
+lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float* mu, float* value) {
+  GUARD();
+  const Dims& d = ctx->d;
+  if (t < 0 || t >= d.T) return fail(ctx, LG_ERR_RANGE, "policy_act: t=%d out of [0,%d)", t, d.T);
+  lg_status s = forward_rows(ctx, ctx->l1_roll[t], d.N);
+  if (s != LG_OK) return s;
+  HeadArgs h = head_args(ctx, d.N);
+  h.mode = 0;
+  h.t = t;
+  h.act = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
+  h.mu = reinterpret_cast<float*>(ctx->buf[LG_BUF_MU]) + (size_t)t * d.N * 12;
+  h.logp = reinterpret_cast<float*>(ctx->buf[LG_BUF_LOGP]) + (size_t)t * d.N;
+  h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE]) + (size_t)t * d.N;
+  h.u_act = actions; h.u_logp = logp; h.u_mu = mu; h.u_value = value;
+  launch_heads(h, ctx->st);
+  CKL();
+  return LG_OK;
+}
+
+lg_status policy_forward(lg_ctx* ctx, const void* x, int32_t M, float* mu, float* value) {
+  GUARD();
+  const Dims& d = ctx->d;
+  if (!x || !mu || !value || M < 1 || M > d.R) return fail(ctx, LG_ERR_INVALID_ARG, "policy_forward: bad arguments");
+  GemmArgs l1 = ctx->l1_upd;
+  if (!make_tmap_bf16(&l1.tmA[0], x, M, d.Dp, d.Dp, 128)) return fail(ctx, LG_ERR_CUDA, "tensor map");
+  lg_status s = forward_rows(ctx, l1, M);
+  if (s != LG_OK) return s;
+  HeadArgs h = head_args(ctx, M);
+  h.mode = 2;
+  h.mu = mu;
+  h.value = value;
+  launch_heads(h, ctx->st);
+  CKL();
+  return LG_OK;
+}
+
+// ------------------------------------------------------------------ learning
+static lg_status allreduce_f(lg_ctx* ctx, float* p, size_t n) {
+  if (ctx->world > 1 && ctx->comm) CKN(ncclAllReduce(p, p, n, ncclFloat32, ncclSum, ctx->comm, ctx->st));
+  return LG_OK;
+}
+static lg_status allreduce_d(lg_ctx* ctx, double* p, size_t n) {
+  if (ctx->world > 1 && ctx->comm) CKN(ncclAllReduce(p, p, n, ncclFloat64, ncclSum, ctx->comm, ctx->st));
+  return LG_OK;
+}
+
+lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
+  GUARD();
+  const Dims& d = ctx->d;
+  void* K = ctx->buf[LG_BUF_WORK];
+  // V(o_T): critic on OBS slot T
+  lg_status s = critic_rows(ctx, ctx->l1_vt, nullptr, d.N);
+  if (s != LG_OK) return s;
+  HeadArgs h = head_args(ctx, d.N);
+  h.mode = 1;
+  h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE_T]);
+  launch_heads(h, ctx->st);
+  CKL();
+  GaeArgs g;
+  g.N = d.N; g.T = d.T;
+  g.r = reinterpret_cast<const float*>(ctx->buf[LG_BUF_REWARD]);
+  g.V = reinterpret_cast<const float*>(ctx->buf[LG_BUF_VALUE]);
+  g.b = reinterpret_cast<const float*>(ctx->buf[LG_BUF_BOOT]);
+  g.flags = reinterpret_cast<const uint8_t*>(ctx->buf[LG_BUF_FLAGS]);
+  g.VT = reinterpret_cast<const float*>(ctx->buf[LG_BUF_VALUE_T]);
+  g.gamma = ctx->cfg.gamma; g.lam = ctx->cfg.lam; g.bootstrap = (ctx->cfg.flags & LG_F_BOOTSTRAP) ? 1 : 0;
+  g.A = reinterpret_cast<float*>(ctx->buf[LG_BUF_ADV]);
+  g.R = reinterpret_cast<float*>(ctx->buf[LG_BUF_RET]);
+  g.part = at<double>(K, ctx->L.k_gae);
+  launch_gae(g, ctx->st);
+  CKL();
+  double* tot = at<double>(K, ctx->L.k_tot);
+  launch_sum_partials(g.part, ctx->L.nblk_gae, tot, ctx->st);
+  CKL();
+  if ((s = allreduce_d(ctx, tot, 1)) != LG_OK) return s;
+  const double count = (double)d.B * ctx->world;
+  double* vp = at<double>(K, ctx->L.k_var);
+  launch_var_partials(g.A, d.B, tot, count, vp, ctx->st);
+  CKL();
+  launch_sum_partials(vp, ctx->L.nblk_var, tot + 1, ctx->st);
+  CKL();
+  if ((s = allreduce_d(ctx, tot + 1, 1)) != LG_OK) return s;
+  launch_adv_finalize(tot, tot + 1, count, ctx->sc, ctx->st);
+  CKL();
+  launch_advance_sbase(ctx->sc, d.T, ctx->st);
+  CKL();
+  if (adv) CK(cudaMemcpyAsync(adv, g.A, (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));
+  if (ret) CK(cudaMemcpyAsync(ret, g.R, (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));
+  return LG_OK;
+}
+
+// gradient of one minibatch (rows already gathered into the ACTIV minibatch arrays)
+static lg_status minibatch_gradient(lg_ctx* ctx) {
+  const Dims& d = ctx->d;
+  const Layout& L = ctx->L;
+  void* W = ctx->buf[LG_BUF_WEIGHTS];
+  void* A = ctx->buf[LG_BUF_ACTIV];
+  void* K = ctx->buf[LG_BUF_WORK];
+  float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
+  GemmArgs l1 = ctx->l1_upd;
+  lg_status s = forward_rows(ctx, l1, d.Mmb);
+  if (s != LG_OK) return s;
+  CK(cudaMemsetAsync(ctx->payload, 0, 16 * 4, ctx->st));
+  LossArgs la;
+  la.nd = NetDims{d.D, d.Dp, d.H0, d.H1, d.H2};
+  la.M = d.Mmb;
+  la.H3 = at<__nv_bfloat16>(A, L.a_H3);
+  la.W4a = at<float>(W, L.w_W4a); la.b4a = at<float>(W, L.w_b4a); la.W4c = at<float>(W, L.w_W4c); la.b4c = at<float>(W, L.w_b4c);
+  la.logstd = at<float>(W, L.w_ls); la.logstd_old = at<float>(W, L.w_lso);
+  la.act = at<float>(A, L.a_act); la.mu_old = at<float>(A, L.a_mu); la.logp_old = at<float>(A, L.a_logp);
+  la.V_old = at<float>(A, L.a_V); la.adv = at<float>(A, L.a_adv); la.ret = at<float>(A, L.a_ret);
+  la.clip = ctx->cfg.clip; la.vclip = ctx->cfg.vclip; la.ent_coef = ctx->cfg.ent_coef; la.vf_coef = ctx->cfg.vf_coef;
+  la.dZ3 = at<__nv_bfloat16>(A, L.a_dZ3);
+  la.part = at<float>(K, L.k_lpart);
+  la.spart = at<double>(K, L.k_spart);
+  la.HP = L.HP;
+  launch_loss_heads(la, ctx->st);
+  CKL();
+  HeadReduceArgs hr;
+  hr.nblk = loss_blocks(d.Mmb); hr.HP = L.HP; hr.H2 = d.H2;
+  hr.part = la.part; hr.spart = la.spart; hr.grad = grad;
+  hr.off_W4a = ctx->cn.W4[0]; hr.off_b4a = ctx->cn.b4[0]; hr.off_W4c = ctx->cn.W4[1]; hr.off_b4c = ctx->cn.b4[1];
+  hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
+  launch_reduce_heads(hr, ctx->st);
+  CKL();
+  auto reduce = [&](const GemmArgs& g, const DwPlan& p, int rows, int cols, const long long* woff, const long long* boff,
+                    int row_split) {
+    DwReduceArgs r;
+    r.part = g.part; r.zstride = g.part_zstride; r.sstride = g.part_sstride;
+    r.ld = p.ld; r.S = p.S; r.rows = rows; r.cols = cols; r.bias_col = g.part_bias_col;
+    r.grad = grad;
+    r.w_off[0] = woff[0]; r.w_off[1] = woff[1]; r.b_off[0] = boff[0]; r.b_off[1] = boff[1];
+    r.nz = row_split > 0 ? 1 : p.nz;
+    r.row_split = row_split;
+    r.payload = ctx->payload;
+    launch_reduce_dw(r, ctx->st);
+  };
+  // layer 3
+  if ((s = gemm(ctx, GEMM_DW, ctx->dw3, L.dw3.bn, 2)) != LG_OK) return s;
+  reduce(ctx->dw3, L.dw3, d.H2, d.H1, ctx->cn.W3, ctx->cn.b3, 0);
+  CKL();
+  GemmArgs x3 = ctx->dx3;
+  x3.M = d.Mmb;
+  if ((s = gemm(ctx, GEMM_DX, x3, bn_for(d.H1), 2)) != LG_OK) return s;
+  // layer 2
+  if ((s = gemm(ctx, GEMM_DW, ctx->dw2, L.dw2.bn, 2)) != LG_OK) return s;
+  reduce(ctx->dw2, L.dw2, d.H1, d.H0, ctx->cn.W2, ctx->cn.b2, 0);
+  CKL();
+  GemmArgs x2 = ctx->dx2;
+  x2.M = d.Mmb;
+  if ((s = gemm(ctx, GEMM_DX, x2, bn_for(d.H0), 2)) != LG_OK) return s;
+  // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
+  if ((s = gemm(ctx, GEMM_DW, ctx->dw1, L.dw1.bn, 1)) != LG_OK) return s;
+  reduce(ctx->dw1, L.dw1, 2 * d.H0, d.D, ctx->cn.W1, ctx->cn.b1, d.H0);
+  CKL();
+  return LG_OK;
+}
+
+static GatherArgs gather_args(lg_ctx* ctx) {
+  const Dims& d = ctx->d;
+  void* A = ctx->buf[LG_BUF_ACTIV];
+  const Layout& L = ctx->L;
+  GatherArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = d.Mmb; g.N = d.N; g.Dp = d.Dp;
+  g.obs = reinterpret_cast<const __nv_bfloat16*>(ctx->buf[LG_BUF_OBS]);
+  g.act = reinterpret_cast<const float*>(ctx->buf[LG_BUF_ACT]);
+  g.mu = reinterpret_cast<const float*>(ctx->buf[LG_BUF_MU]);
+  g.logp = reinterpret_cast<const float*>(ctx->buf[LG_BUF_LOGP]);
+  g.V = reinterpret_cast<const float*>(ctx->buf[LG_BUF_VALUE]);
+  g.A = reinterpret_cast<const float*>(ctx->buf[LG_BUF_ADV]);
+  g.R = reinterpret_cast<const float*>(ctx->buf[LG_BUF_RET]);
+  g.sc = ctx->sc;
+  g.X = at<__nv_bfloat16>(A, L.a_X);
+  g.o_act = at<float>(A, L.a_act); g.o_mu = at<float>(A, L.a_mu); g.o_logp = at<float>(A, L.a_logp);
+  g.o_V = at<float>(A, L.a_V); g.o_adv = at<float>(A, L.a_adv); g.o_ret = at<float>(A, L.a_ret);
+  return g;
+}
+
+static void iter_begin(lg_ctx* ctx) {
+  void* W = ctx->buf[LG_BUF_WEIGHTS];
+  launch_iter_begin(ctx->sc, at<float>(W, ctx->L.w_lso), at<float>(W, ctx->L.w_ls), ctx->step_f + 4, ctx->st);
+}
+
+lg_status ppo_shuffle(lg_ctx* ctx, int32_t epoch, uint32_t* perm) {
+  GUARD();
+  if (!perm || epoch < 0 || epoch >= ctx->d.E) return fail(ctx, LG_ERR_INVALID_ARG, "ppo_shuffle: bad arguments");
+  PermArgs pa;
+  pa.B = (uint32_t)ctx->d.B; pa.E = ctx->d.E; pa.epoch = epoch; pa.rank = ctx->cfg.rank;
+  pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
+  pa.sc = ctx->sc; pa.perm = perm;
+  launch_perm(pa, ctx->st);
+  CKL();
+  return LG_OK;
+}
+
+lg_status ppo_minibatch_grad(lg_ctx* ctx, const int32_t* idx, int32_t M_mb) {
+  GUARD();
+  const Dims& d = ctx->d;
+  if (!idx || M_mb != d.Mmb) return fail(ctx, LG_ERR_SHAPE, "ppo_minibatch_grad: M_mb must equal N*T/K = %d", d.Mmb);
+  iter_begin(ctx);
+  CKL();
+  GatherArgs g = gather_args(ctx);
+  g.idx = idx;
+  launch_gather(g, ctx->st);
+  CKL();
+  return minibatch_gradient(ctx);
+}
+
+lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
+  GUARD();
+  const Dims& d = ctx->d;
+  const Layout& L = ctx->L;
+  void* K = ctx->buf[LG_BUF_WORK];
+  uint32_t* perm = at<uint32_t>(K, L.k_perm);
+  float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
+  iter_begin(ctx);
+  CKL();
+  AdamArgs aa;
+  aa.sh = ctx->shadow;
+  aa.theta = reinterpret_cast<float*>(ctx->buf[LG_BUF_THETA]);
+  aa.m = reinterpret_cast<float*>(ctx->buf[LG_BUF_ADAM_M]);
+  aa.v = reinterpret_cast<float*>(ctx->buf[LG_BUF_ADAM_V]);
+  aa.grad = grad;
+  aa.b1 = ctx->cfg.adam_b1; aa.b2 = ctx->cfg.adam_b2; aa.eps = ctx->cfg.adam_eps;
+  aa.inv_world = 1.0f / (float)ctx->world;
+  aa.sc = ctx->sc;
+  lg_status s;
+  for (int e = 0; e < d.E; ++e) {
+    PermArgs pa;
+    pa.B = (uint32_t)d.B; pa.E = d.E; pa.epoch = e; pa.rank = ctx->cfg.rank;
+    pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
+    pa.sc = ctx->sc; pa.perm = perm;
+    launch_perm(pa, ctx->st);
+    CKL();
+    for (int m = 0; m < d.K; ++m) {
+      GatherArgs g = gather_args(ctx);
+      g.perm = perm + (size_t)m * d.Mmb;
+      launch_gather(g, ctx->st);
+      CKL();
+      if ((s = minibatch_gradient(ctx)) != LG_OK) return s;
+      if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s;
+      launch_alg1_prep(ctx->payload, ctx->sc, ctx->cfg.kl_target, ctx->world, ctx->cfg.adam_b1, ctx->cfg.adam_b2,
+                       ctx->step_f, ctx->st);
+      CKL();
+      launch_adam(aa, ctx->step_f, ctx->st);
+      CKL();
+    }
+  }
+  IterEndArgs ie;
+  memset(&ie, 0, sizeof(ie));
+  ie.sc = ctx->sc;
+  ie.stats = stats ? (void*)stats : (void*)at<lg_update_stats>(K, L.k_stats);
+  ie.n_mb = d.E * d.K; ie.T = d.T; ie.n_levels = d.L;
+  ie.state = reinterpret_cast<const uint32_t*>(ctx->buf[LG_BUF_STATE]);
+  ie.N = d.N;
+  ie.logstd = at<float>(ctx->buf[LG_BUF_WEIGHTS], L.w_ls);
+  launch_iter_end(ie, ctx->step_f + 4, ctx->st);
+  CKL();
+  // o_T becomes o_0 of the next iteration
+  __nv_bfloat16* OBS = reinterpret_cast<__nv_bfloat16*>(ctx->buf[LG_BUF_OBS]);
+  CK(cudaMemcpyAsync(OBS, OBS + (size_t)d.T * d.N * d.Dp, (size_t)d.N * d.Dp * 2, cudaMemcpyDeviceToDevice, ctx->st));
+  return LG_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU
+lg_status lg_nccl_unique_id(uint8_t id_h[128]) {
+  if (!id_h) return LG_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return LG_ERR_NCCL;
+  memcpy(id_h, &id, 128);
+  return LG_OK;
+}
+
+lg_status lg_set_nccl(lg_ctx* ctx, const uint8_t id_h[128]) {
+  GUARD();
+  if (!id_h) return fail(ctx, LG_ERR_INVALID_ARG, "null id");
+  if (ctx->world <= 1) return LG_OK;
+  ncclUniqueId id;
+  memcpy(&id, id_h, 128);
+  CKN(ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->cfg.rank));
+  return LG_OK;
+}
+
+lg_status lg_broadcast_params(lg_ctx* ctx) {
+  GUARD();
+  if (ctx->world > 1 && ctx->comm)
+    CKN(ncclBroadcast(ctx->buf[LG_BUF_THETA], ctx->buf[LG_BUF_THETA], (size_t)ctx->d.P, ncclFloat32, 0, ctx->comm, ctx->st));
+  return lg_params_sync(ctx);
+}
+
+// ------------------------------------------------------------------ whole iteration
+static lg_status run_iteration(lg_ctx* ctx, lg_update_stats* stats) {
+  lg_status s;
+  for (int t = 0; t < ctx->d.T; ++t) {
+    if ((s = policy_act(ctx, t, nullptr, nullptr, nullptr, nullptr)) != LG_OK) return s;
+    if ((s = env_step_obs_reward(ctx, t, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) != LG_OK) return s;
+  }
+  if ((s = storage_compute_gae(ctx, nullptr, nullptr)) != LG_OK) return s;
+  return ppo_update(ctx, stats);
+}
+
+lg_status lg_graph_capture_iteration(lg_ctx* ctx, lg_update_stats* stats) {
+  GUARD();
+  if (!ctx->reset_done) return fail(ctx, LG_ERR_STATE, "graph capture before env_reset");
+  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
+  if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
+  CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+  lg_status s = run_iteration(ctx, stats);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->st, &g);
+  if (s != LG_OK) return s;
+  if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "end capture: %s", cudaGetErrorString(e));
+  ctx->graph = g;
+  CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+  return LG_OK;
+}
+
+lg_status lg_graph_launch(lg_ctx* ctx) {
+  GUARD();
+  if (!ctx->gexec) return fail(ctx, LG_ERR_STATE, "no captured graph");
+  CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+  return LG_OK;
+}
+
+lg_status lg_iterate_host(lg_ctx* ctx, const uint8_t ctrl_h[16], lg_update_stats* stats_h) {
+  GUARD();
+  if (!ctrl_h || !stats_h) return fail(ctx, LG_ERR_INVALID_ARG, "iterate_host: null host buffer");
+  void* K = ctx->buf[LG_BUF_WORK];
+  CK(cudaMemcpyAsync(at<uint8_t>(K, ctx->L.k_ctrl), ctrl_h, 16, cudaMemcpyHostToDevice, ctx->st));
+  lg_update_stats* dstats = at<lg_update_stats>(K, ctx->L.k_stats);
+  lg_status s;
+  if (ctx->gexec) {
+    CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+  } else if ((s = run_iteration(ctx, dstats)) != LG_OK) {
+    return s;
+  }
+  CK(cudaMemcpyAsync(stats_h, dstats, sizeof(lg_update_stats), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return LG_OK;
+}
+
+lg_status lg_device_scalars(lg_ctx* ctx, int32_t* out8_h) {
+  GUARD();
+  if (!out8_h) return fail(ctx, LG_ERR_INVALID_ARG, "null output");
+  DevScalars s;
+  CK(cudaMemcpyAsync(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  out8_h[0] = (int32_t)s.s_base; out8_h[1] = (int32_t)s.iteration; out8_h[2] = s.adam_t;
+  memcpy(&out8_h[3], &s.alpha, 4);
+  out8_h[4] = s.n_to; out8_h[5] = s.nonfinite_skips; out8_h[6] = s.applied;
+  memcpy(&out8_h[7], &s.kl_last, 4);
+  return LG_OK;
+}
+
+}  // extern "C"

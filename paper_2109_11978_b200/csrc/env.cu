@@ -1,0 +1,533 @@
+// env.cu -- environment kernels: reset, transition, reward, flags, curriculum, observation + height
+// scan + noise (§3, Tables 2/4; SPEC env/dynamics/curriculum).
+// Compiled with -fmad=false: every a*b+c is two IEEE roundings, as in the oracle (R26).
+//
+// Layout: state SoA [66][N] (field-major, so every field access is coalesced across the warp).
+// Kernel shape: one thread per env for the per-env serial work (phase A), then the block's threads
+// cooperate on the observation rows (phase B): each item = 4 consecutive observation elements of one
+// env = exactly one Philox block of noise, written as one 8-byte bf16x4 store (coalesced along a row).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lg {
+
+constexpr float M_BASE = 30.0f, GRAV = 9.81f, L_HIP = 0.08f, L_T = 0.35f, L_S = 0.35f;
+constexpr float KP = 80.0f, KD = 2.0f, TAU_MAX = 80.0f, J_J = 0.25f, C_J = 0.5f;
+constexpr float K_N = 5000.0f, C_N = 100.0f, C_T = 60.0f, R_B = 0.25f, DT_SIM = 0.005f, DT = 0.02f;
+
+__constant__ float c_inertia[3] = {0.5f, 1.7f, 2.0f};
+__constant__ float c_hip[4][3] = {{0.30f, 0.15f, 0.0f}, {0.30f, -0.15f, 0.0f}, {-0.30f, 0.15f, 0.0f}, {-0.30f, -0.15f, 0.0f}};
+__constant__ float c_slat[4] = {1.0f, -1.0f, 1.0f, -1.0f};
+__constant__ float c_qdef[12] = {0.0f, 0.7f, -1.4f, 0.0f, 0.7f, -1.4f, 0.0f, -0.7f, 1.4f, 0.0f, -0.7f, 1.4f};
+
+struct St {  // registers of one env (DESIGN.md §3.4 record)
+  float p[3], quat[4], v[3], w[3], q[12], qd[12], tair[4], cmd[3], aprev[12], mu, spawn[2];
+  uint32_t contact;
+  int32_t push_timer, ep_step, level, col;
+  uint32_t crossed;
+  float ep_return;
+};
+
+__device__ __forceinline__ void load_state(const uint32_t* __restrict__ S, int N, int i, St& s) {
+  auto f = [&](int w) { return __uint_as_float(S[(size_t)w * N + i]); };
+  for (int k = 0; k < 3; ++k) { s.p[k] = f(S_P + k); s.v[k] = f(S_V + k); s.w[k] = f(S_W + k); s.cmd[k] = f(S_CMD + k); }
+  for (int k = 0; k < 4; ++k) { s.quat[k] = f(S_QUAT + k); s.tair[k] = f(S_TAIR + k); }
+  for (int k = 0; k < 12; ++k) { s.q[k] = f(S_Q + k); s.qd[k] = f(S_QD + k); s.aprev[k] = f(S_APREV + k); }
+  s.mu = f(S_MU); s.spawn[0] = f(S_SPAWN); s.spawn[1] = f(S_SPAWN + 1);
+  s.contact = S[(size_t)S_CONTACT * N + i];
+  s.push_timer = (int32_t)S[(size_t)S_PUSH * N + i];
+  s.ep_step = (int32_t)S[(size_t)S_EPSTEP * N + i];
+  s.level = (int32_t)S[(size_t)S_LEVEL * N + i];
+  s.col = (int32_t)S[(size_t)S_COL * N + i];
+  s.crossed = S[(size_t)S_CROSSED * N + i];
+  s.ep_return = f(S_EPRET);
+}
+
+__device__ __forceinline__ void store_state(uint32_t* __restrict__ S, int N, int i, const St& s) {
+  auto f = [&](int w, float v) { S[(size_t)w * N + i] = __float_as_uint(v); };
+  for (int k = 0; k < 3; ++k) { f(S_P + k, s.p[k]); f(S_V + k, s.v[k]); f(S_W + k, s.w[k]); f(S_CMD + k, s.cmd[k]); }
+  for (int k = 0; k < 4; ++k) { f(S_QUAT + k, s.quat[k]); f(S_TAIR + k, s.tair[k]); }
+  for (int k = 0; k < 12; ++k) { f(S_Q + k, s.q[k]); f(S_QD + k, s.qd[k]); f(S_APREV + k, s.aprev[k]); }
+  f(S_MU, s.mu); f(S_SPAWN, s.spawn[0]); f(S_SPAWN + 1, s.spawn[1]);
+  S[(size_t)S_CONTACT * N + i] = s.contact;
+  S[(size_t)S_PUSH * N + i] = (uint32_t)s.push_timer;
+  S[(size_t)S_EPSTEP * N + i] = (uint32_t)s.ep_step;
+  S[(size_t)S_LEVEL * N + i] = (uint32_t)s.level;
+  S[(size_t)S_COL * N + i] = (uint32_t)s.col;
+  S[(size_t)S_CROSSED * N + i] = s.crossed;
+  f(S_EPRET, s.ep_return);
+}
+
+struct Mat3 { float m[3][3]; };
+
+__device__ __forceinline__ Mat3 rot(const float* qt) {
+  float w = qt[0], x = qt[1], y = qt[2], z = qt[3];
+  Mat3 R;
+  R.m[0][0] = 1.0f - 2.0f * (y * y + z * z);
+  R.m[0][1] = 2.0f * (x * y - w * z);
+  R.m[0][2] = 2.0f * (x * z + w * y);
+  R.m[1][0] = 2.0f * (x * y + w * z);
+  R.m[1][1] = 1.0f - 2.0f * (x * x + z * z);
+  R.m[1][2] = 2.0f * (y * z - w * x);
+  R.m[2][0] = 2.0f * (x * z - w * y);
+  R.m[2][1] = 2.0f * (y * z + w * x);
+  R.m[2][2] = 1.0f - 2.0f * (x * x + y * y);
+  return R;
+}
+__device__ __forceinline__ void mv(const Mat3& R, const float* u, float* o) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o[i] = (R.m[i][0] * u[0] + R.m[i][1] * u[1]) + R.m[i][2] * u[2];
+}
+__device__ __forceinline__ void mtv(const Mat3& R, const float* u, float* o) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o[i] = (R.m[0][i] * u[0] + R.m[1][i] * u[1]) + R.m[2][i] * u[2];
+}
+__device__ __forceinline__ void cross3(const float* a, const float* b, float* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+__device__ __forceinline__ float dot3(const float* a, const float* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+// leg FK (+ Jacobian columns J[col][xyz]) in the base frame, DESIGN.md §3.5
+__device__ __forceinline__ void leg_fk(int leg, const float* ql, float lsh, float* pt, float (*J)[3]) {
+  float sa, ca, s1, c1, s12, c12;
+  sincos_poly(ql[0], sa, ca);
+  sincos_poly(ql[1], s1, c1);
+  sincos_poly(ql[1] + ql[2], s12, c12);
+  float fx = -L_T * s1 - lsh * s12;
+  float fy = c_slat[leg] * L_HIP;
+  float fz = -L_T * c1 - lsh * c12;
+  pt[0] = c_hip[leg][0] + fx;
+  pt[1] = c_hip[leg][1] + (fy * ca - fz * sa);
+  pt[2] = c_hip[leg][2] + (fy * sa + fz * ca);
+  if (J) {
+    J[0][0] = 0.0f;
+    J[0][1] = -sa * fy - ca * fz;
+    J[0][2] = ca * fy - sa * fz;
+    float dx = -L_T * c1 - lsh * c12, dz = L_T * s1 + lsh * s12;
+    J[1][0] = dx; J[1][1] = -sa * dz; J[1][2] = ca * dz;
+    float ex = -lsh * c12, ez = lsh * s12;
+    J[2][0] = ex; J[2][1] = -sa * ez; J[2][2] = ca * ez;
+  }
+}
+
+__device__ __forceinline__ void heading(const Mat3& R, float& c, float& s) {
+  float f0 = R.m[0][0], f1 = R.m[1][0];
+  float n = sqrtf(f0 * f0 + f1 * f1);
+  if (n > 1e-6f) { c = f0 / n; s = f1 / n; } else { c = 1.0f; s = 0.0f; }
+}
+
+// reset of env g
+__device__ void reset_env(const World& W, const Rng& rng, St& s, uint32_t g, uint32_t ev) {
+  U4 b0 = rng.block(0, g, ev, TAG_RESET), b1 = rng.block(1, g, ev, TAG_RESET), b2 = rng.block(2, g, ev, TAG_RESET),
+     b3 = rng.block(3, g, ev, TAG_RESET), b4 = rng.block(4, g, ev, TAG_RESET);
+  uint32_t wd[20] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y,
+                     b2.z, b2.w, b3.x, b3.y, b3.z, b3.w, b4.x, b4.y, b4.z, b4.w};
+  float x = ((float)s.level * 8.0f + 4.0f) + usym(1.0f, wd[0]);
+  float y = ((float)s.col * 8.0f + 4.0f) + usym(1.0f, wd[1]);
+  float psi = usym(0x1.921fb6p1f, wd[2]);
+  float sh, ch;
+  sincos_poly(0.5f * psi, sh, ch);
+  s.p[0] = x; s.p[1] = y; s.p[2] = h_plate(W, x, y) + 0.6f;
+  s.quat[0] = ch; s.quat[1] = 0.0f; s.quat[2] = 0.0f; s.quat[3] = sh;
+  for (int k = 0; k < 3; ++k) { s.v[k] = 0.0f; s.w[k] = 0.0f; }
+  s.mu = 0.5f + 0.75f * u01(wd[3]);
+  for (int k = 0; k < 3; ++k) s.cmd[k] = usym(1.0f, wd[4 + k]);
+#pragma unroll
+  for (int j = 0; j < 12; ++j) { s.q[j] = c_qdef[j] + usym(0.05f, wd[7 + j]); s.qd[j] = 0.0f; s.aprev[j] = 0.0f; }
+  for (int l = 0; l < 4; ++l) s.tair[l] = 0.0f;
+  s.contact = 0u; s.push_timer = 0; s.ep_step = 0; s.crossed = 0u;
+  s.spawn[0] = x; s.spawn[1] = y; s.ep_return = 0.0f;
+}
+
+// per-env observation record for the cooperative phase
+struct ObsRec {
+  float pro[48];
+  float px, py, pz, c, s;
+  uint32_t g, word0;
+  int32_t row;  // destination row (env index, or compacted terminal row)
+};
+
+__device__ __forceinline__ void fill_obs_rec(const St& s, ObsRec& o) {
+  Mat3 R = rot(s.quat);
+  float t3[3];
+  mtv(R, s.v, t3);
+  o.pro[0] = t3[0]; o.pro[1] = t3[1]; o.pro[2] = t3[2];
+  o.pro[3] = s.w[0]; o.pro[4] = s.w[1]; o.pro[5] = s.w[2];
+  o.pro[6] = -R.m[2][0]; o.pro[7] = -R.m[2][1]; o.pro[8] = -R.m[2][2];
+  o.pro[9] = s.cmd[0]; o.pro[10] = s.cmd[1]; o.pro[11] = s.cmd[2];
+  for (int j = 0; j < 12; ++j) { o.pro[12 + j] = s.q[j]; o.pro[24 + j] = s.qd[j]; o.pro[36 + j] = s.aprev[j]; }
+  heading(R, o.c, o.s);
+  o.px = s.p[0]; o.py = s.p[1]; o.pz = s.p[2];
+}
+
+__device__ __forceinline__ float noise_scale(int e) {
+  if (e < 3) return 0.01f;
+  if (e < 6) return 0.2f;
+  if (e < 9) return 0.05f;
+  if (e < 12) return 0.0f;
+  if (e < 24) return 0.01f;
+  if (e < 36) return 1.5f;
+  if (e < 48) return 0.0f;
+  return 0.1f;
+}
+
+// one observation element e of record o
+__device__ __forceinline__ float obs_elem(const EnvParams& P, const World& W, const ObsRec& o, int e) {
+  if (e < 48) return o.pro[e];
+  int k = e - 48;
+  int ix = k / P.scan_ny, iy = k - ix * P.scan_ny;
+  float dx = (float)(ix - P.scan_nx / 2) * 0.1f;
+  float dy = (float)(iy - P.scan_ny / 2) * 0.1f;
+  float x = o.px + (o.c * dx - o.s * dy);
+  float y = o.py + (o.s * dx + o.c * dy);
+  return o.pz - h_bilinear(W, x, y);
+}
+
+// cooperative write of the observation rows of `cnt` records (items of 4 elements)
+__device__ void write_obs_rows(const EnvParams& P, const World& W, const Rng& rng, uint32_t ev, const ObsRec* recs,
+                               int cnt, __nv_bfloat16* __restrict__ dst_bf16, float* __restrict__ dst_f32) {
+  const int D = P.obs_dim, Dp = P.obs_stride, G = Dp / 4;
+  for (int it = threadIdx.x; it < cnt * G; it += blockDim.x) {
+    int r = it / G, gq = it - r * G;
+    const ObsRec& o = recs[r];
+    float v[4];
+    U4 nb0, nb1;
+    bool noise = (P.flags & F_NOISE) != 0;
+    uint32_t wbase = o.word0 + 4u * (uint32_t)gq;
+    if (noise && 4 * gq < D) {
+      nb0 = rng.block(wbase >> 2, o.g, ev, TAG_OBS);
+      if (wbase & 3u) nb1 = rng.block((wbase >> 2) + 1, o.g, ev, TAG_OBS);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int e = 4 * gq + k;
+      float x = 0.0f;
+      if (e < D) {
+        x = obs_elem(P, W, o, e);
+        if (noise) {
+          float sc = noise_scale(e);
+          if (sc != 0.0f) {
+            uint32_t w = wbase + (uint32_t)k;
+            uint32_t word = ((w >> 2) == (wbase >> 2)) ? pick(nb0, w) : pick(nb1, w);
+            x = x + usym(sc, word);
+          }
+        }
+        if (dst_f32) dst_f32[(size_t)o.row * D + e] = x;
+      }
+      v[k] = x;
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(dst_bf16 + (size_t)o.row * Dp + 4 * gq) = pk;
+  }
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void __launch_bounds__(ENV_BLOCK) k_env_reset(EnvParams P, const uint8_t* __restrict__ mask, int init,
+                                                         float* __restrict__ obs_f32) {
+  __shared__ ObsRec recs[ENV_BLOCK];
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  World W{P.hf, P.R, P.C, P.inv_cell};
+  Rng rng{P.seed_lo, P.seed_hi};
+  const uint32_t ev = P.scalars->s_base;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P.N && (!mask || mask[i])) {
+    St s;
+    load_state(P.state, P.N, i, s);
+    uint32_t g = (uint32_t)(P.rank * P.N + i);
+    if (init) { s.col = (int32_t)(g % (uint32_t)P.n_cols); s.level = 0; }
+    reset_env(W, rng, s, g, ev);
+    store_state(P.state, P.N, i, s);
+    int slot = atomicAdd(&cnt, 1);
+    fill_obs_rec(s, recs[slot]);
+    recs[slot].g = g; recs[slot].word0 = 0u; recs[slot].row = i;
+  }
+  __syncthreads();
+  // obs slot 0
+  write_obs_rows(P, W, rng, ev, recs, cnt, P.obs_out, obs_f32);
+}
+
+__global__ void __launch_bounds__(ENV_BLOCK) k_env_step(EnvParams P, int t, const float* __restrict__ actions,
+                                                        float* __restrict__ obs_f32, float* __restrict__ rew_out,
+                                                        uint8_t* __restrict__ term_out, uint8_t* __restrict__ to_out,
+                                                        float* __restrict__ terms_out) {
+  __shared__ ObsRec recs[ENV_BLOCK];
+  __shared__ ObsRec trecs[ENV_BLOCK];
+  __shared__ int tcnt;
+  if (threadIdx.x == 0) tcnt = 0;
+  __syncthreads();
+  World W{P.hf, P.R, P.C, P.inv_cell};
+  Rng rng{P.seed_lo, P.seed_hi};
+  const uint32_t ev = P.scalars->s_base + (uint32_t)t + 1u;
+  const int N = P.N;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < N;
+  if (active) {
+    St s;
+    load_state(P.state, N, i, s);
+    const uint32_t g = (uint32_t)(P.rank * N + i);
+    float a[12], qstar[12], tau[12], qdd[12];
+    const float* ap = actions + (size_t)i * 12;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) { a[j] = ap[j]; qstar[j] = c_qdef[j] + 0.5f * a[j]; }
+    if ((P.flags & F_PUSH) && s.push_timer >= 500) {
+      U4 pb = rng.block(0, g, ev, TAG_PUSH);
+      s.v[0] = s.v[0] + usym(1.0f, pb.x);
+      s.v[1] = s.v[1] + usym(1.0f, pb.y);
+      s.push_timer = 0;
+    }
+    float airsum = 0.0f;
+    int crash = 0;
+    for (int sub = 0; sub < 4; ++sub) {
+      Mat3 R = rot(s.quat);
+      float ww[3];
+      mv(R, s.w, ww);
+#pragma unroll
+      for (int j = 0; j < 12; ++j) tau[j] = clampf_(KP * (qstar[j] - s.q[j]) - KD * s.qd[j], -TAU_MAX, TAU_MAX);
+      float F[3] = {0.0f, 0.0f, 0.0f}, Tw[3] = {0.0f, 0.0f, 0.0f};
+      uint32_t contact = 0u;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        float fb[3], J[3][3], r[3], pf[3], jq[3], rj[3], cr[3], vf[3];
+        leg_fk(l, &s.q[3 * l], L_S, fb, J);
+        mv(R, fb, r);
+        for (int k = 0; k < 3; ++k) pf[k] = s.p[k] + r[k];
+        const float* qdl = &s.qd[3 * l];
+        for (int k = 0; k < 3; ++k) jq[k] = (J[0][k] * qdl[0] + J[1][k] * qdl[1]) + J[2][k] * qdl[2];
+        cross3(ww, r, cr);
+        mv(R, jq, rj);
+        for (int k = 0; k < 3; ++k) vf[k] = (s.v[k] + cr[k]) + rj[k];
+        float delta = h_plate(W, pf[0], pf[1]) - pf[2];
+        float f[3] = {0.0f, 0.0f, 0.0f};
+        if (delta > 0.0f) {
+          float fn = fmaxf(0.0f, K_N * delta - C_N * vf[2]);
+          float vt = sqrtf(vf[0] * vf[0] + vf[1] * vf[1]);
+          float sc = vt > 0.0f ? fminf(C_T, (s.mu * fn) / vt) : 0.0f;
+          f[0] = -sc * vf[0];
+          f[1] = -sc * vf[1];
+          f[2] = fn;
+          contact |= (1u << l);
+        }
+        float fbb[3];
+        mtv(R, f, fbb);
+        float tc0 = dot3(J[0], fbb), tc1 = dot3(J[1], fbb), tc2 = dot3(J[2], fbb);
+        qdd[3 * l + 0] = ((tau[3 * l + 0] + tc0) - C_J * s.qd[3 * l + 0]) / J_J;
+        qdd[3 * l + 1] = ((tau[3 * l + 1] + tc1) - C_J * s.qd[3 * l + 1]) / J_J;
+        qdd[3 * l + 2] = ((tau[3 * l + 2] + tc2) - C_J * s.qd[3 * l + 2]) / J_J;
+        float rf[3];
+        cross3(r, f, rf);
+        for (int k = 0; k < 3; ++k) { F[k] = F[k] + f[k]; Tw[k] = Tw[k] + rf[k]; }
+      }
+      F[2] = F[2] - M_BASE * GRAV;
+      float tb[3], Iw[3], gy[3], wdot[3];
+      mtv(R, Tw, tb);
+      for (int k = 0; k < 3; ++k) Iw[k] = c_inertia[k] * s.w[k];
+      cross3(s.w, Iw, gy);
+      for (int k = 0; k < 3; ++k) wdot[k] = (tb[k] - gy[k]) / c_inertia[k];
+      for (int k = 0; k < 3; ++k) s.v[k] = s.v[k] + DT_SIM * (F[k] / M_BASE);
+      for (int k = 0; k < 3; ++k) s.w[k] = s.w[k] + DT_SIM * wdot[k];
+#pragma unroll
+      for (int j = 0; j < 12; ++j) s.qd[j] = s.qd[j] + DT_SIM * qdd[j];
+      for (int k = 0; k < 3; ++k) s.p[k] = s.p[k] + DT_SIM * s.v[k];
+#pragma unroll
+      for (int j = 0; j < 12; ++j) s.q[j] = s.q[j] + DT_SIM * s.qd[j];
+      {
+        float h = 0.5f * DT_SIM;
+        float w = s.quat[0], x = s.quat[1], y = s.quat[2], z = s.quat[3];
+        float o0 = s.w[0], o1 = s.w[1], o2 = s.w[2];
+        float w2 = w + h * (((-x * o0) - y * o1) - z * o2);
+        float x2 = x + h * ((w * o0 + y * o2) - z * o1);
+        float y2 = y + h * ((w * o1 + z * o0) - x * o2);
+        float z2 = z + h * ((w * o2 + x * o1) - y * o0);
+        float n = sqrtf(((w2 * w2 + x2 * x2) + y2 * y2) + z2 * z2);
+        s.quat[0] = w2 / n; s.quat[1] = x2 / n; s.quat[2] = y2 / n; s.quat[3] = z2 / n;
+      }
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        uint32_t cn = (contact >> l) & 1u, cp = (s.contact >> l) & 1u;
+        if (cn && !cp) { airsum = airsum + (s.tair[l] - 0.5f); s.tair[l] = 0.0f; }
+        else if (!cn) s.tair[l] = s.tair[l] + DT_SIM;
+      }
+      s.contact = contact;
+      if (s.p[2] - h_plate(W, s.p[0], s.p[1]) < R_B) crash = 1;
+    }
+    // knees (R9)
+    Mat3 R = rot(s.quat);
+    int n_c = 0;
+    for (int l = 0; l < 4; ++l) {
+      float kb[3], r[3];
+      leg_fk(l, &s.q[3 * l], 0.5f * L_S, kb, nullptr);
+      mv(R, kb, r);
+      float kx = s.p[0] + r[0], ky = s.p[1] + r[1], kz = s.p[2] + r[2];
+      if (h_plate(W, kx, ky) - kz > 0.0f) n_c = n_c + 1;
+    }
+    s.ep_step += 1;
+    s.push_timer += 1;
+    {
+      float x0 = (float)s.level * 8.0f, y0 = (float)s.col * 8.0f;
+      if (s.p[0] < x0 || s.p[0] >= x0 + 8.0f || s.p[1] < y0 || s.p[1] >= y0 + 8.0f) s.crossed = 1u;
+    }
+    bool finite = true;
+    for (int k = 0; k < 3; ++k) finite = finite && isfinite(s.p[k]) && isfinite(s.v[k]) && isfinite(s.w[k]);
+    for (int k = 0; k < 4; ++k) finite = finite && isfinite(s.quat[k]);
+    for (int j = 0; j < 12; ++j) finite = finite && isfinite(s.q[j]) && isfinite(s.qd[j]);
+    // reward
+    float rt[9];
+    {
+      float c, sn, wv[3];
+      heading(R, c, sn);
+      float vh0 = c * s.v[0] + sn * s.v[1];
+      float vh1 = -sn * s.v[0] + c * s.v[1];
+      float vh2 = s.v[2];
+      mv(R, s.w, wv);
+      float wh0 = c * wv[0] + sn * wv[1];
+      float wh1 = -sn * wv[0] + c * wv[1];
+      float wh2 = wv[2];
+      float ex = s.cmd[0] - vh0, ey = s.cmd[1] - vh1, ez = s.cmd[2] - wh2;
+      rt[0] = (1.0f * DT) * exp_poly(-((ex * ex + ey * ey) / 0.25f));
+      rt[1] = (0.5f * DT) * exp_poly(-((ez * ez) / 0.25f));
+      rt[2] = (-4.0f * DT) * (vh2 * vh2);
+      rt[3] = (-0.05f * DT) * (wh0 * wh0 + wh1 * wh1);
+      float sa = 0.0f, sb = 0.0f, stq = 0.0f, sr = 0.0f;
+      for (int j = 0; j < 12; ++j) sa = sa + qdd[j] * qdd[j];
+      for (int j = 0; j < 12; ++j) sb = sb + s.qd[j] * s.qd[j];
+      rt[4] = (-0.001f * DT) * (sa + sb);
+      for (int j = 0; j < 12; ++j) stq = stq + tau[j] * tau[j];
+      rt[5] = (-0.00002f * DT) * stq;
+      for (int j = 0; j < 12; ++j) {
+        float qprev = c_qdef[j] + 0.5f * s.aprev[j];
+        float d = (qstar[j] - qprev) / DT;
+        sr = sr + d * d;
+      }
+      rt[6] = (-0.25f * DT) * sr;
+      rt[7] = (-0.001f * DT) * (float)n_c;
+      rt[8] = (2.0f * DT) * airsum;
+    }
+    float r = rt[0];
+    for (int k = 1; k < 9; ++k) r = r + rt[k];
+    if (!finite) { r = 0.0f; for (int k = 0; k < 9; ++k) rt[k] = 0.0f; }
+    s.ep_return = s.ep_return + r;
+    const bool terminated = crash || !finite;
+    const bool to = (s.ep_step >= 1000) && !terminated;
+    const bool done = terminated || to;
+    for (int j = 0; j < 12; ++j) s.aprev[j] = a[j];
+    const size_t ti = (size_t)t * N + i;
+    P.reward[ti] = r;
+    P.flags_out[ti] = (uint8_t)((terminated ? 1u : 0u) | (to ? 2u : 0u));
+    P.boot[ti] = 0.0f;
+    if (rew_out) rew_out[i] = r;
+    if (term_out) term_out[i] = (uint8_t)terminated;
+    if (to_out) to_out[i] = (uint8_t)to;
+    if (terms_out)
+      for (int k = 0; k < 9; ++k) terms_out[(size_t)i * 9 + k] = rt[k];
+    if (done) {
+      if (to && (P.flags & F_BOOTSTRAP)) {
+        int slot = atomicAdd(&tcnt, 1);
+        int row = atomicAdd(&P.scalars->n_to, 1);
+        fill_obs_rec(s, trecs[slot]);
+        trecs[slot].g = g; trecs[slot].word0 = 0u; trecs[slot].row = row;
+        P.term_idx[row] = i;
+      }
+      // episode statistics (stats only; float atomics)
+      atomicAdd(&P.scalars->ep_return_sum, s.ep_return);
+      atomicAdd(&P.scalars->ep_len_sum, (float)s.ep_step);
+      atomicAdd(&P.scalars->episodes, 1);
+      if (P.flags & F_CURRICULUM) {
+        int old = s.level;
+        if (s.crossed) {
+          s.level = s.level + 1;
+          if (s.level > P.n_levels - 1) {
+            uint32_t wrd = rng.block(0, g, ev, TAG_CURR).x;
+            s.level = (int32_t)(((uint64_t)wrd * (uint64_t)P.n_levels) >> 32);
+          }
+        } else {
+          float dx = s.p[0] - s.spawn[0], dy = s.p[1] - s.spawn[1];
+          float T = (float)s.ep_step * DT;
+          float hh = 0.5f * T;
+          if ((dx * dx + dy * dy) < (hh * hh) * (s.cmd[0] * s.cmd[0] + s.cmd[1] * s.cmd[1])) s.level = max(0, s.level - 1);
+        }
+        if (s.level > old) atomicAdd(&P.scalars->promotions, 1);
+        if (s.level < old) atomicAdd(&P.scalars->demotions, 1);
+      }
+      reset_env(W, rng, s, g, ev);
+    }
+    store_state(P.state, N, i, s);
+    fill_obs_rec(s, recs[threadIdx.x]);
+    recs[threadIdx.x].g = g;
+    recs[threadIdx.x].word0 = done ? (uint32_t)P.obs_dim : 0u;
+    recs[threadIdx.x].row = i;
+  }
+  __syncthreads();
+  int cnt = min(ENV_BLOCK, N - (int)(blockIdx.x * blockDim.x));
+  // o_{t+1} into OBS slot t+1 (bf16) and the caller's fp32 obs; records are in thread order
+  write_obs_rows(P, W, rng, ev, recs, cnt, P.obs_out + (size_t)(t + 1) * N * P.obs_stride, obs_f32);
+  if (tcnt > 0) write_obs_rows(P, W, rng, ev, trecs, tcnt, P.term_obs, nullptr);
+}
+
+// standalone curriculum rule (DESIGN.md §3.7 step 9(ii))
+__global__ void k_curriculum(int n, int n_levels, const uint8_t* crossed, const float* disp, const float* cmd,
+                             const int32_t* ep_steps, const uint32_t* words, int32_t* level) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int lv = level[i];
+  if (crossed[i]) {
+    lv = lv + 1;
+    if (lv > n_levels - 1) lv = (int32_t)(((uint64_t)words[i] * (uint64_t)n_levels) >> 32);
+  } else {
+    float dx = disp[2 * i], dy = disp[2 * i + 1], c0 = cmd[2 * i], c1 = cmd[2 * i + 1];
+    float T = (float)ep_steps[i] * DT;
+    float hh = 0.5f * T;
+    if ((dx * dx + dy * dy) < (hh * hh) * (c0 * c0 + c1 * c1)) lv = max(0, lv - 1);
+  }
+  level[i] = lv;
+}
+
+// Gaussian ε for the policy head: eps[i][12] for step event ev
+__device__ void action_eps(const Rng& rng, uint32_t g, uint32_t ev, float* eps) {
+  U4 b0 = rng.block(0, g, ev, TAG_ACTION), b1 = rng.block(1, g, ev, TAG_ACTION), b2 = rng.block(2, g, ev, TAG_ACTION);
+  uint32_t w[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    float u1 = (float)((w[2 * k] >> 8) + 1u) * 0x1p-24f;
+    float u2 = (float)(w[2 * k + 1] >> 8) * 0x1p-24f;
+    float rr = sqrtf(-2.0f * log_poly(u1));
+    float sn, cs;
+    sincos_poly(0x1.921fb6p2f * u2, sn, cs);
+    eps[2 * k] = rr * cs;
+    eps[2 * k + 1] = rr * sn;
+  }
+}
+
+__global__ void k_action_eps(int N, int rank, uint32_t seed_lo, uint32_t seed_hi, const DevScalars* sc, int t, float* eps) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  Rng rng{seed_lo, seed_hi};
+  action_eps(rng, (uint32_t)(rank * N + i), sc->s_base + (uint32_t)t + 1u, eps + (size_t)i * 12);
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* obs_f32, cudaStream_t st) {
+  int nb = (P.N + ENV_BLOCK - 1) / ENV_BLOCK;
+  k_env_reset<<<nb, ENV_BLOCK, 0, st>>>(P, mask, init, obs_f32);
+}
+void launch_env_step(const EnvParams& P, int t, const float* actions, float* obs_f32, float* rew, uint8_t* term,
+                     uint8_t* to, float* terms, cudaStream_t st) {
+  int nb = (P.N + ENV_BLOCK - 1) / ENV_BLOCK;
+  k_env_step<<<nb, ENV_BLOCK, 0, st>>>(P, t, actions, obs_f32, rew, term, to, terms);
+}
+void launch_curriculum(int n, int n_levels, const uint8_t* crossed, const float* disp, const float* cmd,
+                       const int32_t* ep, const uint32_t* words, int32_t* level, cudaStream_t st) {
+  k_curriculum<<<(n + 127) / 128, 128, 0, st>>>(n, n_levels, crossed, disp, cmd, ep, words, level);
+}
+void launch_action_eps(int N, int rank, uint32_t s0, uint32_t s1, const DevScalars* sc, int t, float* eps,
+                       cudaStream_t st) {
+  k_action_eps<<<(N + 127) / 128, 128, 0, st>>>(N, rank, s0, s1, sc, t, eps);
+}
+
+}  // namespace lg

@@ -1,0 +1,196 @@
+// kernels.h -- host/device structures and launchers shared by the translation units of libleggedrl.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/lg.h"
+
+namespace lg {
+
+struct DevScalars;
+using lg_update_stats_dev = ::lg_update_stats;
+
+constexpr int ENV_BLOCK = 64;
+
+struct EnvParams {
+  const float* hf;
+  int R, C;
+  float inv_cell;
+  int N, rank, n_levels, n_cols, scan_nx, scan_ny, obs_dim, obs_stride;
+  uint32_t flags, seed_lo, seed_hi;
+  uint32_t* state;           // SoA [66][N]
+  DevScalars* scalars;
+  __nv_bfloat16* obs_out;    // OBS buffer base (slot 0)
+  float* reward;             // [T][N]
+  uint8_t* flags_out;        // [T][N]
+  float* boot;               // [T][N]
+  __nv_bfloat16* term_obs;   // [N][Dp] compacted pre-reset observations of time-out envs
+  int32_t* term_idx;         // [N]
+};
+
+void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* obs_f32, cudaStream_t st);
+void launch_env_step(const EnvParams& P, int t, const float* actions, float* obs_f32, float* rew, uint8_t* term,
+                     uint8_t* to, float* terms, cudaStream_t st);
+void launch_curriculum(int n, int n_levels, const uint8_t* crossed, const float* disp, const float* cmd,
+                       const int32_t* ep, const uint32_t* words, int32_t* level, cudaStream_t st);
+void launch_action_eps(int N, int rank, uint32_t s0, uint32_t s1, const DevScalars* sc, int t, float* eps,
+                       cudaStream_t st);
+
+// ------------------------------------------------------------------ tcgen05 GEMM
+enum GemmKind { GEMM_FWD = 0, GEMM_DX = 1, GEMM_DW = 2 };
+
+struct GemmArgs {
+  CUtensorMap tmA[2];
+  CUtensorMap tmB[2];
+  int M, N;                  // output rows / cols (per z)
+  const int* M_dev;          // optional device-side M (rows beyond exit early)
+  int kb_total, kb_per_split, n_tiles, n_splits;
+  void* out[2];              // EPI 0/2: bf16 output base per z (already column-offset)
+  int ldo;
+  const float* bias[2];      // EPI 0
+  const __nv_bfloat16* aux[2];  // EPI 2: saved activation for ELU'
+  int ld_aux;
+  float* part;               // EPI 3: split-K partials [z][split][rows][part_ld]
+  long long part_zstride, part_sstride;
+  int part_ld, part_bias_col, bias_col;
+};
+
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
+cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, int m_tiles, int nz, cudaStream_t st);
+
+// ------------------------------------------------------------------ PPO kernels (ppo.cu)
+struct NetDims {
+  int D, Dp, H0, H1, H2;
+};
+
+struct HeadArgs {
+  NetDims nd;
+  const __nv_bfloat16* H3;   // [rows][2*H2]
+  const float* W4a;          // [12][H2]
+  const float* b4a;          // [12]
+  const float* W4c;          // [H2]
+  const float* b4c;          // [1]
+  const float* logstd;       // [12]
+  int M;                     // rows
+  const int* M_dev;          // optional device row count
+  // ACT mode
+  int mode;                  // 0 = act (sample), 1 = value scatter, 2 = forward (mu, V)
+  int t, N, rank;
+  uint32_t seed_lo, seed_hi;
+  const DevScalars* scalars;
+  float* act;                // [rows][12]
+  float* mu;                 // [rows][12]
+  float* logp;               // [rows]
+  float* value;              // [rows]  (mode 1: destination base)
+  const int32_t* idx;        // mode 1: value[idx[r]] = V
+  float* u_act; float* u_logp; float* u_mu; float* u_value;  // optional caller copies
+};
+void launch_heads(const HeadArgs& a, cudaStream_t st);
+
+struct LossArgs {
+  NetDims nd;
+  int M;                     // minibatch rows
+  const __nv_bfloat16* H3;   // [M][2*H2]
+  const float* W4a; const float* b4a; const float* W4c; const float* b4c;
+  const float* logstd; const float* logstd_old;
+  const float* act; const float* mu_old; const float* logp_old; const float* V_old; const float* adv; const float* ret;
+  float clip, vclip, ent_coef, vf_coef;
+  __nv_bfloat16* dZ3;        // [M][2*H2] out
+  float* part;               // [nblk][HP]
+  double* spart;             // [nblk][8]
+  int HP;
+};
+int loss_head_partial_floats(int H2);
+void launch_loss_heads(const LossArgs& a, cudaStream_t st);
+int loss_blocks(int M);
+
+struct HeadReduceArgs {
+  int nblk, HP, H2;
+  const float* part; const double* spart;
+  float* grad;               // canonical gradient base
+  long long off_W4a, off_b4a, off_W4c, off_b4c, off_logstd;
+  float ent_coef;
+  float* payload;            // [16] stats payload (KL sum, surrogate sum, vloss sum, clip count, nonfinite, rows)
+  int M;
+};
+void launch_reduce_heads(const HeadReduceArgs& a, cudaStream_t st);
+
+struct DwReduceArgs {
+  const float* part;         // [z][S][rows_pad][ld]
+  long long zstride, sstride;
+  int ld, S, rows, cols, bias_col;
+  float* grad;
+  long long w_off[2], b_off[2];  // per z: canonical offsets of W ([rows][cols]) and b ([rows])
+  int nz;
+  int row_split;             // L1: rows >= row_split belong to the second net (z=1 segment)
+  float* payload;            // nonfinite counter
+};
+void launch_reduce_dw(const DwReduceArgs& a, cudaStream_t st);
+
+struct GaeArgs {
+  int N, T;
+  const float* r; const float* V; const float* b; const uint8_t* flags; const float* VT;
+  float gamma, lam; int bootstrap;
+  float* A; float* R;
+  double* part;              // [nblk] partial sums
+};
+void launch_gae(const GaeArgs& a, cudaStream_t st);
+int gae_blocks(int N);
+void launch_sum_partials(const double* part, int n, double* out, cudaStream_t st);
+void launch_var_partials(const float* A, int n, const double* mean_total, double count, double* part, cudaStream_t st);
+int var_blocks(int n);
+void launch_adv_finalize(const double* sum_total, const double* sq_total, double count, DevScalars* sc, cudaStream_t st);
+
+struct PermArgs {
+  uint32_t B; int E; int epoch; int rank; uint32_t seed_lo, seed_hi; const DevScalars* sc; uint32_t* perm;
+};
+void launch_perm(const PermArgs& a, cudaStream_t st);
+
+struct GatherArgs {
+  int M, N, Dp;
+  const uint32_t* perm;      // minibatch slice of the permutation (or identity idx)
+  const int32_t* idx;        // alternative explicit indices (parity)
+  const __nv_bfloat16* obs;  // [T+1][N][Dp]
+  const float* act; const float* mu; const float* logp; const float* V; const float* A; const float* R;
+  const DevScalars* sc;
+  __nv_bfloat16* X; float* o_act; float* o_mu; float* o_logp; float* o_V; float* o_adv; float* o_ret;
+};
+void launch_gather(const GatherArgs& a, cudaStream_t st);
+
+struct Segment {
+  long long off;             // canonical offset
+  int rows, cols;
+  int kind;                  // 0 = bf16 dst, 1 = fp32 dst
+  void* dst;
+  int dst_ld;                // elements
+};
+constexpr int MAX_SEG = 20;
+struct ShadowArgs {
+  int nseg;
+  Segment seg[MAX_SEG];
+  long long P;
+};
+
+struct AdamArgs {
+  ShadowArgs sh;
+  float* theta; float* m; float* v; const float* grad;
+  float b1, b2, eps, inv_world;
+  DevScalars* sc;
+};
+void launch_alg1_prep(const float* payload, DevScalars* sc, float kl_target, int world, float b1, float b2,
+                      float* step_f, cudaStream_t st);
+void launch_adam(const AdamArgs& a, const float* step_f, cudaStream_t st);
+void launch_sync_shadow(const ShadowArgs& sh, const float* theta, cudaStream_t st);
+
+struct IterEndArgs {
+  DevScalars* sc; void* stats; int n_mb; int T; int n_levels; const uint32_t* state; int N; float entropy_dummy;
+  const float* logstd;
+};
+void launch_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, cudaStream_t st);
+void launch_iter_end(const IterEndArgs& a, const float* iter_acc, cudaStream_t st);
+void launch_advance_sbase(DevScalars* sc, int T, cudaStream_t st);
+
+}  // namespace lg

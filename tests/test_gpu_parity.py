@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA path (through the C ABI) against the independent oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): bit-exact for env state, resets, curriculum levels, indices and the
+shuffle; |Δ| <= 1e-5·max(|ref|,1) for fp32 GAE/rewards/observations; bf16 MLP outputs and gradients
+‖Δ‖/‖ref‖ <= 2e-2 (elementwise |Δ| <= 2e-2·(|ref| + rms(ref))); parameter drift after one PPO update
+‖θ_gpu − θ_oracle‖/‖θ_oracle‖ <= 1e-3."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes only to be skipped
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+from oracle import learn  # noqa: E402
+import synth  # noqa: E402
+from paper_2109_11978_b200 import lg  # noqa: E402
+from paper_2109_11978_b200.context import Config, Context  # noqa: E402
+
+ALL = lg.F_CURRICULUM | lg.F_NOISE | lg.F_PUSH | lg.F_BOOTSTRAP
+
+
+def make(n_envs=256, T=8, hidden=(512, 256, 128), scan=(17, 11), levels=4, cols=5, flags=ALL, seed=11, K=4, E=5,
+         rough=True):
+    cfg = Config.make(n_envs=n_envs, n_steps=T, hidden=hidden, scan_nx=scan[0], scan_ny=scan[1], n_levels=levels,
+                      n_cols=cols, flags=flags, seed=seed, n_minibatches=K, n_epochs=E)
+    hf = synth.make_world(levels, cols, seed=3, rough=rough)
+    ctx = Context(cfg, hf)
+    theta = synth.init_params(cfg.obs_dim, hidden, seed=seed)
+    ctx.params_set(theta)
+    env = oracle.Env(n_envs, hf, levels, cols, seed=seed, scan=scan, flags=flags)
+    return cfg, ctx, env, theta
+
+
+def gpu_state(ctx):
+    w = ctx.state_words.t().contiguous().cpu().numpy()
+    return w.view(oracle.STATE_DTYPE).reshape(-1)
+
+
+def set_gpu_state(ctx, st):
+    w = np.ascontiguousarray(st).view(np.int32).reshape(len(st), 66)
+    ctx.state_words.copy_(torch.from_numpy(np.ascontiguousarray(w.T)).cuda())
+    torch.cuda.synchronize()
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+def close_mixed(a, b, tol):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.all(np.abs(a - b) <= tol * np.maximum(np.abs(b), 1.0))
+
+
+# ------------------------------------------------------------------ environment (bit-exact)
+@pytest.mark.parametrize("scan,rough,flags", [((17, 11), True, ALL), ((0, 0), False, ALL & ~lg.F_CURRICULUM)])
+def test_env_teacher_forced_bit_exact(scan, rough, flags):
+    cfg, ctx, env, _ = make(n_envs=200, T=24, scan=scan, rough=rough, flags=flags,
+                            levels=4 if rough else 1, cols=5 if rough else 1)
+    N, D = cfg.n_envs, cfg.obs_dim
+    obs_g = torch.zeros(N, D, device="cuda")
+    ctx.reset(obs=obs_g)
+    o0 = env.reset()
+    ctx.sync()
+    assert gpu_state(ctx).tobytes() == env.state.tobytes()
+    assert np.array_equal(obs_g.cpu().numpy(), o0)
+    # force edge cases in both: time-outs, pushes, high levels at the top (loop-back), crashes
+    st = env.state.copy()
+    st["ep_step"][:20] = 998
+    st["push_timer"][20:40] = 499
+    if rough:
+        st["level"][40:60] = 3
+        st["crossed"][40:60] = 1
+        st["ep_step"][40:60] = 999
+    env.state[:] = st
+    set_gpu_state(ctx, st)
+    rng = np.random.default_rng(0)
+    rew_g = torch.zeros(N, device="cuda")
+    term_g = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    to_g = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    terms_g = torch.zeros(N, 9, device="cuda")
+    n_to = n_term = 0
+    for t in range(cfg.n_steps):
+        a = (rng.standard_normal((N, 12)) * (0.3 + 1.5 * (t % 3 == 0))).astype(np.float32)
+        a_g = torch.from_numpy(a).cuda()
+        ctx.env_step(t, actions=a_g, obs=obs_g, reward=rew_g, terminated=term_g, timeout=to_g, terms=terms_g)
+        o, r, te, to, terms, _ = env.step(a)
+        ctx.sync()
+        assert np.array_equal(te, term_g.cpu().numpy()), t
+        assert np.array_equal(to, to_g.cpu().numpy()), t
+        assert gpu_state(ctx).tobytes() == env.state.tobytes(), t
+        assert np.array_equal(r, rew_g.cpu().numpy()), t
+        assert np.array_equal(terms, terms_g.cpu().numpy()), t
+        assert np.array_equal(o, obs_g.cpu().numpy()), t
+        # the bf16 rollout row is the RNE rounding of the fp32 observation, pad columns zero
+        row = ctx.obs[t + 1].float().cpu().numpy()
+        assert np.array_equal(row[:, :D], torch.from_numpy(o).bfloat16().float().numpy())
+        assert np.all(row[:, D:] == 0)
+        n_to += int(to.sum())
+        n_term += int(te.sum())
+    assert n_to >= 20 and n_term > 0
+
+
+def test_curriculum_kernel_bit_exact():
+    cfg, ctx, env, _ = make(n_envs=64, T=4, levels=10, cols=5)
+    rng = np.random.default_rng(1)
+    n = 5000
+    crossed = (rng.random(n) < 0.4).astype(np.uint8)
+    disp = rng.uniform(-12, 12, (n, 2)).astype(np.float32)
+    cmd = rng.uniform(-1, 1, (n, 2)).astype(np.float32)
+    ep = rng.integers(1, 1001, n).astype(np.int32)
+    words = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    level = rng.integers(0, 10, n).astype(np.int32)
+    lv_g = torch.from_numpy(level.copy()).cuda()
+    ctx.curriculum(torch.from_numpy(crossed).cuda(), torch.from_numpy(disp).cuda(), torch.from_numpy(cmd).cuda(),
+                   torch.from_numpy(ep).cuda(), torch.from_numpy(words.view(np.int32)).cuda(), lv_g)
+    ctx.sync()
+    want = [oracle.curriculum_level(int(level[i]), 10, int(crossed[i]), float(disp[i, 0]), float(disp[i, 1]),
+                                    float(cmd[i, 0]), float(cmd[i, 1]), int(ep[i]), int(words[i])) for i in range(n)]
+    assert np.array_equal(lv_g.cpu().numpy(), np.array(want, np.int32))
+
+
+def test_shuffle_bit_exact():
+    cfg, ctx, env, _ = make(n_envs=256, T=24, E=5)
+    B = 256 * 24
+    perm = torch.zeros(B, dtype=torch.int32, device="cuda")
+    for e in range(5):
+        ctx.shuffle(e, perm)
+        ctx.sync()
+        want = oracle.feistel_perm(B, oracle.shuffle_keys(cfg.seed, 0, 0, 5, e))
+        assert np.array_equal(perm.cpu().numpy().view(np.uint32), want)
+
+
+# ------------------------------------------------------------------ MLP (bf16 tolerance)
+def _oracle_forward(theta, x, D, hidden):
+    p = learn.unpack(theta.astype(np.float64), D, hidden)
+    mu, _ = learn.mlp_forward(p, x, "a")
+    v, _ = learn.mlp_forward(p, x, "c")
+    return mu, v[:, 0]
+
+
+@pytest.mark.parametrize("hidden,scan,M", [((512, 256, 128), (17, 11), 1000), ((128, 64, 32), (0, 0), 300),
+                                           ((512, 256, 128), (0, 0), 4096)])
+def test_policy_forward_vs_oracle(hidden, scan, M):
+    cfg, ctx, env, theta = make(n_envs=max(M, 64), T=4, hidden=hidden, scan=scan, rough=scan[0] > 0,
+                                levels=4 if scan[0] else 1, cols=5 if scan[0] else 1)
+    rng = np.random.default_rng(2)
+    x = np.zeros((M, cfg.obs_stride), np.float32)
+    x[:, :cfg.obs_dim] = rng.standard_normal((M, cfg.obs_dim))
+    xb = torch.from_numpy(x).cuda().bfloat16()
+    mu = torch.zeros(M, 12, device="cuda")
+    v = torch.zeros(M, device="cuda")
+    ctx.forward(xb, mu, v)
+    ctx.sync()
+    mu_o, v_o = _oracle_forward(theta, xb.float().cpu().numpy()[:, :cfg.obs_dim], cfg.obs_dim, hidden)
+    mg, vg = mu.cpu().numpy(), v.cpu().numpy()
+    assert rel(mg, mu_o) < 2e-2 and rel(vg, v_o) < 2e-2
+    assert np.all(np.abs(mg - mu_o) <= 2e-2 * (np.abs(mu_o) + np.sqrt(np.mean(mu_o ** 2))))
+
+
+def test_policy_act_rollout_vs_oracle():
+    cfg, ctx, env, theta = make(n_envs=256, T=6)
+    ctx.reset()
+    env.reset()
+    N = cfg.n_envs
+    for t in range(cfg.n_steps):
+        ctx.policy_act(t)
+        ctx.sync()
+        act = ctx.storage("ACT", extra=(12,))[t].cpu().numpy()
+        mu = ctx.storage("MU", extra=(12,))[t].cpu().numpy()
+        logp = ctx.storage("LOGP")[t].cpu().numpy()
+        val = ctx.storage("VALUE")[t].cpu().numpy()
+        x = ctx.obs[t].float().cpu().numpy()[:, :cfg.obs_dim]
+        mu_o, v_o = _oracle_forward(theta, x, cfg.obs_dim, cfg.hidden)
+        assert rel(mu, mu_o) < 2e-2 and rel(val, v_o) < 2e-2
+        eps = env.action_eps(s=t + 1)                         # Box-Muller noise is bit-defined
+        assert np.max(np.abs((act - mu) - eps)) <= 4e-6 * np.max(np.abs(act) + 1)
+        lp_o = learn.logp_gauss(act.astype(np.float64), mu.astype(np.float64), np.zeros(12))
+        assert np.max(np.abs(logp - lp_o)) < 1e-4
+        ctx.env_step(t)
+        ctx.sync()
+        o, *_ = env.step(act)
+        assert gpu_state(ctx).tobytes() == env.state.tobytes()
+
+
+# ------------------------------------------------------------------ GAE (fp32 vs fp64 oracle)
+def _rollout(ctx, cfg):
+    ctx.reset()
+    for t in range(cfg.n_steps):
+        ctx.policy_act(t)
+        ctx.env_step(t)
+    ctx.sync()
+
+
+def _batch_from_gpu(ctx, cfg):
+    T, N = cfg.n_steps, cfg.n_envs
+    flags = ctx.storage("FLAGS", torch.uint8).cpu().numpy()
+    return dict(
+        obs=ctx.obs[:T].float().cpu().numpy(),
+        act=ctx.storage("ACT", extra=(12,)).cpu().numpy(), mu=ctx.storage("MU", extra=(12,)).cpu().numpy(),
+        logp=ctx.storage("LOGP").cpu().numpy(), V=ctx.storage("VALUE").cpu().numpy(),
+        r=ctx.storage("REWARD").cpu().numpy(), b=ctx.storage("BOOT").cpu().numpy(),
+        term=(flags & 1), timeout=(flags >> 1) & 1,
+        V_T=ctx.view("VALUE_T", torch.float32, (N,)).cpu().numpy(),
+        logstd_old=ctx.theta[-12:].cpu().numpy())
+
+
+def test_gae_vs_oracle_and_bootstrap_value():
+    cfg, ctx, env, theta = make(n_envs=512, T=24)
+    _rollout(ctx, cfg)
+    # force some time-outs mid-rollout was done by the env (ep_step) only after 1000 steps; emulate via flags
+    ctx.compute_gae()
+    ctx.sync()
+    bt = _batch_from_gpu(ctx, cfg)
+    A_o, R_o = learn.gae(bt["r"], bt["V"], bt["V_T"], bt["b"], bt["term"], bt["timeout"])
+    A = ctx.storage("ADV").cpu().numpy()
+    R = ctx.storage("RET").cpu().numpy()
+    assert close_mixed(A, A_o, 1e-5) and close_mixed(R, R_o, 1e-5)
+    # V(o_T) is the critic on OBS slot T
+    _, v_o = _oracle_forward(theta, ctx.obs[cfg.n_steps].float().cpu().numpy()[:, :cfg.obs_dim], cfg.obs_dim,
+                             cfg.hidden)
+    assert rel(bt["V_T"], v_o) < 2e-2
+
+
+def test_gae_synthetic_flags_vs_oracle():
+    cfg, ctx, env, theta = make(n_envs=300, T=16)
+    ctx.reset()
+    st = synth.synthetic_storage(cfg.n_steps, cfg.n_envs, cfg.obs_dim, seed=4, p_term=0.1, p_timeout=0.1)
+    for name, key in (("REWARD", "r"), ("VALUE", "V"), ("BOOT", "b")):
+        ctx.storage(name).copy_(torch.from_numpy(st[key]).cuda())
+    ctx.storage("FLAGS", torch.uint8).copy_(torch.from_numpy((st["term"] | (st["timeout"] << 1)).astype(np.uint8)).cuda())
+    torch.cuda.synchronize()
+    ctx.compute_gae()
+    ctx.sync()
+    VT = ctx.view("VALUE_T", torch.float32, (cfg.n_envs,)).cpu().numpy()
+    A_o, R_o = learn.gae(st["r"], st["V"], VT, st["b"], st["term"], st["timeout"])
+    assert close_mixed(ctx.storage("ADV").cpu().numpy(), A_o, 1e-5)
+    assert close_mixed(ctx.storage("RET").cpu().numpy(), R_o, 1e-5)
+
+
+# ------------------------------------------------------------------ update (gradient and drift)
+def _grad_tensors(g, D, hidden):
+    return {k: v for k, v in learn.unpack(np.asarray(g, np.float64), D, hidden).items()}
+
+
+@pytest.mark.parametrize("hidden,scan,N,T,K", [((512, 256, 128), (17, 11), 512, 24, 4),
+                                               ((128, 64, 32), (0, 0), 64, 24, 4)])
+def test_minibatch_gradient_vs_oracle(hidden, scan, N, T, K):
+    cfg, ctx, env, theta = make(n_envs=N, T=T, hidden=hidden, scan=scan, rough=scan[0] > 0, K=K,
+                                levels=4 if scan[0] else 1, cols=5 if scan[0] else 1)
+    _rollout(ctx, cfg)
+    ctx.compute_gae()
+    ctx.sync()
+    bt = _batch_from_gpu(ctx, cfg)
+    B = N * T
+    M = B // K
+    idx = np.random.default_rng(5).permutation(B)[:M].astype(np.int32)
+    ctx.minibatch_grad(torch.from_numpy(idx).cuda())
+    ctx.sync()
+    g_gpu = ctx.grad[:ctx.P].cpu().numpy()
+    A_o, R_o = learn.gae(bt["r"], bt["V"], bt["V_T"], bt["b"], bt["term"], bt["timeout"])
+    An = learn.normalize_adv(A_o).reshape(B)
+    D = cfg.obs_dim
+    obs = bt["obs"].reshape(B, -1)[:, :D]
+    p = learn.unpack(theta.astype(np.float64), D, hidden)
+    g_o, st = learn.ppo_minibatch(p, obs[idx], bt["act"].reshape(B, 12)[idx], bt["logp"].reshape(B)[idx],
+                                  bt["V"].reshape(B)[idx], An[idx], R_o.reshape(B)[idx], bt["mu"].reshape(B, 12)[idx],
+                                  bt["logstd_old"].astype(np.float64))
+    G = _grad_tensors(g_gpu, D, hidden)
+    for k, ref in g_o.items():
+        assert rel(G[k], ref) < 2e-2, (k, rel(G[k], ref))
+    pay = ctx.grad[ctx.P:].cpu().numpy()
+    assert abs(pay[0] - st["kl"]) <= 2e-2 * max(abs(st["kl"]), 1e-4)
+    assert abs(pay[2] - st["value_loss"]) <= 2e-2 * abs(st["value_loss"])
+
+
+def test_ppo_update_parameter_drift_vs_oracle():
+    cfg, ctx, env, theta = make(n_envs=512, T=24)
+    _rollout(ctx, cfg)
+    ctx.compute_gae()
+    ctx.sync()
+    bt = _batch_from_gpu(ctx, cfg)
+    B = cfg.n_envs * cfg.n_steps
+    perms = []
+    pt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    for e in range(cfg.n_epochs):
+        ctx.shuffle(e, pt)
+        ctx.sync()
+        perms.append(pt.cpu().numpy().view(np.uint32).copy())
+    stats = torch.zeros(64, dtype=torch.int32, device="cuda")
+    ctx.update(stats)
+    ctx.sync()
+    th_gpu = ctx.theta.cpu().numpy().astype(np.float64)
+    z = np.zeros(theta.size)
+    th_o, m, v, t, alpha, st = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms,
+                                                cfg.obs_dim, cfg.hidden)
+    assert ctx.scalars()["adam_t"] == t == 20
+    assert abs(ctx.scalars()["alpha"] - alpha) <= 1e-6 * alpha
+    drift = rel(th_gpu, th_o)
+    step = rel(th_o, theta)
+    print(f"drift {drift:.3e}  (update size {step:.3e})")
+    assert drift <= 1e-3
+
+
+# ------------------------------------------------------------------ whole iteration, graph replay
+def test_iteration_graph_replay_matches_eager():
+    cfgs = []
+    for mode in ("eager", "graph"):
+        cfg, ctx, env, theta = make(n_envs=256, T=8, seed=21)
+        ctx.reset()
+        if mode == "eager":
+            for _ in range(3):
+                ctx.iteration()
+        else:
+            ctx.capture()
+            for _ in range(3):
+                ctx.replay()
+        ctx.sync()
+        cfgs.append((ctx.theta.cpu().numpy().copy(), gpu_state(ctx).tobytes(), ctx.scalars()))
+    assert np.array_equal(cfgs[0][0], cfgs[1][0])
+    assert cfgs[0][1] == cfgs[1][1]
+    assert cfgs[0][2]["iteration"] == 3 and cfgs[1][2]["iteration"] == 3
+
+
+def test_iterate_host_stats_finite():
+    cfg, ctx, env, theta = make(n_envs=512, T=24)
+    ctx.reset()
+    s = ctx.iterate_host()
+    d = s.as_dict()
+    assert d["minibatches_applied"] == 20 and d["nonfinite_skips"] == 0
+    for k in ("surrogate_loss", "value_loss", "entropy", "mean_kl", "lr"):
+        assert np.isfinite(d[k])
+    assert 1e-5 <= d["lr"] <= 1e-2
+    assert sum(d["level_hist"]) == cfg.n_envs
