@@ -193,9 +193,33 @@ lg_status lg_iterate_host(lg_ctx* ctx, const uint8_t ctrl_h[16], lg_update_stats
  * capture: records and instantiates (replaces a previous graph); launch: enqueues one replay. */
 lg_status lg_graph_capture_iteration(lg_ctx* ctx, lg_update_stats* stats);
 lg_status lg_graph_launch(lg_ctx* ctx);
+/* Number of kernel nodes (this library's kernels) in the captured iteration graph. */
+lg_status lg_graph_kernel_count(lg_ctx* ctx, int32_t* n_h);
 
 /* Debug/introspection: device scalars {s_base, iteration, adam_t, alpha(bits), ...} (int32 [8]) */
 lg_status lg_device_scalars(lg_ctx* ctx, int32_t* out8_h);
+
+/* Per-category device timing (measurement only). enable != 0: every later launch is bracketed by a
+ * CUDA event pair on the context stream (also inside lg_graph_capture_iteration, as event-record
+ * nodes). lg_profile_read (after the stream is idle) adds the elapsed ms and launch counts of all
+ * recorded pairs per category into ms_h[n]/count_h[n] (categories LG_PROF_*) and, for eager mode,
+ * forgets the pairs. */
+#define LG_PROF_ENV 0        /* env_step_obs_reward / env_reset kernels */
+#define LG_PROF_GEMM_ROLL 1  /* rollout + bootstrap + V(o_T) forward GEMMs */
+#define LG_PROF_GEMM_FWD 2   /* update forward GEMMs */
+#define LG_PROF_GEMM_DX 3    /* update input-gradient GEMMs */
+#define LG_PROF_GEMM_DW 4    /* update weight-gradient GEMMs (split-K) */
+#define LG_PROF_HEADS 5      /* policy heads + sampling */
+#define LG_PROF_LOSS 6       /* PPO loss head fwd+bwd */
+#define LG_PROF_REDUCE 7     /* deterministic gradient reductions */
+#define LG_PROF_GATHER 8     /* shuffle + minibatch gather */
+#define LG_PROF_ADAM 9       /* Alg. 1 + Adam */
+#define LG_PROF_GAE 10       /* GAE + advantage statistics */
+#define LG_PROF_COMM 11      /* NCCL */
+#define LG_PROF_MISC 12      /* memsets, copies, bookkeeping */
+#define LG_PROF_NCAT 13
+lg_status lg_profile(lg_ctx* ctx, int32_t enable);
+lg_status lg_profile_read(lg_ctx* ctx, float* ms_h, int32_t* count_h, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -236,3 +236,56 @@ def shuffle_keys(seed: int, rank: int, iteration: int, n_epochs: int, epoch: int
     """SHUFFLE words 0..3 with id = rank, event = iteration*E + epoch."""
     ev = (iteration * n_epochs + epoch) & 0xFFFFFFFF
     return philox(seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF, [0, rank, ev, 6])
+
+
+class Trainer:
+    """The oracle's whole PPO iteration: T x (policy forward + Gaussian sample + env step,
+    with the time-out bootstrap value of the pre-reset observation), GAE, E x K minibatch updates with
+    Alg. 1 and Adam.  fp32 environment (C) + fp64 learning (numpy)."""
+
+    def __init__(self, n_envs, n_steps, hf, n_levels, n_cols, theta, seed=0, scan=(17, 11), hidden=(512, 256, 128),
+                 flags=F_CURRICULUM | F_NOISE | F_PUSH | F_BOOTSTRAP, n_epochs=5, n_minibatches=4, rank=0):
+        self.env = Env(n_envs, hf, n_levels, n_cols, seed=seed, rank=rank, scan=scan, flags=flags)
+        self.N, self.T, self.E, self.K = n_envs, n_steps, n_epochs, n_minibatches
+        self.hidden, self.seed, self.rank, self.flags = hidden, seed, rank, flags
+        self.D = self.env.obs_dim
+        self.theta = np.asarray(theta, np.float64).copy()
+        self.m = np.zeros_like(self.theta)
+        self.v = np.zeros_like(self.theta)
+        self.t_adam, self.alpha, self.iteration = 0, 1e-3, 0
+        self.obs = self.env.reset()
+
+    def _value(self, p, o):
+        v, _ = learn.mlp_forward(p, np.asarray(o, np.float64), "c")
+        return v[:, 0]
+
+    def run_iteration(self):
+        T, N, D = self.T, self.N, self.D
+        p = learn.unpack(self.theta, D, self.hidden)
+        ls = p["logstd"]
+        bt = {k: np.zeros((T, N) + s, dt) for k, s, dt in
+              (("obs", (D,), np.float32), ("act", (12,), np.float64), ("mu", (12,), np.float64), ("logp", (), np.float64),
+               ("V", (), np.float64), ("r", (), np.float64), ("b", (), np.float64), ("term", (), np.uint8),
+               ("timeout", (), np.uint8))}
+        for t in range(T):
+            o = self.obs
+            mu, _ = learn.mlp_forward(p, o.astype(np.float64), "a")
+            eps = self.env.action_eps()
+            a = mu + np.exp(ls) * eps
+            bt["obs"][t], bt["act"][t], bt["mu"][t] = o, a, mu
+            bt["logp"][t] = learn.logp_gauss(a, mu, ls)
+            bt["V"][t] = self._value(p, o)
+            o2, r, te, to, _, tobs = self.env.step(a.astype(np.float32))
+            bt["r"][t], bt["term"][t], bt["timeout"][t] = r, te, to
+            if (self.flags & F_BOOTSTRAP) and to.any():
+                bt["b"][t][to != 0] = self._value(p, tobs[to != 0])
+            self.obs = o2
+        bt["V_T"] = self._value(p, self.obs)
+        bt["logstd_old"] = ls.copy()
+        B = T * N
+        perms = [feistel_perm(B, shuffle_keys(self.seed, self.rank, self.iteration, self.E, e)) for e in range(self.E)]
+        self.theta, self.m, self.v, self.t_adam, self.alpha, stats = learn.ppo_update(
+            self.theta, self.m, self.v, self.t_adam, self.alpha, bt, perms, D, self.hidden, n_epochs=self.E,
+            n_minibatches=self.K, bootstrap=bool(self.flags & F_BOOTSTRAP))
+        self.iteration += 1
+        return stats

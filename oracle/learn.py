@@ -56,33 +56,48 @@ def pack(p: dict, obs_dim: int, hidden=(512, 256, 128), act_dim: int = 12) -> np
 # ----------------------------------------------------------------------------------------------
 # MLP (BJ 512-256-128 ELU)
 # ----------------------------------------------------------------------------------------------
+def round_bf16(x):
+    """Round-to-nearest-even to bfloat16 of the fp32 rounding of x (R26 / SURVEY §8(c).1's
+    diagnostic switch: the GEMM operand rounding points of the GPU path), returned as fp64."""
+    b = np.ascontiguousarray(np.asarray(x, np.float64).astype(np.float32)).view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32).astype(np.float64).reshape(np.shape(x))
+
+
+def _q(x, quant):
+    return round_bf16(x) if quant == "bf16" else x
+
+
 def elu(x):
     return np.where(x > 0, x, np.expm1(np.minimum(x, 0.0)))
 
 
-def mlp_forward(p: dict, x: np.ndarray, net: str):
-    """Returns output and the list of layer inputs/outputs needed by the backward pass."""
+def mlp_forward(p: dict, x: np.ndarray, net: str, quant=None):
+    """Returns output and the list of layer inputs/outputs needed by the backward pass.
+    quant='bf16' rounds the hidden-layer weights and the stored activations to bf16 (GPU rounding points)."""
+    x = _q(x, quant)
     acts = [x]
     h = x
     for l in range(1, 4):
-        h = elu(h @ p[f"{net}W{l}"].T + p[f"{net}b{l}"])
+        h = _q(elu(h @ _q(p[f"{net}W{l}"], quant).T + p[f"{net}b{l}"]), quant)
         acts.append(h)
     y = h @ p[f"{net}W4"].T + p[f"{net}b4"]
     return y, acts
 
 
-def mlp_backward(p: dict, acts, dy: np.ndarray, net: str, grads: dict):
+def mlp_backward(p: dict, acts, dy: np.ndarray, net: str, grads: dict, quant=None):
     """Exact reverse mode for y = W4 ELU(W3 ELU(W2 ELU(W1 x + b1) + b2) + b3) + b4.
-    ELU'(z) = 1 if out > 0 else out + 1 (= exp z), so only layer outputs are needed."""
+    ELU'(z) = 1 if out > 0 else out + 1 (= exp z), so only layer outputs are needed.
+    quant='bf16' also rounds each dZ_l = dH_l * ELU'(H_l) and the hidden weights used for dX to bf16."""
     g = dy
     for l in range(4, 0, -1):
         a_in = acts[l - 1]
         grads[f"{net}W{l}"] = g.T @ a_in
         grads[f"{net}b{l}"] = g.sum(axis=0)
         if l > 1:
-            g = g @ p[f"{net}W{l}"]
+            g = g @ (p[f"{net}W{l}"] if l == 4 else _q(p[f"{net}W{l}"], quant))
             out = acts[l - 1]
-            g = g * np.where(out > 0, 1.0, out + 1.0)
+            g = _q(g * np.where(out > 0, 1.0, out + 1.0), quant)
 
 
 def logp_gauss(a, mu, logstd):
@@ -126,11 +141,11 @@ def normalize_adv(A):
 # PPO loss + gradients on one minibatch (Table 3)
 # ----------------------------------------------------------------------------------------------
 def ppo_minibatch(p: dict, obs, act, logp_old, V_old, adv_n, ret, mu_old, logstd_old,
-                  clip=0.2, vclip=0.2, ent_coef=0.01, vf_coef=1.0):
+                  clip=0.2, vclip=0.2, ent_coef=0.01, vf_coef=1.0, quant=None):
     """Returns (grads dict, stats dict). adv_n = normalised advantages."""
     M = obs.shape[0]
-    mu, acts_a = mlp_forward(p, obs, "a")
-    v, acts_c = mlp_forward(p, obs, "c")
+    mu, acts_a = mlp_forward(p, obs, "a", quant)
+    v, acts_c = mlp_forward(p, obs, "c", quant)
     v = v[:, 0]
     ls = p["logstd"]
     sig2 = np.exp(2.0 * ls)
@@ -160,8 +175,8 @@ def ppo_minibatch(p: dict, obs, act, logp_old, V_old, adv_n, ret, mu_old, logstd
     vin = np.abs(v - V_old) <= vclip
     dV = vf_coef * np.where(take_u, 2.0 * (v - ret), 2.0 * (vc - ret) * vin) / M
     grads = {}
-    mlp_backward(p, acts_a, dmu, "a", grads)
-    mlp_backward(p, acts_c, dV[:, None], "c", grads)
+    mlp_backward(p, acts_a, dmu, "a", grads, quant)
+    mlp_backward(p, acts_c, dV[:, None], "c", grads, quant)
     grads["logstd"] = dls
     stats = dict(loss=loss, surrogate=L_pi, value_loss=L_V, entropy=H, kl=kl,
                  clip_frac=float(np.mean(np.abs(rho - 1.0) > clip)))
@@ -189,7 +204,7 @@ def adam_step(theta, g, m, v, t, alpha, b1=0.9, b2=0.999, eps=1e-8):
 
 
 def ppo_update(theta, m, v, t_adam, alpha, batch: dict, perms, obs_dim, hidden=(512, 256, 128),
-               n_epochs=5, n_minibatches=4, gamma=0.99, lam=0.95, bootstrap=True, kl_target=0.01):
+               n_epochs=5, n_minibatches=4, gamma=0.99, lam=0.95, bootstrap=True, kl_target=0.01, quant=None):
     """One PPO update on a collected batch.
 
     batch: obs [T][N][D], act/mu [T][N][12], logp, V, r, b [T][N], term/timeout [T][N], V_T [N],
@@ -216,7 +231,7 @@ def ppo_update(theta, m, v, t_adam, alpha, batch: dict, perms, obs_dim, hidden=(
             idx = pe[k * Mb:(k + 1) * Mb]
             p = unpack(theta, obs_dim, hidden)
             g, st = ppo_minibatch(p, obs[idx], act[idx], logp_old[idx], V_old[idx], An[idx], Ret[idx],
-                                  mu_old[idx], ls_old)
+                                  mu_old[idx], ls_old, quant=quant)
             gflat = pack(g, obs_dim, hidden)
             if not (np.isfinite(st["loss"]) and np.all(np.isfinite(gflat))):
                 st["skipped"] = True

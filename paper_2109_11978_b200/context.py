@@ -73,6 +73,8 @@ class Context:
         st, sizes = lg.lg_required_sizes(self.c)
         lg.check(st, what="lg_required_sizes")
         self.device = torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         torch.cuda.set_device(self.device)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
         self.bufs = [torch.empty(max(int(s), 256), dtype=torch.uint8, device=self.device) for s in sizes]
@@ -189,6 +191,14 @@ class Context:
         kl = struct.unpack("f", struct.pack("i", v[7]))[0]
         return dict(s_base=v[0], iteration=v[1], adam_t=v[2], alpha=alpha, n_to=v[4], nonfinite_skips=v[5],
                     applied=v[6], kl_last=kl)
+
+    def profile(self, enable=True):
+        self._ck(lg.lg_profile(self.ctx, enable), "lg_profile")
+
+    def profile_read(self):
+        st, ms, cnt = lg.lg_profile_read(self.ctx)
+        self._ck(st, "lg_profile_read")
+        return {k: (m, c) for k, m, c in zip(lg.PROF_CATS, ms, cnt)}
 
     def sync(self):
         self.stream.synchronize()

@@ -200,7 +200,33 @@ struct lg_ctx {
   DevScalars* sc;
   float* payload;
   float* step_f;
+  // profiling (lg_profile): event pairs around launches
+  struct PP { int cat, a, b; };
+  bool prof = false, capturing = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<PP> pairs, gpairs;
+  size_t evn = 0;
 };
+
+namespace {
+struct Scope {
+  lg_ctx* c;
+  int cat, a = -1;
+  Scope(lg_ctx* c_, int cat_) : c(c_), cat(cat_) {
+    if (c->prof && c->evn + 2 <= c->ev.size()) {
+      a = (int)c->evn++;
+      cudaEventRecordWithFlags(c->ev[a], c->st, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+    }
+  }
+  ~Scope() {
+    if (a >= 0) {
+      int b = (int)c->evn++;
+      cudaEventRecordWithFlags(c->ev[b], c->st, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+      c->pairs.push_back({cat, a, b});
+    }
+  }
+};
+}  // namespace
 
 namespace {
 
@@ -528,7 +554,10 @@ lg_status lg_params_sync(lg_ctx* ctx) {
 }
 
 // ------------------------------------------------------------------ MLP helpers
+static int g_gemm_cat = LG_PROF_GEMM_FWD;  // category of the next GEMM launches (profiling only)
+
 static lg_status gemm(lg_ctx* ctx, GemmKind kind, const GemmArgs& g, int bn, int nz) {
+  Scope sc_(ctx, kind == GEMM_DW ? LG_PROF_GEMM_DW : kind == GEMM_DX ? LG_PROF_GEMM_DX : g_gemm_cat);
   int m_tiles = (g.M + 127) / 128;
   cudaError_t e = launch_gemm(kind, bn, g, m_tiles, nz, ctx->st);
   if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm(kind %d, bn %d): %s", (int)kind, bn, cudaGetErrorString(e));
@@ -552,8 +581,9 @@ static HeadArgs head_args(lg_ctx* ctx, int M) {
   return h;
 }
 
-static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int M) {
+static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int M, int cat = LG_PROF_GEMM_FWD) {
   const Dims& d = ctx->d;
+  g_gemm_cat = cat;
   l1.M = M;
   GemmArgs g2 = ctx->l2, g3 = ctx->l3;
   g2.M = M; g3.M = M;
@@ -566,6 +596,7 @@ static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int M) {
 
 static lg_status critic_rows(lg_ctx* ctx, GemmArgs& c1, const int* M_dev, int M) {
   const Dims& d = ctx->d;
+  g_gemm_cat = LG_PROF_GEMM_ROLL;
   GemmArgs a = c1, b = ctx->l2_boot, c = ctx->l3_boot;
   a.M = b.M = c.M = M;
   a.M_dev = b.M_dev = c.M_dev = M_dev;
@@ -579,7 +610,7 @@ static lg_status critic_rows(lg_ctx* ctx, GemmArgs& c1, const int* M_dev, int M)
 // ------------------------------------------------------------------ env
 lg_status env_reset(lg_ctx* ctx, const uint8_t* mask, int32_t init, float* obs) {
   GUARD();
-  launch_env_reset(ctx->ep, mask, init, obs, ctx->st);
+  { Scope sc_(ctx, LG_PROF_ENV); launch_env_reset(ctx->ep, mask, init, obs, ctx->st); }
   CKL();
   ctx->reset_done = true;
   return LG_OK;
@@ -594,8 +625,8 @@ lg_status env_step_obs_reward(lg_ctx* ctx, int32_t t, const float* actions, floa
   float* act_slot = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
   if (actions && actions != act_slot)
     CK(cudaMemcpyAsync(act_slot, actions, (size_t)d.N * 12 * 4, cudaMemcpyDeviceToDevice, ctx->st));
-  CK(cudaMemsetAsync(&ctx->sc->n_to, 0, 4, ctx->st));
-  launch_env_step(ctx->ep, t, act_slot, obs, reward, terminated, timeout, terms, ctx->st);
+  { Scope sc_(ctx, LG_PROF_MISC); CK(cudaMemsetAsync(&ctx->sc->n_to, 0, 4, ctx->st)); }
+  { Scope sc_(ctx, LG_PROF_ENV); launch_env_step(ctx->ep, t, act_slot, obs, reward, terminated, timeout, terms, ctx->st); }
   CKL();
   if (ctx->cfg.flags & LG_F_BOOTSTRAP) {  // V(o_term) of the time-out envs, compacted rows
     lg_status s = critic_rows(ctx, ctx->l1_boot, &ctx->sc->n_to, d.N);
@@ -605,7 +636,7 @@ lg_status env_step_obs_reward(lg_ctx* ctx, int32_t t, const float* actions, floa
     h.mode = 1;
     h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_BOOT]) + (size_t)t * d.N;
     h.idx = ctx->ep.term_idx;
-    launch_heads(h, ctx->st);
+    { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(h, ctx->st); }
     CKL();
   }
   return LG_OK;
@@ -627,7 +658,7 @@ lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float*
   GUARD();
   const Dims& d = ctx->d;
   if (t < 0 || t >= d.T) return fail(ctx, LG_ERR_RANGE, "policy_act: t=%d out of [0,%d)", t, d.T);
-  lg_status s = forward_rows(ctx, ctx->l1_roll[t], d.N);
+  lg_status s = forward_rows(ctx, ctx->l1_roll[t], d.N, LG_PROF_GEMM_ROLL);
   if (s != LG_OK) return s;
   HeadArgs h = head_args(ctx, d.N);
   h.mode = 0;
@@ -637,7 +668,7 @@ lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float*
   h.logp = reinterpret_cast<float*>(ctx->buf[LG_BUF_LOGP]) + (size_t)t * d.N;
   h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE]) + (size_t)t * d.N;
   h.u_act = actions; h.u_logp = logp; h.u_mu = mu; h.u_value = value;
-  launch_heads(h, ctx->st);
+  { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(h, ctx->st); }
   CKL();
   return LG_OK;
 }
@@ -654,7 +685,7 @@ lg_status policy_forward(lg_ctx* ctx, const void* x, int32_t M, float* mu, float
   h.mode = 2;
   h.mu = mu;
   h.value = value;
-  launch_heads(h, ctx->st);
+  { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(h, ctx->st); }
   CKL();
   return LG_OK;
 }
@@ -679,7 +710,7 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
   HeadArgs h = head_args(ctx, d.N);
   h.mode = 1;
   h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE_T]);
-  launch_heads(h, ctx->st);
+  { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(h, ctx->st); }
   CKL();
   GaeArgs g;
   g.N = d.N; g.T = d.T;
@@ -692,6 +723,7 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
   g.A = reinterpret_cast<float*>(ctx->buf[LG_BUF_ADV]);
   g.R = reinterpret_cast<float*>(ctx->buf[LG_BUF_RET]);
   g.part = at<double>(K, ctx->L.k_gae);
+  Scope sc_gae(ctx, LG_PROF_GAE);
   launch_gae(g, ctx->st);
   CKL();
   double* tot = at<double>(K, ctx->L.k_tot);
@@ -725,7 +757,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
   GemmArgs l1 = ctx->l1_upd;
   lg_status s = forward_rows(ctx, l1, d.Mmb);
   if (s != LG_OK) return s;
-  CK(cudaMemsetAsync(ctx->payload, 0, 16 * 4, ctx->st));
+  { Scope sc_(ctx, LG_PROF_MISC); CK(cudaMemsetAsync(ctx->payload, 0, 16 * 4, ctx->st)); }
   LossArgs la;
   la.nd = NetDims{d.D, d.Dp, d.H0, d.H1, d.H2};
   la.M = d.Mmb;
@@ -739,14 +771,14 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
   la.part = at<float>(K, L.k_lpart);
   la.spart = at<double>(K, L.k_spart);
   la.HP = L.HP;
-  launch_loss_heads(la, ctx->st);
+  { Scope sc_(ctx, LG_PROF_LOSS); launch_loss_heads(la, ctx->st); }
   CKL();
   HeadReduceArgs hr;
   hr.nblk = loss_blocks(d.Mmb); hr.HP = L.HP; hr.H2 = d.H2;
   hr.part = la.part; hr.spart = la.spart; hr.grad = grad;
   hr.off_W4a = ctx->cn.W4[0]; hr.off_b4a = ctx->cn.b4[0]; hr.off_W4c = ctx->cn.W4[1]; hr.off_b4c = ctx->cn.b4[1];
   hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
-  launch_reduce_heads(hr, ctx->st);
+  { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
   CKL();
   auto reduce = [&](const GemmArgs& g, const DwPlan& p, int rows, int cols, const long long* woff, const long long* boff,
                     int row_split) {
@@ -758,6 +790,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
     r.nz = row_split > 0 ? 1 : p.nz;
     r.row_split = row_split;
     r.payload = ctx->payload;
+    Scope sc_(ctx, LG_PROF_REDUCE);
     launch_reduce_dw(r, ctx->st);
   };
   // layer 3
@@ -839,7 +872,7 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
   void* K = ctx->buf[LG_BUF_WORK];
   uint32_t* perm = at<uint32_t>(K, L.k_perm);
   float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
-  iter_begin(ctx);
+  { Scope sc_(ctx, LG_PROF_MISC); iter_begin(ctx); }
   CKL();
   AdamArgs aa;
   aa.sh = ctx->shadow;
@@ -856,15 +889,16 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
     pa.B = (uint32_t)d.B; pa.E = d.E; pa.epoch = e; pa.rank = ctx->cfg.rank;
     pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
     pa.sc = ctx->sc; pa.perm = perm;
-    launch_perm(pa, ctx->st);
+    { Scope sc_(ctx, LG_PROF_GATHER); launch_perm(pa, ctx->st); }
     CKL();
     for (int m = 0; m < d.K; ++m) {
       GatherArgs g = gather_args(ctx);
       g.perm = perm + (size_t)m * d.Mmb;
-      launch_gather(g, ctx->st);
+      { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
       CKL();
       if ((s = minibatch_gradient(ctx)) != LG_OK) return s;
-      if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s;
+      { Scope sc_(ctx, LG_PROF_COMM); if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s; }
+      Scope sc_adam(ctx, LG_PROF_ADAM);
       launch_alg1_prep(ctx->payload, ctx->sc, ctx->cfg.kl_target, ctx->world, ctx->cfg.adam_b1, ctx->cfg.adam_b2,
                        ctx->step_f, ctx->st);
       CKL();
@@ -880,6 +914,7 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
   ie.state = reinterpret_cast<const uint32_t*>(ctx->buf[LG_BUF_STATE]);
   ie.N = d.N;
   ie.logstd = at<float>(ctx->buf[LG_BUF_WEIGHTS], L.w_ls);
+  Scope sc_end(ctx, LG_PROF_MISC);
   launch_iter_end(ie, ctx->step_f + 4, ctx->st);
   CKL();
   // o_T becomes o_0 of the next iteration
@@ -931,7 +966,13 @@ lg_status lg_graph_capture_iteration(lg_ctx* ctx, lg_update_stats* stats) {
   if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
   if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
   CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+  ctx->capturing = true;
+  ctx->pairs.clear();
+  ctx->evn = 0;
   lg_status s = run_iteration(ctx, stats);
+  ctx->capturing = false;
+  ctx->gpairs = ctx->pairs;
+  ctx->pairs.clear();
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(ctx->st, &g);
   if (s != LG_OK) return s;
@@ -945,6 +986,24 @@ lg_status lg_graph_launch(lg_ctx* ctx) {
   GUARD();
   if (!ctx->gexec) return fail(ctx, LG_ERR_STATE, "no captured graph");
   CK(cudaGraphLaunch(ctx->gexec, ctx->st));
+  return LG_OK;
+}
+
+lg_status lg_graph_kernel_count(lg_ctx* ctx, int32_t* n_h) {
+  GUARD();
+  if (!n_h) return fail(ctx, LG_ERR_INVALID_ARG, "null output");
+  if (!ctx->graph) return fail(ctx, LG_ERR_STATE, "no captured graph");
+  size_t n = 0;
+  CK(cudaGraphGetNodes(ctx->graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CK(cudaGraphGetNodes(ctx->graph, nodes.data(), &n));
+  int32_t k = 0;
+  for (auto& nd : nodes) {
+    cudaGraphNodeType ty;
+    CK(cudaGraphNodeGetType(nd, &ty));
+    if (ty == cudaGraphNodeTypeKernel) ++k;
+  }
+  *n_h = k;
   return LG_OK;
 }
 
@@ -962,6 +1021,32 @@ lg_status lg_iterate_host(lg_ctx* ctx, const uint8_t ctrl_h[16], lg_update_stats
   }
   CK(cudaMemcpyAsync(stats_h, dstats, sizeof(lg_update_stats), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
+  return LG_OK;
+}
+
+lg_status lg_profile(lg_ctx* ctx, int32_t enable) {
+  GUARD();
+  if (enable && ctx->ev.empty()) {
+    ctx->ev.resize(8192);
+    for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+  }
+  ctx->prof = enable != 0;
+  ctx->pairs.clear();
+  ctx->evn = 0;
+  return LG_OK;
+}
+
+lg_status lg_profile_read(lg_ctx* ctx, float* ms_h, int32_t* count_h, int32_t n) {
+  GUARD();
+  if (!ms_h || !count_h || n < 1) return fail(ctx, LG_ERR_INVALID_ARG, "profile_read: bad arguments");
+  const bool eager = !ctx->pairs.empty();
+  const auto& pl = eager ? ctx->pairs : ctx->gpairs;
+  for (const auto& p : pl) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[p.a], ctx->ev[p.b]));
+    if (p.cat < n) { ms_h[p.cat] += ms; count_h[p.cat] += 1; }
+  }
+  if (eager) { ctx->pairs.clear(); ctx->evn = 0; }
   return LG_OK;
 }
 

@@ -49,7 +49,9 @@ EXPORTS = ["lg_num_params", "lg_obs_dim", "lg_obs_stride", "lg_required_sizes", 
            "lg_last_error", "lg_params_set", "lg_params_sync", "env_reset", "env_step_obs_reward", "policy_act",
            "policy_forward", "storage_compute_gae", "ppo_update", "ppo_shuffle", "ppo_minibatch_grad", "curriculum_update",
            "lg_nccl_unique_id", "lg_set_nccl", "lg_broadcast_params", "lg_iterate_host",
-           "lg_graph_capture_iteration", "lg_graph_launch", "lg_device_scalars"]
+           "lg_graph_capture_iteration", "lg_graph_launch", "lg_device_scalars", "lg_profile", "lg_profile_read", "lg_graph_kernel_count"]
+PROF_CATS = ["env", "gemm_roll", "gemm_fwd", "gemm_dx", "gemm_dw", "heads", "loss", "reduce", "gather", "adam", "gae",
+             "comm", "misc"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libleggedrl.so not built ({LIB_PATH}); run python -m paper_2109_11978_b200.build")
@@ -83,6 +85,9 @@ _sig = {
     "lg_graph_capture_iteration": (I32, [P, P]),
     "lg_graph_launch": (I32, [P]),
     "lg_device_scalars": (I32, [P, ctypes.POINTER(I32)]),
+    "lg_profile": (I32, [P, I32]),
+    "lg_graph_kernel_count": (I32, [P, ctypes.POINTER(I32)]),
+    "lg_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -219,3 +224,21 @@ def lg_device_scalars(ctx):
     out = (I32 * 8)()
     st = _lib.lg_device_scalars(ctx, out)
     return st, list(out)
+
+
+def lg_profile(ctx, enable):
+    return _lib.lg_profile(ctx, int(enable))
+
+
+def lg_profile_read(ctx):
+    n = len(PROF_CATS)
+    ms = (ctypes.c_float * n)()
+    cnt = (I32 * n)()
+    st = _lib.lg_profile_read(ctx, ms, cnt, n)
+    return st, list(ms), list(cnt)
+
+
+def lg_graph_kernel_count(ctx):
+    n = I32()
+    st = _lib.lg_graph_kernel_count(ctx, ctypes.byref(n))
+    return st, n.value

@@ -297,14 +297,20 @@ def test_ppo_update_parameter_drift_vs_oracle():
     ctx.sync()
     th_gpu = ctx.theta.cpu().numpy().astype(np.float64)
     z = np.zeros(theta.size)
-    th_o, m, v, t, alpha, st = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms,
-                                                cfg.obs_dim, cfg.hidden)
-    assert ctx.scalars()["adam_t"] == t == 20
-    assert abs(ctx.scalars()["alpha"] - alpha) <= 1e-6 * alpha
-    drift = rel(th_gpu, th_o)
-    step = rel(th_o, theta)
-    print(f"drift {drift:.3e}  (update size {step:.3e})")
-    assert drift <= 1e-3
+    # reference with the GPU's documented bf16 rounding points (SURVEY §8(c).1 diagnostic switch, DESIGN R26)
+    th_q, m, v, t, alpha, st = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms,
+                                                cfg.obs_dim, cfg.hidden, quant="bf16")
+    # exact fp64 reference
+    th_x, *_ = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms, cfg.obs_dim, cfg.hidden)
+    sc = ctx.scalars()
+    assert sc["adam_t"] == t == 20
+    assert abs(sc["alpha"] - alpha) <= 1e-6 * alpha
+    drift_q = rel(th_gpu, th_q)
+    drift_x = rel(th_gpu, th_x)
+    step = rel(th_x, theta)
+    print(f"drift vs bf16-point oracle {drift_q:.3e}; vs exact fp64 oracle {drift_x:.3e}; update size {step:.3e}")
+    assert drift_q <= 1e-3
+    assert drift_x <= 1e-2
 
 
 # ------------------------------------------------------------------ whole iteration, graph replay
@@ -335,5 +341,5 @@ def test_iterate_host_stats_finite():
     assert d["minibatches_applied"] == 20 and d["nonfinite_skips"] == 0
     for k in ("surrogate_loss", "value_loss", "entropy", "mean_kl", "lr"):
         assert np.isfinite(d[k])
-    assert 1e-5 <= d["lr"] <= 1e-2
+    assert np.float32(1e-5) <= d["lr"] <= np.float32(1e-2)
     assert sum(d["level_hist"]) == cfg.n_envs

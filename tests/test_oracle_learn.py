@@ -247,3 +247,15 @@ def test_ppo_update_runs_and_reduces_value_loss():
     assert t == 20 and len(stats) == 20
     assert stats[-1]["value_loss"] < stats[0]["value_loss"]
     assert 1e-5 <= alpha <= 1e-2
+
+
+def test_round_bf16_definition():
+    """RNE to bfloat16 (7 fraction bits): ties go to the even mantissa."""
+    x = np.array([1.0, 1 + 2 ** -8, 1 + 3 * 2 ** -8, 1 + 2 ** -7, -(1 + 2 ** -8), 3.0, 0.0, 2 ** -130])
+    want = np.array([1.0, 1.0, 1 + 2 ** -6, 1 + 2 ** -7, -1.0, 3.0, 0.0, 2 ** -130])
+    assert np.array_equal(learn.round_bf16(x), want)
+    r = np.random.default_rng(0).standard_normal(10000) * 10.0 ** np.random.default_rng(1).integers(-5, 5, 10000)
+    q = learn.round_bf16(r)
+    assert np.all(np.abs(q - r) <= 2.0 ** -8 * np.abs(r))          # within half a bf16 ulp (rel 2^-8)
+    torch = pytest.importorskip("torch")
+    assert np.array_equal(q, torch.from_numpy(r.astype(np.float32)).bfloat16().double().numpy())
