@@ -83,7 +83,7 @@ typedef struct {
   int32_t n_steps;      /* T, >= 1 */
   int32_t n_epochs;     /* E (Table 3: 5) */
   int32_t n_minibatches;/* K_mb (Table 3: 4); N*T must be divisible by it */
-  int32_t hidden[3];    /* MLP widths, each a multiple of 32 and <= 512 (BJ: 512,256,128) */
+  int32_t hidden[3];    /* MLP widths: h0,h1 multiples of 64 <= 512, h2 multiple of 32 <= 128 (BJ: 512,256,128) */
   int32_t scan_nx, scan_ny; /* height-scan grid (17, 11); (0,0) = flat 48-dim obs */
   int32_t n_levels, n_cols; /* world tiles (R = 80*n_levels, C = 80*n_cols), each >= 1 */
   float inv_cell;           /* 10.0 (0.1 m cells) */

@@ -68,7 +68,7 @@ Canon canon_of(const Dims& d) {
   return c;
 }
 
-int bn_for(int n) { return n >= 256 ? 256 : (n > 64 ? 128 : (n > 32 ? 64 : 32)); }
+int bn_for(int n) { return n >= 256 ? 256 : (n > 64 ? 128 : 64); }
 
 struct DwPlan {
   int rows, N, bn, n_tiles, m_tiles, kb_total, kb_per_split, S, ld, rows_pad, nz;
@@ -77,7 +77,7 @@ struct DwPlan {
 DwPlan dw_plan(int rows, int N, int K, int nz) {
   DwPlan p;
   p.rows = rows; p.N = N; p.nz = nz;
-  p.bn = bn_for(N);
+  p.bn = N > 64 ? 128 : 64;  // dW: 128-wide tiles leave room for a deeper TMA pipeline
   p.n_tiles = (N + p.bn - 1) / p.bn;
   p.m_tiles = (rows + 127) / 128;
   p.kb_total = (K + 63) / 64;
@@ -99,7 +99,7 @@ struct Layout {
   size_t a_X, a_H1, a_H2, a_H3, a_dZ1, a_dZ2, a_dZ3, a_act, a_mu, a_logp, a_V, a_adv, a_ret, a_omu, a_oV;
   // WORK
   size_t k_sc, k_gae, k_var, k_tot, k_lpart, k_spart, k_dw1, k_dw2, k_dw3, k_perm, k_tobs, k_tidx, k_step, k_stats,
-      k_ctrl;
+      k_ctrl, k_rec, k_trec;
   int HP, nblk_loss, nblk_gae, nblk_var;
   DwPlan dw1, dw2, dw3;
 };
@@ -171,6 +171,8 @@ Layout layout_of(const Dims& d) {
   L.k_step = o; o = al(o + 16 * 4);
   L.k_stats = o; o = al(o + sizeof(lg_update_stats));
   L.k_ctrl = o; o = al(o + 64);
+  L.k_rec = o; o = al(o + (size_t)d.N * 256);
+  L.k_trec = o; o = al(o + (size_t)d.N * 256);
   L.bytes[LG_BUF_WORK] = o;
   return L;
 }
@@ -272,6 +274,7 @@ lg_status validate(const lg_config* c) {
   for (int k = 0; k < 3; ++k)
     if (c->hidden[k] < 32 || c->hidden[k] > 512 || c->hidden[k] % 32 != 0) return LG_ERR_SHAPE;
   if (c->hidden[0] % 64 != 0 || c->hidden[1] % 64 != 0) return LG_ERR_SHAPE;  // K of the next layer in 64-blocks
+  if (c->hidden[2] > 128) return LG_ERR_SHAPE;  // heads: <= 4 columns per lane (warp-per-row kernels)
   if (c->scan_nx < 0 || c->scan_ny < 0 || (c->scan_nx == 0) != (c->scan_ny == 0)) return LG_ERR_SHAPE;
   if (c->n_levels < 1 || c->n_cols < 1) return LG_ERR_RANGE;
   if (!(c->gamma > 0.f && c->gamma <= 1.f) || !(c->lam >= 0.f && c->lam <= 1.f)) return LG_ERR_RANGE;
@@ -363,7 +366,10 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   bool ok = true;
   const int bn1 = bn_for(2 * d.H0), bn1c = bn_for(d.H0), bn2 = bn_for(d.H1), bn3 = bn_for(d.H2);
   const uint64_t R = d.R;
-
+  // output maps (TMA stores, box 64 x 32, clipped to the per-net column range)
+  auto cmap = [&](CUtensorMap* m, const __nv_bfloat16* base, int cols, int ld) {
+    ok &= make_tmap_bf16(m, base, R, cols, ld, 32);
+  };
   // ---- forward, layer 1 (both nets concatenated: N = 2*H0)
   ctx->l1_roll.resize(d.T + 1);
   for (int t = 0; t <= d.T; ++t) {
@@ -371,15 +377,17 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     memset(&g, 0, sizeof(g));
     ok &= make_tmap_bf16(&g.tmA[0], OBS + (size_t)t * d.N * d.Dp, d.N, d.Dp, d.Dp, 128);
     ok &= make_tmap_bf16(&g.tmB[0], W1, 2 * d.H0, d.Dp, d.Dp, bn1);
+    cmap(&g.tmC[0], H1, 2 * d.H0, 2 * d.H0);
     set_fwd_common(g, d.N, 2 * d.H0, d.Dp, bn1, 1);
-    g.out[0] = H1; g.ldo = 2 * d.H0; g.bias[0] = b1;
+    g.ldo = 2 * d.H0; g.bias[0] = b1;
   }
   GemmArgs& u1 = ctx->l1_upd;
   memset(&u1, 0, sizeof(u1));
   ok &= make_tmap_bf16(&u1.tmA[0], X, R, d.Dp, d.Dp, 128);
   ok &= make_tmap_bf16(&u1.tmB[0], W1, 2 * d.H0, d.Dp, d.Dp, bn1);
+  cmap(&u1.tmC[0], H1, 2 * d.H0, 2 * d.H0);
   set_fwd_common(u1, d.Mmb, 2 * d.H0, d.Dp, bn1, 1);
-  u1.out[0] = H1; u1.ldo = 2 * d.H0; u1.bias[0] = b1;
+  u1.ldo = 2 * d.H0; u1.bias[0] = b1;
   // ---- forward, layers 2, 3 (z = net)
   GemmArgs& g2 = ctx->l2;
   memset(&g2, 0, sizeof(g2));
@@ -388,10 +396,12 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   for (int z = 0; z < 2; ++z) {
     ok &= make_tmap_bf16(&g2.tmA[z], H1 + z * d.H0, R, d.H0, 2 * d.H0, 128);
     ok &= make_tmap_bf16(&g2.tmB[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, bn2);
-    g2.out[z] = H2 + z * d.H1; g2.bias[z] = b2 + z * d.H1;
+    cmap(&g2.tmC[z], H2 + z * d.H1, d.H1, 2 * d.H1);
+    g2.bias[z] = b2 + z * d.H1;
     ok &= make_tmap_bf16(&g3.tmA[z], H2 + z * d.H1, R, d.H1, 2 * d.H1, 128);
     ok &= make_tmap_bf16(&g3.tmB[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, bn3);
-    g3.out[z] = H3 + z * d.H2; g3.bias[z] = b3 + z * d.H2;
+    cmap(&g3.tmC[z], H3 + z * d.H2, d.H2, 2 * d.H2);
+    g3.bias[z] = b3 + z * d.H2;
   }
   set_fwd_common(g2, d.Mmb, d.H1, d.H0, bn2, 2); g2.ldo = 2 * d.H1;
   set_fwd_common(g3, d.Mmb, d.H2, d.H1, bn3, 2); g3.ldo = 2 * d.H2;
@@ -400,23 +410,24 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   memset(&c1, 0, sizeof(c1));
   ok &= make_tmap_bf16(&c1.tmA[0], TOBS, d.N, d.Dp, d.Dp, 128);
   ok &= make_tmap_bf16(&c1.tmB[0], W1 + (size_t)d.H0 * d.Dp, d.H0, d.Dp, d.Dp, bn1c);
+  cmap(&c1.tmC[0], H1 + d.H0, d.H0, 2 * d.H0);
   set_fwd_common(c1, d.N, d.H0, d.Dp, bn1c, 1);
   c1.M_dev = &ctx->sc->n_to;
-  c1.out[0] = H1 + d.H0; c1.ldo = 2 * d.H0; c1.bias[0] = b1 + d.H0;
+  c1.ldo = 2 * d.H0; c1.bias[0] = b1 + d.H0;
   GemmArgs& cv = ctx->l1_vt;
   cv = c1;
   ok &= make_tmap_bf16(&cv.tmA[0], OBS + (size_t)d.T * d.N * d.Dp, d.N, d.Dp, d.Dp, 128);
   cv.M_dev = nullptr;
   GemmArgs& c2 = ctx->l2_boot;
   memset(&c2, 0, sizeof(c2));
-  c2.tmA[0] = g2.tmA[1]; c2.tmB[0] = g2.tmB[1];
+  c2.tmA[0] = g2.tmA[1]; c2.tmB[0] = g2.tmB[1]; c2.tmC[0] = g2.tmC[1];
   set_fwd_common(c2, d.N, d.H1, d.H0, bn2, 1);
-  c2.out[0] = g2.out[1]; c2.bias[0] = g2.bias[1]; c2.ldo = 2 * d.H1;
+  c2.bias[0] = g2.bias[1]; c2.ldo = 2 * d.H1;
   GemmArgs& c3 = ctx->l3_boot;
   memset(&c3, 0, sizeof(c3));
-  c3.tmA[0] = g3.tmA[1]; c3.tmB[0] = g3.tmB[1];
+  c3.tmA[0] = g3.tmA[1]; c3.tmB[0] = g3.tmB[1]; c3.tmC[0] = g3.tmC[1];
   set_fwd_common(c3, d.N, d.H2, d.H1, bn3, 1);
-  c3.out[0] = g3.out[1]; c3.bias[0] = g3.bias[1]; c3.ldo = 2 * d.H2;
+  c3.bias[0] = g3.bias[1]; c3.ldo = 2 * d.H2;
   // ---- backward dX (A = dZ K-major, B = W MN-major), epilogue * ELU'(H)
   GemmArgs& x3 = ctx->dx3;
   memset(&x3, 0, sizeof(x3));
@@ -425,10 +436,12 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   for (int z = 0; z < 2; ++z) {
     ok &= make_tmap_bf16(&x3.tmA[z], dZ3 + z * d.H2, R, d.H2, 2 * d.H2, 128);
     ok &= make_tmap_bf16(&x3.tmB[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, 64);
-    x3.out[z] = dZ2 + z * d.H1; x3.aux[z] = H2 + z * d.H1;
+    cmap(&x3.tmC[z], dZ2 + z * d.H1, d.H1, 2 * d.H1);
+    x3.aux[z] = H2 + z * d.H1;
     ok &= make_tmap_bf16(&x2.tmA[z], dZ2 + z * d.H1, R, d.H1, 2 * d.H1, 128);
     ok &= make_tmap_bf16(&x2.tmB[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, 64);
-    x2.out[z] = dZ1 + z * d.H0; x2.aux[z] = H1 + z * d.H0;
+    cmap(&x2.tmC[z], dZ1 + z * d.H0, d.H0, 2 * d.H0);
+    x2.aux[z] = H1 + z * d.H0;
   }
   set_fwd_common(x3, d.Mmb, d.H1, d.H2, bn_for(d.H1), 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
   set_fwd_common(x2, d.Mmb, d.H0, d.H1, bn_for(d.H0), 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
@@ -437,9 +450,11 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     g.M = p.rows; g.N = p.N; g.M_dev = nullptr;
     g.kb_total = p.kb_total; g.kb_per_split = p.kb_per_split; g.n_tiles = p.n_tiles; g.n_splits = p.S;
     g.part = at<float>(K, part_off);
+    g.part_rows = p.rows_pad;
     g.part_sstride = (long long)p.rows_pad * p.ld;
     g.part_zstride = (long long)p.S * g.part_sstride;
     g.part_ld = p.ld; g.part_bias_col = p.n_tiles * p.bn; g.bias_col = 1;
+    ok &= make_tmap_f32(&g.tmC[0], g.part, (uint64_t)p.nz * p.S * p.rows_pad, p.ld, p.ld, 32);
   };
   GemmArgs& w3 = ctx->dw3;
   memset(&w3, 0, sizeof(w3));
@@ -478,6 +493,8 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   ep.boot = reinterpret_cast<float*>(ctx->buf[LG_BUF_BOOT]);
   ep.term_obs = TOBS;
   ep.term_idx = at<int32_t>(K, L.k_tidx);
+  ep.recs = at<void>(K, L.k_rec);
+  ep.trecs = at<void>(K, L.k_trec);
   // ---- shadow segments (canonical θ -> GEMM layouts)
   ShadowArgs& sh = ctx->shadow;
   memset(&sh, 0, sizeof(sh));
@@ -558,8 +575,10 @@ static int g_gemm_cat = LG_PROF_GEMM_FWD;  // category of the next GEMM launches
 
 static lg_status gemm(lg_ctx* ctx, GemmKind kind, const GemmArgs& g, int bn, int nz) {
   Scope sc_(ctx, kind == GEMM_DW ? LG_PROF_GEMM_DW : kind == GEMM_DX ? LG_PROF_GEMM_DX : g_gemm_cat);
-  int m_tiles = (g.M + 127) / 128;
-  cudaError_t e = launch_gemm(kind, bn, g, m_tiles, nz, ctx->st);
+  GemmArgs gg = g;
+  gg.m_tiles = (g.M + 127) / 128;
+  gg.nz = nz;
+  cudaError_t e = launch_gemm(kind, bn, gg, ctx->st);
   if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm(kind %d, bn %d): %s", (int)kind, bn, cudaGetErrorString(e));
   return LG_OK;
 }

@@ -3,8 +3,9 @@
 // Compiled with -fmad=false: every a*b+c is two IEEE roundings, as in the oracle (R26).
 //
 // Layout: state SoA [66][N] (field-major, so every field access is coalesced across the warp).
-// Kernel shape: one thread per env for the per-env serial work (phase A), then the block's threads
-// cooperate on the observation rows (phase B): each item = 4 consecutive observation elements of one
+// Kernel shape: k_env_step runs one thread per env for the per-env serial work (push, substeps, reward,
+// flags, curriculum, reset) and writes a 256-B observation record per env; k_env_obs then spreads the
+// observation rows over the whole GPU: one thread per item = 4 consecutive observation elements of one
 // env = exactly one Philox block of noise, written as one 8-byte bf16x4 store (coalesced along a row).
 #include "common.cuh"
 #include "kernels.h"
@@ -142,12 +143,14 @@ __device__ void reset_env(const World& W, const Rng& rng, St& s, uint32_t g, uin
 }
 
 // per-env observation record for the cooperative phase
-struct ObsRec {
+struct ObsRec {  // 64 words: everything the observation of one env needs (written by phase A)
   float pro[48];
   float px, py, pz, c, s;
   uint32_t g, word0;
   int32_t row;  // destination row (env index, or compacted terminal row)
+  uint32_t pad[8];
 };
+static_assert(sizeof(ObsRec) == 256, "ObsRec layout");
 
 __device__ __forceinline__ void fill_obs_rec(const St& s, ObsRec& o) {
   Mat3 R = rot(s.quat);
@@ -185,83 +188,94 @@ __device__ __forceinline__ float obs_elem(const EnvParams& P, const World& W, co
   return o.pz - h_bilinear(W, x, y);
 }
 
-// cooperative write of the observation rows of `cnt` records (items of 4 elements)
-__device__ void write_obs_rows(const EnvParams& P, const World& W, const Rng& rng, uint32_t ev, const ObsRec* recs,
-                               int cnt, __nv_bfloat16* __restrict__ dst_bf16, float* __restrict__ dst_f32) {
+// Observation rows (DESIGN.md §3.7 step 10): one thread per item = 4 consecutive elements of one row
+// = one Philox block of noise; written as one 8-byte bf16x4 store, so consecutive threads write
+// consecutive bytes of a row. Items [0, N*G) are the post-step rows of OBS slot `slot`; items
+// [N*G, 2*N*G) are the compacted pre-reset rows of time-out envs (rows < n_to, for the bootstrap critic).
+__global__ void __launch_bounds__(256) k_env_obs(EnvParams P, int ev_off, __nv_bfloat16* __restrict__ dst_bf16,
+                                                 float* __restrict__ dst_f32, int with_terminal) {
   const int D = P.obs_dim, Dp = P.obs_stride, G = Dp / 4;
-  for (int it = threadIdx.x; it < cnt * G; it += blockDim.x) {
-    int r = it / G, gq = it - r * G;
-    const ObsRec& o = recs[r];
-    float v[4];
-    U4 nb0, nb1;
-    bool noise = (P.flags & F_NOISE) != 0;
-    uint32_t wbase = o.word0 + 4u * (uint32_t)gq;
-    if (noise && 4 * gq < D) {
-      nb0 = rng.block(wbase >> 2, o.g, ev, TAG_OBS);
-      if (wbase & 3u) nb1 = rng.block((wbase >> 2) + 1, o.g, ev, TAG_OBS);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int e = 4 * gq + k;
-      float x = 0.0f;
-      if (e < D) {
-        x = obs_elem(P, W, o, e);
-        if (noise) {
-          float sc = noise_scale(e);
-          if (sc != 0.0f) {
-            uint32_t w = wbase + (uint32_t)k;
-            uint32_t word = ((w >> 2) == (wbase >> 2)) ? pick(nb0, w) : pick(nb1, w);
-            x = x + usym(sc, word);
-          }
-        }
-        if (dst_f32) dst_f32[(size_t)o.row * D + e] = x;
-      }
-      v[k] = x;
-    }
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    *reinterpret_cast<uint2*>(dst_bf16 + (size_t)o.row * Dp + 4 * gq) = pk;
+  const uint32_t ev = P.scalars->s_base + (uint32_t)ev_off;
+  const long long NG = (long long)P.N * G;
+  long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const ObsRec* recs = reinterpret_cast<const ObsRec*>(P.recs);
+  __nv_bfloat16* dst = dst_bf16;
+  float* df = dst_f32;
+  if (it >= NG) {
+    if (!with_terminal) return;
+    it -= NG;
+    if (it >= (long long)P.scalars->n_to * G) return;
+    recs = reinterpret_cast<const ObsRec*>(P.trecs);
+    dst = P.term_obs;
+    df = nullptr;
   }
+  const int r = (int)(it / G), gq = (int)(it - (long long)r * G);
+  const ObsRec& o = recs[r];
+  World W{P.hf, P.R, P.C, P.inv_cell};
+  Rng rng{P.seed_lo, P.seed_hi};
+  float v[4];
+  U4 nb0, nb1;
+  const bool noise = (P.flags & F_NOISE) != 0;
+  const uint32_t wbase = o.word0 + 4u * (uint32_t)gq;
+  if (noise && 4 * gq < D) {
+    nb0 = rng.block(wbase >> 2, o.g, ev, TAG_OBS);
+    if (wbase & 3u) nb1 = rng.block((wbase >> 2) + 1, o.g, ev, TAG_OBS);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int e = 4 * gq + k;
+    float x = 0.0f;
+    if (e < D) {
+      x = obs_elem(P, W, o, e);
+      if (noise) {
+        const float sc = noise_scale(e);
+        if (sc != 0.0f) {
+          const uint32_t w = wbase + (uint32_t)k;
+          const uint32_t word = ((w >> 2) == (wbase >> 2)) ? pick(nb0, w) : pick(nb1, w);
+          x = x + usym(sc, word);
+        }
+      }
+      if (df) df[(size_t)o.row * D + e] = x;
+    }
+    v[k] = x;
+  }
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst + (size_t)o.row * Dp + 4 * gq) = pk;
+}
+
+static void launch_obs(const EnvParams& P, int ev_off, __nv_bfloat16* dst, float* f32, int with_terminal,
+                       cudaStream_t st) {
+  const long long items = (long long)P.N * (P.obs_stride / 4) * (with_terminal ? 2 : 1);
+  k_env_obs<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(P, ev_off, dst, f32, with_terminal);
 }
 
 // ------------------------------------------------------------------ kernels
-__global__ void __launch_bounds__(ENV_BLOCK) k_env_reset(EnvParams P, const uint8_t* __restrict__ mask, int init,
-                                                         float* __restrict__ obs_f32) {
-  __shared__ ObsRec recs[ENV_BLOCK];
-  __shared__ int cnt;
-  if (threadIdx.x == 0) cnt = 0;
-  __syncthreads();
+__global__ void __launch_bounds__(ENV_BLOCK) k_env_reset(EnvParams P, const uint8_t* __restrict__ mask, int init) {
   World W{P.hf, P.R, P.C, P.inv_cell};
   Rng rng{P.seed_lo, P.seed_hi};
   const uint32_t ev = P.scalars->s_base;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P.N && (!mask || mask[i])) {
-    St s;
-    load_state(P.state, P.N, i, s);
-    uint32_t g = (uint32_t)(P.rank * P.N + i);
+  if (i >= P.N) return;
+  St s;
+  load_state(P.state, P.N, i, s);
+  uint32_t g = (uint32_t)(P.rank * P.N + i);
+  if (!mask || mask[i]) {
     if (init) { s.col = (int32_t)(g % (uint32_t)P.n_cols); s.level = 0; }
     reset_env(W, rng, s, g, ev);
     store_state(P.state, P.N, i, s);
-    int slot = atomicAdd(&cnt, 1);
-    fill_obs_rec(s, recs[slot]);
-    recs[slot].g = g; recs[slot].word0 = 0u; recs[slot].row = i;
   }
-  __syncthreads();
-  // obs slot 0
-  write_obs_rows(P, W, rng, ev, recs, cnt, P.obs_out, obs_f32);
+  ObsRec& rec = reinterpret_cast<ObsRec*>(P.recs)[i];
+  fill_obs_rec(s, rec);
+  rec.g = g; rec.word0 = 0u; rec.row = i;
 }
 
 __global__ void __launch_bounds__(ENV_BLOCK) k_env_step(EnvParams P, int t, const float* __restrict__ actions,
-                                                        float* __restrict__ obs_f32, float* __restrict__ rew_out,
+                                                        float* __restrict__ rew_out,
                                                         uint8_t* __restrict__ term_out, uint8_t* __restrict__ to_out,
                                                         float* __restrict__ terms_out) {
-  __shared__ ObsRec recs[ENV_BLOCK];
-  __shared__ ObsRec trecs[ENV_BLOCK];
-  __shared__ int tcnt;
-  if (threadIdx.x == 0) tcnt = 0;
-  __syncthreads();
   World W{P.hf, P.R, P.C, P.inv_cell};
   Rng rng{P.seed_lo, P.seed_hi};
   const uint32_t ev = P.scalars->s_base + (uint32_t)t + 1u;
@@ -428,10 +442,10 @@ __global__ void __launch_bounds__(ENV_BLOCK) k_env_step(EnvParams P, int t, cons
       for (int k = 0; k < 9; ++k) terms_out[(size_t)i * 9 + k] = rt[k];
     if (done) {
       if (to && (P.flags & F_BOOTSTRAP)) {
-        int slot = atomicAdd(&tcnt, 1);
         int row = atomicAdd(&P.scalars->n_to, 1);
-        fill_obs_rec(s, trecs[slot]);
-        trecs[slot].g = g; trecs[slot].word0 = 0u; trecs[slot].row = row;
+        ObsRec& tr = reinterpret_cast<ObsRec*>(P.trecs)[row];
+        fill_obs_rec(s, tr);
+        tr.g = g; tr.word0 = 0u; tr.row = row;
         P.term_idx[row] = i;
       }
       // episode statistics (stats only; float atomics)
@@ -458,16 +472,12 @@ __global__ void __launch_bounds__(ENV_BLOCK) k_env_step(EnvParams P, int t, cons
       reset_env(W, rng, s, g, ev);
     }
     store_state(P.state, N, i, s);
-    fill_obs_rec(s, recs[threadIdx.x]);
-    recs[threadIdx.x].g = g;
-    recs[threadIdx.x].word0 = done ? (uint32_t)P.obs_dim : 0u;
-    recs[threadIdx.x].row = i;
+    ObsRec& rec = reinterpret_cast<ObsRec*>(P.recs)[i];
+    fill_obs_rec(s, rec);
+    rec.g = g;
+    rec.word0 = done ? (uint32_t)P.obs_dim : 0u;
+    rec.row = i;
   }
-  __syncthreads();
-  int cnt = min(ENV_BLOCK, N - (int)(blockIdx.x * blockDim.x));
-  // o_{t+1} into OBS slot t+1 (bf16) and the caller's fp32 obs; records are in thread order
-  write_obs_rows(P, W, rng, ev, recs, cnt, P.obs_out + (size_t)(t + 1) * N * P.obs_stride, obs_f32);
-  if (tcnt > 0) write_obs_rows(P, W, rng, ev, trecs, tcnt, P.term_obs, nullptr);
 }
 
 // standalone curriculum rule (DESIGN.md §3.7 step 9(ii))
@@ -514,12 +524,15 @@ __global__ void k_action_eps(int N, int rank, uint32_t seed_lo, uint32_t seed_hi
 // ------------------------------------------------------------------ launchers
 void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* obs_f32, cudaStream_t st) {
   int nb = (P.N + ENV_BLOCK - 1) / ENV_BLOCK;
-  k_env_reset<<<nb, ENV_BLOCK, 0, st>>>(P, mask, init, obs_f32);
+  k_env_reset<<<nb, ENV_BLOCK, 0, st>>>(P, mask, init);
+  launch_obs(P, 0, P.obs_out, obs_f32, 0, st);  // noise event s_base
 }
 void launch_env_step(const EnvParams& P, int t, const float* actions, float* obs_f32, float* rew, uint8_t* term,
                      uint8_t* to, float* terms, cudaStream_t st) {
   int nb = (P.N + ENV_BLOCK - 1) / ENV_BLOCK;
-  k_env_step<<<nb, ENV_BLOCK, 0, st>>>(P, t, actions, obs_f32, rew, term, to, terms);
+  k_env_step<<<nb, ENV_BLOCK, 0, st>>>(P, t, actions, rew, term, to, terms);
+  launch_obs(P, t + 1, P.obs_out + (size_t)(t + 1) * P.N * P.obs_stride, obs_f32, (P.flags & F_BOOTSTRAP) ? 1 : 0,
+             st);  // noise event s_base + t + 1
 }
 void launch_curriculum(int n, int n_levels, const uint8_t* crossed, const float* disp, const float* cmd,
                        const int32_t* ep, const uint32_t* words, int32_t* level, cudaStream_t st) {

@@ -1,6 +1,6 @@
-// gemm_tc.cu -- tcgen05 (5th-gen tensor core) bf16 GEMM for sm_100a with TMA operand staging,
-// an mbarrier producer/consumer pipeline and the fp32 accumulator in TMEM, with the MLP's epilogues
-// fused (the one dense contraction of the path, BJ north_star).
+// gemm_tc.cu -- persistent, warp-specialized tcgen05 bf16 GEMM for sm_100a (TMA operand staging,
+// mbarrier pipelines, fp32 accumulators in TMEM, TMA stores), with the MLP's epilogues fused
+// (the one dense contraction of the path, BJ north_star).
 //
 //   D[m][n] = sum_k A[m][k] * B[n][k]       (tile 128 x BN, K-blocks of 64 = one 128-B swizzle atom)
 //
@@ -12,8 +12,13 @@
 //                                same pass (bias gradients for free).
 // Epilogues: 0 = +bias, ELU -> bf16 ; 2 = * ELU'(saved activation) -> bf16 ; 3 = fp32 split-K partial.
 //
-// Warp roles (128 threads): warp 0 lane 0 issues TMA, warp 1 lane 0 issues tcgen05.mma, warp 2 owns
-// the TMEM allocation, all four warps run the epilogue (warp w reads TMEM lanes 32w..32w+31 = rows).
+// CTA = 12 warps, one CTA per SM, grid = min(tiles, #SMs), static round-robin tile schedule:
+//   warp 0 lane 0: TMA producer (STAGES-deep smem ring, full/empty mbarriers)
+//   warp 1 lane 0: tcgen05.mma issuer; accumulators double-buffered in TMEM (tmem_full/empty mbarriers)
+//   warp 2      : TMEM allocation owner
+//   warps 4..11 : epilogue; warp 4+e reads TMEM lanes 32(e%4).. and column half e/4, stages 32x64 bf16
+//                 (or 32x32 fp32) sub-tiles in 128-B-swizzled smem and writes them with TMA stores, so the
+//                 epilogue of tile i overlaps the MMA of tile i+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -30,6 +35,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -48,6 +56,16 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -61,8 +79,8 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
+// 32 consecutive fp32 columns of this thread's TMEM lane (no wait)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
       "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -71,10 +89,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
         "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptor (SM100 version 1), 128-byte swizzle.
 //  K-major : rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO); LBO unused.
@@ -96,54 +112,84 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int BN>
+constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
+constexpr int EPI_WARPS = 8;
+
+template <int BN, int EPI>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
-  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (BN < 64 ? 64 : BN) * BK * 2;  // MN-major B pads to one 64-wide atom
-  template <bool B_MN>
-  static constexpr int b_load_bytes() { return B_MN ? B_BYTES : BN * BK * 2; }
-  static constexpr int ONES_BYTES = 16 * 128;                    // 16 rows x 64 bf16 of 1.0
-  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + ONES_BYTES + 256;
-  static constexpr int TMEM_COLS = (BN + 16) <= 32 ? 32 : (BN + 16) <= 64 ? 64 : (BN + 16) <= 128 ? 128 : (BN + 16) <= 256 ? 256 : 512;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int ONES_BYTES = 16 * 128;  // 16 rows x 64 bf16 of 1.0
+  static constexpr int EPI_BUF = 4096;         // one 32 x 128-B staging sub-tile
+  static constexpr int EPI_NBUF = EPI == 3 ? 1 : 2;
+  static constexpr int BIAS_BYTES = EPI == 0 ? EPI_WARPS * 128 * 4 : 0;
+  static constexpr int FIXED = 1024 + ONES_BYTES + EPI_WARPS * EPI_NBUF * EPI_BUF + BIAS_BYTES + 512;
+  static constexpr int STAGES_FIT = (232448 - FIXED) / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int ACC_COLS = ((BN + (EPI == 3 ? 16 : 0)) + 31) / 32 * 32;
+  static constexpr int ACC_STAGES = 2 * ACC_COLS <= 512 ? 2 : 1;
+  static constexpr int TMEM_NEED = ACC_STAGES * ACC_COLS;
+  static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
+  static constexpr int SMEM = FIXED + STAGES * (A_BYTES + B_BYTES);
 };
 
-__device__ __forceinline__ float elu(float x) { return x > 0.0f ? x : expm1f(x); }
+__device__ __forceinline__ float elu_fast(float x) { return x > 0.0f ? x : __expf(x) - 1.0f; }
+
+// write one thread's 128-byte row chunk (8 x 16 B) into a 32-row, 128-B-swizzled staging buffer
+__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const uint32_t* w32) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint4 v = make_uint4(w32[4 * j], w32[4 * j + 1], w32[4 * j + 2], w32[4 * j + 3]);
+    *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
+  }
+}
+
+struct TileCoord {
+  int z, m0, n0, split, ntile;
+};
+__device__ __forceinline__ TileCoord decode(const GemmArgs& a, int t, int m_tiles, int BN) {
+  TileCoord c;
+  c.ntile = t % a.n_tiles;
+  int r = t / a.n_tiles;
+  c.m0 = (r % m_tiles) * 128;
+  r /= m_tiles;
+  c.split = r % a.n_splits;
+  c.z = r / a.n_splits;
+  c.n0 = c.ntile * BN;
+  return c;
+}
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ GemmArgs args) {
-  using C = GemmCfg<BN>;
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_constant__ GemmArgs args) {
+  using C = GemmCfg<BN, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint8_t* sOnes = sB + C::STAGES * C::B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  uint8_t* sEpi = sB + C::STAGES * C::B_BYTES;
+  uint8_t* sOnes = sEpi + EPI_WARPS * C::EPI_NBUF * C::EPI_BUF;
+  float* sBias = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES + C::BIAS_BYTES);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* accb = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accb + 1);
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int z = blockIdx.z;
-  const int m0 = blockIdx.x * C::BM;
-  const int ntile = blockIdx.y % args.n_tiles, split = blockIdx.y / args.n_tiles;
-  const int n0 = ntile * BN;
   const int M = args.M_dev ? *args.M_dev : args.M;
-  if (m0 >= M) return;  // uniform early exit (device-sized M)
-  const int kb0 = split * args.kb_per_split;
-  const int nkb = min(args.kb_per_split, args.kb_total - kb0);
-  const bool bias_col = (EPI == 3) && args.bias_col && ntile == 0;
+  const int m_tiles = args.m_tiles;
+  const int total = args.nz * m_tiles * args.n_tiles * args.n_splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(accb, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (EPI == 3) {  // 16 x 64 bf16 ones (any swizzle of a constant tile is the same tile)
     uint32_t* o = reinterpret_cast<uint32_t*>(sOnes);
     for (int k = threadIdx.x; k < C::ONES_BYTES / 4; k += blockDim.x) o[k] = 0x3F803F80u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fence_async_smem();
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -154,36 +200,44 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ Gemm
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const CUtensorMap* tmA = &args.tmA[z];
-  const CUtensorMap* tmB = &args.tmB[z];
 
   if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1u);
-        const int k0 = (kb0 + kb) * C::BK;
-        uint8_t* a = sA + stage * C::A_BYTES;
-        uint8_t* b = sB + stage * C::B_BYTES;
-        mbar_expect_tx(&full[stage], C::A_BYTES + C::template b_load_bytes<B_MN>());
-        if (!A_MN) {
-          tma_load_2d(tmA, &full[stage], a, k0, m0);
-        } else {
-          tma_load_2d(tmA, &full[stage], a, m0, k0);
-          tma_load_2d(tmA, &full[stage], a + 8192, m0 + 64, k0);
-        }
-        if (!B_MN) {
-          tma_load_2d(tmB, &full[stage], b, k0, n0);
-        } else {
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord tc = decode(args, t, m_tiles, BN);
+        if (tc.m0 >= M) continue;
+        const CUtensorMap* tmA = &args.tmA[tc.z];
+        const CUtensorMap* tmB = &args.tmB[tc.z];
+        const int kb0 = tc.split * args.kb_per_split;
+        const int nkb = min(args.kb_per_split, args.kb_total - kb0);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          const int k0 = (kb0 + kb) * C::BK;
+          uint8_t* a = sA + stage * C::A_BYTES;
+          uint8_t* b = sB + stage * C::B_BYTES;
+          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          if (!A_MN) {
+            tma_load_2d(tmA, &full[stage], a, k0, tc.m0);
+          } else {
+            tma_load_2d(tmA, &full[stage], a, tc.m0, k0);
+            tma_load_2d(tmA, &full[stage], a + 8192, tc.m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(tmB, &full[stage], b, k0, tc.n0);
+          } else {
 #pragma unroll
-          for (int i = 0; i < (BN < 64 ? 1 : BN / 64); ++i) tma_load_2d(tmB, &full[stage], b + i * 8192, n0 + 64 * i, k0);
+            for (int i = 0; i < BN / 64; ++i) tma_load_2d(tmB, &full[stage], b + i * 8192, tc.n0 + 64 * i, k0);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
         }
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN, A_MN, B_MN);
       constexpr uint32_t idesc_ones = idesc_bf16(128, 16, A_MN, false);
@@ -191,92 +245,167 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ Gemm
       const uint32_t a_step = A_MN ? 2048u : 32u, b_step = B_MN ? 2048u : 32u;  // bytes per UMMA_K = 16
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
+      int local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord tc = decode(args, t, m_tiles, BN);
+        if (tc.m0 >= M) continue;
+        const int acc = local % C::ACC_STAGES;
+        const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
+        ++local;
+        mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
+        const uint32_t tacc = tmem + acc * C::ACC_COLS;
+        const bool bias_col = (EPI == 3) && args.bias_col && tc.ntile == 0;
+        const int kb0 = tc.split * args.kb_per_split;
+        const int nkb = min(args.kb_per_split, args.kb_total - kb0);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-        for (int k = 0; k < C::BK / 16; ++k) {
-          uint64_t ad = sdesc(a0 + k * a_step, a_lbo, 1024u);
-          uint64_t bd = sdesc(b0 + k * b_step, b_lbo, 1024u);
-          tc_mma(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-          if (bias_col) {
-            uint64_t od = sdesc(smem_u32(sOnes) + k * 32u, 0u, 1024u);
-            tc_mma(tmem + BN, ad, od, idesc_ones, (kb > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < C::BK / 16; ++k) {
+            const uint64_t ad = sdesc(a0 + k * a_step, a_lbo, 1024u);
+            const uint64_t bd = sdesc(b0 + k * b_step, b_lbo, 1024u);
+            tc_mma(tacc, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            if (bias_col) {
+              const uint64_t od = sdesc(smem_u32(sOnes) + k * 32u, 0u, 1024u);
+              tc_mma(tacc + BN, ad, od, idesc_ones, (kb > 0 || k > 0) ? 1u : 0u);
+            }
           }
+          tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
         }
-        tc_commit(&empty[stage]);
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+        tc_commit(&tfull[acc]);
       }
-      tc_commit(accb);
     }
     __syncwarp();
-  }
-
-  // ---------------- epilogue: TMEM -> registers -> global
-  mbar_wait(accb, 0);
-  __syncwarp();
-  tc_fence_after();
-  const int row = m0 + warp * 32 + lane;
-  const bool row_ok = row < M;
-  const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
-  const int ncols = min(BN, args.N - n0);
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 32) {
-    float v[32];
-    tmem_ld32(tbase + c, v);
-    if (!row_ok || c >= ncols) continue;
-    if (EPI == 0) {
-      const float* bias = args.bias[z] + n0 + c;
-      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out[z]) + (size_t)row * args.ldo + n0 + c;
-      uint32_t pk[16];
-#pragma unroll
-      for (int k = 0; k < 32; k += 2) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(elu(v[k] + __ldg(bias + k)), elu(v[k + 1] + __ldg(bias + k + 1)));
-        pk[k / 2] = *reinterpret_cast<uint32_t*>(&h);
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue
+    const int e = warp - 4, q = e & 3, h = e >> 2;
+    uint8_t* mybuf = sEpi + e * C::EPI_NBUF * C::EPI_BUF;
+    float* mybias = sBias + e * 128;
+    constexpr int WCOLS = BN >= 128 ? BN / 2 : BN;  // columns handled by this warp
+    const bool active = BN >= 128 || h == 0;
+    int local = 0, nst = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileCoord tc = decode(args, t, m_tiles, BN);
+      if (tc.m0 >= M) continue;
+      const int acc = local % C::ACC_STAGES;
+      const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
+      ++local;
+      const int row = tc.m0 + q * 32 + lane;
+      // work that does not depend on the accumulator, done while the MMA runs
+      uint32_t av[32];
+      if (EPI == 0 && active) {
+        const float* bias = args.bias[tc.z];
+        for (int i = lane; i < WCOLS; i += 32) {
+          const int n = tc.n0 + h * WCOLS + i;
+          mybias[i] = n < args.N ? __ldg(bias + n) : 0.0f;
+        }
+        __syncwarp();
       }
-      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      if (EPI == 2 && active) {
+        const int nb = tc.n0 + h * WCOLS;
+        const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nb);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-    } else if (EPI == 2) {
-      const __nv_bfloat16* aux = args.aux[z] + (size_t)row * args.ld_aux + n0 + c;
-      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out[z]) + (size_t)row * args.ldo + n0 + c;
-      const uint4* a4 = reinterpret_cast<const uint4*>(aux);
-      uint32_t pk[16];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 u = a4[q];
-        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 hb = *reinterpret_cast<__nv_bfloat162*>(&w4[e]);
-          float2 hf = __bfloat1622float2(hb);
-          int k = 8 * q + 2 * e;
-          float g0 = v[k] * (hf.x > 0.0f ? 1.0f : hf.x + 1.0f);
-          float g1 = v[k + 1] * (hf.y > 0.0f ? 1.0f : hf.y + 1.0f);
-          __nv_bfloat162 o = __floats2bfloat162_rn(g0, g1);
-          pk[k / 2] = *reinterpret_cast<uint32_t*>(&o);
+        for (int j = 0; j < 8; ++j) {
+          uint4 u = (row < M && nb + 8 * j < args.N) ? a4[j] : make_uint4(0, 0, 0, 0);
+          av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
         }
       }
-      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      mbar_wait(&tfull[acc], aph);
+      __syncwarp();
+      tc_fence_after();
+      const uint32_t tbase = tmem + acc * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
+      if (active) {
+        if (EPI == 3) {
+          // fp32 split-K partial: 32-column chunks
+          const int prow = (tc.z * args.n_splits + tc.split) * args.part_rows + tc.m0 + q * 32;
+#pragma unroll 1
+          for (int c = h * WCOLS; c < (h + 1) * WCOLS; c += 32) {
+            uint32_t r[32];
+            tmem_ld32_nowait(tbase + c, r);
+            tmem_wait_ld();
+            uint8_t* buf = mybuf;
+            if (lane == 0) bulk_wait_all();
+            __syncwarp();
+            stage_row(buf, lane, r);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) { tma_store_2d(&args.tmC[0], buf, tc.n0 + c, prow); bulk_commit(); }
+            ++nst;
+          }
+          if (args.bias_col && tc.ntile == 0 && h == 0) {
+            uint32_t r[32];
+            tmem_ld32_nowait(tbase + BN, r);
+            tmem_wait_ld();
+            if (row < M)
+              args.part[(size_t)(prow + lane) * args.part_ld + args.part_bias_col] = __uint_as_float(r[0]);
+          }
+        } else {
+          // bf16 outputs: 64-column chunks (two TMEM loads)
+#pragma unroll 1
+          for (int c = h * WCOLS; c < (h + 1) * WCOLS; c += 64) {
+            uint32_t r0[32], r1[32];
+            tmem_ld32_nowait(tbase + c, r0);
+            tmem_ld32_nowait(tbase + c + 32, r1);
+            tmem_wait_ld();
+            uint32_t pk[32];
+            const int nb = tc.n0 + c;
+            if (EPI == 0) {
+              const float* bb = mybias + (c - h * WCOLS);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-    } else {
-      float* dst = args.part + (size_t)z * args.part_zstride + (size_t)split * args.part_sstride +
-                   (size_t)row * args.part_ld + n0 + c;
-      float4* d4 = reinterpret_cast<float4*>(dst);
+              for (int k = 0; k < 64; k += 4) {
+                const uint32_t* rr = k < 32 ? r0 : r1;
+                const int kk = k & 31;
+                const float4 b4 = *reinterpret_cast<const float4*>(bb + k);
+                __nv_bfloat162 o0 = __floats2bfloat162_rn(elu_fast(__uint_as_float(rr[kk]) + b4.x),
+                                                          elu_fast(__uint_as_float(rr[kk + 1]) + b4.y));
+                __nv_bfloat162 o1 = __floats2bfloat162_rn(elu_fast(__uint_as_float(rr[kk + 2]) + b4.z),
+                                                          elu_fast(__uint_as_float(rr[kk + 3]) + b4.w));
+                pk[k / 2] = *reinterpret_cast<uint32_t*>(&o0);
+                pk[k / 2 + 1] = *reinterpret_cast<uint32_t*>(&o1);
+              }
+            } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              for (int k = 0; k < 64; k += 2) {
+                const uint32_t* rr = k < 32 ? r0 : r1;
+                const int kk = k & 31;
+                uint32_t w = av[k / 2];
+                float2 hf = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w));
+                const float g0 = __uint_as_float(rr[kk]) * (hf.x > 0.0f ? 1.0f : hf.x + 1.0f);
+                const float g1 = __uint_as_float(rr[kk + 1]) * (hf.y > 0.0f ? 1.0f : hf.y + 1.0f);
+                __nv_bfloat162 o = __floats2bfloat162_rn(g0, g1);
+                pk[k / 2] = *reinterpret_cast<uint32_t*>(&o);
+              }
+            }
+            if (EPI == 2 && c + 64 < (h + 1) * WCOLS) {  // prefetch the next chunk's saved activation
+              const int nn = nb + 64;
+              const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nn);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                uint4 u = (row < M && nn + 8 * j < args.N) ? a4[j] : make_uint4(0, 0, 0, 0);
+                av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+              }
+            }
+            uint8_t* buf = mybuf + (nst & 1) * C::EPI_BUF;
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+            stage_row(buf, lane, pk);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) { tma_store_2d(&args.tmC[tc.z], buf, nb, tc.m0 + q * 32); bulk_commit(); }
+            ++nst;
+          }
+        }
+      }
+      // release the accumulator stage to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-  }
-  if (EPI == 3 && args.bias_col) {
-    float v[32];
-    if (bias_col) tmem_ld32(tbase + BN, v);  // (warp-uniform branch)
-    if (bias_col && row_ok) {
-      float* dst = args.part + (size_t)z * args.part_zstride + (size_t)split * args.part_sstride +
-                   (size_t)row * args.part_ld + args.part_bias_col;
-      *dst = v[0];
-    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -285,6 +414,7 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ Gemm
 
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static int g_num_sms = 0;
 
 bool tma_init() {
   if (g_encode) return true;
@@ -295,49 +425,63 @@ bool tma_init() {
   return true;
 }
 
-// 2D bf16 tensor [rows][cols] with row stride ld (elements); box {64, box_rows}; 128-B swizzle; OOB = 0
-bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+static bool encode(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, uint64_t rows, uint64_t cols,
+                   uint64_t ld, uint32_t box_cols, uint32_t box_rows) {
   if (!tma_init()) return false;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint64_t strides[1] = {ld * (uint64_t)esize};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = g_encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
+// 2D bf16 tensor [rows][cols] with row stride ld (elements); box {64, box_rows}; 128-B swizzle; OOB = 0
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, rows, cols, ld, 64, box_rows);
+}
+// 2D fp32 tensor, box {32, box_rows} (128 B inner), 128-B swizzle
+bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, rows, cols, ld, 32, box_rows);
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
-static cudaError_t launch_one(const GemmArgs& a, int m_tiles, int nz, cudaStream_t st) {
-  using C = GemmCfg<BN>;
+static cudaError_t launch_one(const GemmArgs& a, cudaStream_t st) {
+  using C = GemmCfg<BN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, A_MN, B_MN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(m_tiles, a.n_tiles * a.n_splits, nz);
-  k_gemm_tc<BN, A_MN, B_MN, EPI><<<grid, 128, C::SMEM, st>>>(a);
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  const int total = a.nz * a.m_tiles * a.n_tiles * a.n_splits;
+  const int grid = total < g_num_sms ? total : g_num_sms;
+  k_gemm_tc<BN, A_MN, B_MN, EPI><<<grid, GEMM_THREADS, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-static cudaError_t dispatch_bn(int bn, const GemmArgs& a, int m_tiles, int nz, cudaStream_t st) {
+static cudaError_t dispatch_bn(int bn, const GemmArgs& a, cudaStream_t st) {
   switch (bn) {
-    case 32: return launch_one<32, A_MN, B_MN, EPI>(a, m_tiles, nz, st);
-    case 64: return launch_one<64, A_MN, B_MN, EPI>(a, m_tiles, nz, st);
-    case 128: return launch_one<128, A_MN, B_MN, EPI>(a, m_tiles, nz, st);
-    case 256: return launch_one<256, A_MN, B_MN, EPI>(a, m_tiles, nz, st);
+    case 64: return launch_one<64, A_MN, B_MN, EPI>(a, st);
+    case 128: return launch_one<128, A_MN, B_MN, EPI>(a, st);
+    case 256: return launch_one<256, A_MN, B_MN, EPI>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, int m_tiles, int nz, cudaStream_t st) {
+cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, cudaStream_t st) {
   switch (kind) {
-    case GEMM_FWD: return dispatch_bn<false, false, 0>(bn, a, m_tiles, nz, st);
-    case GEMM_DX: return dispatch_bn<false, true, 2>(bn, a, m_tiles, nz, st);
-    case GEMM_DW: return dispatch_bn<true, true, 3>(bn, a, m_tiles, nz, st);
+    case GEMM_FWD: return dispatch_bn<false, false, 0>(bn, a, st);
+    case GEMM_DX: return dispatch_bn<false, true, 2>(bn, a, st);
+    case GEMM_DW: return dispatch_bn<true, true, 3>(bn, a, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -13,7 +13,7 @@ namespace lg {
 struct DevScalars;
 using lg_update_stats_dev = ::lg_update_stats;
 
-constexpr int ENV_BLOCK = 64;
+constexpr int ENV_BLOCK = 32;
 
 struct EnvParams {
   const float* hf;
@@ -29,6 +29,8 @@ struct EnvParams {
   float* boot;               // [T][N]
   __nv_bfloat16* term_obs;   // [N][Dp] compacted pre-reset observations of time-out envs
   int32_t* term_idx;         // [N]
+  void* recs;                // [N] 256-B observation records (written by the transition kernel)
+  void* trecs;               // [N] records of the pre-reset state of time-out envs (compacted)
 };
 
 void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* obs_f32, cudaStream_t st);
@@ -45,21 +47,23 @@ enum GemmKind { GEMM_FWD = 0, GEMM_DX = 1, GEMM_DW = 2 };
 struct GemmArgs {
   CUtensorMap tmA[2];
   CUtensorMap tmB[2];
+  CUtensorMap tmC[2];        // EPI 0/2: bf16 output per z (box 64x32); EPI 3: fp32 partial buffer (box 32x32)
   int M, N;                  // output rows / cols (per z)
-  const int* M_dev;          // optional device-side M (rows beyond exit early)
+  const int* M_dev;          // optional device-side M (tiles beyond are skipped)
+  int m_tiles, nz;
   int kb_total, kb_per_split, n_tiles, n_splits;
-  void* out[2];              // EPI 0/2: bf16 output base per z (already column-offset)
   int ldo;
   const float* bias[2];      // EPI 0
   const __nv_bfloat16* aux[2];  // EPI 2: saved activation for ELU'
   int ld_aux;
-  float* part;               // EPI 3: split-K partials [z][split][rows][part_ld]
+  float* part;               // EPI 3: split-K partials [z][split][part_rows][part_ld] (bias column direct)
   long long part_zstride, part_sstride;
-  int part_ld, part_bias_col, bias_col;
+  int part_rows, part_ld, part_bias_col, bias_col;
 };
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
-cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, int m_tiles, int nz, cudaStream_t st);
+bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
+cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, cudaStream_t st);
 
 // ------------------------------------------------------------------ PPO kernels (ppo.cu)
 struct NetDims {

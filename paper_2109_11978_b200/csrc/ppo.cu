@@ -11,39 +11,43 @@ namespace lg {
 constexpr float SIX_LN_2PI = 11.027262398456072f;
 constexpr float HALF_LN_2PI = 0.9189385332046727f;
 
-// ------------------------------------------------------------------ heads
-__device__ __forceinline__ void bf16x8(const __nv_bfloat16* p, float* f) {
-  uint4 u = *reinterpret_cast<const uint4*>(p);
-  uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    float2 t = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[e]));
-    f[2 * e] = t.x;
-    f[2 * e + 1] = t.y;
-  }
+// ------------------------------------------------------------------ heads (4 threads per row)
+// A "quad" of 4 consecutive threads owns one row; member q holds the columns [qC, qC+C) (C = H2/4) of
+// the actor and of the critic half of H3. The 13 head dot products are reduced over the quad with two
+// xor-shuffles and the quad leader's sums are broadcast, so all members hold bit-identical mu and V.
+// The same head_fwd_quad serves the rollout (k_heads) and the update (k_loss_heads): the ratio of the
+// first minibatch of an iteration is therefore exactly 1.
+constexpr int MAXC = 32;  // H2 <= 128
+
+__device__ __forceinline__ int wpad_index(int j, int col, int H2) {
+  const int C = H2 >> 2, q = col / C, c = col - q * C;
+  return j * (H2 + 16) + q * (C + 4) + c;  // 4 column groups, padded to stay bank-conflict free
 }
 
-// mu_j = (sum_k W4a[j][k] h_a[k]) + b4a_j, V = (sum_k W4c[k] h_c[k]) + b4c, sequential in k.
-__device__ __forceinline__ void head_forward(const __nv_bfloat16* ha, const __nv_bfloat16* hc, int H2, const float* sW4a,
-                                             const float* sb4a, const float* sW4c, float b4c, float* mu, float& V) {
-  float acc[12];
+__device__ __forceinline__ float quad_sum(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return __shfl_sync(0xffffffffu, v, (threadIdx.x & 31) & ~3);
+}
+
+// ha/hc: this member's C columns; sW: padded [13][H2+16] (row 12 = critic W4c); returns mu[12], V
+__device__ __forceinline__ void head_fwd_quad(const float* ha, const float* hc, int H2, int q, const float* sW,
+                                              const float* sb4a, float b4c, float* mu, float& V) {
+  const int C = H2 >> 2;
+  const float* w0 = sW + q * (C + 4);
 #pragma unroll
-  for (int j = 0; j < 12; ++j) acc[j] = 0.0f;
-  float vac = 0.0f;
-  for (int k = 0; k < H2; k += 8) {
-    float h[8], g[8];
-    bf16x8(ha + k, h);
-    bf16x8(hc + k, g);
+  for (int j = 0; j < 12; ++j) {
+    float p = 0.0f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-#pragma unroll
-      for (int j = 0; j < 12; ++j) acc[j] = acc[j] + sW4a[j * H2 + k + e] * h[e];
-      vac = vac + sW4c[k + e] * g[e];
-    }
+    for (int c = 0; c < MAXC; ++c)
+      if (c < C) p = fmaf(w0[j * (H2 + 16) + c], ha[c], p);
+    mu[j] = quad_sum(p) + sb4a[j];
   }
+  float pv = 0.0f;
 #pragma unroll
-  for (int j = 0; j < 12; ++j) mu[j] = acc[j] + sb4a[j];
-  V = vac + b4c;
+  for (int c = 0; c < MAXC; ++c)
+    if (c < C) pv = fmaf(w0[12 * (H2 + 16) + c], hc[c], pv);
+  V = quad_sum(pv) + b4c;
 }
 
 __device__ __forceinline__ float logp_gauss(const float* a, const float* mu, const float* ls) {
@@ -56,26 +60,58 @@ __device__ __forceinline__ float logp_gauss(const float* a, const float* mu, con
   return -s - SIX_LN_2PI;
 }
 
-__global__ void k_heads(HeadArgs a) {
+__device__ __forceinline__ void load_head_weights(const float* W4a, const float* b4a, const float* W4c,
+                                                  const float* b4c, const float* ls, int H2, float* sW,
+                                                  float* sb4a, float* sls, float* sb4c) {
+  for (int k = threadIdx.x; k < 13 * H2; k += blockDim.x) {
+    const int j = k / H2, col = k - j * H2;
+    sW[wpad_index(j, col, H2)] = j < 12 ? W4a[k] : W4c[col];
+  }
+  if (threadIdx.x < 12) { sb4a[threadIdx.x] = b4a[threadIdx.x]; sls[threadIdx.x] = ls[threadIdx.x]; }
+  if (threadIdx.x == 12) *sb4c = *b4c;
+}
+
+__device__ __forceinline__ void bf16_cols(const __nv_bfloat16* p, int C, float* f) {
+#pragma unroll
+  for (int c = 0; c < MAXC; c += 8) {
+    if (c < C) {
+      uint4 u = *reinterpret_cast<const uint4*>(p + c);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+        f[c + 2 * e] = t.x;
+        f[c + 2 * e + 1] = t.y;
+      }
+    }
+  }
+}
+
+constexpr int HEAD_ROWS = 64;  // rows per 256-thread block
+
+__global__ void __launch_bounds__(256) k_heads(HeadArgs a) {
   extern __shared__ float sh[];
-  const int H2 = a.nd.H2;
-  float* sW4a = sh;
-  float* sb4a = sW4a + 12 * H2;
-  float* sW4c = sb4a + 12;
-  float* sls = sW4c + H2;
-  for (int k = threadIdx.x; k < 12 * H2; k += blockDim.x) sW4a[k] = a.W4a[k];
-  for (int k = threadIdx.x; k < H2; k += blockDim.x) sW4c[k] = a.W4c[k];
-  if (threadIdx.x < 12) { sb4a[threadIdx.x] = a.b4a[threadIdx.x]; sls[threadIdx.x] = a.logstd[threadIdx.x]; }
+  const int H2 = a.nd.H2, C = H2 >> 2;
+  float* sW = sh;
+  float* sb4a = sW + 13 * (H2 + 16);
+  float* sls = sb4a + 12;
+  float* sb4c = sls + 12;
+  load_head_weights(a.W4a, a.b4a, a.W4c, a.b4c, a.logstd, H2, sW, sb4a, sls, sb4c);
   __syncthreads();
   const int M = a.M_dev ? *a.M_dev : a.M;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= M) return;
-  const __nv_bfloat16* ha = a.H3 + (size_t)r * 2 * H2;
+  const int q = threadIdx.x & 3;
+  const int r = blockIdx.x * HEAD_ROWS + (threadIdx.x >> 2);
+  if (blockIdx.x * HEAD_ROWS >= M) return;  // block-uniform
+  const bool valid = r < M;
+  float ha[MAXC], hc[MAXC];
+  const __nv_bfloat16* hrow = a.H3 + (size_t)(valid ? r : 0) * 2 * H2;
+  bf16_cols(hrow + q * C, C, ha);
+  bf16_cols(hrow + H2 + q * C, C, hc);
   float mu[12], V;
-  head_forward(ha, ha + H2, H2, sW4a, sb4a, sW4c, __ldg(a.b4c), mu, V);
+  head_fwd_quad(ha, hc, H2, q, sW, sb4a, *sb4c, mu, V);
+  if (!valid || q != 0) return;
   if (a.mode == 1) {  // value scatter (time-out bootstrap or V(o_T))
-    int dst = a.idx ? a.idx[r] : r;
-    a.value[dst] = V;
+    a.value[a.idx ? a.idx[r] : r] = V;
     return;
   }
   if (a.mode == 2) {
@@ -83,26 +119,30 @@ __global__ void k_heads(HeadArgs a) {
     a.value[r] = V;
     return;
   }
-  // act: a = mu + sigma * eps (ACTION stream of env g at step s_base + t + 1), logp
+  // act: a = mu + sigma * eps, eps = Box-Muller pairs (2k, 2k+1) of the ACTION stream
   Rng rng{a.seed_lo, a.seed_hi};
   const uint32_t g = (uint32_t)(a.rank * a.N + r);
   const uint32_t ev = a.scalars->s_base + (uint32_t)a.t + 1u;
-  U4 b0 = rng.block(0, g, ev, TAG_ACTION), b1 = rng.block(1, g, ev, TAG_ACTION), b2 = rng.block(2, g, ev, TAG_ACTION);
-  uint32_t w[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+  const U4 b0 = rng.block(0, g, ev, TAG_ACTION), b1 = rng.block(1, g, ev, TAG_ACTION), b2 = rng.block(2, g, ev, TAG_ACTION);
+  const uint32_t w[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
   float act[12];
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
-    float u1 = (float)((w[2 * k] >> 8) + 1u) * 0x1p-24f;
-    float u2 = (float)(w[2 * k + 1] >> 8) * 0x1p-24f;
-    float rr = sqrtf(-2.0f * log_poly(u1));
+    const float u1 = (float)((w[2 * k] >> 8) + 1u) * 0x1p-24f;
+    const float u2 = (float)(w[2 * k + 1] >> 8) * 0x1p-24f;
+    const float rr = sqrtf(-2.0f * log_poly(u1));
     float sn, cs;
     sincos_poly(0x1.921fb6p2f * u2, sn, cs);
     act[2 * k] = mu[2 * k] + expf(sls[2 * k]) * (rr * cs);
     act[2 * k + 1] = mu[2 * k + 1] + expf(sls[2 * k + 1]) * (rr * sn);
   }
-  float lp = logp_gauss(act, mu, sls);
+  const float lp = logp_gauss(act, mu, sls);
   const size_t o = (size_t)r * 12;
-  for (int j = 0; j < 12; ++j) { a.act[o + j] = act[j]; a.mu[o + j] = mu[j]; }
+#pragma unroll
+  for (int j = 0; j < 12; ++j) {
+    a.act[o + j] = act[j];
+    a.mu[o + j] = mu[j];
+  }
   a.logp[r] = lp;
   a.value[r] = V;
   if (a.u_act) for (int j = 0; j < 12; ++j) a.u_act[o + j] = act[j];
@@ -112,65 +152,74 @@ __global__ void k_heads(HeadArgs a) {
 }
 
 void launch_heads(const HeadArgs& a, cudaStream_t st) {
-  int smem = (13 * a.nd.H2 + 24) * 4;
-  int rows = a.M;
-  k_heads<<<(rows + 127) / 128, 128, smem, st>>>(a);
+  int smem = (13 * (a.nd.H2 + 16) + 28) * 4;
+  k_heads<<<(a.M + HEAD_ROWS - 1) / HEAD_ROWS, 256, smem, st>>>(a);
 }
 
 // ------------------------------------------------------------------ PPO loss head (fwd + bwd)
-constexpr int LOSS_BLOCK = 128;
+// Block = 256 threads = 64 rows x 4 members. The block's H3 rows (contiguous in memory) are staged in
+// smem with coalesced 16-B loads; dmu/dV per row go to smem; the block then forms its partial of
+// dW4 = dY^T H3 column-wise (each thread a few output columns, rows summed in order).
+constexpr int LOSS_BLOCK = 64;
 int loss_head_partial_floats(int H2) { return ((13 * H2 + 25) + 3) / 4 * 4; }
 int loss_blocks(int M) { return (M + LOSS_BLOCK - 1) / LOSS_BLOCK; }
 
 __device__ __forceinline__ float elu_grad_from_out(float h) { return h > 0.0f ? 1.0f : h + 1.0f; }
 
-__global__ void __launch_bounds__(LOSS_BLOCK) k_loss_heads(LossArgs a) {
+__global__ void __launch_bounds__(256, 2) k_loss_heads(LossArgs a) {
   extern __shared__ float sh[];
-  const int H2 = a.nd.H2;
-  float* sW4a = sh;
-  float* sb4a = sW4a + 12 * H2;
-  float* sW4c = sb4a + 12;
-  float* sls = sW4c + H2;       // 12
-  float* slso = sls + 12;       // 12
-  float* sdmu = slso + 12;      // [LOSS_BLOCK][12]
-  float* sdls = sdmu + LOSS_BLOCK * 12;  // [LOSS_BLOCK][12]
-  float* sdV = sdls + LOSS_BLOCK * 12;   // [LOSS_BLOCK]
-  double* sst = reinterpret_cast<double*>(sdV + LOSS_BLOCK);  // [LOSS_BLOCK/32][5]
-  for (int k = threadIdx.x; k < 12 * H2; k += blockDim.x) sW4a[k] = a.W4a[k];
-  for (int k = threadIdx.x; k < H2; k += blockDim.x) sW4c[k] = a.W4c[k];
-  if (threadIdx.x < 12) {
-    sb4a[threadIdx.x] = a.b4a[threadIdx.x];
-    sls[threadIdx.x] = a.logstd[threadIdx.x];
-    slso[threadIdx.x] = a.logstd_old[threadIdx.x];
+  const int H2 = a.nd.H2, C = H2 >> 2, HP = a.HP;
+  const int SHLD = 2 * H2 + 8;  // bf16 row stride of the staged H3 tile
+  float* sW = sh;
+  float* sb4a = sW + 13 * (H2 + 16);
+  float* sls = sb4a + 12;
+  float* slso = sls + 12;
+  float* sb4c = slso + 12;
+  float* sdy = sb4c + 4;                       // [64][13] dmu | dV
+  float* sdl = sdy + LOSS_BLOCK * 13;          // [64][12] dlogstd per row
+  double* sst = reinterpret_cast<double*>(sdl + LOSS_BLOCK * 12);  // [64][5]
+  __nv_bfloat16* sH = reinterpret_cast<__nv_bfloat16*>(sst + LOSS_BLOCK * 5);  // [64][SHLD]
+  load_head_weights(a.W4a, a.b4a, a.W4c, a.b4c, a.logstd, H2, sW, sb4a, sls, sb4c);
+  if (threadIdx.x < 12) slso[threadIdx.x] = a.logstd_old[threadIdx.x];
+  const int row0 = blockIdx.x * LOSS_BLOCK;
+  const int nrows = min(LOSS_BLOCK, a.M - row0);
+  {  // stage H3 rows [row0, row0 + nrows) (contiguous) into smem
+    const int v_per_row = (2 * H2) / 8;
+    const uint4* src = reinterpret_cast<const uint4*>(a.H3 + (size_t)row0 * 2 * H2);
+    for (int k = threadIdx.x; k < nrows * v_per_row; k += blockDim.x) {
+      const int rr = k / v_per_row, cc = k - rr * v_per_row;
+      *reinterpret_cast<uint4*>(sH + rr * SHLD + cc * 8) = src[k];
+    }
   }
   __syncthreads();
-  const int row0 = blockIdx.x * LOSS_BLOCK;
-  const int r = row0 + threadIdx.x;
+  const int q = threadIdx.x & 3, rl = threadIdx.x >> 2;
+  const int r = row0 + rl;
+  const bool valid = rl < nrows;
   const float invM = 1.0f / (float)a.M;
-  double st_surr = 0.0, st_vl = 0.0, st_kl = 0.0, st_clip = 0.0, st_bad = 0.0;
-  float dmu[12], dls[12], dV = 0.0f;
+  float ha[MAXC], hc[MAXC];
 #pragma unroll
-  for (int j = 0; j < 12; ++j) { dmu[j] = 0.0f; dls[j] = 0.0f; }
-  if (r < a.M) {
-    const __nv_bfloat16* ha = a.H3 + (size_t)r * 2 * H2;
-    float mu[12], V;
-    head_forward(ha, ha + H2, H2, sW4a, sb4a, sW4c, __ldg(a.b4c), mu, V);
+  for (int c = 0; c < MAXC; ++c) {
+    ha[c] = c < C ? __bfloat162float(sH[rl * SHLD + q * C + c]) : 0.0f;
+    hc[c] = c < C ? __bfloat162float(sH[rl * SHLD + H2 + q * C + c]) : 0.0f;
+  }
+  float mu[12], V;
+  head_fwd_quad(ha, hc, H2, q, sW, sb4a, *sb4c, mu, V);
+  float dmu[12], dV = 0.0f;
+  if (valid) {
     float act[12];
 #pragma unroll
-    for (int j = 0; j < 12; ++j) act[j] = a.act[(size_t)r * 12 + j];
+    for (int j = 0; j < 12; ++j) act[j] = __ldg(a.act + (size_t)r * 12 + j);
     const float lp = logp_gauss(act, mu, sls);
-    const float ratio = expf(lp - a.logp_old[r]);
-    const float adv = a.adv[r];
+    const float ratio = expf(lp - __ldg(a.logp_old + r));
+    const float adv = __ldg(a.adv + r);
     const float s1 = ratio * adv;
     const float rc = fminf(fmaxf(ratio, 1.0f - a.clip), 1.0f + a.clip);
     const float s2 = rc * adv;
     const bool take1 = s1 <= s2;
     const bool inside = ratio >= 1.0f - a.clip && ratio <= 1.0f + a.clip;
-    const float dLdr = -(take1 ? adv : (inside ? adv : 0.0f)) * invM;
-    const float dLdlp = dLdr * ratio;
-    const float Vo = a.V_old[r], ret = a.ret[r];
-    const float vd = fminf(fmaxf(V - Vo, -a.vclip), a.vclip);
-    const float vc = Vo + vd;
+    const float dLdlp = -(take1 ? adv : (inside ? adv : 0.0f)) * invM * ratio;
+    const float Vo = __ldg(a.V_old + r), ret = __ldg(a.ret + r);
+    const float vc = Vo + fminf(fmaxf(V - Vo, -a.vclip), a.vclip);
     const float e1 = (V - ret) * (V - ret), e2 = (vc - ret) * (vc - ret);
     const bool take_u = e1 >= e2;
     const bool vin = fabsf(V - Vo) <= a.vclip;
@@ -179,155 +228,165 @@ __global__ void __launch_bounds__(LOSS_BLOCK) k_loss_heads(LossArgs a) {
 #pragma unroll
     for (int j = 0; j < 12; ++j) {
       const float d = act[j] - mu[j];
-      const float is2 = expf(-2.0f * sls[j]);
-      dmu[j] = dLdlp * d * is2;
-      dls[j] = dLdlp * (d * d * is2 - 1.0f);
-      const float dm = a.mu_old[(size_t)r * 12 + j] - mu[j];
-      kl += sls[j] - slso[j] + (expf(2.0f * slso[j]) + dm * dm) * (0.5f * is2) - 0.5f;
+      const float iv = expf(-2.0f * sls[j]);
+      dmu[j] = dLdlp * d * iv;
+      const float dm = __ldg(a.mu_old + (size_t)r * 12 + j) - mu[j];
+      kl += sls[j] - slso[j] + (expf(2.0f * slso[j]) + dm * dm) * (0.5f * iv) - 0.5f;
+      if (q == 0) sdl[rl * 12 + j] = dLdlp * (d * d * iv - 1.0f);
     }
-    st_surr = (double)(take1 ? s1 : s2);
-    st_vl = (double)(take_u ? e1 : e2);
-    st_kl = (double)kl;
-    st_clip = fabsf(ratio - 1.0f) > a.clip ? 1.0 : 0.0;
-    st_bad = (isfinite(st_surr) && isfinite(st_vl) && isfinite(st_kl)) ? 0.0 : 1.0;
-    // dZ3 = (dH3) * ELU'(H3), actor columns then critic columns
-    __nv_bfloat16* dz = a.dZ3 + (size_t)r * 2 * H2;
-    for (int k = 0; k < H2; k += 8) {
-      float h[8], g[8];
-      bf16x8(ha + k, h);
-      bf16x8(ha + H2 + k, g);
-      uint32_t pa[4], pc[4];
+    if (q == 0) {
+      for (int j = 0; j < 12; ++j) sdy[rl * 13 + j] = dmu[j];
+      sdy[rl * 13 + 12] = dV;
+      const double sv = (double)(take1 ? s1 : s2), vv = (double)(take_u ? e1 : e2), kv = (double)kl;
+      double* s = sst + rl * 5;
+      s[0] = sv; s[1] = vv; s[2] = kv;
+      s[3] = fabsf(ratio - 1.0f) > a.clip ? 1.0 : 0.0;
+      s[4] = (isfinite(sv) && isfinite(vv) && isfinite(kv)) ? 0.0 : 1.0;
+    }
+    // dZ3 = dH3 * ELU'(H3) for this member's columns (actor, then critic)
+    const float* w0 = sW + q * (C + 4);
+    __nv_bfloat16* dz = a.dZ3 + (size_t)r * 2 * H2 + q * C;
 #pragma unroll
-      for (int e = 0; e < 8; e += 2) {
-        float da0 = 0.0f, da1 = 0.0f;
+    for (int c = 0; c < MAXC; c += 2) {
+      if (c < C) {
+        float d0 = 0.0f, d1 = 0.0f;
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
-          da0 = da0 + dmu[j] * sW4a[j * H2 + k + e];
-          da1 = da1 + dmu[j] * sW4a[j * H2 + k + e + 1];
+          d0 = fmaf(dmu[j], w0[j * (H2 + 16) + c], d0);
+          d1 = fmaf(dmu[j], w0[j * (H2 + 16) + c + 1], d1);
         }
-        __nv_bfloat162 za = __floats2bfloat162_rn(da0 * elu_grad_from_out(h[e]), da1 * elu_grad_from_out(h[e + 1]));
-        __nv_bfloat162 zc = __floats2bfloat162_rn(dV * sW4c[k + e] * elu_grad_from_out(g[e]),
-                                                  dV * sW4c[k + e + 1] * elu_grad_from_out(g[e + 1]));
-        pa[e / 2] = *reinterpret_cast<uint32_t*>(&za);
-        pc[e / 2] = *reinterpret_cast<uint32_t*>(&zc);
+        *reinterpret_cast<__nv_bfloat162*>(dz + c) =
+            __floats2bfloat162_rn(d0 * elu_grad_from_out(ha[c]), d1 * elu_grad_from_out(ha[c + 1]));
+        const float g0 = dV * w0[12 * (H2 + 16) + c], g1 = dV * w0[12 * (H2 + 16) + c + 1];
+        *reinterpret_cast<__nv_bfloat162*>(dz + H2 + c) =
+            __floats2bfloat162_rn(g0 * elu_grad_from_out(hc[c]), g1 * elu_grad_from_out(hc[c + 1]));
       }
-      *reinterpret_cast<uint4*>(dz + k) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-      *reinterpret_cast<uint4*>(dz + H2 + k) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
     }
-  }
-#pragma unroll
-  for (int j = 0; j < 12; ++j) { sdmu[threadIdx.x * 12 + j] = dmu[j]; sdls[threadIdx.x * 12 + j] = dls[j]; }
-  sdV[threadIdx.x] = dV;
-  // block statistics (fixed butterfly order)
-  st_surr = warp_sum_d(st_surr); st_vl = warp_sum_d(st_vl); st_kl = warp_sum_d(st_kl);
-  st_clip = warp_sum_d(st_clip); st_bad = warp_sum_d(st_bad);
-  const int wid = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sst[wid * 5 + 0] = st_surr; sst[wid * 5 + 1] = st_vl; sst[wid * 5 + 2] = st_kl;
-    sst[wid * 5 + 3] = st_clip; sst[wid * 5 + 4] = st_bad;
   }
   __syncthreads();
-  float* out = a.part + (size_t)blockIdx.x * a.HP;
-  const int nrows = min(LOSS_BLOCK, a.M - row0);
-  // dW4a[j][k] = sum_r dmu[r][j] h_a[r][k]; dW4c[k] = sum_r dV[r] h_c[r][k]  (rows in order)
-  for (int k = threadIdx.x; k < H2; k += blockDim.x) {
-    float acc[12], accc = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 12; ++j) acc[j] = 0.0f;
-    for (int rr = 0; rr < nrows; ++rr) {
-      const __nv_bfloat16* hrow = a.H3 + (size_t)(row0 + rr) * 2 * H2;
-      const float h = __bfloat162float(hrow[k]), g = __bfloat162float(hrow[H2 + k]);
-#pragma unroll
-      for (int j = 0; j < 12; ++j) acc[j] = acc[j] + sdmu[rr * 12 + j] * h;
-      accc = accc + sdV[rr] * g;
-    }
-#pragma unroll
-    for (int j = 0; j < 12; ++j) out[j * H2 + k] = acc[j];
-    out[12 * H2 + 12 + k] = accc;
+  // block partial of the head/log-std gradients (rows in order)
+  float* out = a.part + (size_t)blockIdx.x * HP;
+  for (int e = threadIdx.x; e < 13 * H2; e += blockDim.x) {
+    const int j = e / H2, k = e - j * H2;
+    const int col = j < 12 ? k : H2 + k;
+    float acc = 0.0f;
+    for (int rr = 0; rr < nrows; ++rr) acc = fmaf(sdy[rr * 13 + j], __bfloat162float(sH[rr * SHLD + col]), acc);
+    out[j < 12 ? e : 12 * H2 + 12 + k] = acc;
   }
-  if (threadIdx.x < 12) {
-    const int j = threadIdx.x;
-    float sb = 0.0f, sl = 0.0f;
-    for (int rr = 0; rr < nrows; ++rr) { sb = sb + sdmu[rr * 12 + j]; sl = sl + sdls[rr * 12 + j]; }
-    out[12 * H2 + j] = sb;
+  if (threadIdx.x < 13) {
+    float sb = 0.0f;
+    for (int rr = 0; rr < nrows; ++rr) sb = sb + sdy[rr * 13 + threadIdx.x];
+    out[threadIdx.x < 12 ? 12 * H2 + threadIdx.x : 13 * H2 + 12] = sb;
+  } else if (threadIdx.x >= 32 && threadIdx.x < 44) {
+    const int j = threadIdx.x - 32;
+    float sl = 0.0f;
+    for (int rr = 0; rr < nrows; ++rr) sl = sl + sdl[rr * 12 + j];
     out[13 * H2 + 13 + j] = sl;
-  }
-  if (threadIdx.x == 32) {
-    float sv = 0.0f;
-    for (int rr = 0; rr < nrows; ++rr) sv = sv + sdV[rr];
-    out[13 * H2 + 12] = sv;
-  }
-  if (threadIdx.x < 5) {
+  } else if (threadIdx.x >= 64 && threadIdx.x < 69) {
+    const int k = threadIdx.x - 64;
     double s = 0.0;
-    for (int w = 0; w < LOSS_BLOCK / 32; ++w) s += sst[w * 5 + threadIdx.x];
-    a.spart[(size_t)blockIdx.x * 8 + threadIdx.x] = s;
+    for (int rr = 0; rr < nrows; ++rr) s += sst[rr * 5 + k];
+    a.spart[(size_t)blockIdx.x * 8 + k] = s;
   }
 }
 
 void launch_loss_heads(const LossArgs& a, cudaStream_t st) {
-  int H2 = a.nd.H2;
-  int smem = (13 * H2 + 36 + LOSS_BLOCK * 25) * 4 + 8 + (LOSS_BLOCK / 32) * 5 * 8;
-  k_loss_heads<<<loss_blocks(a.M), LOSS_BLOCK, smem, st>>>(a);
+  const int H2 = a.nd.H2;
+  const size_t smem = (13 * (H2 + 16) + 40 + LOSS_BLOCK * 25) * 4 + 16 + LOSS_BLOCK * 5 * 8 +
+                      (size_t)LOSS_BLOCK * (2 * H2 + 8) * 2 + 64;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_loss_heads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = smem;
+  }
+  k_loss_heads<<<loss_blocks(a.M), 256, smem, st>>>(a);
 }
 
-// sums over blocks (fixed order) -> canonical gradient of heads/log-std + stats payload
-__global__ void k_reduce_heads(HeadReduceArgs a) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+// sums over blocks (fixed order) -> canonical gradient of heads/log-std + stats payload.
+// Block = 32 warps x 32 elements; warp w sums partial rows b = w, w+32, ... (in order), then lane-wise the
+// 32 warp sums are added in warp order: a fixed, run-to-run deterministic tree.
+constexpr int RH_WARPS = 32;
+__global__ void __launch_bounds__(RH_WARPS * 32) k_reduce_heads(HeadReduceArgs a) {
+  __shared__ float ssum[RH_WARPS][33];
   const int H2 = a.H2;
   const int nval = 13 * H2 + 25;
-  if (e < nval) {
-    float s = 0.0f;
-    for (int b = 0; b < a.nblk; ++b) s = s + a.part[(size_t)b * a.HP + e];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 32 + lane;
+  float s = 0.0f;
+  if (e < nval)
+    for (int b = warp; b < a.nblk; b += RH_WARPS) s = s + a.part[(size_t)b * a.HP + e];
+  ssum[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && e < nval) {
+    float t = 0.0f;
+    for (int w = 0; w < RH_WARPS; ++w) t = t + ssum[w][lane];
     long long dst;
     if (e < 12 * H2) dst = a.off_W4a + e;
     else if (e < 12 * H2 + 12) dst = a.off_b4a + (e - 12 * H2);
     else if (e < 13 * H2 + 12) dst = a.off_W4c + (e - 12 * H2 - 12);
     else if (e == 13 * H2 + 12) dst = a.off_b4c;
-    else { dst = a.off_logstd + (e - 13 * H2 - 13); s = s - a.ent_coef; }
-    a.grad[dst] = s;
-    if (!isfinite(s)) atomicAdd(&a.payload[4], 1.0f);
+    else { dst = a.off_logstd + (e - 13 * H2 - 13); t = t - a.ent_coef; }
+    a.grad[dst] = t;
+    if (!isfinite(t)) atomicAdd(&a.payload[4], 1.0f);
   }
-  if (blockIdx.x == 0 && threadIdx.x < 5) {
-    double s = 0.0;
-    for (int b = 0; b < a.nblk; ++b) s += a.spart[(size_t)b * 8 + threadIdx.x];
+  if (blockIdx.x == 0 && warp == 1) {
     const double invM = 1.0 / (double)a.M;
-    if (threadIdx.x == 0) a.payload[1] = (float)(s * invM);       // surrogate mean
-    if (threadIdx.x == 1) a.payload[2] = (float)(s * invM);       // value loss mean
-    if (threadIdx.x == 2) a.payload[0] = (float)(s * invM);       // KL mean (Alg. 1)
-    if (threadIdx.x == 3) a.payload[3] = (float)(s * invM);       // clip fraction
-    if (threadIdx.x == 4 && s > 0.0) atomicAdd(&a.payload[4], (float)s);
-    if (threadIdx.x == 0) a.payload[5] = 1.0f;                    // rank count (allreduce sums it)
+    for (int k = 0; k < 5; ++k) {
+      double v = 0.0;
+      for (int b = lane; b < a.nblk; b += 32) v += a.spart[(size_t)b * 8 + k];
+      v = warp_sum_d(v);
+      if (lane == 0) {
+        if (k == 0) a.payload[1] = (float)(v * invM);       // surrogate mean
+        if (k == 1) a.payload[2] = (float)(v * invM);       // value loss mean
+        if (k == 2) a.payload[0] = (float)(v * invM);       // KL mean (Alg. 1)
+        if (k == 3) a.payload[3] = (float)(v * invM);       // clip fraction
+        if (k == 4 && v > 0.0) atomicAdd(&a.payload[4], (float)v);
+      }
+    }
+    if (lane == 0) a.payload[5] = 1.0f;                     // rank count (allreduce sums it)
   }
 }
 
 void launch_reduce_heads(const HeadReduceArgs& a, cudaStream_t st) {
   int n = 13 * a.H2 + 25;
-  k_reduce_heads<<<(n + 127) / 128, 128, 0, st>>>(a);
+  k_reduce_heads<<<(n + 31) / 32, RH_WARPS * 32, 0, st>>>(a);
 }
 
-// split-K partials -> canonical W and b gradients (fixed split order)
-__global__ void k_reduce_dw(DwReduceArgs a) {
+// split-K partials -> canonical W and b gradients. Block = 8 warps x 32 consecutive elements; warp w
+// sums splits s = w, w+8, ... in order, then the 8 warp sums are added in warp order (deterministic).
+__global__ void __launch_bounds__(256) k_reduce_dw(DwReduceArgs a) {
+  __shared__ float ssum[8][33];
   const int z = blockIdx.z;
   const int per = a.cols + 1;  // cols + bias column
-  const long long total = (long long)a.rows * per;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(e / per), c = (int)(e % per);
+  const int total = a.rows * per;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 32 + lane;
+  float s = 0.0f;
+  int r = 0, c = 0;
+  if (e < total) {
+    r = e / per;
+    c = e - r * per;
     const int pc = c < a.cols ? c : a.bias_col;
     const float* p = a.part + z * a.zstride + (size_t)r * a.ld + pc;
-    float s = 0.0f;
-    for (int k = 0; k < a.S; ++k) s = s + p[k * a.sstride];
+    for (int k = warp; k < a.S; k += 8) s = s + __ldg(p + (size_t)k * a.sstride);
+  }
+  ssum[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && e < total) {
+    float t = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t = t + ssum[w][lane];
     int zz = z, rr = r;
     if (a.row_split > 0 && r >= a.row_split) { zz = 1; rr = r - a.row_split; }
-    if (c < a.cols) a.grad[a.w_off[zz] + (long long)rr * a.cols + c] = s;
-    else a.grad[a.b_off[zz] + rr] = s;
-    if (!isfinite(s)) atomicAdd(&a.payload[4], 1.0f);
+    if (c < a.cols) a.grad[a.w_off[zz] + (long long)rr * a.cols + c] = t;
+    else a.grad[a.b_off[zz] + rr] = t;
+    if (!isfinite(t)) atomicAdd(&a.payload[4], 1.0f);
   }
 }
 
 void launch_reduce_dw(const DwReduceArgs& a, cudaStream_t st) {
-  long long total = (long long)a.rows * (a.cols + 1);
-  int nb = (int)min((total + 255) / 256, 2048LL);
-  k_reduce_dw<<<dim3(nb, 1, a.nz), 256, 0, st>>>(a);
+  const int total = a.rows * (a.cols + 1);
+  k_reduce_dw<<<dim3((total + 31) / 32, 1, a.nz), 256, 0, st>>>(a);
 }
 
 // ------------------------------------------------------------------ GAE (reverse time scan, thread per env)
