@@ -77,17 +77,18 @@ struct DwPlan {
 DwPlan dw_plan(int rows, int N, int K, int nz) {
   DwPlan p;
   p.rows = rows; p.N = N; p.nz = nz;
-  p.bn = N > 64 ? 128 : 64;  // dW: 128-wide tiles leave room for a deeper TMA pipeline
+  p.bn = N > 128 ? 256 : (N > 64 ? 128 : 64);  // wide tiles: fewer operand re-reads (the dW GEMMs are L2-bound)
   p.n_tiles = (N + p.bn - 1) / p.bn;
   p.m_tiles = (rows + 127) / 128;
   p.kb_total = (K + 63) / 64;
-  int tiles = p.n_tiles * p.m_tiles * nz;
-  int S = std::max(1, std::min(p.kb_total, 148 / std::max(1, tiles)));
+  const int tiles = p.n_tiles * p.m_tiles * nz;
+  // split-K over a cluster of S CTAs (S <= 16), reduced on chip (k_gemm_dw)
+  int S = std::max(1, std::min(std::min(p.kb_total, 16), 148 / std::max(1, tiles)));
   p.kb_per_split = (p.kb_total + S - 1) / S;
   p.S = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
   p.ld = p.n_tiles * p.bn + 16;
   p.rows_pad = p.m_tiles * 128;
-  p.bytes = (size_t)nz * p.S * p.rows_pad * p.ld * 4;
+  p.bytes = 0;
   return p;
 }
 
@@ -446,15 +447,10 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   set_fwd_common(x3, d.Mmb, d.H1, d.H2, bn_for(d.H1), 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
   set_fwd_common(x2, d.Mmb, d.H0, d.H1, bn_for(d.H0), 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
   // ---- backward dW (A = dZ MN-major, B = activations MN-major), split-K over the minibatch
-  auto dw_setup = [&](GemmArgs& g, const DwPlan& p, size_t part_off) {
+  auto dw_setup = [&](GemmArgs& g, const DwPlan& p, size_t) {
     g.M = p.rows; g.N = p.N; g.M_dev = nullptr;
-    g.kb_total = p.kb_total; g.kb_per_split = p.kb_per_split; g.n_tiles = p.n_tiles; g.n_splits = p.S;
-    g.part = at<float>(K, part_off);
-    g.part_rows = p.rows_pad;
-    g.part_sstride = (long long)p.rows_pad * p.ld;
-    g.part_zstride = (long long)p.S * g.part_sstride;
-    g.part_ld = p.ld; g.part_bias_col = p.n_tiles * p.bn; g.bias_col = 1;
-    ok &= make_tmap_f32(&g.tmC[0], g.part, (uint64_t)p.nz * p.S * p.rows_pad, p.ld, p.ld, 32);
+    g.kb_total = p.kb_total; g.kb_per_split = p.kb_per_split; g.n_tiles = p.n_tiles; g.n_splits = 1;
+    g.m_tiles = p.m_tiles; g.nz = p.nz;
   };
   GemmArgs& w3 = ctx->dw3;
   memset(&w3, 0, sizeof(w3));
@@ -799,37 +795,31 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
   hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
   { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
   CKL();
-  auto reduce = [&](const GemmArgs& g, const DwPlan& p, int rows, int cols, const long long* woff, const long long* boff,
-                    int row_split) {
-    DwReduceArgs r;
-    r.part = g.part; r.zstride = g.part_zstride; r.sstride = g.part_sstride;
-    r.ld = p.ld; r.S = p.S; r.rows = rows; r.cols = cols; r.bias_col = g.part_bias_col;
-    r.grad = grad;
-    r.w_off[0] = woff[0]; r.w_off[1] = woff[1]; r.b_off[0] = boff[0]; r.b_off[1] = boff[1];
-    r.nz = row_split > 0 ? 1 : p.nz;
-    r.row_split = row_split;
-    r.payload = ctx->payload;
-    Scope sc_(ctx, LG_PROF_REDUCE);
-    launch_reduce_dw(r, ctx->st);
+  auto dw = [&](const GemmArgs& g, const DwPlan& p, int cols, const long long* woff, const long long* boff,
+                int row_split) -> lg_status {
+    DwOut o;
+    o.grad = grad;
+    o.w_off[0] = woff[0]; o.w_off[1] = woff[1]; o.b_off[0] = boff[0]; o.b_off[1] = boff[1];
+    o.cols = cols;
+    o.row_split = row_split;
+    o.payload = ctx->payload;
+    Scope sc_(ctx, LG_PROF_GEMM_DW);
+    cudaError_t e = launch_gemm_dw(p.bn, g, o, p.S, ctx->st);
+    if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm_dw: %s", cudaGetErrorString(e));
+    return LG_OK;
   };
   // layer 3
-  if ((s = gemm(ctx, GEMM_DW, ctx->dw3, L.dw3.bn, 2)) != LG_OK) return s;
-  reduce(ctx->dw3, L.dw3, d.H2, d.H1, ctx->cn.W3, ctx->cn.b3, 0);
-  CKL();
+  if ((s = dw(ctx->dw3, L.dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
   GemmArgs x3 = ctx->dx3;
   x3.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x3, bn_for(d.H1), 2)) != LG_OK) return s;
   // layer 2
-  if ((s = gemm(ctx, GEMM_DW, ctx->dw2, L.dw2.bn, 2)) != LG_OK) return s;
-  reduce(ctx->dw2, L.dw2, d.H1, d.H0, ctx->cn.W2, ctx->cn.b2, 0);
-  CKL();
+  if ((s = dw(ctx->dw2, L.dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   GemmArgs x2 = ctx->dx2;
   x2.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x2, bn_for(d.H0), 2)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
-  if ((s = gemm(ctx, GEMM_DW, ctx->dw1, L.dw1.bn, 1)) != LG_OK) return s;
-  reduce(ctx->dw1, L.dw1, 2 * d.H0, d.D, ctx->cn.W1, ctx->cn.b1, d.H0);
-  CKL();
+  if ((s = dw(ctx->dw1, L.dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
   return LG_OK;
 }
 
@@ -918,10 +908,7 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
       if ((s = minibatch_gradient(ctx)) != LG_OK) return s;
       { Scope sc_(ctx, LG_PROF_COMM); if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s; }
       Scope sc_adam(ctx, LG_PROF_ADAM);
-      launch_alg1_prep(ctx->payload, ctx->sc, ctx->cfg.kl_target, ctx->world, ctx->cfg.adam_b1, ctx->cfg.adam_b2,
-                       ctx->step_f, ctx->st);
-      CKL();
-      launch_adam(aa, ctx->step_f, ctx->st);
+      launch_adam(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, e * d.K + m, ctx->step_f + 4, ctx->st);
       CKL();
     }
   }

@@ -32,6 +32,9 @@ struct DevScalars {
   float ep_return_sum, ep_len_sum;
   int32_t episodes, promotions, demotions, pad2;
   int32_t level_hist[16];
+  // Alg. 1 / Adam state per minibatch slot m of the iteration (read slot m&1, write slot (m+1)&1)
+  float alpha_ring[2];
+  int32_t adamt_ring[2];
 };
 
 // ------------------------------------------------------------------ Philox4x32-10

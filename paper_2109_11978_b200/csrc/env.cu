@@ -196,20 +196,20 @@ __global__ void __launch_bounds__(256) k_env_obs(EnvParams P, int ev_off, __nv_b
                                                  float* __restrict__ dst_f32, int with_terminal) {
   const int D = P.obs_dim, Dp = P.obs_stride, G = Dp / 4;
   const uint32_t ev = P.scalars->s_base + (uint32_t)ev_off;
-  const long long NG = (long long)P.N * G;
-  long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int NG = P.N * G;
+  int it = blockIdx.x * blockDim.x + threadIdx.x;
   const ObsRec* recs = reinterpret_cast<const ObsRec*>(P.recs);
   __nv_bfloat16* dst = dst_bf16;
   float* df = dst_f32;
   if (it >= NG) {
     if (!with_terminal) return;
     it -= NG;
-    if (it >= (long long)P.scalars->n_to * G) return;
+    if (it >= P.scalars->n_to * G) return;
     recs = reinterpret_cast<const ObsRec*>(P.trecs);
     dst = P.term_obs;
     df = nullptr;
   }
-  const int r = (int)(it / G), gq = (int)(it - (long long)r * G);
+  const int r = it / G, gq = it - r * G;
   const ObsRec& o = recs[r];
   World W{P.hf, P.R, P.C, P.inv_cell};
   Rng rng{P.seed_lo, P.seed_hi};

@@ -180,6 +180,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   const int M = args.M_dev ? *args.M_dev : args.M;
   const int m_tiles = args.m_tiles;
   const int total = args.nz * m_tiles * args.n_tiles * args.n_splits;
+  {  // CTA-uniform early exit when none of this CTA's tiles has rows (device-sized M, e.g. no time-outs)
+    bool any = false;
+    for (int t = blockIdx.x; t < total && !any; t += gridDim.x) any = decode(args, t, m_tiles, BN).m0 < M;
+    if (!any) return;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -412,6 +417,209 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
 
+// ------------------------------------------------------------------ dW with on-chip split-K reduction
+// dW = dZ^T X (+ db = colsum dZ via the ones MMA) for one 128 x BN output tile per CLUSTER of S CTAs:
+// CTA s (cluster rank) contracts batch rows [s*kb_per_split*64, ...). After its MMAs it copies the fp32
+// accumulator (+ bias column) from TMEM into its own shared memory; after a cluster barrier, CTA s
+// reduces rows i = s, s+S, ... over the S CTAs' shared memory (DSMEM loads, splits summed in order 0..S-1,
+// i.e. deterministically) and writes the final gradient rows straight into the canonical gradient vector.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem4(const float* local, uint32_t cta) {
+  uint32_t a = smem_u32(local), ra;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra));
+  return v;
+}
+
+template <int BN>
+struct DwCfg {  // k_gemm_dw: no epilogue staging buffers, the operand ring is reused for the reduction
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int ONES_BYTES = 16 * 128;
+  static constexpr int EPI_WARPS_ = EPI_WARPS;
+  static constexpr int EPI_NBUF = 0, EPI_BUF = 0, BIAS_BYTES = 0;
+  static constexpr int FIXED = 1024 + ONES_BYTES + 512;
+  static constexpr int STAGES_FIT = (232448 - FIXED) / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int ACC_COLS = ((BN + 16) + 31) / 32 * 32;
+  static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
+  static constexpr int SMEM = FIXED + STAGES * (A_BYTES + B_BYTES);
+};
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_constant__ GemmArgs args, const DwOut out) {
+  using C = DwCfg<BN>;
+  constexpr int RLD = BN + 20;  // fp32 row stride of the reduction buffer (16-B rows, conflict-free float4 writes)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  float* red = reinterpret_cast<float*>(smem);  // reuses the operand ring after the last MMA
+  uint8_t* sOnes = sB + C::STAGES * C::B_BYTES + EPI_WARPS * C::EPI_NBUF * C::EPI_BUF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES + C::BIAS_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
+  static_assert(128 * RLD * 4 <= C::STAGES * (C::A_BYTES + C::B_BYTES), "reduction buffer must fit the ring");
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t S = gridDim.x, split = cluster_rank();
+  const TileCoord tc = decode(args, blockIdx.y, args.m_tiles, BN);
+  const bool bias_col = tc.ntile == 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    uint32_t* o = reinterpret_cast<uint32_t*>(sOnes);
+    for (int k = threadIdx.x; k < C::ONES_BYTES / 4; k += blockDim.x) o[k] = 0x3F803F80u;
+    fence_async_smem();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kb0 = (int)split * args.kb_per_split;
+  const int nkb = max(0, min(args.kb_per_split, args.kb_total - kb0));
+  const CUtensorMap* tmA = &args.tmA[tc.z];
+  const CUtensorMap* tmB = &args.tmB[tc.z];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        const int k0 = (kb0 + kb) * C::BK;
+        uint8_t* a = sA + stage * C::A_BYTES;
+        uint8_t* b = sB + stage * C::B_BYTES;
+        mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+        tma_load_2d(tmA, &full[stage], a, tc.m0, k0);
+        tma_load_2d(tmA, &full[stage], a + 8192, tc.m0 + 64, k0);
+#pragma unroll
+        for (int i = 0; i < BN / 64; ++i) tma_load_2d(tmB, &full[stage], b + i * 8192, tc.n0 + 64 * i, k0);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN, true, true);
+      constexpr uint32_t idesc_ones = idesc_bf16(128, 16, true, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k) {
+          const uint64_t ad = sdesc(a0 + k * 2048u, 8192u, 1024u);
+          const uint64_t bd = sdesc(b0 + k * 2048u, 8192u, 1024u);
+          tc_mma(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          if (bias_col) {
+            const uint64_t od = sdesc(smem_u32(sOnes) + k * 32u, 0u, 1024u);
+            tc_mma(tmem + BN, ad, od, idesc_ones, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+        }
+        tc_commit(&empty[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+      }
+      tc_commit(&tfull[0]);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // TMEM -> smem partial (an empty split contributes zeros)
+    const int e = warp - 4, q = e & 3, h = e >> 2;
+    const int row = q * 32 + lane;
+    if (nkb > 0) {
+      mbar_wait(&tfull[0], 0);
+      __syncwarp();
+      tc_fence_after();
+    }
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    for (int c = h * (BN / 2); c < (h + 1) * (BN / 2); c += 32) {
+      uint32_t r[32];
+      if (nkb > 0) {
+        tmem_ld32_nowait(tbase + c, r);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) r[k] = 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 32; k += 4)
+        *reinterpret_cast<float4*>(red + row * RLD + c + k) =
+            make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]), __uint_as_float(r[k + 2]), __uint_as_float(r[k + 3]));
+    }
+    if (h == 0) {
+      uint32_t r[32];
+      if (nkb > 0 && bias_col) {
+        tmem_ld32_nowait(tbase + BN, r);
+        tmem_wait_ld();
+      }
+      *reinterpret_cast<float4*>(red + row * RLD + BN) =
+          make_float4((nkb > 0 && bias_col) ? __uint_as_float(r[0]) : 0.0f, 0.0f, 0.0f, 0.0f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // every CTA's partial is in its shared memory
+  // cluster-wide reduction: rows i = split, split + S, ...; splits summed in order 0..S-1
+  const int rows_valid = min(128, args.M - tc.m0);
+  const int cols_valid = min(BN, out.cols - tc.n0);
+  constexpr int PER = BN / 4 + 1;  // float4 column groups + the bias group
+  for (int idx = threadIdx.x; idx < 128 * PER; idx += blockDim.x) {
+    const int ii = idx / PER, g = idx - ii * PER;
+    const int i = ii * (int)S + (int)split;
+    if (i >= rows_valid) continue;
+    const bool isb = g == BN / 4;
+    const int c = 4 * g;
+    if (isb ? !bias_col : c >= cols_valid) continue;
+    const float* loc = red + i * RLD + c;
+    float4 vs[16];
+#pragma unroll
+    for (uint32_t s = 0; s < 16; ++s)
+      if (s < S) vs[s] = ld_dsmem4(loc, s);
+    float4 v = vs[0];
+#pragma unroll
+    for (uint32_t s = 1; s < 16; ++s)
+      if (s < S) { v.x = v.x + vs[s].x; v.y = v.y + vs[s].y; v.z = v.z + vs[s].z; v.w = v.w + vs[s].w; }
+    int zz = tc.z, rr = tc.m0 + i;
+    if (out.row_split > 0 && rr >= out.row_split) { zz = 1; rr -= out.row_split; }
+    if (isb) {
+      out.grad[out.b_off[zz] + rr] = v.x;
+      if (!isfinite(v.x)) atomicAdd(out.payload + 4, 1.0f);
+    } else {
+      float* dst = out.grad + out.w_off[zz] + (long long)rr * out.cols + tc.n0 + c;
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (c + k < cols_valid) {
+          dst[k] = vv[k];
+          if (!isfinite(vv[k])) atomicAdd(out.payload + 4, 1.0f);
+        }
+    }
+  }
+  cluster_sync_all();  // keep shared memory alive until every CTA has read it
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static int g_num_sms = 0;
@@ -473,6 +681,41 @@ static cudaError_t dispatch_bn(int bn, const GemmArgs& a, cudaStream_t st) {
     case 64: return launch_one<64, A_MN, B_MN, EPI>(a, st);
     case 128: return launch_one<128, A_MN, B_MN, EPI>(a, st);
     case 256: return launch_one<256, A_MN, B_MN, EPI>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int BN>
+static cudaError_t launch_dw_bn(const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
+  using C = DwCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = a.nz * a.m_tiles * a.n_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(S, tiles, 1);
+  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_dw<BN>, a, o);
+}
+
+cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
+  switch (bn) {
+    case 64: return launch_dw_bn<64>(a, o, S, st);
+    case 128: return launch_dw_bn<128>(a, o, S, st);
+    case 256: return launch_dw_bn<256>(a, o, S, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -65,6 +65,16 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
 cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, cudaStream_t st);
 
+struct DwOut {                 // canonical destinations of a weight-gradient GEMM (see k_gemm_dw)
+  float* grad;
+  long long w_off[2], b_off[2];
+  int cols;                    // real input width (the W row length in the canonical vector)
+  int row_split;               // layer 1: rows >= row_split belong to the critic (second net)
+  float* payload;              // non-finite counter at payload[4]
+};
+// split-K over a thread-block cluster of S CTAs (S <= 16) with the reduction in distributed shared memory
+cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);
+
 // ------------------------------------------------------------------ PPO kernels (ppo.cu)
 struct NetDims {
   int D, Dp, H0, H1, H2;
@@ -184,9 +194,8 @@ struct AdamArgs {
   float b1, b2, eps, inv_world;
   DevScalars* sc;
 };
-void launch_alg1_prep(const float* payload, DevScalars* sc, float kl_target, int world, float b1, float b2,
-                      float* step_f, cudaStream_t st);
-void launch_adam(const AdamArgs& a, const float* step_f, cudaStream_t st);
+void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc,
+                 cudaStream_t st);
 void launch_sync_shadow(const ShadowArgs& sh, const float* theta, cudaStream_t st);
 
 struct IterEndArgs {

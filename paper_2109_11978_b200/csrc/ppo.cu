@@ -39,14 +39,20 @@ __device__ __forceinline__ void head_fwd_quad(const float* ha, const float* hc, 
   for (int j = 0; j < 12; ++j) {
     float p = 0.0f;
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c)
-      if (c < C) p = fmaf(w0[j * (H2 + 16) + c], ha[c], p);
+    for (int c = 0; c < MAXC; c += 4)
+      if (c < C) {
+        const float4 w = *reinterpret_cast<const float4*>(w0 + j * (H2 + 16) + c);
+        p = fmaf(w.x, ha[c], p); p = fmaf(w.y, ha[c + 1], p); p = fmaf(w.z, ha[c + 2], p); p = fmaf(w.w, ha[c + 3], p);
+      }
     mu[j] = quad_sum(p) + sb4a[j];
   }
   float pv = 0.0f;
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c)
-    if (c < C) pv = fmaf(w0[12 * (H2 + 16) + c], hc[c], pv);
+  for (int c = 0; c < MAXC; c += 4)
+    if (c < C) {
+      const float4 w = *reinterpret_cast<const float4*>(w0 + 12 * (H2 + 16) + c);
+      pv = fmaf(w.x, hc[c], pv); pv = fmaf(w.y, hc[c + 1], pv); pv = fmaf(w.z, hc[c + 2], pv); pv = fmaf(w.w, hc[c + 3], pv);
+    }
   V = quad_sum(pv) + b4c;
 }
 
@@ -87,10 +93,12 @@ __device__ __forceinline__ void bf16_cols(const __nv_bfloat16* p, int C, float* 
   }
 }
 
-constexpr int HEAD_ROWS = 64;  // rows per 256-thread block
+constexpr int HEAD_ROWS = 16;  // rows per 64-thread block
 
-__global__ void __launch_bounds__(256) k_heads(HeadArgs a) {
+__global__ void __launch_bounds__(64) k_heads(HeadArgs a) {
   extern __shared__ float sh[];
+  const int M = a.M_dev ? *a.M_dev : a.M;
+  if (blockIdx.x * HEAD_ROWS >= M) return;  // block-uniform, before any work (empty bootstrap launches)
   const int H2 = a.nd.H2, C = H2 >> 2;
   float* sW = sh;
   float* sb4a = sW + 13 * (H2 + 16);
@@ -98,10 +106,8 @@ __global__ void __launch_bounds__(256) k_heads(HeadArgs a) {
   float* sb4c = sls + 12;
   load_head_weights(a.W4a, a.b4a, a.W4c, a.b4c, a.logstd, H2, sW, sb4a, sls, sb4c);
   __syncthreads();
-  const int M = a.M_dev ? *a.M_dev : a.M;
   const int q = threadIdx.x & 3;
   const int r = blockIdx.x * HEAD_ROWS + (threadIdx.x >> 2);
-  if (blockIdx.x * HEAD_ROWS >= M) return;  // block-uniform
   const bool valid = r < M;
   float ha[MAXC], hc[MAXC];
   const __nv_bfloat16* hrow = a.H3 + (size_t)(valid ? r : 0) * 2 * H2;
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(256) k_heads(HeadArgs a) {
 
 void launch_heads(const HeadArgs& a, cudaStream_t st) {
   int smem = (13 * (a.nd.H2 + 16) + 28) * 4;
-  k_heads<<<(a.M + HEAD_ROWS - 1) / HEAD_ROWS, 256, smem, st>>>(a);
+  k_heads<<<(a.M + HEAD_ROWS - 1) / HEAD_ROWS, HEAD_ROWS * 4, smem, st>>>(a);
 }
 
 // ------------------------------------------------------------------ PPO loss head (fwd + bwd)
@@ -247,31 +253,41 @@ __global__ void __launch_bounds__(256, 2) k_loss_heads(LossArgs a) {
     const float* w0 = sW + q * (C + 4);
     __nv_bfloat16* dz = a.dZ3 + (size_t)r * 2 * H2 + q * C;
 #pragma unroll
-    for (int c = 0; c < MAXC; c += 2) {
+    for (int c = 0; c < MAXC; c += 4) {
       if (c < C) {
-        float d0 = 0.0f, d1 = 0.0f;
+        float d0 = 0.0f, d1 = 0.0f, d2 = 0.0f, d3 = 0.0f;
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
-          d0 = fmaf(dmu[j], w0[j * (H2 + 16) + c], d0);
-          d1 = fmaf(dmu[j], w0[j * (H2 + 16) + c + 1], d1);
+          const float4 w = *reinterpret_cast<const float4*>(w0 + j * (H2 + 16) + c);
+          d0 = fmaf(dmu[j], w.x, d0); d1 = fmaf(dmu[j], w.y, d1); d2 = fmaf(dmu[j], w.z, d2); d3 = fmaf(dmu[j], w.w, d3);
         }
-        *reinterpret_cast<__nv_bfloat162*>(dz + c) =
-            __floats2bfloat162_rn(d0 * elu_grad_from_out(ha[c]), d1 * elu_grad_from_out(ha[c + 1]));
-        const float g0 = dV * w0[12 * (H2 + 16) + c], g1 = dV * w0[12 * (H2 + 16) + c + 1];
-        *reinterpret_cast<__nv_bfloat162*>(dz + H2 + c) =
-            __floats2bfloat162_rn(g0 * elu_grad_from_out(hc[c]), g1 * elu_grad_from_out(hc[c + 1]));
+        __nv_bfloat162 za = __floats2bfloat162_rn(d0 * elu_grad_from_out(ha[c]), d1 * elu_grad_from_out(ha[c + 1]));
+        __nv_bfloat162 zb = __floats2bfloat162_rn(d2 * elu_grad_from_out(ha[c + 2]), d3 * elu_grad_from_out(ha[c + 3]));
+        *reinterpret_cast<uint2*>(dz + c) = make_uint2(*reinterpret_cast<uint32_t*>(&za), *reinterpret_cast<uint32_t*>(&zb));
+        const float4 wc = *reinterpret_cast<const float4*>(w0 + 12 * (H2 + 16) + c);
+        __nv_bfloat162 ca = __floats2bfloat162_rn(dV * wc.x * elu_grad_from_out(hc[c]), dV * wc.y * elu_grad_from_out(hc[c + 1]));
+        __nv_bfloat162 cb = __floats2bfloat162_rn(dV * wc.z * elu_grad_from_out(hc[c + 2]), dV * wc.w * elu_grad_from_out(hc[c + 3]));
+        *reinterpret_cast<uint2*>(dz + H2 + c) = make_uint2(*reinterpret_cast<uint32_t*>(&ca), *reinterpret_cast<uint32_t*>(&cb));
       }
     }
   }
   __syncthreads();
   // block partial of the head/log-std gradients (rows in order)
   float* out = a.part + (size_t)blockIdx.x * HP;
-  for (int e = threadIdx.x; e < 13 * H2; e += blockDim.x) {
+  for (int e2 = threadIdx.x; e2 < 13 * H2 / 2; e2 += blockDim.x) {
+    const int e = 2 * e2;
     const int j = e / H2, k = e - j * H2;
     const int col = j < 12 ? k : H2 + k;
-    float acc = 0.0f;
-    for (int rr = 0; rr < nrows; ++rr) acc = fmaf(sdy[rr * 13 + j], __bfloat162float(sH[rr * SHLD + col]), acc);
-    out[j < 12 ? e : 12 * H2 + 12 + k] = acc;
+    float acc0 = 0.0f, acc1 = 0.0f;
+    for (int rr = 0; rr < nrows; ++rr) {
+      const float dy = sdy[rr * 13 + j];
+      const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sH + rr * SHLD + col));
+      acc0 = fmaf(dy, h.x, acc0);
+      acc1 = fmaf(dy, h.y, acc1);
+    }
+    const int o = j < 12 ? e : 12 * H2 + 12 + k;
+    out[o] = acc0;
+    out[o + 1] = acc1;
   }
   if (threadIdx.x < 13) {
     float sb = 0.0f;
@@ -529,37 +545,9 @@ void launch_gather(const GatherArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ Alg. 1 + Adam
-// step_f = {apply, alpha, bias-correction1, bias-correction2}; iteration accumulators in iter_acc
-__global__ void k_alg1_prep(const float* payload, DevScalars* sc, float kl_target, int world, float b1, float b2,
-                            float* step_f) {
-  const float W = (float)world;
-  const float kl = payload[0] / W;
-  const bool bad = payload[4] > 0.0f || !isfinite(kl);
-  float* acc = step_f + 4;  // iteration accumulators [surr, vloss, kl, clip, count]
-  if (bad) {
-    sc->nonfinite_skips += 1;
-    step_f[0] = 0.0f;
-    return;
-  }
-  float alpha = sc->alpha;
-  if (kl > 2.0f * kl_target) alpha = fmaxf(1e-5f, alpha / 1.5f);
-  else if (kl < 0.5f * kl_target) alpha = fminf(1e-2f, 1.5f * alpha);
-  sc->alpha = alpha;
-  sc->kl_last = kl;
-  const int t = sc->adam_t + 1;
-  sc->adam_t = t;
-  sc->applied += 1;
-  step_f[0] = 1.0f;
-  step_f[1] = alpha;
-  step_f[2] = (float)(1.0 - pow((double)b1, (double)t));
-  step_f[3] = (float)(1.0 - pow((double)b2, (double)t));
-  acc[0] += payload[1] / W; acc[1] += payload[2] / W; acc[2] += kl; acc[3] += payload[3] / W; acc[4] += 1.0f;
-}
-void launch_alg1_prep(const float* payload, DevScalars* sc, float kl_target, int world, float b1, float b2,
-                      float* step_f, cudaStream_t st) {
-  k_alg1_prep<<<1, 1, 0, st>>>(payload, sc, kl_target, world, b1, b2, step_f);
-}
-
+// One kernel per minibatch m: thread 0 of every block evaluates Alg. 1 on the reduced KL of
+// the payload and the bias corrections (same inputs -> same values in every block); block 0 publishes
+// alpha/t into ring slot (m+1)&1 while every block reads slot m&1, so no block reads a value being written.
 __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, float th) {
   for (int s = 0; s < sh.nseg; ++s) {
     const Segment& g = sh.seg[s];
@@ -574,24 +562,55 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
   }
 }
 
-__global__ void k_adam(AdamArgs a, const float* step_f) {
-  if (step_f[0] == 0.0f) return;
-  const float alpha = step_f[1], bc1 = step_f[2], bc2 = step_f[3];
+__global__ void k_adam(AdamArgs a, const float* payload, float kl_target, int world, int m, float* acc) {
+  __shared__ float s_alpha, s_bc1, s_bc2;
+  __shared__ int s_apply;
+  if (threadIdx.x == 0) {
+    DevScalars* sc = a.sc;
+    const float W = (float)world;
+    const float kl = payload[0] / W;
+    const bool bad = payload[4] > 0.0f || !isfinite(kl);
+    float alpha = sc->alpha_ring[m & 1];
+    int t = sc->adamt_ring[m & 1];
+    if (!bad) {
+      if (kl > 2.0f * kl_target) alpha = fmaxf(1e-5f, alpha / 1.5f);
+      else if (kl < 0.5f * kl_target) alpha = fminf(1e-2f, 1.5f * alpha);
+      t = t + 1;
+    }
+    s_apply = bad ? 0 : 1;
+    s_alpha = alpha;
+    s_bc1 = (float)(1.0 - pow((double)a.b1, (double)t));
+    s_bc2 = (float)(1.0 - pow((double)a.b2, (double)t));
+    if (blockIdx.x == 0) {
+      sc->alpha_ring[(m + 1) & 1] = alpha;
+      sc->adamt_ring[(m + 1) & 1] = t;
+      if (bad) {
+        sc->nonfinite_skips += 1;
+      } else {
+        sc->applied += 1;
+        sc->kl_last = kl;
+        acc[0] += payload[1] / W; acc[1] += payload[2] / W; acc[2] += kl; acc[3] += payload[3] / W; acc[4] += 1.0f;
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_apply) return;
+  const float alpha = s_alpha, bc1 = s_bc1, bc2 = s_bc2;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.sh.P; i += (long long)gridDim.x * blockDim.x) {
     const float g = a.grad[i] * a.inv_world;
-    const float m = a.b1 * a.m[i] + (1.0f - a.b1) * g;
+    const float mm = a.b1 * a.m[i] + (1.0f - a.b1) * g;
     const float v = a.b2 * a.v[i] + (1.0f - a.b2) * g * g;
-    a.m[i] = m;
+    a.m[i] = mm;
     a.v[i] = v;
-    const float mh = m / bc1, vh = v / bc2;
+    const float mh = mm / bc1, vh = v / bc2;
     const float th = a.theta[i] - alpha * mh / (sqrtf(vh) + a.eps);
     a.theta[i] = th;
     write_shadow(a.sh, i, th);
   }
 }
-void launch_adam(const AdamArgs& a, const float* step_f, cudaStream_t st) {
+void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc, cudaStream_t st) {
   int nb = (int)min((a.sh.P + 255) / 256, 148LL * 8);
-  k_adam<<<nb, 256, 0, st>>>(a, step_f);
+  k_adam<<<nb, 256, 0, st>>>(a, payload, kl_target, world, m, acc);
 }
 
 __global__ void k_sync_shadow(ShadowArgs sh, const float* theta) {
@@ -608,7 +627,7 @@ __global__ void k_iter_begin(DevScalars* sc, float* logstd_old, const float* log
   const int j = threadIdx.x;
   if (j < 12) logstd_old[j] = logstd[j];
   if (j < 8) iter_acc[j] = 0.0f;
-  (void)sc;
+  if (j == 0) { sc->alpha_ring[0] = sc->alpha; sc->adamt_ring[0] = sc->adam_t; }
 }
 void launch_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, cudaStream_t st) {
   k_iter_begin<<<1, 32, 0, st>>>(sc, logstd_old, logstd, iter_acc);
@@ -625,6 +644,8 @@ __global__ void k_iter_end(IterEndArgs a, const float* acc) {
   __syncthreads();
   if (threadIdx.x == 0) {
     DevScalars* sc = a.sc;
+    sc->alpha = sc->alpha_ring[a.n_mb & 1];
+    sc->adam_t = sc->adamt_ring[a.n_mb & 1];
     if (a.stats) {
       lg_update_stats_dev* s = reinterpret_cast<lg_update_stats_dev*>(a.stats);
       const float n = fmaxf(acc[4], 1.0f);
