@@ -39,7 +39,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef LG_MBAR_MODE
+#define LG_MBAR_MODE 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if LG_MBAR_MODE == 0
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
@@ -48,6 +52,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680));
+#elif LG_MBAR_MODE == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity));
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity));
+#endif
 }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
   asm volatile(
@@ -223,6 +246,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
           const int k0 = (kb0 + kb) * C::BK;
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
+          if (args.probe & 2) { mbar_arrive(&full[stage]); if (++stage == C::STAGES) { stage = 0; phase ^= 1u; } continue; }
           mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           if (!A_MN) {
             tma_load_2d(tmA, &full[stage], a, k0, tc.m0);
@@ -266,6 +290,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (args.probe & 1) { mbar_arrive(&empty[stage]); if (++stage == C::STAGES) { stage = 0; phase ^= 1u; } continue; }
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k) {
@@ -472,8 +497,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   static_assert(128 * RLD * 4 <= C::STAGES * (C::A_BYTES + C::B_BYTES), "reduction buffer must fit the ring");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t S = gridDim.x, split = cluster_rank();
-  const TileCoord tc = decode(args, blockIdx.y, args.m_tiles, BN);
+  const uint32_t S = gridDim.x, crank = cluster_rank();  // S = cluster size (splits reduced on chip)
+  const int G = out.G;                                   // cluster groups per tile (reduced through L2)
+  const int tile = blockIdx.y / G, grp = blockIdx.y - tile * G;
+  const uint32_t split = (uint32_t)grp * S + crank;
+  const TileCoord tc = decode(args, tile, args.m_tiles, BN);
   const bool bias_col = tc.ntile == 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -508,6 +536,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
         const int k0 = (kb0 + kb) * C::BK;
         uint8_t* a = sA + stage * C::A_BYTES;
         uint8_t* b = sB + stage * C::B_BYTES;
+        if (args.probe & 2) { mbar_arrive(&full[stage]); if (++stage == C::STAGES) { stage = 0; phase ^= 1u; } continue; }
         mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
         tma_load_2d(tmA, &full[stage], a, tc.m0, k0);
         tma_load_2d(tmA, &full[stage], a + 8192, tc.m0 + 64, k0);
@@ -526,6 +555,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (args.probe & 1) { mbar_arrive(&empty[stage]); if (++stage == C::STAGES) { stage = 0; phase ^= 1u; } continue; }
         const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
         for (int k = 0; k < C::BK / 16; ++k) {
@@ -580,26 +610,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // every CTA's partial is in its shared memory
-  // cluster-wide reduction: rows i = split, split + S, ...; splits summed in order 0..S-1
+  // level 1 (on chip): rows i = crank, crank + S, ...; the S splits of the cluster summed in order 0..S-1.
+  // level 2 (G > 1): each group writes its cluster sum to an L2-resident partial buffer; the last group to
+  // arrive at a row slice (per-slice counter) sums the G partials in group order 0..G-1 -- deterministic.
   const int rows_valid = min(128, args.M - tc.m0);
   const int cols_valid = min(BN, out.cols - tc.n0);
   constexpr int PER = BN / 4 + 1;  // float4 column groups + the bias group
-  for (int idx = threadIdx.x; idx < 128 * PER; idx += blockDim.x) {
-    const int ii = idx / PER, g = idx - ii * PER;
-    const int i = ii * (int)S + (int)split;
-    if (i >= rows_valid) continue;
+  constexpr int PLD = BN + 4;      // fp32 row stride of a level-2 partial
+  auto emit = [&](int i, int g, float4 v) {
     const bool isb = g == BN / 4;
     const int c = 4 * g;
-    if (isb ? !bias_col : c >= cols_valid) continue;
-    const float* loc = red + i * RLD + c;
-    float4 vs[16];
-#pragma unroll
-    for (uint32_t s = 0; s < 16; ++s)
-      if (s < S) vs[s] = ld_dsmem4(loc, s);
-    float4 v = vs[0];
-#pragma unroll
-    for (uint32_t s = 1; s < 16; ++s)
-      if (s < S) { v.x = v.x + vs[s].x; v.y = v.y + vs[s].y; v.z = v.z + vs[s].z; v.w = v.w + vs[s].w; }
     int zz = tc.z, rr = tc.m0 + i;
     if (out.row_split > 0 && rr >= out.row_split) { zz = 1; rr -= out.row_split; }
     if (isb) {
@@ -614,6 +634,56 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
           dst[k] = vv[k];
           if (!isfinite(vv[k])) atomicAdd(out.payload + 4, 1.0f);
         }
+    }
+  };
+  float* part_tile = out.part + (size_t)tile * G * 128 * PLD;
+  for (int idx = threadIdx.x; idx < 128 * PER; idx += blockDim.x) {
+    const int ii = idx / PER, g = idx - ii * PER;
+    const int i = ii * (int)S + (int)crank;
+    if (i >= rows_valid) continue;
+    const bool isb = g == BN / 4;
+    const int c = 4 * g;
+    if (isb ? !bias_col : c >= cols_valid) continue;
+    const float* loc = red + i * RLD + c;
+    float4 vs[16];
+#pragma unroll
+    for (uint32_t s = 0; s < 16; ++s)
+      if (s < S) vs[s] = ld_dsmem4(loc, s);
+    float4 v = vs[0];
+#pragma unroll
+    for (uint32_t s = 1; s < 16; ++s)
+      if (s < S) { v.x = v.x + vs[s].x; v.y = v.y + vs[s].y; v.z = v.z + vs[s].z; v.w = v.w + vs[s].w; }
+    if (G == 1) emit(i, g, v);
+    else __stcg(reinterpret_cast<float4*>(part_tile + ((size_t)grp * 128 + i) * PLD + c), v);
+  }
+  if (G > 1) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* cnt = out.cnt + tile * (int)S + (int)crank;
+      const int old = atomicAdd(cnt, 1);
+      s_last = old == G - 1;
+      if (old == G - 1) *cnt = 0;  // every group of this launch has arrived: re-arm for the next launch
+      __threadfence();
+    }
+    __syncthreads();
+    if (s_last) {
+      for (int idx = threadIdx.x; idx < 128 * PER; idx += blockDim.x) {
+        const int ii = idx / PER, g = idx - ii * PER;
+        const int i = ii * (int)S + (int)crank;
+        if (i >= rows_valid) continue;
+        const bool isb = g == BN / 4;
+        const int c = 4 * g;
+        if (isb ? !bias_col : c >= cols_valid) continue;
+        const float* src = part_tile + (size_t)i * PLD + c;
+        float4 v = __ldcg(reinterpret_cast<const float4*>(src));
+        for (int q = 1; q < G; ++q) {
+          const float4 w = __ldcg(reinterpret_cast<const float4*>(src + (size_t)q * 128 * PLD));
+          v.x = v.x + w.x; v.y = v.y + w.y; v.z = v.z + w.z; v.w = v.w + w.w;
+        }
+        emit(i, g, v);
+      }
     }
   }
   cluster_sync_all();  // keep shared memory alive until every CTA has read it
@@ -697,7 +767,7 @@ static cudaError_t launch_dw_bn(const GemmArgs& a, const DwOut& o, int S, cudaSt
   }
   const int tiles = a.nz * a.m_tiles * a.n_tiles;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(S, tiles, 1);
+  cfg.gridDim = dim3(S, tiles * o.G, 1);
   cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
@@ -709,6 +779,36 @@ static cudaError_t launch_dw_bn(const GemmArgs& a, const DwOut& o, int S, cudaSt
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_gemm_dw<BN>, a, o);
+}
+
+template <int BN>
+static int dw_clusters_bn(int S) {
+  using C = DwCfg<BN>;
+  if (cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess) return 0;
+  if (cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(S, 1, 1);
+  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_gemm_dw<BN>, &cfg) != cudaSuccess) return 0;
+  return n;
+}
+
+int dw_max_active_clusters(int bn, int S) {
+  switch (bn) {
+    case 64: return dw_clusters_bn<64>(S);
+    case 128: return dw_clusters_bn<128>(S);
+    case 256: return dw_clusters_bn<256>(S);
+    default: return 0;
+  }
 }
 
 cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {

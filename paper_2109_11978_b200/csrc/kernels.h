@@ -59,6 +59,7 @@ struct GemmArgs {
   float* part;               // EPI 3: split-K partials [z][split][part_rows][part_ld] (bias column direct)
   long long part_zstride, part_sstride;
   int part_rows, part_ld, part_bias_col, bias_col;
+  int probe;                 // diagnostics only (tools/gemm_probe): bit0 = skip the MMAs, bit1 = skip the TMA loads
 };
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
@@ -71,9 +72,14 @@ struct DwOut {                 // canonical destinations of a weight-gradient GE
   int cols;                    // real input width (the W row length in the canonical vector)
   int row_split;               // layer 1: rows >= row_split belong to the critic (second net)
   float* payload;              // non-finite counter at payload[4]
+  int G;                       // cluster groups per output tile (level-2 reduction through L2 when > 1)
+  float* part;                 // G > 1: [tile][G][128][BN + 4] fp32 cluster sums
+  int* cnt;                    // G > 1: [tile][S] arrival counters, zero between launches
 };
-// split-K over a thread-block cluster of S CTAs (S <= 16) with the reduction in distributed shared memory
+// split-K over G thread-block clusters of S CTAs (S <= 16) per output tile: on-chip (DSMEM) reduction
+// inside a cluster, deterministic reduction of the G cluster sums through L2
 cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);
+int dw_max_active_clusters(int bn, int S);  // co-resident clusters of S CTAs (0 on failure)
 
 // ------------------------------------------------------------------ PPO kernels (ppo.cu)
 struct NetDims {

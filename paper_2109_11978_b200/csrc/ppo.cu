@@ -3,6 +3,8 @@
 // (§2.2, Table 3, Alg. 1; SPEC ppo/net.)
 // Memory-bound kernels: one thread (or warp) per row/env, coalesced along the contiguous dimension;
 // every cross-thread reduction uses a fixed tree order so results are run-to-run deterministic.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -11,311 +13,290 @@ namespace lg {
 constexpr float SIX_LN_2PI = 11.027262398456072f;
 constexpr float HALF_LN_2PI = 0.9189385332046727f;
 
-// ------------------------------------------------------------------ heads (4 threads per row)
-// A "quad" of 4 consecutive threads owns one row; member q holds the columns [qC, qC+C) (C = H2/4) of
-// the actor and of the critic half of H3. The 13 head dot products are reduced over the quad with two
-// xor-shuffles and the quad leader's sums are broadcast, so all members hold bit-identical mu and V.
-// The same head_fwd_quad serves the rollout (k_heads) and the update (k_loss_heads): the ratio of the
-// first minibatch of an iteration is therefore exactly 1.
-constexpr int MAXC = 32;  // H2 <= 128
+// ------------------------------------------------------------------ heads (one warp per row)
+// Lane l owns the H3 columns [4l, 4l+4) of the actor and of the critic half (H2 <= 128, a multiple of 32)
+// and keeps the matching head weights in registers. The 13 head dot products (12 action means + value)
+// are reduced over the warp by a 16-value butterfly (offsets 16, 8, 4, 2 halve the value set, offset 1
+// finishes), after which lanes 2v and 2v+1 both hold total v (bit-identical: a+b == b+a). Lane 2j then
+// owns action dimension j. The rollout (k_heads) and the update (k_loss_heads) use the same functions, so
+// the ratio of the first minibatch of an iteration is exactly 1.
+struct HeadRegs {
+  float wa[12][4];
+  float wc[4];
+};
 
-__device__ __forceinline__ int wpad_index(int j, int col, int H2) {
-  const int C = H2 >> 2, q = col / C, c = col - q * C;
-  return j * (H2 + 16) + q * (C + 4) + c;  // 4 column groups, padded to stay bank-conflict free
-}
-
-__device__ __forceinline__ float quad_sum(float v) {
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
-  v += __shfl_xor_sync(0xffffffffu, v, 2);
-  return __shfl_sync(0xffffffffu, v, (threadIdx.x & 31) & ~3);
-}
-
-// ha/hc: this member's C columns; sW: padded [13][H2+16] (row 12 = critic W4c); returns mu[12], V
-__device__ __forceinline__ void head_fwd_quad(const float* ha, const float* hc, int H2, int q, const float* sW,
-                                              const float* sb4a, float b4c, float* mu, float& V) {
-  const int C = H2 >> 2;
-  const float* w0 = sW + q * (C + 4);
+__device__ __forceinline__ void load_head_regs(const float* W4a, const float* W4c, int H2, int lane, HeadRegs& w) {
+  const int c0 = 4 * lane;
+  const bool on = c0 < H2;
 #pragma unroll
   for (int j = 0; j < 12; ++j) {
-    float p = 0.0f;
-#pragma unroll
-    for (int c = 0; c < MAXC; c += 4)
-      if (c < C) {
-        const float4 w = *reinterpret_cast<const float4*>(w0 + j * (H2 + 16) + c);
-        p = fmaf(w.x, ha[c], p); p = fmaf(w.y, ha[c + 1], p); p = fmaf(w.z, ha[c + 2], p); p = fmaf(w.w, ha[c + 3], p);
-      }
-    mu[j] = quad_sum(p) + sb4a[j];
+    const float4 v = on ? *reinterpret_cast<const float4*>(W4a + j * H2 + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    w.wa[j][0] = v.x; w.wa[j][1] = v.y; w.wa[j][2] = v.z; w.wa[j][3] = v.w;
   }
-  float pv = 0.0f;
-#pragma unroll
-  for (int c = 0; c < MAXC; c += 4)
-    if (c < C) {
-      const float4 w = *reinterpret_cast<const float4*>(w0 + 12 * (H2 + 16) + c);
-      pv = fmaf(w.x, hc[c], pv); pv = fmaf(w.y, hc[c + 1], pv); pv = fmaf(w.z, hc[c + 2], pv); pv = fmaf(w.w, hc[c + 3], pv);
-    }
-  V = quad_sum(pv) + b4c;
+  const float4 v = on ? *reinterpret_cast<const float4*>(W4c + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  w.wc[0] = v.x; w.wc[1] = v.y; w.wc[2] = v.z; w.wc[3] = v.w;
 }
 
-__device__ __forceinline__ float logp_gauss(const float* a, const float* mu, const float* ls) {
-  float s = 0.0f;
+// this lane's 4 actor and 4 critic columns of row `hrow` (zeros for lanes beyond H2)
+__device__ __forceinline__ void load_h3(const __nv_bfloat16* hrow, int H2, int lane, float* ha, float* hc) {
+  const int c0 = 4 * lane;
+  uint2 ua = make_uint2(0u, 0u), uc = make_uint2(0u, 0u);
+  if (c0 < H2) {
+    ua = *reinterpret_cast<const uint2*>(hrow + c0);
+    uc = *reinterpret_cast<const uint2*>(hrow + H2 + c0);
+  }
+  float2 t;
+  t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ua.x)); ha[0] = t.x; ha[1] = t.y;
+  t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ua.y)); ha[2] = t.x; ha[3] = t.y;
+  t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uc.x)); hc[0] = t.x; hc[1] = t.y;
+  t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uc.y)); hc[2] = t.x; hc[3] = t.y;
+}
+
+// returns, on lanes 2v and 2v+1, the warp total of head product v (v < 12: mu_v - b4a_v; v = 12: V - b4c)
+__device__ __forceinline__ float head_fwd_warp(const HeadRegs& w, const float* ha, const float* hc, int lane) {
+  float v[16];
 #pragma unroll
   for (int j = 0; j < 12; ++j) {
-    float z = (a[j] - mu[j]) * expf(-ls[j]);
-    s = s + (0.5f * z * z + ls[j]);
+    float p = w.wa[j][0] * ha[0];
+    p = fmaf(w.wa[j][1], ha[1], p);
+    p = fmaf(w.wa[j][2], ha[2], p);
+    v[j] = fmaf(w.wa[j][3], ha[3], p);
   }
-  return -s - SIX_LN_2PI;
-}
-
-__device__ __forceinline__ void load_head_weights(const float* W4a, const float* b4a, const float* W4c,
-                                                  const float* b4c, const float* ls, int H2, float* sW,
-                                                  float* sb4a, float* sls, float* sb4c) {
-  for (int k = threadIdx.x; k < 13 * H2; k += blockDim.x) {
-    const int j = k / H2, col = k - j * H2;
-    sW[wpad_index(j, col, H2)] = j < 12 ? W4a[k] : W4c[col];
+  {
+    float p = w.wc[0] * hc[0];
+    p = fmaf(w.wc[1], hc[1], p);
+    p = fmaf(w.wc[2], hc[2], p);
+    v[12] = fmaf(w.wc[3], hc[3], p);
   }
-  if (threadIdx.x < 12) { sb4a[threadIdx.x] = b4a[threadIdx.x]; sls[threadIdx.x] = ls[threadIdx.x]; }
-  if (threadIdx.x == 12) *sb4c = *b4c;
-}
-
-__device__ __forceinline__ void bf16_cols(const __nv_bfloat16* p, int C, float* f) {
+  v[13] = v[14] = v[15] = 0.0f;
 #pragma unroll
-  for (int c = 0; c < MAXC; c += 8) {
-    if (c < C) {
-      uint4 u = *reinterpret_cast<const uint4*>(p + c);
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  for (int half = 8, off = 16; half >= 1; half >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-        f[c + 2 * e] = t.x;
-        f[c + 2 * e + 1] = t.y;
-      }
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? v[i] : v[i + half];
+      const float keep = up ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
   }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-constexpr int HEAD_ROWS = 16;  // rows per 64-thread block
+// sum over the action-dimension lanes (2j, j < 12) of x; fixed butterfly order, result on every lane
+__device__ __forceinline__ float dim_sum(float x, int lane) {
+  float s = (lane < 24 && (lane & 1) == 0) ? x : 0.0f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
 
-__global__ void __launch_bounds__(64) k_heads(HeadArgs a) {
-  extern __shared__ float sh[];
+// log N(a | mu, exp(ls)) from the per-dimension lanes
+__device__ __forceinline__ float logp_warp(float a_j, float mu_j, float ls_j, int lane) {
+  const float z = (a_j - mu_j) * expf(-ls_j);
+  return -dim_sum(0.5f * z * z + ls_j, lane) - SIX_LN_2PI;
+}
+
+constexpr int HEAD_WARPS = 8;      // rollout heads: warps per block
+constexpr int HEAD_ROWS_PER_WARP = 4;
+
+__global__ void __launch_bounds__(HEAD_WARPS * 32) k_heads(HeadArgs a) {
   const int M = a.M_dev ? *a.M_dev : a.M;
-  if (blockIdx.x * HEAD_ROWS >= M) return;  // block-uniform, before any work (empty bootstrap launches)
-  const int H2 = a.nd.H2, C = H2 >> 2;
-  float* sW = sh;
-  float* sb4a = sW + 13 * (H2 + 16);
-  float* sls = sb4a + 12;
-  float* sb4c = sls + 12;
-  load_head_weights(a.W4a, a.b4a, a.W4c, a.b4c, a.logstd, H2, sW, sb4a, sls, sb4c);
-  __syncthreads();
-  const int q = threadIdx.x & 3;
-  const int r = blockIdx.x * HEAD_ROWS + (threadIdx.x >> 2);
-  const bool valid = r < M;
-  float ha[MAXC], hc[MAXC];
-  const __nv_bfloat16* hrow = a.H3 + (size_t)(valid ? r : 0) * 2 * H2;
-  bf16_cols(hrow + q * C, C, ha);
-  bf16_cols(hrow + H2 + q * C, C, hc);
-  float mu[12], V;
-  head_fwd_quad(ha, hc, H2, q, sW, sb4a, *sb4c, mu, V);
-  if (!valid || q != 0) return;
-  if (a.mode == 1) {  // value scatter (time-out bootstrap or V(o_T))
-    a.value[a.idx ? a.idx[r] : r] = V;
-    return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (blockIdx.x * HEAD_WARPS + warp) * HEAD_ROWS_PER_WARP;
+  if (r0 >= M) return;  // warp-uniform (empty bootstrap launches)
+  const int H2 = a.nd.H2;
+  HeadRegs w;
+  load_head_regs(a.W4a, a.W4c, H2, lane, w);
+  const int j = lane >> 1;  // this lane's head output (valid for j <= 12)
+  const float bias = j < 12 ? __ldg(a.b4a + j) : (j == 12 ? __ldg(a.b4c) : 0.0f);
+  const float ls = j < 12 ? __ldg(a.logstd + j) : 0.0f;
+  const int rend = min(r0 + HEAD_ROWS_PER_WARP, M);
+  for (int r = r0; r < rend; ++r) {
+    float ha[4], hc[4];
+    load_h3(a.H3 + (size_t)r * 2 * H2, H2, lane, ha, hc);
+    const float tot = head_fwd_warp(w, ha, hc, lane) + bias;  // lanes 2j: mu_j; lanes 24, 25: V
+    const float V = __shfl_sync(0xffffffffu, tot, 24);
+    const bool dl = lane < 24 && (lane & 1) == 0;               // dimension-owner lane
+    if (a.mode == 1) {  // value scatter (time-out bootstrap or V(o_T))
+      if (lane == 0) a.value[a.idx ? a.idx[r] : r] = V;
+      continue;
+    }
+    if (a.mode == 2) {
+      if (dl) a.mu[(size_t)r * 12 + j] = tot;
+      if (lane == 0) a.value[r] = V;
+      continue;
+    }
+    // act: a_j = mu_j + sigma_j eps_j, eps = Box-Muller pairs (2k, 2k+1) of the ACTION stream
+    float act = 0.0f;
+    if (dl) {
+      Rng rng{a.seed_lo, a.seed_hi};
+      const uint32_t g = (uint32_t)(a.rank * a.N + r);
+      const uint32_t ev = a.scalars->s_base + (uint32_t)a.t + 1u;
+      const U4 b = rng.block((uint32_t)(j >> 2), g, ev, TAG_ACTION);  // words 2k, 2k+1 (k = j/2) lie in block j/4
+      const int k2 = (j & ~1) & 3;
+      const uint32_t w0 = pick(b, (uint32_t)k2), w1 = pick(b, (uint32_t)k2 + 1u);
+      const float u1 = (float)((w0 >> 8) + 1u) * 0x1p-24f;
+      const float u2 = (float)(w1 >> 8) * 0x1p-24f;
+      const float rr = sqrtf(-2.0f * log_poly(u1));
+      float sn, cs;
+      sincos_poly(0x1.921fb6p2f * u2, sn, cs);
+      act = tot + expf(ls) * (rr * ((j & 1) ? sn : cs));
+    }
+    const float lp = logp_warp(act, tot, ls, lane);
+    const size_t o = (size_t)r * 12 + j;
+    if (dl) {
+      a.act[o] = act;
+      a.mu[o] = tot;
+      if (a.u_act) a.u_act[o] = act;
+      if (a.u_mu) a.u_mu[o] = tot;
+    }
+    if (lane == 0) {
+      a.logp[r] = lp;
+      a.value[r] = V;
+      if (a.u_logp) a.u_logp[r] = lp;
+      if (a.u_value) a.u_value[r] = V;
+    }
   }
-  if (a.mode == 2) {
-    for (int j = 0; j < 12; ++j) a.mu[(size_t)r * 12 + j] = mu[j];
-    a.value[r] = V;
-    return;
-  }
-  // act: a = mu + sigma * eps, eps = Box-Muller pairs (2k, 2k+1) of the ACTION stream
-  Rng rng{a.seed_lo, a.seed_hi};
-  const uint32_t g = (uint32_t)(a.rank * a.N + r);
-  const uint32_t ev = a.scalars->s_base + (uint32_t)a.t + 1u;
-  const U4 b0 = rng.block(0, g, ev, TAG_ACTION), b1 = rng.block(1, g, ev, TAG_ACTION), b2 = rng.block(2, g, ev, TAG_ACTION);
-  const uint32_t w[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
-  float act[12];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    const float u1 = (float)((w[2 * k] >> 8) + 1u) * 0x1p-24f;
-    const float u2 = (float)(w[2 * k + 1] >> 8) * 0x1p-24f;
-    const float rr = sqrtf(-2.0f * log_poly(u1));
-    float sn, cs;
-    sincos_poly(0x1.921fb6p2f * u2, sn, cs);
-    act[2 * k] = mu[2 * k] + expf(sls[2 * k]) * (rr * cs);
-    act[2 * k + 1] = mu[2 * k + 1] + expf(sls[2 * k + 1]) * (rr * sn);
-  }
-  const float lp = logp_gauss(act, mu, sls);
-  const size_t o = (size_t)r * 12;
-#pragma unroll
-  for (int j = 0; j < 12; ++j) {
-    a.act[o + j] = act[j];
-    a.mu[o + j] = mu[j];
-  }
-  a.logp[r] = lp;
-  a.value[r] = V;
-  if (a.u_act) for (int j = 0; j < 12; ++j) a.u_act[o + j] = act[j];
-  if (a.u_mu) for (int j = 0; j < 12; ++j) a.u_mu[o + j] = mu[j];
-  if (a.u_logp) a.u_logp[r] = lp;
-  if (a.u_value) a.u_value[r] = V;
 }
 
 void launch_heads(const HeadArgs& a, cudaStream_t st) {
-  int smem = (13 * (a.nd.H2 + 16) + 28) * 4;
-  k_heads<<<(a.M + HEAD_ROWS - 1) / HEAD_ROWS, HEAD_ROWS * 4, smem, st>>>(a);
+  const int rows_per_block = HEAD_WARPS * HEAD_ROWS_PER_WARP;
+  k_heads<<<(a.M + rows_per_block - 1) / rows_per_block, HEAD_WARPS * 32, 0, st>>>(a);
 }
 
 // ------------------------------------------------------------------ PPO loss head (fwd + bwd)
-// Block = 256 threads = 64 rows x 4 members. The block's H3 rows (contiguous in memory) are staged in
-// smem with coalesced 16-B loads; dmu/dV per row go to smem; the block then forms its partial of
-// dW4 = dY^T H3 column-wise (each thread a few output columns, rows summed in order).
-constexpr int LOSS_BLOCK = 64;
+// Warp per row (head_fwd_warp), rows strided over all warps of the grid (fixed assignment). Each lane keeps
+// its slice of the head/log-std gradients in registers (dW4a[12][4 cols], dW4c[4 cols]; lanes 2j: db4a_j,
+// dlogstd_j; lane 0: db4c and the loss statistics in fp64) summed over its warp's rows in order; the warps
+// of a block are then summed in warp order into the block partial (k_reduce_heads sums blocks in order).
+constexpr int LOSS_WARPS = 4;
+constexpr int LOSS_MAX_BLOCKS = 148 * 3;
 int loss_head_partial_floats(int H2) { return ((13 * H2 + 25) + 3) / 4 * 4; }
-int loss_blocks(int M) { return (M + LOSS_BLOCK - 1) / LOSS_BLOCK; }
+int loss_blocks(int M) { return std::max(1, std::min(LOSS_MAX_BLOCKS, (M + LOSS_WARPS - 1) / LOSS_WARPS)); }
 
 __device__ __forceinline__ float elu_grad_from_out(float h) { return h > 0.0f ? 1.0f : h + 1.0f; }
 
-__global__ void __launch_bounds__(256, 2) k_loss_heads(LossArgs a) {
-  extern __shared__ float sh[];
-  const int H2 = a.nd.H2, C = H2 >> 2, HP = a.HP;
-  const int SHLD = 2 * H2 + 8;  // bf16 row stride of the staged H3 tile
-  float* sW = sh;
-  float* sb4a = sW + 13 * (H2 + 16);
-  float* sls = sb4a + 12;
-  float* slso = sls + 12;
-  float* sb4c = slso + 12;
-  float* sdy = sb4c + 4;                       // [64][13] dmu | dV
-  float* sdl = sdy + LOSS_BLOCK * 13;          // [64][12] dlogstd per row
-  double* sst = reinterpret_cast<double*>(sdl + LOSS_BLOCK * 12);  // [64][5]
-  __nv_bfloat16* sH = reinterpret_cast<__nv_bfloat16*>(sst + LOSS_BLOCK * 5);  // [64][SHLD]
-  load_head_weights(a.W4a, a.b4a, a.W4c, a.b4c, a.logstd, H2, sW, sb4a, sls, sb4c);
-  if (threadIdx.x < 12) slso[threadIdx.x] = a.logstd_old[threadIdx.x];
-  const int row0 = blockIdx.x * LOSS_BLOCK;
-  const int nrows = min(LOSS_BLOCK, a.M - row0);
-  {  // stage H3 rows [row0, row0 + nrows) (contiguous) into smem
-    const int v_per_row = (2 * H2) / 8;
-    const uint4* src = reinterpret_cast<const uint4*>(a.H3 + (size_t)row0 * 2 * H2);
-    for (int k = threadIdx.x; k < nrows * v_per_row; k += blockDim.x) {
-      const int rr = k / v_per_row, cc = k - rr * v_per_row;
-      *reinterpret_cast<uint4*>(sH + rr * SHLD + cc * 8) = src[k];
-    }
-  }
-  __syncthreads();
-  const int q = threadIdx.x & 3, rl = threadIdx.x >> 2;
-  const int r = row0 + rl;
-  const bool valid = rl < nrows;
+__global__ void __launch_bounds__(LOSS_WARPS * 32, 3) k_loss_heads(LossArgs a) {
+  extern __shared__ float sacc[];  // [LOSS_WARPS][HP] warp partials, then [LOSS_WARPS][5] fp64 statistics
+  const int H2 = a.nd.H2, HP = a.HP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * LOSS_WARPS + warp, TW = gridDim.x * LOSS_WARPS;
+  HeadRegs w;
+  load_head_regs(a.W4a, a.W4c, H2, lane, w);
+  const int j = lane >> 1;
+  const bool dl = lane < 24 && (lane & 1) == 0;
+  const float bias = j < 12 ? __ldg(a.b4a + j) : (j == 12 ? __ldg(a.b4c) : 0.0f);
+  const float ls = j < 12 ? __ldg(a.logstd + j) : 0.0f;
+  const float lso = j < 12 ? __ldg(a.logstd_old + j) : 0.0f;
+  const float iv = expf(-2.0f * ls);
+  const float klc = ls - lso + expf(2.0f * lso) * (0.5f * iv) - 0.5f;  // KL terms independent of mu
   const float invM = 1.0f / (float)a.M;
-  float ha[MAXC], hc[MAXC];
+  float gWa[12][4], gWc[4];
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) {
-    ha[c] = c < C ? __bfloat162float(sH[rl * SHLD + q * C + c]) : 0.0f;
-    hc[c] = c < C ? __bfloat162float(sH[rl * SHLD + H2 + q * C + c]) : 0.0f;
-  }
-  float mu[12], V;
-  head_fwd_quad(ha, hc, H2, q, sW, sb4a, *sb4c, mu, V);
-  float dmu[12], dV = 0.0f;
-  if (valid) {
-    float act[12];
-#pragma unroll
-    for (int j = 0; j < 12; ++j) act[j] = __ldg(a.act + (size_t)r * 12 + j);
-    const float lp = logp_gauss(act, mu, sls);
-    const float ratio = expf(lp - __ldg(a.logp_old + r));
-    const float adv = __ldg(a.adv + r);
+  for (int jj = 0; jj < 12; ++jj) gWa[jj][0] = gWa[jj][1] = gWa[jj][2] = gWa[jj][3] = 0.0f;
+  gWc[0] = gWc[1] = gWc[2] = gWc[3] = 0.0f;
+  float gb = 0.0f, gls = 0.0f, gbv = 0.0f;           // lanes 2j: db4a_j, dlogstd_j; lane 0: db4c
+  double st0 = 0.0, st1 = 0.0, st2 = 0.0, st3 = 0.0, st4 = 0.0;
+  for (int r = gw; r < a.M; r += TW) {
+    float ha[4], hc[4];
+    load_h3(a.H3 + (size_t)r * 2 * H2, H2, lane, ha, hc);
+    const float act = dl ? __ldg(a.act + (size_t)r * 12 + j) : 0.0f;
+    const float muo = dl ? __ldg(a.mu_old + (size_t)r * 12 + j) : 0.0f;
+    const float lpo = __ldg(a.logp_old + r), adv = __ldg(a.adv + r), Vo = __ldg(a.V_old + r), ret = __ldg(a.ret + r);
+    const float tot = head_fwd_warp(w, ha, hc, lane) + bias;
+    const float V = __shfl_sync(0xffffffffu, tot, 24);
+    const float lp = logp_warp(act, tot, ls, lane);
+    // clipped surrogate (§2.2 / DESIGN.md §3.11); every lane evaluates the row scalars
+    const float ratio = expf(lp - lpo);
     const float s1 = ratio * adv;
     const float rc = fminf(fmaxf(ratio, 1.0f - a.clip), 1.0f + a.clip);
     const float s2 = rc * adv;
     const bool take1 = s1 <= s2;
     const bool inside = ratio >= 1.0f - a.clip && ratio <= 1.0f + a.clip;
     const float dLdlp = -(take1 ? adv : (inside ? adv : 0.0f)) * invM * ratio;
-    const float Vo = __ldg(a.V_old + r), ret = __ldg(a.ret + r);
     const float vc = Vo + fminf(fmaxf(V - Vo, -a.vclip), a.vclip);
     const float e1 = (V - ret) * (V - ret), e2 = (vc - ret) * (vc - ret);
     const bool take_u = e1 >= e2;
     const bool vin = fabsf(V - Vo) <= a.vclip;
-    dV = a.vf_coef * (take_u ? 2.0f * (V - ret) : (vin ? 2.0f * (vc - ret) : 0.0f)) * invM;
-    float kl = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 12; ++j) {
-      const float d = act[j] - mu[j];
-      const float iv = expf(-2.0f * sls[j]);
-      dmu[j] = dLdlp * d * iv;
-      const float dm = __ldg(a.mu_old + (size_t)r * 12 + j) - mu[j];
-      kl += sls[j] - slso[j] + (expf(2.0f * slso[j]) + dm * dm) * (0.5f * iv) - 0.5f;
-      if (q == 0) sdl[rl * 12 + j] = dLdlp * (d * d * iv - 1.0f);
+    const float dV = a.vf_coef * (take_u ? 2.0f * (V - ret) : (vin ? 2.0f * (vc - ret) : 0.0f)) * invM;
+    const float d = act - tot;
+    const float dmu = dLdlp * d * iv;
+    const float dm = muo - tot;
+    const float kl = dim_sum(klc + dm * dm * (0.5f * iv), lane);
+    if (dl) {
+      gb = gb + dmu;
+      gls = gls + dLdlp * (d * d * iv - 1.0f);
     }
-    if (q == 0) {
-      for (int j = 0; j < 12; ++j) sdy[rl * 13 + j] = dmu[j];
-      sdy[rl * 13 + 12] = dV;
+    if (lane == 0) {
+      gbv = gbv + dV;
       const double sv = (double)(take1 ? s1 : s2), vv = (double)(take_u ? e1 : e2), kv = (double)kl;
-      double* s = sst + rl * 5;
-      s[0] = sv; s[1] = vv; s[2] = kv;
-      s[3] = fabsf(ratio - 1.0f) > a.clip ? 1.0 : 0.0;
-      s[4] = (isfinite(sv) && isfinite(vv) && isfinite(kv)) ? 0.0 : 1.0;
+      st0 += sv; st1 += vv; st2 += kv;
+      st3 += fabsf(ratio - 1.0f) > a.clip ? 1.0 : 0.0;
+      st4 += (isfinite(sv) && isfinite(vv) && isfinite(kv)) ? 0.0 : 1.0;
     }
-    // dZ3 = dH3 * ELU'(H3) for this member's columns (actor, then critic)
-    const float* w0 = sW + q * (C + 4);
-    __nv_bfloat16* dz = a.dZ3 + (size_t)r * 2 * H2 + q * C;
+    // dH3 = W4a^T dmu (actor), dV w4c (critic); dZ3 = dH3 * ELU'(H3); dW4 += dY h
+    float dmuj[12];
 #pragma unroll
-    for (int c = 0; c < MAXC; c += 4) {
-      if (c < C) {
-        float d0 = 0.0f, d1 = 0.0f, d2 = 0.0f, d3 = 0.0f;
+    for (int jj = 0; jj < 12; ++jj) dmuj[jj] = __shfl_sync(0xffffffffu, dmu, 2 * jj);
+    float za[4], zc[4];
 #pragma unroll
-        for (int j = 0; j < 12; ++j) {
-          const float4 w = *reinterpret_cast<const float4*>(w0 + j * (H2 + 16) + c);
-          d0 = fmaf(dmu[j], w.x, d0); d1 = fmaf(dmu[j], w.y, d1); d2 = fmaf(dmu[j], w.z, d2); d3 = fmaf(dmu[j], w.w, d3);
-        }
-        __nv_bfloat162 za = __floats2bfloat162_rn(d0 * elu_grad_from_out(ha[c]), d1 * elu_grad_from_out(ha[c + 1]));
-        __nv_bfloat162 zb = __floats2bfloat162_rn(d2 * elu_grad_from_out(ha[c + 2]), d3 * elu_grad_from_out(ha[c + 3]));
-        *reinterpret_cast<uint2*>(dz + c) = make_uint2(*reinterpret_cast<uint32_t*>(&za), *reinterpret_cast<uint32_t*>(&zb));
-        const float4 wc = *reinterpret_cast<const float4*>(w0 + 12 * (H2 + 16) + c);
-        __nv_bfloat162 ca = __floats2bfloat162_rn(dV * wc.x * elu_grad_from_out(hc[c]), dV * wc.y * elu_grad_from_out(hc[c + 1]));
-        __nv_bfloat162 cb = __floats2bfloat162_rn(dV * wc.z * elu_grad_from_out(hc[c + 2]), dV * wc.w * elu_grad_from_out(hc[c + 3]));
-        *reinterpret_cast<uint2*>(dz + H2 + c) = make_uint2(*reinterpret_cast<uint32_t*>(&ca), *reinterpret_cast<uint32_t*>(&cb));
+    for (int e = 0; e < 4; ++e) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < 12; ++jj) {
+        acc = fmaf(dmuj[jj], w.wa[jj][e], acc);
+        gWa[jj][e] = fmaf(dmuj[jj], ha[e], gWa[jj][e]);
       }
+      za[e] = acc * elu_grad_from_out(ha[e]);
+      zc[e] = dV * w.wc[e] * elu_grad_from_out(hc[e]);
+      gWc[e] = fmaf(dV, hc[e], gWc[e]);
     }
+    if (4 * lane < H2) {
+      __nv_bfloat16* dz = a.dZ3 + (size_t)r * 2 * H2 + 4 * lane;
+      const __nv_bfloat162 a0 = __floats2bfloat162_rn(za[0], za[1]), a1 = __floats2bfloat162_rn(za[2], za[3]);
+      const __nv_bfloat162 c0 = __floats2bfloat162_rn(zc[0], zc[1]), c1 = __floats2bfloat162_rn(zc[2], zc[3]);
+      *reinterpret_cast<uint2*>(dz) = make_uint2(*reinterpret_cast<const uint32_t*>(&a0), *reinterpret_cast<const uint32_t*>(&a1));
+      *reinterpret_cast<uint2*>(dz + H2) = make_uint2(*reinterpret_cast<const uint32_t*>(&c0), *reinterpret_cast<const uint32_t*>(&c1));
+    }
+  }
+  // warp partials -> smem (partial layout: W4a [12][H2], b4a [12], W4c [H2], b4c, logstd [12])
+  float* my = sacc + warp * HP;
+  if (4 * lane < H2) {
+#pragma unroll
+    for (int jj = 0; jj < 12; ++jj)
+      *reinterpret_cast<float4*>(my + jj * H2 + 4 * lane) = make_float4(gWa[jj][0], gWa[jj][1], gWa[jj][2], gWa[jj][3]);
+    *reinterpret_cast<float4*>(my + 12 * H2 + 12 + 4 * lane) = make_float4(gWc[0], gWc[1], gWc[2], gWc[3]);
+  }
+  if (dl) { my[12 * H2 + j] = gb; my[13 * H2 + 13 + j] = gls; }
+  if (lane == 0) {
+    my[13 * H2 + 12] = gbv;
+    double* sd = reinterpret_cast<double*>(sacc + LOSS_WARPS * HP) + warp * 5;
+    sd[0] = st0; sd[1] = st1; sd[2] = st2; sd[3] = st3; sd[4] = st4;
   }
   __syncthreads();
-  // block partial of the head/log-std gradients (rows in order)
   float* out = a.part + (size_t)blockIdx.x * HP;
-  for (int e2 = threadIdx.x; e2 < 13 * H2 / 2; e2 += blockDim.x) {
-    const int e = 2 * e2;
-    const int j = e / H2, k = e - j * H2;
-    const int col = j < 12 ? k : H2 + k;
-    float acc0 = 0.0f, acc1 = 0.0f;
-    for (int rr = 0; rr < nrows; ++rr) {
-      const float dy = sdy[rr * 13 + j];
-      const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sH + rr * SHLD + col));
-      acc0 = fmaf(dy, h.x, acc0);
-      acc1 = fmaf(dy, h.y, acc1);
-    }
-    const int o = j < 12 ? e : 12 * H2 + 12 + k;
-    out[o] = acc0;
-    out[o + 1] = acc1;
+  for (int e = threadIdx.x; e < 13 * H2 + 25; e += blockDim.x) {
+    float t = sacc[e];
+#pragma unroll
+    for (int ww = 1; ww < LOSS_WARPS; ++ww) t = t + sacc[ww * HP + e];
+    out[e] = t;
   }
-  if (threadIdx.x < 13) {
-    float sb = 0.0f;
-    for (int rr = 0; rr < nrows; ++rr) sb = sb + sdy[rr * 13 + threadIdx.x];
-    out[threadIdx.x < 12 ? 12 * H2 + threadIdx.x : 13 * H2 + 12] = sb;
-  } else if (threadIdx.x >= 32 && threadIdx.x < 44) {
-    const int j = threadIdx.x - 32;
-    float sl = 0.0f;
-    for (int rr = 0; rr < nrows; ++rr) sl = sl + sdl[rr * 12 + j];
-    out[13 * H2 + 13 + j] = sl;
-  } else if (threadIdx.x >= 64 && threadIdx.x < 69) {
-    const int k = threadIdx.x - 64;
-    double s = 0.0;
-    for (int rr = 0; rr < nrows; ++rr) s += sst[rr * 5 + k];
-    a.spart[(size_t)blockIdx.x * 8 + k] = s;
+  if (threadIdx.x < 5) {
+    const double* sd = reinterpret_cast<const double*>(sacc + LOSS_WARPS * HP);
+    double t = sd[threadIdx.x];
+    for (int ww = 1; ww < LOSS_WARPS; ++ww) t += sd[ww * 5 + threadIdx.x];
+    a.spart[(size_t)blockIdx.x * 8 + threadIdx.x] = t;
   }
 }
 
 void launch_loss_heads(const LossArgs& a, cudaStream_t st) {
-  const int H2 = a.nd.H2;
-  const size_t smem = (13 * (H2 + 16) + 40 + LOSS_BLOCK * 25) * 4 + 16 + LOSS_BLOCK * 5 * 8 +
-                      (size_t)LOSS_BLOCK * (2 * H2 + 8) * 2 + 64;
+  const size_t smem = (size_t)LOSS_WARPS * a.HP * 4 + LOSS_WARPS * 5 * 8;
   static size_t set = 0;
   if (smem > set) {
     cudaFuncSetAttribute(k_loss_heads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  k_loss_heads<<<loss_blocks(a.M), 256, smem, st>>>(a);
+  k_loss_heads<<<loss_blocks(a.M), LOSS_WARPS * 32, smem, st>>>(a);
 }
 
 // sums over blocks (fixed order) -> canonical gradient of heads/log-std + stats payload.
