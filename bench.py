@@ -175,7 +175,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="rough", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-iters", type=int, default=3)
+    ap.add_argument("--profile-iters", type=int, default=3)  # >= 1 (the roofline needs the per-category times)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.workload]
@@ -266,7 +266,7 @@ def main():
             cats[k][1] += c
     ctx.profile(False)
     ctx.capture()
-    P = args.profile_iters
+    P = max(1, args.profile_iters)
     per_iter = {k: {"ms": v[0] / P, "launches": v[1] // P} for k, v in cats.items() if v[1]}
     alg = algorithmic(cfg, w)
     pk = peaks()

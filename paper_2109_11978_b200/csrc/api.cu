@@ -278,6 +278,7 @@ lg_status validate(const lg_config* c) {
   if (c->hidden[0] % 64 != 0 || c->hidden[1] % 64 != 0) return LG_ERR_SHAPE;  // K of the next layer in 64-blocks
   if (c->hidden[2] > 128) return LG_ERR_SHAPE;  // heads: <= 4 columns per lane (warp-per-row kernels)
   if (c->scan_nx < 0 || c->scan_ny < 0 || (c->scan_nx == 0) != (c->scan_ny == 0)) return LG_ERR_SHAPE;
+  if (48LL + (long long)c->scan_nx * c->scan_ny > 512) return LG_ERR_SHAPE;  // observation row <= 512 (gather)
   if (c->n_levels < 1 || c->n_cols < 1) return LG_ERR_RANGE;
   if (!(c->gamma > 0.f && c->gamma <= 1.f) || !(c->lam >= 0.f && c->lam <= 1.f)) return LG_ERR_RANGE;
   if (!(c->clip > 0.f) || !(c->vclip > 0.f) || !(c->kl_target > 0.f)) return LG_ERR_RANGE;

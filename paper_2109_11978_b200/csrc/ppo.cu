@@ -169,14 +169,14 @@ void launch_heads(const HeadArgs& a, cudaStream_t st) {
 // its slice of the head/log-std gradients in registers (dW4a[12][4 cols], dW4c[4 cols]; lanes 2j: db4a_j,
 // dlogstd_j; lane 0: db4c and the loss statistics in fp64) summed over its warp's rows in order; the warps
 // of a block are then summed in warp order into the block partial (k_reduce_heads sums blocks in order).
-constexpr int LOSS_WARPS = 4;
-constexpr int LOSS_MAX_BLOCKS = 148 * 3;
+constexpr int LOSS_WARPS = 12;       // one block per SM
+constexpr int LOSS_MAX_BLOCKS = 148;
 int loss_head_partial_floats(int H2) { return ((13 * H2 + 25) + 3) / 4 * 4; }
 int loss_blocks(int M) { return std::max(1, std::min(LOSS_MAX_BLOCKS, (M + LOSS_WARPS - 1) / LOSS_WARPS)); }
 
 __device__ __forceinline__ float elu_grad_from_out(float h) { return h > 0.0f ? 1.0f : h + 1.0f; }
 
-__global__ void __launch_bounds__(LOSS_WARPS * 32, 3) k_loss_heads(LossArgs a) {
+__global__ void __launch_bounds__(LOSS_WARPS * 32, 1) k_loss_heads(LossArgs a) {
   extern __shared__ float sacc[];  // [LOSS_WARPS][HP] warp partials, then [LOSS_WARPS][5] fp64 statistics
   const int H2 = a.nd.H2, HP = a.HP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -303,6 +303,7 @@ void launch_loss_heads(const LossArgs& a, cudaStream_t st) {
 // Block = 32 warps x 32 elements; warp w sums partial rows b = w, w+32, ... (in order), then lane-wise the
 // 32 warp sums are added in warp order: a fixed, run-to-run deterministic tree.
 constexpr int RH_WARPS = 32;
+constexpr int RH_UNROLL = 8;
 __global__ void __launch_bounds__(RH_WARPS * 32) k_reduce_heads(HeadReduceArgs a) {
   __shared__ float ssum[RH_WARPS][33];
   const int H2 = a.H2;
@@ -310,8 +311,20 @@ __global__ void __launch_bounds__(RH_WARPS * 32) k_reduce_heads(HeadReduceArgs a
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = blockIdx.x * 32 + lane;
   float s = 0.0f;
-  if (e < nval)
-    for (int b = warp; b < a.nblk; b += RH_WARPS) s = s + a.part[(size_t)b * a.HP + e];
+  if (e < nval) {
+    // partial rows b = warp, warp + 32, ... summed in order; loads issued RH_UNROLL at a time
+    for (int b0 = warp; b0 < a.nblk; b0 += RH_WARPS * RH_UNROLL) {
+      float v[RH_UNROLL];
+#pragma unroll
+      for (int u = 0; u < RH_UNROLL; ++u) {
+        const int b = b0 + u * RH_WARPS;
+        v[u] = b < a.nblk ? __ldg(a.part + (size_t)b * a.HP + e) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < RH_UNROLL; ++u)
+        if (b0 + u * RH_WARPS < a.nblk) s = s + v[u];
+    }
+  }
   ssum[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && e < nval) {
@@ -326,21 +339,29 @@ __global__ void __launch_bounds__(RH_WARPS * 32) k_reduce_heads(HeadReduceArgs a
     a.grad[dst] = t;
     if (!isfinite(t)) atomicAdd(&a.payload[4], 1.0f);
   }
-  if (blockIdx.x == 0 && warp == 1) {
+  if (blockIdx.x == 0 && warp >= 1 && warp <= 5) {  // loss statistics: warp 1 + k sums statistic k
+    const int k = warp - 1;
     const double invM = 1.0 / (double)a.M;
-    for (int k = 0; k < 5; ++k) {
-      double v = 0.0;
-      for (int b = lane; b < a.nblk; b += 32) v += a.spart[(size_t)b * 8 + k];
-      v = warp_sum_d(v);
-      if (lane == 0) {
-        if (k == 0) a.payload[1] = (float)(v * invM);       // surrogate mean
-        if (k == 1) a.payload[2] = (float)(v * invM);       // value loss mean
-        if (k == 2) a.payload[0] = (float)(v * invM);       // KL mean (Alg. 1)
-        if (k == 3) a.payload[3] = (float)(v * invM);       // clip fraction
-        if (k == 4 && v > 0.0) atomicAdd(&a.payload[4], (float)v);
+    double v = 0.0;
+    for (int b0 = lane; b0 < a.nblk; b0 += 32 * RH_UNROLL) {
+      double x[RH_UNROLL];
+#pragma unroll
+      for (int u = 0; u < RH_UNROLL; ++u) {
+        const int b = b0 + 32 * u;
+        x[u] = b < a.nblk ? a.spart[(size_t)b * 8 + k] : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < RH_UNROLL; ++u) v += x[u];
     }
-    if (lane == 0) a.payload[5] = 1.0f;                     // rank count (allreduce sums it)
+    v = warp_sum_d(v);
+    if (lane == 0) {
+      if (k == 0) a.payload[1] = (float)(v * invM);       // surrogate mean
+      if (k == 1) a.payload[2] = (float)(v * invM);       // value loss mean
+      if (k == 2) a.payload[0] = (float)(v * invM);       // KL mean (Alg. 1)
+      if (k == 3) a.payload[3] = (float)(v * invM);       // clip fraction
+      if (k == 4 && v > 0.0) atomicAdd(&a.payload[4], (float)v);
+      if (k == 0) a.payload[5] = 1.0f;                    // rank count (allreduce sums it)
+    }
   }
 }
 
@@ -499,30 +520,68 @@ __global__ void k_perm(PermArgs a) {
 void launch_perm(const PermArgs& a, cudaStream_t st) { k_perm<<<(a.B + 255) / 256, 256, 0, st>>>(a); }
 
 // ------------------------------------------------------------------ minibatch gather (warp per row)
-__global__ void k_gather(GatherArgs a) {
+constexpr int GATHER_ROWS = 4;  // rows per warp: the permutation loads and the row copies are all in flight together
+__global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= a.M) return;
-  const uint32_t b = a.idx ? (uint32_t)a.idx[warp] : a.perm[warp];
-  const uint32_t t = b / (uint32_t)a.N, i = b - t * (uint32_t)a.N;
-  const uint4* src = reinterpret_cast<const uint4*>(a.obs + ((size_t)t * a.N + i) * a.Dp);
-  uint4* dst = reinterpret_cast<uint4*>(a.X + (size_t)warp * a.Dp);
-  for (int q = lane; q < a.Dp / 8; q += 32) dst[q] = src[q];
-  if (lane < 12) {
-    a.o_act[(size_t)warp * 12 + lane] = a.act[(size_t)b * 12 + lane];
-    a.o_mu[(size_t)warp * 12 + lane] = a.mu[(size_t)b * 12 + lane];
-  } else if (lane == 12) {
-    a.o_logp[warp] = a.logp[b];
-  } else if (lane == 13) {
-    a.o_V[warp] = a.V[b];
-  } else if (lane == 14) {
-    a.o_adv[warp] = (float)(((double)a.A[b] - a.sc->adv_mean) * a.sc->adv_inv_std);
-  } else if (lane == 15) {
-    a.o_ret[warp] = a.R[b];
+  const int r0 = warp * GATHER_ROWS;
+  if (r0 >= a.M) return;
+  const int nr = min(GATHER_ROWS, a.M - r0);
+  uint32_t bl = 0;
+  if (lane < nr) bl = a.idx ? (uint32_t)a.idx[r0 + lane] : a.perm[r0 + lane];
+  uint32_t b[GATHER_ROWS];
+#pragma unroll
+  for (int k = 0; k < GATHER_ROWS; ++k) b[k] = __shfl_sync(0xffffffffu, bl, k);
+  const int nq = a.Dp / 8;  // 16-B chunks per row
+  uint4 v[GATHER_ROWS][2];
+#pragma unroll
+  for (int k = 0; k < GATHER_ROWS; ++k) {
+    const uint32_t t = b[k] / (uint32_t)a.N, i = b[k] - t * (uint32_t)a.N;
+    const uint4* src = reinterpret_cast<const uint4*>(a.obs + ((size_t)t * a.N + i) * a.Dp);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h;
+      if (k < nr && q < nq) v[k][h] = src[q];
+    }
+  }
+  // scalar fields: lane 16k + f handles field f (< 16) of row k (two rows per pass)
+  float sv[GATHER_ROWS / 2][2];
+#pragma unroll
+  for (int pss = 0; pss < GATHER_ROWS / 2; ++pss) {
+    const int k = 2 * pss + (lane >> 4), f = lane & 15;
+    const uint32_t bb = k == 2 * pss ? b[2 * pss] : b[2 * pss + 1];
+    sv[pss][0] = sv[pss][1] = 0.0f;
+    if (k < nr) {
+      if (f < 12) { sv[pss][0] = a.act[(size_t)bb * 12 + f]; sv[pss][1] = a.mu[(size_t)bb * 12 + f]; }
+      else if (f == 12) sv[pss][0] = a.logp[bb];
+      else if (f == 13) sv[pss][0] = a.V[bb];
+      else if (f == 14) sv[pss][0] = (float)(((double)a.A[bb] - a.sc->adv_mean) * a.sc->adv_inv_std);
+      else sv[pss][0] = a.R[bb];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < GATHER_ROWS; ++k) {
+    uint4* dst = reinterpret_cast<uint4*>(a.X + (size_t)(r0 + k) * a.Dp);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h;
+      if (k < nr && q < nq) dst[q] = v[k][h];
+    }
+  }
+#pragma unroll
+  for (int pss = 0; pss < GATHER_ROWS / 2; ++pss) {
+    const int k = 2 * pss + (lane >> 4), f = lane & 15;
+    if (k >= nr) continue;
+    const int w = r0 + k;
+    if (f < 12) { a.o_act[(size_t)w * 12 + f] = sv[pss][0]; a.o_mu[(size_t)w * 12 + f] = sv[pss][1]; }
+    else if (f == 12) a.o_logp[w] = sv[pss][0];
+    else if (f == 13) a.o_V[w] = sv[pss][0];
+    else if (f == 14) a.o_adv[w] = sv[pss][0];
+    else a.o_ret[w] = sv[pss][0];
   }
 }
 void launch_gather(const GatherArgs& a, cudaStream_t st) {
-  long long threads = (long long)a.M * 32;
-  k_gather<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a);
+  const long long warps = (a.M + GATHER_ROWS - 1) / GATHER_ROWS;
+  k_gather<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a);
 }
 
 // ------------------------------------------------------------------ Alg. 1 + Adam
@@ -534,8 +593,8 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
     const Segment& g = sh.seg[s];
     const long long n = (long long)g.rows * g.cols;
     if (i >= g.off && i < g.off + n) {
-      const long long l = i - g.off;
-      const int r = (int)(l / g.cols), c = (int)(l - (long long)r * g.cols);
+      const uint32_t l = (uint32_t)(i - g.off);
+      const int r = (int)(l / (uint32_t)g.cols), c = (int)(l - (uint32_t)r * (uint32_t)g.cols);
       if (g.kind == 0) reinterpret_cast<__nv_bfloat16*>(g.dst)[(size_t)r * g.dst_ld + c] = __float2bfloat16_rn(th);
       else reinterpret_cast<float*>(g.dst)[(size_t)r * g.dst_ld + c] = th;
       return;
@@ -543,9 +602,19 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
   }
 }
 
-__global__ void k_adam(AdamArgs a, const float* payload, float kl_target, int world, int m, float* acc) {
+constexpr int ADAM_PER_THREAD = 2;
+__global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, float kl_target, int world, int m,
+                                              float* acc) {
   __shared__ float s_alpha, s_bc1, s_bc2;
   __shared__ int s_apply;
+  // this thread's elements are loaded first, so their latency overlaps the Alg. 1 / bias-correction scalars
+  const long long i0 = (blockIdx.x * (long long)blockDim.x) * ADAM_PER_THREAD + threadIdx.x;
+  float g[ADAM_PER_THREAD], mo[ADAM_PER_THREAD], vo[ADAM_PER_THREAD], tho[ADAM_PER_THREAD];
+#pragma unroll
+  for (int u = 0; u < ADAM_PER_THREAD; ++u) {
+    const long long i = i0 + (long long)u * blockDim.x;
+    if (i < a.sh.P) { g[u] = a.grad[i]; mo[u] = a.m[i]; vo[u] = a.v[i]; tho[u] = a.theta[i]; }
+  }
   if (threadIdx.x == 0) {
     DevScalars* sc = a.sc;
     const float W = (float)world;
@@ -577,20 +646,24 @@ __global__ void k_adam(AdamArgs a, const float* payload, float kl_target, int wo
   __syncthreads();
   if (!s_apply) return;
   const float alpha = s_alpha, bc1 = s_bc1, bc2 = s_bc2;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.sh.P; i += (long long)gridDim.x * blockDim.x) {
-    const float g = a.grad[i] * a.inv_world;
-    const float mm = a.b1 * a.m[i] + (1.0f - a.b1) * g;
-    const float v = a.b2 * a.v[i] + (1.0f - a.b2) * g * g;
+#pragma unroll
+  for (int u = 0; u < ADAM_PER_THREAD; ++u) {
+    const long long i = i0 + (long long)u * blockDim.x;
+    if (i >= a.sh.P) break;
+    const float gg = g[u] * a.inv_world;
+    const float mm = a.b1 * mo[u] + (1.0f - a.b1) * gg;
+    const float v = a.b2 * vo[u] + (1.0f - a.b2) * gg * gg;
     a.m[i] = mm;
     a.v[i] = v;
     const float mh = mm / bc1, vh = v / bc2;
-    const float th = a.theta[i] - alpha * mh / (sqrtf(vh) + a.eps);
+    const float th = tho[u] - alpha * mh / (sqrtf(vh) + a.eps);
     a.theta[i] = th;
     write_shadow(a.sh, i, th);
   }
 }
 void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc, cudaStream_t st) {
-  int nb = (int)min((a.sh.P + 255) / 256, 148LL * 8);
+  const long long per_block = 256LL * ADAM_PER_THREAD;
+  const int nb = (int)((a.sh.P + per_block - 1) / per_block);
   k_adam<<<nb, 256, 0, st>>>(a, payload, kl_target, world, m, acc);
 }
 
