@@ -272,212 +272,350 @@ __global__ void __launch_bounds__(ENV_BLOCK) k_env_reset(EnvParams P, const uint
   rec.g = g; rec.word0 = 0u; rec.row = i;
 }
 
-__global__ void __launch_bounds__(ENV_BLOCK) k_env_step(EnvParams P, int t, const float* __restrict__ actions,
-                                                        float* __restrict__ rew_out,
-                                                        uint8_t* __restrict__ term_out, uint8_t* __restrict__ to_out,
-                                                        float* __restrict__ terms_out) {
+// ------------------------------------------------------------------ leg-parallel transition
+// k_env_step: a group of 4 consecutive lanes per env; lane l owns leg l (its 3 joints: targets, torques,
+// FK/Jacobian, contact force, joint accelerations, air time). The base state is replicated in the 4 lanes
+// and updated identically. Every sum the definition takes over legs or joints is formed in every lane of
+// the group from group shuffles, in the definition's order (legs 0..3, joints 0..11), so the result is
+// bit-identical to the sequential form (-fmad=false).
+struct Com {  // per-env common state (identical copy in every lane of the group)
+  float p[3], quat[4], v[3], w[3], cmd[3], mu, spawn[2];
+  uint32_t contact;
+  int32_t push_timer, ep_step, level, col;
+  uint32_t crossed;
+  float ep_return;
+};
+struct Leg {  // the lane's own leg
+  float q[3], qd[3], aprev[3], tair;
+};
+
+__device__ __forceinline__ void load_com(const uint32_t* __restrict__ S, int N, int i, Com& c) {
+  auto f = [&](int w) { return __uint_as_float(S[(size_t)w * N + i]); };
+  for (int k = 0; k < 3; ++k) { c.p[k] = f(S_P + k); c.v[k] = f(S_V + k); c.w[k] = f(S_W + k); c.cmd[k] = f(S_CMD + k); }
+  for (int k = 0; k < 4; ++k) c.quat[k] = f(S_QUAT + k);
+  c.mu = f(S_MU); c.spawn[0] = f(S_SPAWN); c.spawn[1] = f(S_SPAWN + 1);
+  c.contact = S[(size_t)S_CONTACT * N + i];
+  c.push_timer = (int32_t)S[(size_t)S_PUSH * N + i];
+  c.ep_step = (int32_t)S[(size_t)S_EPSTEP * N + i];
+  c.level = (int32_t)S[(size_t)S_LEVEL * N + i];
+  c.col = (int32_t)S[(size_t)S_COL * N + i];
+  c.crossed = S[(size_t)S_CROSSED * N + i];
+  c.ep_return = f(S_EPRET);
+}
+__device__ __forceinline__ void load_leg(const uint32_t* __restrict__ S, int N, int i, int l, Leg& g) {
+  auto f = [&](int w) { return __uint_as_float(S[(size_t)w * N + i]); };
+  for (int k = 0; k < 3; ++k) { g.q[k] = f(S_Q + 3 * l + k); g.qd[k] = f(S_QD + 3 * l + k); g.aprev[k] = f(S_APREV + 3 * l + k); }
+  g.tair = f(S_TAIR + l);
+}
+__device__ __forceinline__ void store_com(uint32_t* __restrict__ S, int N, int i, const Com& c) {
+  auto f = [&](int w, float v) { S[(size_t)w * N + i] = __float_as_uint(v); };
+  for (int k = 0; k < 3; ++k) { f(S_P + k, c.p[k]); f(S_V + k, c.v[k]); f(S_W + k, c.w[k]); f(S_CMD + k, c.cmd[k]); }
+  for (int k = 0; k < 4; ++k) f(S_QUAT + k, c.quat[k]);
+  f(S_MU, c.mu); f(S_SPAWN, c.spawn[0]); f(S_SPAWN + 1, c.spawn[1]);
+  S[(size_t)S_CONTACT * N + i] = c.contact;
+  S[(size_t)S_PUSH * N + i] = (uint32_t)c.push_timer;
+  S[(size_t)S_EPSTEP * N + i] = (uint32_t)c.ep_step;
+  S[(size_t)S_LEVEL * N + i] = (uint32_t)c.level;
+  S[(size_t)S_COL * N + i] = (uint32_t)c.col;
+  S[(size_t)S_CROSSED * N + i] = c.crossed;
+  f(S_EPRET, c.ep_return);
+}
+__device__ __forceinline__ void store_leg(uint32_t* __restrict__ S, int N, int i, int l, const Leg& g) {
+  auto f = [&](int w, float v) { S[(size_t)w * N + i] = __float_as_uint(v); };
+  for (int k = 0; k < 3; ++k) { f(S_Q + 3 * l + k, g.q[k]); f(S_QD + 3 * l + k, g.qd[k]); f(S_APREV + 3 * l + k, g.aprev[k]); }
+  f(S_TAIR + l, g.tair);
+}
+
+// reset (same draws as reset_env): common part in every lane, joints of the own leg
+__device__ void reset_group(const World& W, const Rng& rng, Com& c, Leg& g, int l, uint32_t gid, uint32_t ev) {
+  U4 b0 = rng.block(0, gid, ev, TAG_RESET), b1 = rng.block(1, gid, ev, TAG_RESET), b2 = rng.block(2, gid, ev, TAG_RESET),
+     b3 = rng.block(3, gid, ev, TAG_RESET), b4 = rng.block(4, gid, ev, TAG_RESET);
+  uint32_t wd[20] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y,
+                     b2.z, b2.w, b3.x, b3.y, b3.z, b3.w, b4.x, b4.y, b4.z, b4.w};
+  float x = ((float)c.level * 8.0f + 4.0f) + usym(1.0f, wd[0]);
+  float y = ((float)c.col * 8.0f + 4.0f) + usym(1.0f, wd[1]);
+  float psi = usym(0x1.921fb6p1f, wd[2]);
+  float sh, ch;
+  sincos_poly(0.5f * psi, sh, ch);
+  c.p[0] = x; c.p[1] = y; c.p[2] = h_plate(W, x, y) + 0.6f;
+  c.quat[0] = ch; c.quat[1] = 0.0f; c.quat[2] = 0.0f; c.quat[3] = sh;
+  for (int k = 0; k < 3; ++k) { c.v[k] = 0.0f; c.w[k] = 0.0f; }
+  c.mu = 0.5f + 0.75f * u01(wd[3]);
+  for (int k = 0; k < 3; ++k) c.cmd[k] = usym(1.0f, wd[4 + k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int j = 3 * l + k;
+    g.q[k] = c_qdef[j] + usym(0.05f, wd[7 + j]);
+    g.qd[k] = 0.0f;
+    g.aprev[k] = 0.0f;
+  }
+  g.tair = 0.0f;
+  c.contact = 0u; c.push_timer = 0; c.ep_step = 0; c.crossed = 0u;
+  c.spawn[0] = x; c.spawn[1] = y; c.ep_return = 0.0f;
+}
+
+// observation record: common part from lane 0 of the group, joint columns from every lane
+__device__ __forceinline__ void fill_rec_group(const Com& c, const Leg& g, int l, ObsRec& o) {
+  if (l == 0) {
+    Mat3 R = rot(c.quat);
+    float t3[3];
+    mtv(R, c.v, t3);
+    o.pro[0] = t3[0]; o.pro[1] = t3[1]; o.pro[2] = t3[2];
+    o.pro[3] = c.w[0]; o.pro[4] = c.w[1]; o.pro[5] = c.w[2];
+    o.pro[6] = -R.m[2][0]; o.pro[7] = -R.m[2][1]; o.pro[8] = -R.m[2][2];
+    o.pro[9] = c.cmd[0]; o.pro[10] = c.cmd[1]; o.pro[11] = c.cmd[2];
+    heading(R, o.c, o.s);
+    o.px = c.p[0]; o.py = c.p[1]; o.pz = c.p[2];
+  }
+  for (int k = 0; k < 3; ++k) {
+    o.pro[12 + 3 * l + k] = g.q[k];
+    o.pro[24 + 3 * l + k] = g.qd[k];
+    o.pro[36 + 3 * l + k] = g.aprev[k];
+  }
+}
+
+// ordered sum over the 12 joints (j = 3L + k) of a per-lane triple, identical in every lane of the group
+__device__ __forceinline__ float joint_sum(const float* x3, int gbase, unsigned gm) {
+  float s = 0.0f;
+#pragma unroll
+  for (int L = 0; L < 4; ++L)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s = s + __shfl_sync(gm, x3[k], gbase + L);
+  return s;
+}
+
+constexpr int STEP_THREADS = 128;  // 32 envs per block
+
+__global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, const float* __restrict__ actions,
+                                                            float* __restrict__ rew_out,
+                                                            uint8_t* __restrict__ term_out, uint8_t* __restrict__ to_out,
+                                                            float* __restrict__ terms_out) {
   World W{P.hf, P.R, P.C, P.inv_cell};
   Rng rng{P.seed_lo, P.seed_hi};
   const uint32_t ev = P.scalars->s_base + (uint32_t)t + 1u;
   const int N = P.N;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i < N;
-  if (active) {
-    St s;
-    load_state(P.state, N, i, s);
-    const uint32_t g = (uint32_t)(P.rank * N + i);
-    float a[12], qstar[12], tau[12], qdd[12];
-    const float* ap = actions + (size_t)i * 12;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = gt >> 2, l = gt & 3;
+  if (i >= N) return;  // whole groups leave together (4 | blockDim)
+  const int lane = threadIdx.x & 31, gbase = lane & ~3;
+  const unsigned gm = 0xFu << gbase;
+  Com c;
+  Leg g;
+  load_com(P.state, N, i, c);
+  load_leg(P.state, N, i, l, g);
+  const uint32_t gid = (uint32_t)(P.rank * N + i);
+  float a[3], qstar[3], tau[3], qdd[3];
+  const float* ap = actions + (size_t)i * 12 + 3 * l;
 #pragma unroll
-    for (int j = 0; j < 12; ++j) { a[j] = ap[j]; qstar[j] = c_qdef[j] + 0.5f * a[j]; }
-    if ((P.flags & F_PUSH) && s.push_timer >= 500) {
-      U4 pb = rng.block(0, g, ev, TAG_PUSH);
-      s.v[0] = s.v[0] + usym(1.0f, pb.x);
-      s.v[1] = s.v[1] + usym(1.0f, pb.y);
-      s.push_timer = 0;
-    }
-    float airsum = 0.0f;
-    int crash = 0;
-    for (int sub = 0; sub < 4; ++sub) {
-      Mat3 R = rot(s.quat);
-      float ww[3];
-      mv(R, s.w, ww);
+  for (int k = 0; k < 3; ++k) { a[k] = ap[k]; qstar[k] = c_qdef[3 * l + k] + 0.5f * a[k]; }
+  if ((P.flags & F_PUSH) && c.push_timer >= 500) {
+    U4 pb = rng.block(0, gid, ev, TAG_PUSH);
+    c.v[0] = c.v[0] + usym(1.0f, pb.x);
+    c.v[1] = c.v[1] + usym(1.0f, pb.y);
+    c.push_timer = 0;
+  }
+  float airsum = 0.0f;
+  int crash = 0;
+  for (int sub = 0; sub < 4; ++sub) {
+    Mat3 R = rot(c.quat);
+    float ww[3];
+    mv(R, c.w, ww);
 #pragma unroll
-      for (int j = 0; j < 12; ++j) tau[j] = clampf_(KP * (qstar[j] - s.q[j]) - KD * s.qd[j], -TAU_MAX, TAU_MAX);
-      float F[3] = {0.0f, 0.0f, 0.0f}, Tw[3] = {0.0f, 0.0f, 0.0f};
-      uint32_t contact = 0u;
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        float fb[3], J[3][3], r[3], pf[3], jq[3], rj[3], cr[3], vf[3];
-        leg_fk(l, &s.q[3 * l], L_S, fb, J);
-        mv(R, fb, r);
-        for (int k = 0; k < 3; ++k) pf[k] = s.p[k] + r[k];
-        const float* qdl = &s.qd[3 * l];
-        for (int k = 0; k < 3; ++k) jq[k] = (J[0][k] * qdl[0] + J[1][k] * qdl[1]) + J[2][k] * qdl[2];
-        cross3(ww, r, cr);
-        mv(R, jq, rj);
-        for (int k = 0; k < 3; ++k) vf[k] = (s.v[k] + cr[k]) + rj[k];
-        float delta = h_plate(W, pf[0], pf[1]) - pf[2];
-        float f[3] = {0.0f, 0.0f, 0.0f};
-        if (delta > 0.0f) {
-          float fn = fmaxf(0.0f, K_N * delta - C_N * vf[2]);
-          float vt = sqrtf(vf[0] * vf[0] + vf[1] * vf[1]);
-          float sc = vt > 0.0f ? fminf(C_T, (s.mu * fn) / vt) : 0.0f;
-          f[0] = -sc * vf[0];
-          f[1] = -sc * vf[1];
-          f[2] = fn;
-          contact |= (1u << l);
-        }
-        float fbb[3];
-        mtv(R, f, fbb);
-        float tc0 = dot3(J[0], fbb), tc1 = dot3(J[1], fbb), tc2 = dot3(J[2], fbb);
-        qdd[3 * l + 0] = ((tau[3 * l + 0] + tc0) - C_J * s.qd[3 * l + 0]) / J_J;
-        qdd[3 * l + 1] = ((tau[3 * l + 1] + tc1) - C_J * s.qd[3 * l + 1]) / J_J;
-        qdd[3 * l + 2] = ((tau[3 * l + 2] + tc2) - C_J * s.qd[3 * l + 2]) / J_J;
-        float rf[3];
-        cross3(r, f, rf);
-        for (int k = 0; k < 3; ++k) { F[k] = F[k] + f[k]; Tw[k] = Tw[k] + rf[k]; }
-      }
-      F[2] = F[2] - M_BASE * GRAV;
-      float tb[3], Iw[3], gy[3], wdot[3];
-      mtv(R, Tw, tb);
-      for (int k = 0; k < 3; ++k) Iw[k] = c_inertia[k] * s.w[k];
-      cross3(s.w, Iw, gy);
-      for (int k = 0; k < 3; ++k) wdot[k] = (tb[k] - gy[k]) / c_inertia[k];
-      for (int k = 0; k < 3; ++k) s.v[k] = s.v[k] + DT_SIM * (F[k] / M_BASE);
-      for (int k = 0; k < 3; ++k) s.w[k] = s.w[k] + DT_SIM * wdot[k];
-#pragma unroll
-      for (int j = 0; j < 12; ++j) s.qd[j] = s.qd[j] + DT_SIM * qdd[j];
-      for (int k = 0; k < 3; ++k) s.p[k] = s.p[k] + DT_SIM * s.v[k];
-#pragma unroll
-      for (int j = 0; j < 12; ++j) s.q[j] = s.q[j] + DT_SIM * s.qd[j];
-      {
-        float h = 0.5f * DT_SIM;
-        float w = s.quat[0], x = s.quat[1], y = s.quat[2], z = s.quat[3];
-        float o0 = s.w[0], o1 = s.w[1], o2 = s.w[2];
-        float w2 = w + h * (((-x * o0) - y * o1) - z * o2);
-        float x2 = x + h * ((w * o0 + y * o2) - z * o1);
-        float y2 = y + h * ((w * o1 + z * o0) - x * o2);
-        float z2 = z + h * ((w * o2 + x * o1) - y * o0);
-        float n = sqrtf(((w2 * w2 + x2 * x2) + y2 * y2) + z2 * z2);
-        s.quat[0] = w2 / n; s.quat[1] = x2 / n; s.quat[2] = y2 / n; s.quat[3] = z2 / n;
-      }
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        uint32_t cn = (contact >> l) & 1u, cp = (s.contact >> l) & 1u;
-        if (cn && !cp) { airsum = airsum + (s.tair[l] - 0.5f); s.tair[l] = 0.0f; }
-        else if (!cn) s.tair[l] = s.tair[l] + DT_SIM;
-      }
-      s.contact = contact;
-      if (s.p[2] - h_plate(W, s.p[0], s.p[1]) < R_B) crash = 1;
-    }
-    // knees (R9)
-    Mat3 R = rot(s.quat);
-    int n_c = 0;
-    for (int l = 0; l < 4; ++l) {
-      float kb[3], r[3];
-      leg_fk(l, &s.q[3 * l], 0.5f * L_S, kb, nullptr);
-      mv(R, kb, r);
-      float kx = s.p[0] + r[0], ky = s.p[1] + r[1], kz = s.p[2] + r[2];
-      if (h_plate(W, kx, ky) - kz > 0.0f) n_c = n_c + 1;
-    }
-    s.ep_step += 1;
-    s.push_timer += 1;
+    for (int k = 0; k < 3; ++k) tau[k] = clampf_(KP * (qstar[k] - g.q[k]) - KD * g.qd[k], -TAU_MAX, TAU_MAX);
+    float f[3] = {0.0f, 0.0f, 0.0f}, rf[3];
+    bool touch;
     {
-      float x0 = (float)s.level * 8.0f, y0 = (float)s.col * 8.0f;
-      if (s.p[0] < x0 || s.p[0] >= x0 + 8.0f || s.p[1] < y0 || s.p[1] >= y0 + 8.0f) s.crossed = 1u;
-    }
-    bool finite = true;
-    for (int k = 0; k < 3; ++k) finite = finite && isfinite(s.p[k]) && isfinite(s.v[k]) && isfinite(s.w[k]);
-    for (int k = 0; k < 4; ++k) finite = finite && isfinite(s.quat[k]);
-    for (int j = 0; j < 12; ++j) finite = finite && isfinite(s.q[j]) && isfinite(s.qd[j]);
-    // reward
-    float rt[9];
-    {
-      float c, sn, wv[3];
-      heading(R, c, sn);
-      float vh0 = c * s.v[0] + sn * s.v[1];
-      float vh1 = -sn * s.v[0] + c * s.v[1];
-      float vh2 = s.v[2];
-      mv(R, s.w, wv);
-      float wh0 = c * wv[0] + sn * wv[1];
-      float wh1 = -sn * wv[0] + c * wv[1];
-      float wh2 = wv[2];
-      float ex = s.cmd[0] - vh0, ey = s.cmd[1] - vh1, ez = s.cmd[2] - wh2;
-      rt[0] = (1.0f * DT) * exp_poly(-((ex * ex + ey * ey) / 0.25f));
-      rt[1] = (0.5f * DT) * exp_poly(-((ez * ez) / 0.25f));
-      rt[2] = (-4.0f * DT) * (vh2 * vh2);
-      rt[3] = (-0.05f * DT) * (wh0 * wh0 + wh1 * wh1);
-      float sa = 0.0f, sb = 0.0f, stq = 0.0f, sr = 0.0f;
-      for (int j = 0; j < 12; ++j) sa = sa + qdd[j] * qdd[j];
-      for (int j = 0; j < 12; ++j) sb = sb + s.qd[j] * s.qd[j];
-      rt[4] = (-0.001f * DT) * (sa + sb);
-      for (int j = 0; j < 12; ++j) stq = stq + tau[j] * tau[j];
-      rt[5] = (-0.00002f * DT) * stq;
-      for (int j = 0; j < 12; ++j) {
-        float qprev = c_qdef[j] + 0.5f * s.aprev[j];
-        float d = (qstar[j] - qprev) / DT;
-        sr = sr + d * d;
+      float fb[3], J[3][3], r[3], pf[3], jq[3], rj[3], cr[3], vf[3];
+      leg_fk(l, g.q, L_S, fb, J);
+      mv(R, fb, r);
+      for (int k = 0; k < 3; ++k) pf[k] = c.p[k] + r[k];
+      for (int k = 0; k < 3; ++k) jq[k] = (J[0][k] * g.qd[0] + J[1][k] * g.qd[1]) + J[2][k] * g.qd[2];
+      cross3(ww, r, cr);
+      mv(R, jq, rj);
+      for (int k = 0; k < 3; ++k) vf[k] = (c.v[k] + cr[k]) + rj[k];
+      float delta = h_plate(W, pf[0], pf[1]) - pf[2];
+      touch = delta > 0.0f;
+      if (touch) {
+        float fn = fmaxf(0.0f, K_N * delta - C_N * vf[2]);
+        float vt = sqrtf(vf[0] * vf[0] + vf[1] * vf[1]);
+        float sc = vt > 0.0f ? fminf(C_T, (c.mu * fn) / vt) : 0.0f;
+        f[0] = -sc * vf[0];
+        f[1] = -sc * vf[1];
+        f[2] = fn;
       }
-      rt[6] = (-0.25f * DT) * sr;
-      rt[7] = (-0.001f * DT) * (float)n_c;
-      rt[8] = (2.0f * DT) * airsum;
+      float fbb[3];
+      mtv(R, f, fbb);
+      float tc0 = dot3(J[0], fbb), tc1 = dot3(J[1], fbb), tc2 = dot3(J[2], fbb);
+      qdd[0] = ((tau[0] + tc0) - C_J * g.qd[0]) / J_J;
+      qdd[1] = ((tau[1] + tc1) - C_J * g.qd[1]) / J_J;
+      qdd[2] = ((tau[2] + tc2) - C_J * g.qd[2]) / J_J;
+      cross3(r, f, rf);
     }
-    float r = rt[0];
-    for (int k = 1; k < 9; ++k) r = r + rt[k];
-    if (!finite) { r = 0.0f; for (int k = 0; k < 9; ++k) rt[k] = 0.0f; }
-    s.ep_return = s.ep_return + r;
-    const bool terminated = crash || !finite;
-    const bool to = (s.ep_step >= 1000) && !terminated;
-    const bool done = terminated || to;
-    for (int j = 0; j < 12; ++j) s.aprev[j] = a[j];
-    const size_t ti = (size_t)t * N + i;
+    const uint32_t contact = (__ballot_sync(gm, touch) >> gbase) & 0xFu;
+    float F[3] = {0.0f, 0.0f, 0.0f}, Tw[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int L = 0; L < 4; ++L)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        F[k] = F[k] + __shfl_sync(gm, f[k], gbase + L);
+        Tw[k] = Tw[k] + __shfl_sync(gm, rf[k], gbase + L);
+      }
+    F[2] = F[2] - M_BASE * GRAV;
+    float tb[3], Iw[3], gy[3], wdot[3];
+    mtv(R, Tw, tb);
+    for (int k = 0; k < 3; ++k) Iw[k] = c_inertia[k] * c.w[k];
+    cross3(c.w, Iw, gy);
+    for (int k = 0; k < 3; ++k) wdot[k] = (tb[k] - gy[k]) / c_inertia[k];
+    for (int k = 0; k < 3; ++k) c.v[k] = c.v[k] + DT_SIM * (F[k] / M_BASE);
+    for (int k = 0; k < 3; ++k) c.w[k] = c.w[k] + DT_SIM * wdot[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g.qd[k] = g.qd[k] + DT_SIM * qdd[k];
+    for (int k = 0; k < 3; ++k) c.p[k] = c.p[k] + DT_SIM * c.v[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g.q[k] = g.q[k] + DT_SIM * g.qd[k];
+    {
+      float h = 0.5f * DT_SIM;
+      float w = c.quat[0], x = c.quat[1], y = c.quat[2], z = c.quat[3];
+      float o0 = c.w[0], o1 = c.w[1], o2 = c.w[2];
+      float w2 = w + h * (((-x * o0) - y * o1) - z * o2);
+      float x2 = x + h * ((w * o0 + y * o2) - z * o1);
+      float y2 = y + h * ((w * o1 + z * o0) - x * o2);
+      float z2 = z + h * ((w * o2 + x * o1) - y * o0);
+      float n = sqrtf(((w2 * w2 + x2 * x2) + y2 * y2) + z2 * z2);
+      c.quat[0] = w2 / n; c.quat[1] = x2 / n; c.quat[2] = y2 / n; c.quat[3] = z2 / n;
+    }
+    {
+      const uint32_t cn = (contact >> l) & 1u, cp = (c.contact >> l) & 1u;
+      const bool td = cn && !cp;
+      float term = 0.0f;
+      if (td) { term = g.tair - 0.5f; g.tair = 0.0f; }
+      else if (!cn) g.tair = g.tair + DT_SIM;
+      const uint32_t tds = (__ballot_sync(gm, td) >> gbase) & 0xFu;
+#pragma unroll
+      for (int L = 0; L < 4; ++L) {
+        const float tL = __shfl_sync(gm, term, gbase + L);
+        if ((tds >> L) & 1u) airsum = airsum + tL;
+      }
+    }
+    c.contact = contact;
+    if (c.p[2] - h_plate(W, c.p[0], c.p[1]) < R_B) crash = 1;
+  }
+  // knees (R9)
+  Mat3 R = rot(c.quat);
+  int n_c;
+  {
+    float kb[3], r[3];
+    leg_fk(l, g.q, 0.5f * L_S, kb, nullptr);
+    mv(R, kb, r);
+    float kx = c.p[0] + r[0], ky = c.p[1] + r[1], kz = c.p[2] + r[2];
+    const bool kin = h_plate(W, kx, ky) - kz > 0.0f;
+    n_c = __popc((__ballot_sync(gm, kin) >> gbase) & 0xFu);
+  }
+  c.ep_step += 1;
+  c.push_timer += 1;
+  {
+    float x0 = (float)c.level * 8.0f, y0 = (float)c.col * 8.0f;
+    if (c.p[0] < x0 || c.p[0] >= x0 + 8.0f || c.p[1] < y0 || c.p[1] >= y0 + 8.0f) c.crossed = 1u;
+  }
+  bool fin = true;
+  for (int k = 0; k < 3; ++k) fin = fin && isfinite(c.p[k]) && isfinite(c.v[k]) && isfinite(c.w[k]);
+  for (int k = 0; k < 4; ++k) fin = fin && isfinite(c.quat[k]);
+  for (int k = 0; k < 3; ++k) fin = fin && isfinite(g.q[k]) && isfinite(g.qd[k]);
+  const bool finite = ((__ballot_sync(gm, fin) >> gbase) & 0xFu) == 0xFu;
+  // reward
+  float rt[9];
+  {
+    float cc, sn, wv[3];
+    heading(R, cc, sn);
+    float vh0 = cc * c.v[0] + sn * c.v[1];
+    float vh1 = -sn * c.v[0] + cc * c.v[1];
+    float vh2 = c.v[2];
+    mv(R, c.w, wv);
+    float wh0 = cc * wv[0] + sn * wv[1];
+    float wh1 = -sn * wv[0] + cc * wv[1];
+    float wh2 = wv[2];
+    float ex = c.cmd[0] - vh0, ey = c.cmd[1] - vh1, ez = c.cmd[2] - wh2;
+    rt[0] = (1.0f * DT) * exp_poly(-((ex * ex + ey * ey) / 0.25f));
+    rt[1] = (0.5f * DT) * exp_poly(-((ez * ez) / 0.25f));
+    rt[2] = (-4.0f * DT) * (vh2 * vh2);
+    rt[3] = (-0.05f * DT) * (wh0 * wh0 + wh1 * wh1);
+    float x3[3];
+    for (int k = 0; k < 3; ++k) x3[k] = qdd[k] * qdd[k];
+    const float sa = joint_sum(x3, gbase, gm);
+    for (int k = 0; k < 3; ++k) x3[k] = g.qd[k] * g.qd[k];
+    const float sb = joint_sum(x3, gbase, gm);
+    rt[4] = (-0.001f * DT) * (sa + sb);
+    for (int k = 0; k < 3; ++k) x3[k] = tau[k] * tau[k];
+    rt[5] = (-0.00002f * DT) * joint_sum(x3, gbase, gm);
+    for (int k = 0; k < 3; ++k) {
+      float qprev = c_qdef[3 * l + k] + 0.5f * g.aprev[k];
+      float d = (qstar[k] - qprev) / DT;
+      x3[k] = d * d;
+    }
+    rt[6] = (-0.25f * DT) * joint_sum(x3, gbase, gm);
+    rt[7] = (-0.001f * DT) * (float)n_c;
+    rt[8] = (2.0f * DT) * airsum;
+  }
+  float r = rt[0];
+  for (int k = 1; k < 9; ++k) r = r + rt[k];
+  if (!finite) { r = 0.0f; for (int k = 0; k < 9; ++k) rt[k] = 0.0f; }
+  c.ep_return = c.ep_return + r;
+  const bool terminated = crash || !finite;
+  const bool to = (c.ep_step >= 1000) && !terminated;
+  const bool done = terminated || to;
+  for (int k = 0; k < 3; ++k) g.aprev[k] = a[k];
+  const size_t ti = (size_t)t * N + i;
+  if (l == 0) {
     P.reward[ti] = r;
     P.flags_out[ti] = (uint8_t)((terminated ? 1u : 0u) | (to ? 2u : 0u));
     P.boot[ti] = 0.0f;
     if (rew_out) rew_out[i] = r;
     if (term_out) term_out[i] = (uint8_t)terminated;
     if (to_out) to_out[i] = (uint8_t)to;
-    if (terms_out)
-      for (int k = 0; k < 9; ++k) terms_out[(size_t)i * 9 + k] = rt[k];
-    if (done) {
-      if (to && (P.flags & F_BOOTSTRAP)) {
-        int row = atomicAdd(&P.scalars->n_to, 1);
-        ObsRec& tr = reinterpret_cast<ObsRec*>(P.trecs)[row];
-        fill_obs_rec(s, tr);
-        tr.g = g; tr.word0 = 0u; tr.row = row;
-        P.term_idx[row] = i;
-      }
-      // episode statistics (stats only; float atomics)
-      atomicAdd(&P.scalars->ep_return_sum, s.ep_return);
-      atomicAdd(&P.scalars->ep_len_sum, (float)s.ep_step);
-      atomicAdd(&P.scalars->episodes, 1);
-      if (P.flags & F_CURRICULUM) {
-        int old = s.level;
-        if (s.crossed) {
-          s.level = s.level + 1;
-          if (s.level > P.n_levels - 1) {
-            uint32_t wrd = rng.block(0, g, ev, TAG_CURR).x;
-            s.level = (int32_t)(((uint64_t)wrd * (uint64_t)P.n_levels) >> 32);
-          }
-        } else {
-          float dx = s.p[0] - s.spawn[0], dy = s.p[1] - s.spawn[1];
-          float T = (float)s.ep_step * DT;
-          float hh = 0.5f * T;
-          if ((dx * dx + dy * dy) < (hh * hh) * (s.cmd[0] * s.cmd[0] + s.cmd[1] * s.cmd[1])) s.level = max(0, s.level - 1);
-        }
-        if (s.level > old) atomicAdd(&P.scalars->promotions, 1);
-        if (s.level < old) atomicAdd(&P.scalars->demotions, 1);
-      }
-      reset_env(W, rng, s, g, ev);
-    }
-    store_state(P.state, N, i, s);
-    ObsRec& rec = reinterpret_cast<ObsRec*>(P.recs)[i];
-    fill_obs_rec(s, rec);
-    rec.g = g;
-    rec.word0 = done ? (uint32_t)P.obs_dim : 0u;
-    rec.row = i;
   }
+  if (terms_out) {  // lane l writes terms l, l+4, l+8
+    for (int k = l; k < 9; k += 4) terms_out[(size_t)i * 9 + k] = rt[k];
+  }
+  if (done) {  // group-uniform
+    if (to && (P.flags & F_BOOTSTRAP)) {
+      int row = 0;
+      if (l == 0) row = atomicAdd(&P.scalars->n_to, 1);
+      row = __shfl_sync(gm, row, gbase);
+      ObsRec& tr = reinterpret_cast<ObsRec*>(P.trecs)[row];
+      fill_rec_group(c, g, l, tr);
+      if (l == 0) { tr.g = gid; tr.word0 = 0u; tr.row = row; P.term_idx[row] = i; }
+    }
+    if (l == 0) {  // episode statistics (stats only; float atomics)
+      atomicAdd(&P.scalars->ep_return_sum, c.ep_return);
+      atomicAdd(&P.scalars->ep_len_sum, (float)c.ep_step);
+      atomicAdd(&P.scalars->episodes, 1);
+    }
+    if (P.flags & F_CURRICULUM) {
+      int old = c.level;
+      if (c.crossed) {
+        c.level = c.level + 1;
+        if (c.level > P.n_levels - 1) {
+          uint32_t wrd = rng.block(0, gid, ev, TAG_CURR).x;
+          c.level = (int32_t)(((uint64_t)wrd * (uint64_t)P.n_levels) >> 32);
+        }
+      } else {
+        float dx = c.p[0] - c.spawn[0], dy = c.p[1] - c.spawn[1];
+        float T = (float)c.ep_step * DT;
+        float hh = 0.5f * T;
+        if ((dx * dx + dy * dy) < (hh * hh) * (c.cmd[0] * c.cmd[0] + c.cmd[1] * c.cmd[1])) c.level = max(0, c.level - 1);
+      }
+      if (l == 0) {
+        if (c.level > old) atomicAdd(&P.scalars->promotions, 1);
+        if (c.level < old) atomicAdd(&P.scalars->demotions, 1);
+      }
+    }
+    reset_group(W, rng, c, g, l, gid, ev);
+  }
+  if (l == 0) store_com(P.state, N, i, c);
+  store_leg(P.state, N, i, l, g);
+  ObsRec& rec = reinterpret_cast<ObsRec*>(P.recs)[i];
+  fill_rec_group(c, g, l, rec);
+  if (l == 0) { rec.g = gid; rec.word0 = done ? (uint32_t)P.obs_dim : 0u; rec.row = i; }
 }
 
 // standalone curriculum rule (DESIGN.md §3.7 step 9(ii))
@@ -529,8 +667,9 @@ void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* 
 }
 void launch_env_step(const EnvParams& P, int t, const float* actions, float* obs_f32, float* rew, uint8_t* term,
                      uint8_t* to, float* terms, cudaStream_t st) {
-  int nb = (P.N + ENV_BLOCK - 1) / ENV_BLOCK;
-  k_env_step<<<nb, ENV_BLOCK, 0, st>>>(P, t, actions, rew, term, to, terms);
+  const long long threads = 4LL * P.N;
+  k_env_step<<<(unsigned)((threads + STEP_THREADS - 1) / STEP_THREADS), STEP_THREADS, 0, st>>>(P, t, actions, rew, term,
+                                                                                               to, terms);
   launch_obs(P, t + 1, P.obs_out + (size_t)(t + 1) * P.N * P.obs_stride, obs_f32, (P.flags & F_BOOTSTRAP) ? 1 : 0,
              st);  // noise event s_base + t + 1
 }
