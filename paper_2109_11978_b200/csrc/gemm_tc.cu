@@ -157,7 +157,22 @@ struct GemmCfg {
   static constexpr int SMEM = FIXED + STAGES * (A_BYTES + B_BYTES);
 };
 
-__device__ __forceinline__ float elu_fast(float x) { return x > 0.0f ? x : __expf(x) - 1.0f; }
+// ELU(x) = x > 0 ? x : e^x - 1, with e^x = 2^(x log2 e) from ex2.approx.ftz (one MUFU op, no subnormal
+// rescaling path: the bf16 output cannot resolve e^x - 1 differences below 2^-126 anyway)
+__device__ __forceinline__ float ex2_ftz(float t) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(t));
+  return e;
+}
+__device__ __forceinline__ float elu_fast(float x) {
+  const float e = ex2_ftz(x * 1.4426950408889634f) - 1.0f;
+  return x > 0.0f ? x : e;
+}
+__device__ __forceinline__ float4 lds4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_u32(p)));
+  return v;
+}
 
 // write one thread's 128-byte row chunk (8 x 16 B) into a 32-row, 128-B-swizzled staging buffer
 __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const uint32_t* w32) {
@@ -388,7 +403,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
               for (int k = 0; k < 64; k += 4) {
                 const uint32_t* rr = k < 32 ? r0 : r1;
                 const int kk = k & 31;
-                const float4 b4 = *reinterpret_cast<const float4*>(bb + k);
+                const float4 b4 = lds4(bb + k);
                 __nv_bfloat162 o0 = __floats2bfloat162_rn(elu_fast(__uint_as_float(rr[kk]) + b4.x),
                                                           elu_fast(__uint_as_float(rr[kk + 1]) + b4.y));
                 __nv_bfloat162 o1 = __floats2bfloat162_rn(elu_fast(__uint_as_float(rr[kk + 2]) + b4.z),

@@ -171,7 +171,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&g_flush, 512u << 20));
   const char* which = argc > 1 ? argv[1] : "all";
   if (argc > 2 && !strcmp(argv[2], "noflush")) g_do_flush = false;
-  if (!strcmp(which, "one")) g_do_flush = false;
+  if (!strcmp(which, "one") || !strcmp(which, "onefwd")) g_do_flush = false;
   if (argc > 2 && !strcmp(argv[2], "batch")) { g_do_flush = false; g_batch = true; }
   printf("L2 flush between reps: %s\n", g_do_flush ? "yes" : "no");
   {
@@ -179,6 +179,11 @@ int main(int argc, char** argv) {
     float us0 = time_us([&] { k_empty<<<1, 32, 0, st>>>(nullptr); }, st);
     float us1 = time_us([&] { k_empty<<<148, 384, 200 * 1024, st>>>(nullptr); }, st);
     printf("empty kernel: 1x32 %.2f us, 148x384 with 200 KB smem %.2f us\n", us0, us1);
+  }
+  if (!strcmp(which, "onefwd") && argc >= 6) {  // one forward config: onefwd M N K bn (for ncu)
+    g_do_flush = false;
+    probe_fwd(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), st);
+    return 0;
   }
   if (!strcmp(which, "one") && argc >= 9) {  // one dW config: one Nout Nin K bn S G (for ncu)
     g_do_flush = false;
