@@ -71,12 +71,11 @@ Canon canon_of(const Dims& d) {
 int bn_for(int n) { return n >= 256 ? 256 : (n > 64 ? 128 : 64); }
 
 struct DwPlan {
-  int rows, N, bn, n_tiles, m_tiles, kb_total, tiles, CL, Gmax;
+  int rows, N, bn, n_tiles, m_tiles, kb_total, tiles, S, kb_per_split;
   size_t part_bytes, bytes;
 };
-// Weight-gradient GEMM plan (k_gemm_dw): 128 x bn output tiles; the minibatch (K) is split over CL x G CTAs
-// per tile -- clusters of CL <= 8 (portable, co-schedulable) reduced on chip, G groups reduced through L2.
-// Gmax fills the 148 SMs in one wave; lg_create lowers G to what the device co-schedules.
+// Weight-gradient GEMM plan (k_gemm_dw): 128 x bn output tiles; the minibatch (K) is split over S CTAs per
+// tile so that tiles * S fills the 148 SMs in one wave; the S fp32 partials are reduced through L2.
 DwPlan dw_plan(int rows, int N, int K, int nz) {
   DwPlan p;
   p.rows = rows; p.N = N;
@@ -85,10 +84,12 @@ DwPlan dw_plan(int rows, int N, int K, int nz) {
   p.m_tiles = (rows + 127) / 128;
   p.kb_total = (K + 63) / 64;
   p.tiles = p.n_tiles * p.m_tiles * nz;
-  p.CL = std::max(1, std::min(8, p.kb_total));
-  p.Gmax = std::max(1, std::min(p.kb_total / p.CL, 148 / (p.CL * p.tiles)));
-  p.part_bytes = p.Gmax > 1 ? al((size_t)p.tiles * p.Gmax * 128 * (p.bn + 4) * 4) : 0;
-  p.bytes = p.part_bytes + al((size_t)p.tiles * p.CL * 4);
+  // one wave of <= 148 CTAs, and >= 8 k-blocks per CTA (the fp32 partial costs ~3 k-blocks of traffic)
+  const int S = std::max(1, std::min(std::max(1, p.kb_total / 8), 148 / std::max(1, p.tiles)));
+  p.kb_per_split = (p.kb_total + S - 1) / S;
+  p.S = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.part_bytes = al((size_t)p.tiles * p.S * 128 * (p.bn + 20) * 4);
+  p.bytes = p.part_bytes + 256;  // + the grid-barrier counter
   return p;
 }
 
@@ -195,7 +196,6 @@ struct lg_ctx {
   // prebuilt launch descriptors
   std::vector<GemmArgs> l1_roll;  // per OBS slot 0..T
   GemmArgs l1_upd, l2, l3, l1_boot, l2_boot, l3_boot, l1_vt, dx3, dx2, dw3, dw2, dw1;
-  int dwG[3] = {1, 1, 1};  // runtime cluster groups of dw1..dw3 (<= plan Gmax, co-schedulable)
   EnvParams ep;
   ShadowArgs shadow;
   cudaGraph_t graph = nullptr;
@@ -449,12 +449,10 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   set_fwd_common(x3, d.Mmb, d.H1, d.H2, bn_for(d.H1), 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
   set_fwd_common(x2, d.Mmb, d.H0, d.H1, bn_for(d.H0), 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
   // ---- backward dW (A = dZ MN-major, B = activations MN-major), split-K over the minibatch
-  auto dw_setup = [&](GemmArgs& g, const DwPlan& p, int& G, int nz) {
-    const int fit = dw_max_active_clusters(p.bn, p.CL);
-    G = std::max(1, std::min(p.Gmax, fit / std::max(1, p.tiles)));
+  auto dw_setup = [&](GemmArgs& g, const DwPlan& p, int nz) {
     g.M = p.rows; g.N = p.N; g.M_dev = nullptr;
     g.kb_total = p.kb_total; g.n_tiles = p.n_tiles; g.n_splits = 1;
-    g.kb_per_split = (p.kb_total + p.CL * G - 1) / (p.CL * G);
+    g.kb_per_split = p.kb_per_split;
     g.m_tiles = p.m_tiles; g.nz = nz;
   };
   GemmArgs& w3 = ctx->dw3;
@@ -472,9 +470,9 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   }
   ok &= make_tmap_bf16(&w1.tmA[0], dZ1, Mr, 2 * d.H0, 2 * d.H0, 64);
   ok &= make_tmap_bf16(&w1.tmB[0], X, Mr, d.Dp, d.Dp, 64);
-  dw_setup(w3, L.dw3, ctx->dwG[2], 2);
-  dw_setup(w2, L.dw2, ctx->dwG[1], 2);
-  dw_setup(w1, L.dw1, ctx->dwG[0], 1);
+  dw_setup(w3, L.dw3, 2);
+  dw_setup(w2, L.dw2, 2);
+  dw_setup(w1, L.dw1, 1);
   if (!ok) {
     delete ctx;
     return LG_ERR_CUDA;
@@ -800,10 +798,11 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
   hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
   { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
   CKL();
-  auto dw = [&](const GemmArgs& g, const DwPlan& p, size_t koff, int G, int cols, const long long* woff,
+  auto dw = [&](const GemmArgs& g, const DwPlan& p, size_t koff, int cols, const long long* woff,
                 const long long* boff, int row_split) -> lg_status {
     DwOut o;
-    o.G = G;
+    memset(&o, 0, sizeof(o));
+    o.G = 1;
     o.part = at<float>(ctx->buf[LG_BUF_WORK], koff);
     o.cnt = at<int>(ctx->buf[LG_BUF_WORK], koff + p.part_bytes);
     o.grad = grad;
@@ -812,22 +811,22 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
     o.row_split = row_split;
     o.payload = ctx->payload;
     Scope sc_(ctx, LG_PROF_GEMM_DW);
-    cudaError_t e = launch_gemm_dw(p.bn, g, o, p.CL, ctx->st);
+    cudaError_t e = launch_gemm_dw(p.bn, g, o, p.S, ctx->st);
     if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm_dw: %s", cudaGetErrorString(e));
     return LG_OK;
   };
   // layer 3
-  if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, ctx->dwG[2], d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
+  if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
   GemmArgs x3 = ctx->dx3;
   x3.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x3, bn_for(d.H1), 2)) != LG_OK) return s;
   // layer 2
-  if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, ctx->dwG[1], d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
+  if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   GemmArgs x2 = ctx->dx2;
   x2.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x2, bn_for(d.H0), 2)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
-  if ((s = dw(ctx->dw1, L.dw1, L.k_dw1, ctx->dwG[0], d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
+  if ((s = dw(ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
   return LG_OK;
 }
 

@@ -457,27 +457,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
 
-// ------------------------------------------------------------------ dW with on-chip split-K reduction
-// dW = dZ^T X (+ db = colsum dZ via the ones MMA) for one 128 x BN output tile per CLUSTER of S CTAs:
-// CTA s (cluster rank) contracts batch rows [s*kb_per_split*64, ...). After its MMAs it copies the fp32
-// accumulator (+ bias column) from TMEM into its own shared memory; after a cluster barrier, CTA s
-// reduces rows i = s, s+S, ... over the S CTAs' shared memory (DSMEM loads, splits summed in order 0..S-1,
-// i.e. deterministically) and writes the final gradient rows straight into the canonical gradient vector.
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ float4 ld_dsmem4(const float* local, uint32_t cta) {
-  uint32_t a = smem_u32(local), ra;
-  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra));
+// ------------------------------------------------------------------ dW: one-wave split-K with an L2 reduction
+// dW = dZ^T X (+ db = colsum dZ via the ones MMA) for 128 x BN output tiles. Grid (S, tiles), one wave
+// (cooperative launch: every CTA is resident). CTA (s, tile) contracts batch rows of k-blocks
+// [s*kb_per_split, ...), copies its fp32 accumulator (+ bias column) TMEM -> smem -> an L2-resident partial
+// buffer with coalesced 16-B stores, and arrives at a grid barrier. All CTAs then share the reduction: each
+// output element is the sum of its S partials in split order 0..S-1 (deterministic), written straight into
+// the canonical gradient vector. (DSMEM would move the same bytes at ~20 B/clk per SM; L2 is several times
+// faster per SM, and the reduction is spread over the whole grid.)
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define DW_STAMP(k)                                                                                         \
+  do {                                                                                                      \
+    if (out.dbg && threadIdx.x == 0) out.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (k)] = gtimer(); \
+  } while (0)
 
 template <int BN>
 struct DwCfg {  // k_gemm_dw: no epilogue staging buffers, the operand ring is reused for the reduction
@@ -495,7 +497,7 @@ struct DwCfg {  // k_gemm_dw: no epilogue staging buffers, the operand ring is r
   static constexpr int SMEM = FIXED + STAGES * (A_BYTES + B_BYTES);
 };
 
-template <int BN>
+template <int BN, bool KMAJ = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_constant__ GemmArgs args, const DwOut out) {
   using C = DwCfg<BN>;
   constexpr int RLD = BN + 20;  // fp32 row stride of the reduction buffer (16-B rows, conflict-free float4 writes)
@@ -511,11 +513,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
   static_assert(128 * RLD * 4 <= C::STAGES * (C::A_BYTES + C::B_BYTES), "reduction buffer must fit the ring");
 
+  DW_STAMP(0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t S = gridDim.x, crank = cluster_rank();  // S = cluster size (splits reduced on chip)
-  const int G = out.G;                                   // cluster groups per tile (reduced through L2)
-  const int tile = blockIdx.y / G, grp = blockIdx.y - tile * G;
-  const uint32_t split = (uint32_t)grp * S + crank;
+  const int S = gridDim.x;  // splits per tile
+  const int tile = blockIdx.y;
+  const uint32_t split = blockIdx.x;
   const TileCoord tc = decode(args, tile, args.m_tiles, BN);
   const bool bias_col = tc.ntile == 0;
   if (threadIdx.x == 0) {
@@ -537,6 +539,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  DW_STAMP(1);
   const int kb0 = (int)split * args.kb_per_split;
   const int nkb = max(0, min(args.kb_per_split, args.kb_total - kb0));
   const CUtensorMap* tmA = &args.tmA[tc.z];
@@ -553,18 +556,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
         uint8_t* b = sB + stage * C::B_BYTES;
         if (args.probe & 2) { mbar_arrive(&full[stage]); if (++stage == C::STAGES) { stage = 0; phase ^= 1u; } continue; }
         mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
-        tma_load_2d(tmA, &full[stage], a, tc.m0, k0);
-        tma_load_2d(tmA, &full[stage], a + 8192, tc.m0 + 64, k0);
+        if (KMAJ) {  // operands stored transposed ([out][batch], [in][batch]): one K-major box each
+          tma_load_2d(tmA, &full[stage], a, k0, tc.m0);
+          tma_load_2d(tmB, &full[stage], b, k0, tc.n0);
+        } else {
+          tma_load_2d(tmA, &full[stage], a, tc.m0, k0);
+          tma_load_2d(tmA, &full[stage], a + 8192, tc.m0 + 64, k0);
 #pragma unroll
-        for (int i = 0; i < BN / 64; ++i) tma_load_2d(tmB, &full[stage], b + i * 8192, tc.n0 + 64 * i, k0);
+          for (int i = 0; i < BN / 64; ++i) tma_load_2d(tmB, &full[stage], b + i * 8192, tc.n0 + 64 * i, k0);
+        }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, BN, true, true);
-      constexpr uint32_t idesc_ones = idesc_bf16(128, 16, true, false);
+      constexpr uint32_t idesc = idesc_bf16(128, BN, !KMAJ, !KMAJ);
+      constexpr uint32_t idesc_ones = idesc_bf16(128, 16, !KMAJ, false);
+      constexpr uint32_t lbo = KMAJ ? 0u : 8192u, kstep = KMAJ ? 32u : 2048u;
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = 0; kb < nkb; ++kb) {
@@ -574,8 +583,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
         const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
         for (int k = 0; k < C::BK / 16; ++k) {
-          const uint64_t ad = sdesc(a0 + k * 2048u, 8192u, 1024u);
-          const uint64_t bd = sdesc(b0 + k * 2048u, 8192u, 1024u);
+          const uint64_t ad = sdesc(a0 + k * kstep, lbo, 1024u);
+          const uint64_t bd = sdesc(b0 + k * kstep, lbo, 1024u);
           tc_mma(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           if (bias_col) {
             const uint64_t od = sdesc(smem_u32(sOnes) + k * 32u, 0u, 1024u);
@@ -597,6 +606,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
       __syncwarp();
       tc_fence_after();
     }
+    if (out.dbg && threadIdx.x == 128) out.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + 2] = gtimer();
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
     for (int c = h * (BN / 2); c < (h + 1) * (BN / 2); c += 32) {
       uint32_t r[32];
@@ -624,90 +634,97 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();  // every CTA's partial is in its shared memory
-  // level 1 (on chip): rows i = crank, crank + S, ...; the S splits of the cluster summed in order 0..S-1.
-  // level 2 (G > 1): each group writes its cluster sum to an L2-resident partial buffer; the last group to
-  // arrive at a row slice (per-slice counter) sums the G partials in group order 0..G-1 -- deterministic.
-  const int rows_valid = min(128, args.M - tc.m0);
-  const int cols_valid = min(BN, out.cols - tc.n0);
+  DW_STAMP(3);
+  // partial -> L2 buffer [tile][split][128][RLD] (rows of 128 consecutive floats per warp pass, coalesced)
+  float* part_me = out.part + ((size_t)tile * S + split) * 128 * RLD;
+  {
+    const int n4 = 128 * RLD / 4;
+    const float4* src = reinterpret_cast<const float4*>(red);
+    float4* dst = reinterpret_cast<float4*>(part_me);
+    for (int k = threadIdx.x; k < n4; k += blockDim.x) __stcg(dst + k, src[k]);
+  }
+  // grid barrier (all CTAs resident: cooperative launch); the counter only grows, the target is the next
+  // multiple of the grid size, so no reset is needed between launches
+  __shared__ uint32_t s_target;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t n = gridDim.x * gridDim.y;
+    const uint32_t old = atomicAdd(reinterpret_cast<uint32_t*>(out.cnt), 1u);
+    const uint32_t target = (old / n + 1u) * n;
+    while ((int32_t)(ld_acquire_gpu(reinterpret_cast<const uint32_t*>(out.cnt)) - target) < 0) __nanosleep(64);
+    s_target = target;
+  }
+  __syncthreads();
+  DW_STAMP(4);
+  // grid-wide reduction: items (tile, row, column group) split evenly over the CTAs, S partials per item
   constexpr int PER = BN / 4 + 1;  // float4 column groups + the bias group
-  constexpr int PLD = BN + 4;      // fp32 row stride of a level-2 partial
-  auto emit = [&](int i, int g, float4 v) {
+  float* const gw0 = out.grad + out.w_off[0];
+  float* const gw1 = out.grad + out.w_off[1];
+  float* const gb0 = out.grad + out.b_off[0];
+  float* const gb1 = out.grad + out.b_off[1];
+  const int row_split = out.row_split, ocols = out.cols;
+  const int ntiles = gridDim.y;
+  const long long n_items = (long long)ntiles * 128 * PER;
+  const int n_cta = gridDim.x * gridDim.y, cid = blockIdx.y * gridDim.x + blockIdx.x;
+  const long long per_cta = (n_items + n_cta - 1) / n_cta;
+  const long long lo = (long long)cid * per_cta, hi = min(n_items, lo + per_cta);
+  bool bad = false;
+  for (long long it = lo + threadIdx.x; it < hi; it += blockDim.x) {
+    const int t = (int)(it / (128 * PER));
+    const int rem = (int)(it - (long long)t * 128 * PER);
+    const int i = rem / PER, g = rem - i * PER;
+    const TileCoord c2 = decode(args, t, args.m_tiles, BN);
+    if (i >= args.M - c2.m0) continue;
+    const int cv = min(BN, ocols - c2.n0);
     const bool isb = g == BN / 4;
-    const int c = 4 * g;
-    int zz = tc.z, rr = tc.m0 + i;
-    if (out.row_split > 0 && rr >= out.row_split) { zz = 1; rr -= out.row_split; }
+    if (isb ? c2.ntile != 0 : 4 * g >= cv) continue;
+    const float* src = out.part + ((size_t)t * S * 128 + i) * RLD + 4 * g;
+    float4 v = __ldcg(reinterpret_cast<const float4*>(src));
+    for (int s0 = 1; s0 < S; s0 += 8) {  // splits in order, 8 loads in flight
+      float4 w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (s0 + q < S) w[q] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(s0 + q) * 128 * RLD));
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (s0 + q < S) { v.x = v.x + w[q].x; v.y = v.y + w[q].y; v.z = v.z + w[q].z; v.w = v.w + w[q].w; }
+    }
+    int rr = c2.m0 + i;
+    bool second = c2.z == 1;
+    if (row_split > 0 && rr >= row_split) { second = true; rr -= row_split; }
     if (isb) {
-      out.grad[out.b_off[zz] + rr] = v.x;
-      if (!isfinite(v.x)) atomicAdd(out.payload + 4, 1.0f);
+      bad |= !isfinite(v.x);
+      (second ? gb1 : gb0)[rr] = v.x;
     } else {
-      float* dst = out.grad + out.w_off[zz] + (long long)rr * out.cols + tc.n0 + c;
-      const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (c + k < cols_valid) {
-          dst[k] = vv[k];
-          if (!isfinite(vv[k])) atomicAdd(out.payload + 4, 1.0f);
-        }
-    }
-  };
-  float* part_tile = out.part + (size_t)tile * G * 128 * PLD;
-  for (int idx = threadIdx.x; idx < 128 * PER; idx += blockDim.x) {
-    const int ii = idx / PER, g = idx - ii * PER;
-    const int i = ii * (int)S + (int)crank;
-    if (i >= rows_valid) continue;
-    const bool isb = g == BN / 4;
-    const int c = 4 * g;
-    if (isb ? !bias_col : c >= cols_valid) continue;
-    const float* loc = red + i * RLD + c;
-    float4 vs[16];
-#pragma unroll
-    for (uint32_t s = 0; s < 16; ++s)
-      if (s < S) vs[s] = ld_dsmem4(loc, s);
-    float4 v = vs[0];
-#pragma unroll
-    for (uint32_t s = 1; s < 16; ++s)
-      if (s < S) { v.x = v.x + vs[s].x; v.y = v.y + vs[s].y; v.z = v.z + vs[s].z; v.w = v.w + vs[s].w; }
-    if (G == 1) emit(i, g, v);
-    else __stcg(reinterpret_cast<float4*>(part_tile + ((size_t)grp * 128 + i) * PLD + c), v);
-  }
-  if (G > 1) {
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int* cnt = out.cnt + tile * (int)S + (int)crank;
-      const int old = atomicAdd(cnt, 1);
-      s_last = old == G - 1;
-      if (old == G - 1) *cnt = 0;  // every group of this launch has arrived: re-arm for the next launch
-      __threadfence();
-    }
-    __syncthreads();
-    if (s_last) {
-      for (int idx = threadIdx.x; idx < 128 * PER; idx += blockDim.x) {
-        const int ii = idx / PER, g = idx - ii * PER;
-        const int i = ii * (int)S + (int)crank;
-        if (i >= rows_valid) continue;
-        const bool isb = g == BN / 4;
-        const int c = 4 * g;
-        if (isb ? !bias_col : c >= cols_valid) continue;
-        const float* src = part_tile + (size_t)i * PLD + c;
-        float4 v = __ldcg(reinterpret_cast<const float4*>(src));
-        for (int q = 1; q < G; ++q) {
-          const float4 w = __ldcg(reinterpret_cast<const float4*>(src + (size_t)q * 128 * PLD));
-          v.x = v.x + w.x; v.y = v.y + w.y; v.z = v.z + w.z; v.w = v.w + w.w;
-        }
-        emit(i, g, v);
-      }
+      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+      const int c = 4 * g;
+      float* dst = (second ? gw1 : gw0) + (long long)rr * ocols + c2.n0 + c;
+      const int nv = cv - c;
+      dst[0] = v.x;
+      if (nv > 1) dst[1] = v.y;
+      if (nv > 2) dst[2] = v.z;
+      if (nv > 3) dst[3] = v.w;
     }
   }
-  cluster_sync_all();  // keep shared memory alive until every CTA has read it
+  if (bad) atomicAdd(out.payload + 4, 1.0f);
+  DW_STAMP(7);
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  (void)s_target;
 }
 
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static int g_num_sms = 0;
+static int g_dw_max_ctas() {  // one k_gemm_dw CTA per SM (its shared memory allows no more)
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
 
 bool tma_init() {
   if (g_encode) return true;
@@ -770,63 +787,40 @@ static cudaError_t dispatch_bn(int bn, const GemmArgs& a, cudaStream_t st) {
   }
 }
 
-template <int BN>
+template <int BN, bool KMAJ = false>
 static cudaError_t launch_dw_bn(const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
   using C = DwCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_dw<BN, KMAJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = a.nz * a.m_tiles * a.n_tiles;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(S, tiles * o.G, 1);
+  cfg.gridDim = dim3(S, tiles, 1);
   cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gemm_dw<BN>, a, o);
+  return cudaLaunchKernelEx(&cfg, k_gemm_dw<BN, KMAJ>, a, o);
 }
 
-template <int BN>
-static int dw_clusters_bn(int S) {
-  using C = DwCfg<BN>;
-  if (cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess) return 0;
-  if (cudaFuncSetAttribute(k_gemm_dw<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return 0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(S, 1, 1);
-  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_gemm_dw<BN>, &cfg) != cudaSuccess) return 0;
-  return n;
-}
-
-int dw_max_active_clusters(int bn, int S) {
+// diagnostics (tools/gemm_probe): dW from transposed, K-major operand copies
+cudaError_t launch_gemm_dw_kmajor(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
   switch (bn) {
-    case 64: return dw_clusters_bn<64>(S);
-    case 128: return dw_clusters_bn<128>(S);
-    case 256: return dw_clusters_bn<256>(S);
-    default: return 0;
+    case 128: return launch_dw_bn<128, true>(a, o, S, st);
+    case 256: return launch_dw_bn<256, true>(a, o, S, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
+  if (S < 1 || S * a.nz * a.m_tiles * a.n_tiles > g_dw_max_ctas()) return cudaErrorInvalidValue;  // one wave
   switch (bn) {
     case 64: return launch_dw_bn<64>(a, o, S, st);
     case 128: return launch_dw_bn<128>(a, o, S, st);

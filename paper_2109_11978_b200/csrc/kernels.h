@@ -72,14 +72,16 @@ struct DwOut {                 // canonical destinations of a weight-gradient GE
   int cols;                    // real input width (the W row length in the canonical vector)
   int row_split;               // layer 1: rows >= row_split belong to the critic (second net)
   float* payload;              // non-finite counter at payload[4]
-  int G;                       // cluster groups per output tile (level-2 reduction through L2 when > 1)
-  float* part;                 // G > 1: [tile][G][128][BN + 4] fp32 cluster sums
-  int* cnt;                    // G > 1: [tile][S] arrival counters, zero between launches
+  int G;                       // unused (1)
+  float* part;                 // [tile][S][128][BN + 20] fp32 split partials (L2-resident scratch)
+  int* cnt;                    // grid-barrier counter (only grows; zero at creation)
+  unsigned long long* dbg;     // diagnostics only (tools/gemm_probe): per-CTA phase timestamps, else null
+  int dbg_mode;                // diagnostics only: 1 = skip the reduction, 2 = loads only, 3 = stores only
 };
-// split-K over G thread-block clusters of S CTAs (S <= 16) per output tile: on-chip (DSMEM) reduction
-// inside a cluster, deterministic reduction of the G cluster sums through L2
+// split-K over S CTAs per output tile in one cooperative wave (S * tiles <= #SMs), deterministic reduction
+// of the S fp32 partials through L2 by the whole grid
 cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);
-int dw_max_active_clusters(int bn, int S);  // co-resident clusters of S CTAs (0 on failure)
+cudaError_t launch_gemm_dw_kmajor(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);  // diagnostics
 
 // ------------------------------------------------------------------ PPO kernels (ppo.cu)
 struct NetDims {

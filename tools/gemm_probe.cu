@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
+#include <algorithm>
 #include <vector>
 
 #include "../paper_2109_11978_b200/csrc/kernels.h"
@@ -124,10 +125,12 @@ static std::vector<float> probe_dw(int Nout, int Nin, int K, int bn, int S, int 
   g.M = Nout; g.N = Nin; g.m_tiles = (Nout + 127) / 128; g.nz = 1;
   g.kb_total = (K + 63) / 64; g.n_tiles = (Nin + bn - 1) / bn; g.n_splits = 1;
   const int tiles = g.m_tiles * g.n_tiles;
-  g.kb_per_split = (g.kb_total + S * G - 1) / (S * G);
-  CK(cudaMalloc(&part, (size_t)tiles * G * 128 * (bn + 4) * 4));
-  CK(cudaMalloc(&cnt, (size_t)tiles * S * 4));
-  CK(cudaMemset(cnt, 0, (size_t)tiles * S * 4));
+  S = S * G; G = 1;
+  g.kb_per_split = (g.kb_total + S - 1) / S;
+  S = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  CK(cudaMalloc(&part, (size_t)tiles * S * 128 * (bn + 20) * 4));
+  CK(cudaMalloc(&cnt, 256));
+  CK(cudaMemset(cnt, 0, 256));
   DwOut o;
   memset(&o, 0, sizeof(o));
   o.grad = grad; o.w_off[0] = 0; o.b_off[0] = (long long)Nout * Nin; o.cols = Nin; o.row_split = 0;
@@ -151,12 +154,125 @@ static std::vector<float> probe_dw(int Nout, int Nin, int K, int bn, int S, int 
   return h;
 }
 
+// dW1-like problem from K-major (transposed) operand copies vs the MN-major originals
+static void probe_dw_kmajor(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st) {
+  __nv_bfloat16 *dZ, *X, *dZT, *XT;
+  float *g1, *g2, *part;
+  int* cnt;
+  const size_t gsz = (size_t)Nout * Nin + Nout + 64;
+  CK(cudaMalloc(&dZ, (size_t)K * Nout * 2)); CK(cudaMalloc(&X, (size_t)K * Nin * 2));
+  CK(cudaMalloc(&dZT, (size_t)K * Nout * 2)); CK(cudaMalloc(&XT, (size_t)K * Nin * 2));
+  CK(cudaMalloc(&g1, gsz * 4)); CK(cudaMalloc(&g2, gsz * 4));
+  std::vector<__nv_bfloat16> h1((size_t)K * Nout), h2((size_t)K * Nin), t1(h1.size()), t2(h2.size());
+  uint32_t sd = 777u;
+  for (auto& v : h1) { sd = sd * 1664525u + 1013904223u; v = __float2bfloat16(((sd >> 9) & 1023) / 1024.0f - 0.5f); }
+  for (auto& v : h2) { sd = sd * 1664525u + 1013904223u; v = __float2bfloat16(((sd >> 9) & 1023) / 1024.0f - 0.5f); }
+  for (int k = 0; k < K; ++k) {
+    for (int o = 0; o < Nout; ++o) t1[(size_t)o * K + k] = h1[(size_t)k * Nout + o];
+    for (int i = 0; i < Nin; ++i) t2[(size_t)i * K + k] = h2[(size_t)k * Nin + i];
+  }
+  CK(cudaMemcpy(dZ, h1.data(), h1.size() * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(X, h2.data(), h2.size() * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dZT, t1.data(), t1.size() * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(XT, t2.data(), t2.size() * 2, cudaMemcpyHostToDevice));
+  GemmArgs g, gt;
+  memset(&g, 0, sizeof(g));
+  make_tmap_bf16(&g.tmA[0], dZ, K, Nout, Nout, 64);
+  make_tmap_bf16(&g.tmB[0], X, K, Nin, Nin, 64);
+  g.M = Nout; g.N = Nin; g.m_tiles = (Nout + 127) / 128; g.nz = 1;
+  g.kb_total = (K + 63) / 64; g.n_tiles = (Nin + bn - 1) / bn; g.n_splits = 1;
+  const int tiles = g.m_tiles * g.n_tiles;
+  S = S * G; G = 1;
+  g.kb_per_split = (g.kb_total + S - 1) / S;
+  S = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  gt = g;
+  make_tmap_bf16(&gt.tmA[0], dZT, Nout, K, K, 128);
+  make_tmap_bf16(&gt.tmB[0], XT, Nin, K, K, bn);
+  CK(cudaMalloc(&part, (size_t)tiles * S * 128 * (bn + 20) * 4));
+  CK(cudaMalloc(&cnt, 256));
+  CK(cudaMemset(cnt, 0, 256));
+  DwOut o;
+  memset(&o, 0, sizeof(o));
+  o.grad = g1; o.b_off[0] = (long long)Nout * Nin; o.cols = Nin; o.payload = g1 + (size_t)Nout * Nin + Nout;
+  o.G = G; o.part = part; o.cnt = cnt;
+  DwOut o2 = o;
+  o2.grad = g2; o2.payload = g2 + (size_t)Nout * Nin + Nout;
+  const double fl = 2.0 * Nout * Nin * K;
+  for (int probe = 0; probe < 2; ++probe) {
+    g.probe = gt.probe = probe;
+    float u1 = time_us([&] { CK(launch_gemm_dw(bn, g, o, S, st)); }, st);
+    float u2 = time_us([&] { CK(launch_gemm_dw_kmajor(bn, gt, o2, S, st)); }, st);
+    printf("dw Nout=%d Nin=%d K=%d bn=%d S=%d G=%d probe=%d  MN-major %8.2f us (%6.1f TF)  K-major %8.2f us (%6.1f TF)\n",
+           Nout, Nin, K, bn, S, G, probe, u1, fl / u1 * 1e-6, u2, fl / u2 * 1e-6);
+  }
+  g.probe = gt.probe = 0;
+  CK(cudaMemset(g1, 0, gsz * 4)); CK(cudaMemset(g2, 0, gsz * 4));
+  CK(launch_gemm_dw(bn, g, o, S, st));
+  CK(launch_gemm_dw_kmajor(bn, gt, o2, S, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<float> a(gsz), b(gsz);
+  CK(cudaMemcpy(a.data(), g1, gsz * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(b.data(), g2, gsz * 4, cudaMemcpyDeviceToHost));
+  double num = 0, den = 0;
+  for (size_t i = 0; i + 64 < gsz; ++i) { num += (a[i] - b[i]) * (double)(a[i] - b[i]); den += (double)a[i] * a[i]; }
+  printf("   K-major vs MN-major: rel l2 %.3e\n", std::sqrt(num / den));
+  CK(cudaFree(dZ)); CK(cudaFree(X)); CK(cudaFree(dZT)); CK(cudaFree(XT)); CK(cudaFree(g1)); CK(cudaFree(g2));
+  CK(cudaFree(part)); CK(cudaFree(cnt));
+}
+
+// phase timestamps of every CTA of one dW launch (globaltimer ns, relative to the earliest CTA start)
+static void probe_dw_phases(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st, int dmode = 0) {
+  __nv_bfloat16 *dZ, *X;
+  float *grad, *part;
+  int* cnt;
+  unsigned long long* dbg;
+  const size_t gsz = (size_t)Nout * Nin + Nout + 64;
+  CK(cudaMalloc(&dZ, (size_t)K * Nout * 2)); CK(cudaMalloc(&X, (size_t)K * Nin * 2)); CK(cudaMalloc(&grad, gsz * 4));
+  fill(dZ, (size_t)K * Nout); fill(X, (size_t)K * Nin);
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  make_tmap_bf16(&g.tmA[0], dZ, K, Nout, Nout, 64);
+  make_tmap_bf16(&g.tmB[0], X, K, Nin, Nin, 64);
+  g.M = Nout; g.N = Nin; g.m_tiles = (Nout + 127) / 128; g.nz = 1;
+  g.kb_total = (K + 63) / 64; g.n_tiles = (Nin + bn - 1) / bn; g.n_splits = 1;
+  const int tiles = g.m_tiles * g.n_tiles;
+  S = S * G; G = 1;
+  g.kb_per_split = (g.kb_total + S - 1) / S;
+  S = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  const int nct = tiles * S * G;
+  CK(cudaMalloc(&part, (size_t)tiles * S * 128 * (bn + 20) * 4));
+  CK(cudaMalloc(&cnt, 256)); CK(cudaMemset(cnt, 0, 256));
+  CK(cudaMalloc(&dbg, (size_t)nct * 8 * 8));
+  DwOut o;
+  memset(&o, 0, sizeof(o));
+  o.grad = grad; o.b_off[0] = (long long)Nout * Nin; o.cols = Nin; o.payload = grad + (size_t)Nout * Nin + Nout;
+  o.G = G; o.part = part; o.cnt = cnt; o.dbg = dbg; o.dbg_mode = dmode;
+  for (int r = 0; r < 4; ++r) CK(launch_gemm_dw(bn, g, o, S, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> h((size_t)nct * 8);
+  CK(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+  unsigned long long t0 = ~0ull, tend = 0;
+  for (int c = 0; c < nct; ++c) { t0 = std::min(t0, h[(size_t)c * 8]); tend = std::max(tend, h[(size_t)c * 8 + 7]); }
+  double avg[8] = {0}, mx[8] = {0};
+  for (int c = 0; c < nct; ++c)
+    for (int k = 0; k < 8; ++k) {
+      const double v = (h[(size_t)c * 8 + k] - t0) * 1e-3;
+      avg[k] += v / nct;
+      mx[k] = std::max(mx[k], v);
+    }
+  printf("dw phases Nout=%d Nin=%d K=%d S=%d G=%d ctas=%d kb/cta=%d dbg_mode=%d (us from first CTA start; avg | max):\n",
+         Nout, Nin, K, S, G, nct, g.kb_per_split, dmode);
+  const char* nm[8] = {"start", "tmem alloc", "mma done", "partial->smem", "grid barrier", "-", "-", "reduced"};
+  for (int k = 0; k < 8; ++k) printf("   %-14s %8.2f | %8.2f\n", nm[k], avg[k], mx[k]);
+  CK(cudaFree(dZ)); CK(cudaFree(X)); CK(cudaFree(grad)); CK(cudaFree(part)); CK(cudaFree(cnt)); CK(cudaFree(dbg));
+}
+
 static void check_dw(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st) {
-  std::vector<float> a = probe_dw(Nout, Nin, K, bn, S, 1, st, true);
+  std::vector<float> a = probe_dw(Nout, Nin, K, bn, 1, 1, st, true);  // unsplit K
   std::vector<float> b = probe_dw(Nout, Nin, K, bn, S, G, st, true);
   double num = 0, den = 0;
   for (size_t i = 0; i + 64 < a.size(); ++i) { num += (a[i] - b[i]) * (double)(a[i] - b[i]); den += (double)a[i] * a[i]; }
-  printf("check dw Nout=%d Nin=%d G=%d vs G=1: rel l2 %.3e (payload %g)\n", Nout, Nin, G, std::sqrt(num / den),
+  printf("check dw Nout=%d Nin=%d S=%d vs S=1: rel l2 %.3e (payload %g)\n", Nout, Nin, S, std::sqrt(num / den),
          b[(size_t)Nout * Nin + Nout + 4]);
 }
 
@@ -190,6 +306,18 @@ int main(int argc, char** argv) {
     probe_dw(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), atoi(argv[6]), atoi(argv[7]), st, true);
     return 0;
   }
+  if (!strcmp(which, "phases")) {
+    probe_dw_phases(1024, 240, 24576, 256, 18, 1, st);   // dW1 (both nets): 8 tiles x 18
+    probe_dw_phases(512, 512, 24576, 256, 18, 1, st);    // dW2 both nets as 8 tiles
+    probe_dw_phases(256, 256, 24576, 256, 74, 1, st);    // dW3 both nets as 2 tiles
+    probe_dw_phases(128, 64, 64, 64, 1, 1, st);
+    return 0;
+  }
+  if (!strcmp(which, "kmaj")) {
+    probe_dw_kmajor(1024, 240, 24576, 256, 18, 1, st);
+    probe_dw_kmajor(512, 512, 24576, 256, 18, 1, st);
+    return 0;
+  }
   if (!strcmp(which, "all") || !strcmp(which, "fwd")) {
     probe_fwd(16384, 8192, 8192, 256, st);   // large square-ish: pipeline/peak sanity
     probe_fwd(24576, 1024, 256, 256, st);    // layer 1 (both nets), K = Dp (256 padded)
@@ -200,21 +328,15 @@ int main(int argc, char** argv) {
     probe_fwd(4096, 256, 512, 256, st);      // rollout layer 2 (one net)
   }
   if (!strcmp(which, "all") || !strcmp(which, "dw")) {
-    printf("max active clusters: bn256 S8 %d, S4 %d, S16 %d; bn128 S8 %d\n", dw_max_active_clusters(256, 8),
-           dw_max_active_clusters(256, 4), dw_max_active_clusters(256, 16), dw_max_active_clusters(128, 8));
-    const int cfgs[][2] = {{8, 1}, {4, 4}, {2, 8}, {1, 16}};
-    for (auto& c : cfgs) probe_dw(1024, 240, 24576, 256, c[0], c[1], st);  // dW1 (both nets)
-    for (auto& c : cfgs) probe_dw(256, 512, 24576, 256, c[0], c[1], st);   // dW2 (one net: x2 for both)
-    probe_dw(512, 512, 24576, 256, 8, 2, st);                                // dW2 both nets as 4 tiles
-    const int cfg3[][2] = {{8, 1}, {8, 4}, {8, 8}, {4, 16}};
-    for (auto& c : cfg3) probe_dw(128, 256, 24576, 256, c[0], c[1], st);   // dW3 (one net)
-    probe_dw(256, 256, 24576, 256, 8, 8, st);                                // dW3 both nets as 2 tiles
+    const int sp1[] = {8, 12, 16, 18};
+    for (int S : sp1) probe_dw(1024, 240, 24576, 256, S, 1, st);  // dW1 (both nets)
+    for (int S : sp1) probe_dw(512, 512, 24576, 256, S, 1, st);   // dW2 both nets as 8 tiles
+    const int sp3[] = {16, 32, 48, 74};
+    for (int S : sp3) probe_dw(256, 256, 24576, 256, S, 1, st);   // dW3 both nets as 2 tiles
     probe_dw(128, 64, 64, 64, 1, 1, st);       // one CTA, one k-block: fixed cost of a launch
-    probe_dw(128, 64, 1024, 64, 8, 1, st);     // one cluster of 8, 2 k-blocks each
-    probe_dw(1024, 256, 4096, 256, 8, 1, st);  // 64 CTAs, 8 k-blocks each
-    check_dw(1024, 240, 24576, 256, 8, 2, st);
-    check_dw(128, 256, 24576, 256, 8, 8, st);
-    check_dw(200, 96, 1000, 128, 4, 3, st);
+    check_dw(1024, 240, 24576, 256, 18, 1, st);
+    check_dw(256, 256, 24576, 256, 74, 1, st);
+    check_dw(200, 96, 1000, 128, 12, 1, st);
   }
   printf("done\n");
   return 0;
