@@ -97,6 +97,25 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+CAT_KERNEL = {"gemm_dw": "k_gemm_dw", "gemm_fwd": "k_gemm_tc", "gemm_dx": "k_gemm_tc", "gemm_roll": "k_gemm_tc",
+              "env": "k_env_step", "loss": "k_loss_heads"}
+
+
+def measured_traffic(cat):
+    """DRAM bytes per launch of the category's kernel from the newest committed ncu --set full summary
+    (profiles/rNN_traffic.json, written by tools/make_profile_summary.py), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        if d.get("kernel") == CAT_KERNEL.get(cat):
+            return {"bytes_per_launch": d["traffic_bytes_per_launch"], "source": "profiles/" + os.path.basename(f)}
+    return None
+
+
 def algorithmic(cfg, w):
     """Algorithmic FLOPs per iteration by category and bytes of the env kernel."""
     D = 48 + w["scan"][0] * w["scan"][1]
@@ -277,7 +296,7 @@ def main():
     if dom in gemm_cats:
         ach = alg[dom] / (per_iter[dom]["ms"] * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": f"tcgen05 GEMM ({dom})", "achieved": ach, "peak": pk["bf16_sus"],
-                "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"], "traffic": None,
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"], "traffic": measured_traffic(dom),
                 "peak_src": pk["src"] + " bf16 sustained"}
     else:
         if dom == "env":
@@ -286,7 +305,7 @@ def main():
             nb = None
         ach = (nb / (per_iter[dom]["ms"] * 1e-3) / 1e9) if nb else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm"], "unit": "GB/s",
-                "frac": (ach / pk["hbm"]) if ach else None, "traffic": None, "peak_src": pk["src"]}
+                "frac": (ach / pk["hbm"]) if ach else None, "traffic": measured_traffic(dom), "peak_src": pk["src"]}
     roof["all_gemms"] = {"achieved": gflops / (gms * 1e-3) / 1e12 if gms else None, "unit": "TFLOP/s",
                          "frac": (gflops / (gms * 1e-3) / 1e12) / pk["bf16_sus"] if gms else None}
     roof["step_roofline_ms"] = alg["total_flops"] / (pk["bf16_sus"] * 1e12) * 1e3
