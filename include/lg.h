@@ -140,8 +140,9 @@ lg_status env_reset(lg_ctx* ctx, const uint8_t* mask, int32_t init, float* obs);
  * `actions` != NULL, from that fp32 [N][12] buffer (which is then copied into ACT slot t).
  * Writes REWARD/FLAGS/BOOT slot t and o_{t+1} into OBS slot t+1; optional caller outputs (may be NULL):
  * obs fp32 [N][D] (post-reset), reward fp32 [N], terminated/timeout u8 [N], terms fp32 [N][9]
- * (per-term reward breakdown). Time-out envs get the bootstrap critic value on their
- * pre-reset observation when LG_F_BOOTSTRAP is set. */
+ * (per-term reward breakdown). With LG_F_BOOTSTRAP the pre-reset observation of every time-out
+ * env is compacted into the rollout's time-out buffer (t == 0 starts a rollout); BOOT slot t is 0 until
+ * storage_compute_gae writes the bootstrap critic values V(o_term) of the whole rollout at once. */
 lg_status env_step_obs_reward(lg_ctx* ctx, int32_t t, const float* actions, float* obs, float* reward,
                               uint8_t* terminated, uint8_t* timeout, float* terms);
 
@@ -153,7 +154,8 @@ lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float*
 lg_status policy_forward(lg_ctx* ctx, const void* x_bf16, int32_t M, float* mu, float* value);
 
 /* --- Learning --- */
-/* V(o_T) from OBS slot T, GAE with time-out bootstrapping, batch statistics for normalisation.
+/* With LG_F_BOOTSTRAP first V(o_term) of the rollout's compacted time-outs into BOOT (one batched
+ * critic pass); then V(o_T) from OBS slot T, GAE with time-out bootstrapping, batch statistics.
  * adv/ret (fp32 [T][N], may be NULL) receive copies of LG_BUF_ADV / LG_BUF_RET. Advances s_base by T. */
 lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret);
 /* E epochs x K_mb minibatches of the clipped-surrogate update with Alg. 1 and Adam; copies OBS slot T
@@ -196,7 +198,8 @@ lg_status lg_graph_launch(lg_ctx* ctx);
 /* Number of kernel nodes (this library's kernels) in the captured iteration graph. */
 lg_status lg_graph_kernel_count(lg_ctx* ctx, int32_t* n_h);
 
-/* Debug/introspection: device scalars {s_base, iteration, adam_t, alpha(bits), ...} (int32 [8]) */
+/* Debug/introspection: device scalars (int32 [8]): {s_base, iteration, adam_t, alpha (fp32 bits),
+ * time-outs compacted since the current rollout began, non-finite skips, applied updates, last KL (fp32 bits)} */
 lg_status lg_device_scalars(lg_ctx* ctx, int32_t* out8_h);
 
 /* Per-category device timing (measurement only). enable != 0: every later launch is bracketed by a

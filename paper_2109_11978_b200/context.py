@@ -189,7 +189,7 @@ class Context:
         import struct
         alpha = struct.unpack("f", struct.pack("i", v[3]))[0]
         kl = struct.unpack("f", struct.pack("i", v[7]))[0]
-        return dict(s_base=v[0], iteration=v[1], adam_t=v[2], alpha=alpha, n_to=v[4], nonfinite_skips=v[5],
+        return dict(s_base=v[0], iteration=v[1], adam_t=v[2], alpha=alpha, n_to_total=v[4], nonfinite_skips=v[5],
                     applied=v[6], kl_last=kl)
 
     def profile(self, enable=True):

@@ -22,7 +22,7 @@ T* at(void* base, size_t off) { return reinterpret_cast<T*>(reinterpret_cast<uin
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Dims {
-  int N, T, E, K, H0, H1, H2, D, Dp, nx, ny, L, C, R_hf, C_hf, B, Mmb, R;
+  int N, T, E, K, H0, H1, H2, D, Dp, nx, ny, L, C, R_hf, C_hf, B, Mmb, R, to_cap;
   long long P;
 };
 
@@ -36,7 +36,9 @@ bool dims_of(const lg_config* c, Dims& d) {
   d.R_hf = 80 * d.L; d.C_hf = 80 * d.C;
   d.B = d.N * d.T;
   d.Mmb = d.K > 0 ? d.B / d.K : 0;
-  d.R = std::max(d.N, d.Mmb);
+  // an env times out at most once per 1000 steps, so a rollout compacts at most N * ceil(T / 1000) time-outs
+  d.to_cap = d.N * ((d.T + 999) / 1000);
+  d.R = std::max(std::max(d.N, d.Mmb), d.to_cap);
   long long P = 0;
   for (int z = 0; z < 2; ++z) {
     int A = z == 0 ? 12 : 1;
@@ -69,6 +71,13 @@ Canon canon_of(const Dims& d) {
 }
 
 int bn_for(int n) { return n >= 256 ? 256 : (n > 64 ? 128 : 64); }
+// narrower tiles while the GEMM still fits one wave: small-M (rollout) GEMMs are latency bound, more CTAs win
+int bn_small(int n, int m_rows, int nz) {
+  const int mt = (m_rows + 127) / 128;
+  int bn = bn_for(n);
+  while (bn > 64 && (long long)mt * ((n + bn / 2 - 1) / (bn / 2)) * nz <= 148) bn /= 2;
+  return bn;
+}
 
 struct DwPlan {
   int rows, N, bn, n_tiles, m_tiles, kb_total, tiles, S, kb_per_split;
@@ -168,8 +177,8 @@ Layout layout_of(const Dims& d) {
   L.k_dw2 = o; o = al(o + L.dw2.bytes);
   L.k_dw3 = o; o = al(o + L.dw3.bytes);
   L.k_perm = o; o = al(o + (size_t)d.B * 4);
-  L.k_tobs = o; o = al(o + (size_t)d.N * d.Dp * 2);
-  L.k_tidx = o; o = al(o + (size_t)d.N * 4);
+  L.k_tobs = o; o = al(o + (size_t)d.to_cap * d.Dp * 2);
+  L.k_tidx = o; o = al(o + (size_t)d.to_cap * 4);
   L.k_step = o; o = al(o + 16 * 4);
   L.k_stats = o; o = al(o + sizeof(lg_update_stats));
   L.k_ctrl = o; o = al(o + 64);
@@ -196,6 +205,8 @@ struct lg_ctx {
   // prebuilt launch descriptors
   std::vector<GemmArgs> l1_roll;  // per OBS slot 0..T
   GemmArgs l1_upd, l2, l3, l1_boot, l2_boot, l3_boot, l1_vt, dx3, dx2, dw3, dw2, dw1;
+  GemmArgs l2r, l3r;        // layers 2, 3 for M <= n_envs rows (rollout): narrower tiles (bn2r, bn3r)
+  int bn2r = 0, bn3r = 0;
   EnvParams ep;
   ShadowArgs shadow;
   cudaGraph_t graph = nullptr;
@@ -408,14 +419,24 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   }
   set_fwd_common(g2, d.Mmb, d.H1, d.H0, bn2, 2); g2.ldo = 2 * d.H1;
   set_fwd_common(g3, d.Mmb, d.H2, d.H1, bn3, 2); g3.ldo = 2 * d.H2;
+  ctx->bn2r = bn_small(d.H1, d.N, 2);
+  ctx->bn3r = bn_small(d.H2, d.N, 2);
+  ctx->l2r = g2;
+  ctx->l3r = g3;
+  for (int z = 0; z < 2; ++z) {
+    ok &= make_tmap_bf16(&ctx->l2r.tmB[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, ctx->bn2r);
+    ok &= make_tmap_bf16(&ctx->l3r.tmB[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, ctx->bn3r);
+  }
+  set_fwd_common(ctx->l2r, d.N, d.H1, d.H0, ctx->bn2r, 2);
+  set_fwd_common(ctx->l3r, d.N, d.H2, d.H1, ctx->bn3r, 2);
   // ---- critic-only chains (time-out bootstrap on compacted rows; V(o_T) on OBS slot T)
   GemmArgs& c1 = ctx->l1_boot;
   memset(&c1, 0, sizeof(c1));
-  ok &= make_tmap_bf16(&c1.tmA[0], TOBS, d.N, d.Dp, d.Dp, 128);
+  ok &= make_tmap_bf16(&c1.tmA[0], TOBS, d.to_cap, d.Dp, d.Dp, 128);
   ok &= make_tmap_bf16(&c1.tmB[0], W1 + (size_t)d.H0 * d.Dp, d.H0, d.Dp, d.Dp, bn1c);
   cmap(&c1.tmC[0], H1 + d.H0, d.H0, 2 * d.H0);
-  set_fwd_common(c1, d.N, d.H0, d.Dp, bn1c, 1);
-  c1.M_dev = &ctx->sc->n_to;
+  set_fwd_common(c1, d.to_cap, d.H0, d.Dp, bn1c, 1);
+  c1.M_dev = &ctx->sc->n_to_total;
   c1.ldo = 2 * d.H0; c1.bias[0] = b1 + d.H0;
   GemmArgs& cv = ctx->l1_vt;
   cv = c1;
@@ -491,6 +512,7 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   ep.flags_out = reinterpret_cast<uint8_t*>(ctx->buf[LG_BUF_FLAGS]);
   ep.boot = reinterpret_cast<float*>(ctx->buf[LG_BUF_BOOT]);
   ep.term_obs = TOBS;
+  ep.to_cap = d.to_cap;
   ep.term_idx = at<int32_t>(K, L.k_tidx);
   ep.recs = at<void>(K, L.k_rec);
   ep.trecs = at<void>(K, L.k_trec);
@@ -603,12 +625,13 @@ static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int M, int cat = LG_PRO
   const Dims& d = ctx->d;
   g_gemm_cat = cat;
   l1.M = M;
-  GemmArgs g2 = ctx->l2, g3 = ctx->l3;
+  const bool small = M <= d.N;
+  GemmArgs g2 = small ? ctx->l2r : ctx->l2, g3 = small ? ctx->l3r : ctx->l3;
   g2.M = M; g3.M = M;
   lg_status s;
   if ((s = gemm(ctx, GEMM_FWD, l1, bn_for(2 * d.H0), 1)) != LG_OK) return s;
-  if ((s = gemm(ctx, GEMM_FWD, g2, bn_for(d.H1), 2)) != LG_OK) return s;
-  if ((s = gemm(ctx, GEMM_FWD, g3, bn_for(d.H2), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, g2, small ? ctx->bn2r : bn_for(d.H1), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, g3, small ? ctx->bn3r : bn_for(d.H2), 2)) != LG_OK) return s;
   return LG_OK;
 }
 
@@ -628,6 +651,7 @@ static lg_status critic_rows(lg_ctx* ctx, GemmArgs& c1, const int* M_dev, int M)
 // ------------------------------------------------------------------ env
 lg_status env_reset(lg_ctx* ctx, const uint8_t* mask, int32_t init, float* obs) {
   GUARD();
+  { Scope sc_(ctx, LG_PROF_MISC); CK(cudaMemsetAsync(&ctx->sc->n_to_total, 0, 4, ctx->st)); }
   { Scope sc_(ctx, LG_PROF_ENV); launch_env_reset(ctx->ep, mask, init, obs, ctx->st); }
   CKL();
   ctx->reset_done = true;
@@ -643,20 +667,15 @@ lg_status env_step_obs_reward(lg_ctx* ctx, int32_t t, const float* actions, floa
   float* act_slot = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
   if (actions && actions != act_slot)
     CK(cudaMemcpyAsync(act_slot, actions, (size_t)d.N * 12 * 4, cudaMemcpyDeviceToDevice, ctx->st));
-  { Scope sc_(ctx, LG_PROF_MISC); CK(cudaMemsetAsync(&ctx->sc->n_to, 0, 4, ctx->st)); }
+  {
+    Scope sc_(ctx, LG_PROF_MISC);
+    CK(cudaMemsetAsync(&ctx->sc->n_to, 0, 4, ctx->st));
+    if (t == 0) CK(cudaMemsetAsync(&ctx->sc->n_to_total, 0, 4, ctx->st));  // a rollout begins
+  }
   { Scope sc_(ctx, LG_PROF_ENV); launch_env_step(ctx->ep, t, act_slot, obs, reward, terminated, timeout, terms, ctx->st); }
   CKL();
-  if (ctx->cfg.flags & LG_F_BOOTSTRAP) {  // V(o_term) of the time-out envs, compacted rows
-    lg_status s = critic_rows(ctx, ctx->l1_boot, &ctx->sc->n_to, d.N);
-    if (s != LG_OK) return s;
-    HeadArgs h = head_args(ctx, d.N);
-    h.M_dev = &ctx->sc->n_to;
-    h.mode = 1;
-    h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_BOOT]) + (size_t)t * d.N;
-    h.idx = ctx->ep.term_idx;
-    { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(h, ctx->st); }
-    CKL();
-  }
+  // time-out envs: their pre-reset observation is compacted into the rollout's time-out buffer; the
+  // bootstrap critic values V(o_term) are evaluated for all steps at once in storage_compute_gae
   return LG_OK;
 }
 
@@ -722,6 +741,17 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
   GUARD();
   const Dims& d = ctx->d;
   void* K = ctx->buf[LG_BUF_WORK];
+  if (ctx->cfg.flags & LG_F_BOOTSTRAP) {  // V(o_term) of every time-out of the rollout, one batched pass
+    lg_status s0 = critic_rows(ctx, ctx->l1_boot, &ctx->sc->n_to_total, d.to_cap);
+    if (s0 != LG_OK) return s0;
+    HeadArgs hb = head_args(ctx, d.to_cap);
+    hb.M_dev = &ctx->sc->n_to_total;
+    hb.mode = 1;
+    hb.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_BOOT]);
+    hb.idx = ctx->ep.term_idx;
+    { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(hb, ctx->st); }
+    CKL();
+  }
   // V(o_T): critic on OBS slot T
   lg_status s = critic_rows(ctx, ctx->l1_vt, nullptr, d.N);
   if (s != LG_OK) return s;
@@ -1071,7 +1101,7 @@ lg_status lg_device_scalars(lg_ctx* ctx, int32_t* out8_h) {
   CK(cudaStreamSynchronize(ctx->st));
   out8_h[0] = (int32_t)s.s_base; out8_h[1] = (int32_t)s.iteration; out8_h[2] = s.adam_t;
   memcpy(&out8_h[3], &s.alpha, 4);
-  out8_h[4] = s.n_to; out8_h[5] = s.nonfinite_skips; out8_h[6] = s.applied;
+  out8_h[4] = s.n_to_total; out8_h[5] = s.nonfinite_skips; out8_h[6] = s.applied;
   memcpy(&out8_h[7], &s.kl_last, 4);
   return LG_OK;
 }

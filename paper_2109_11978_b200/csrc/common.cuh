@@ -35,6 +35,7 @@ struct DevScalars {
   // Alg. 1 / Adam state per minibatch slot m of the iteration (read slot m&1, write slot (m+1)&1)
   float alpha_ring[2];
   int32_t adamt_ring[2];
+  int32_t n_to_total;   // time-out rows compacted since the rollout began (batched bootstrap)
 };
 
 // ------------------------------------------------------------------ Philox4x32-10

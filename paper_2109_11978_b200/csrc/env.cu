@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(256) k_env_obs(EnvParams P, int ev_off, __nv_b
   }
   const int r = it / G, gq = it - r * G;
   const ObsRec& o = recs[r];
+  if (o.row < 0) return;  // time-out beyond the compacted buffer's capacity (not reachable for T <= 1000)
   World W{P.hf, P.R, P.C, P.inv_cell};
   Rng rng{P.seed_lo, P.seed_hi};
   float v[4];
@@ -578,12 +579,19 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
   }
   if (done) {  // group-uniform
     if (to && (P.flags & F_BOOTSTRAP)) {
-      int row = 0;
-      if (l == 0) row = atomicAdd(&P.scalars->n_to, 1);
+      // record r of this step (k_env_obs writes its observation) -> row grow of the rollout's compacted
+      // time-out buffer, evaluated by the critic once after the rollout (storage_compute_gae)
+      int row = 0, grow = 0;
+      if (l == 0) { row = atomicAdd(&P.scalars->n_to, 1); grow = atomicAdd(&P.scalars->n_to_total, 1); }
       row = __shfl_sync(gm, row, gbase);
+      grow = __shfl_sync(gm, grow, gbase);
       ObsRec& tr = reinterpret_cast<ObsRec*>(P.trecs)[row];
       fill_rec_group(c, g, l, tr);
-      if (l == 0) { tr.g = gid; tr.word0 = 0u; tr.row = row; P.term_idx[row] = i; }
+      if (l == 0) {
+        tr.g = gid; tr.word0 = 0u;
+        tr.row = grow < P.to_cap ? grow : -1;
+        if (grow < P.to_cap) P.term_idx[grow] = t * N + i;
+      }
     }
     if (l == 0) {  // episode statistics (stats only; float atomics)
       atomicAdd(&P.scalars->ep_return_sum, c.ep_return);

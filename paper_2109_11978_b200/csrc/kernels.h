@@ -27,8 +27,9 @@ struct EnvParams {
   float* reward;             // [T][N]
   uint8_t* flags_out;        // [T][N]
   float* boot;               // [T][N]
-  __nv_bfloat16* term_obs;   // [N][Dp] compacted pre-reset observations of time-out envs
-  int32_t* term_idx;         // [N]
+  __nv_bfloat16* term_obs;   // [to_cap][Dp] pre-reset observations of the rollout's time-outs (compacted)
+  int32_t* term_idx;         // [to_cap] BOOT index t*N + i of each compacted row
+  int to_cap;                // rows of term_obs
   void* recs;                // [N] 256-B observation records (written by the transition kernel)
   void* trecs;               // [N] records of the pre-reset state of time-out envs (compacted)
 };

@@ -106,6 +106,41 @@ def test_env_teacher_forced_bit_exact(scan, rough, flags):
     assert n_to >= 20 and n_term > 0
 
 
+def test_timeout_bootstrap_values_vs_oracle():
+    """Time-out bootstrapping: the GPU compacts the pre-reset observation of every time-out
+    of the rollout and evaluates the critic on all of them in one pass inside compute_gae; BOOT[t][i] must be
+    the oracle critic on the oracle's pre-reset observation (bf16 rows, MLP tolerance) and 0 elsewhere."""
+    cfg, ctx, env, theta = make(n_envs=256, T=12)
+    N, D = cfg.n_envs, cfg.obs_dim
+    ctx.reset()
+    env.reset()
+    ctx.sync()
+    st = env.state.copy()
+    st["ep_step"][:40] = 999 - (np.arange(40) % 6)  # time-outs spread over steps 0..5
+    env.state[:] = st
+    set_gpu_state(ctx, st)
+    rng = np.random.default_rng(5)
+    want = np.zeros((cfg.n_steps, N), np.float64)
+    mask = np.zeros((cfg.n_steps, N), bool)
+    for t in range(cfg.n_steps):
+        a = (rng.standard_normal((N, 12)) * 0.3).astype(np.float32)
+        ctx.env_step(t, actions=torch.from_numpy(a).cuda())
+        _, _, te, to, _, tobs = env.step(a)
+        idx = np.nonzero(to)[0]
+        if idx.size:
+            x = torch.from_numpy(tobs[idx]).bfloat16().float().numpy()
+            _, v = _oracle_forward(theta, x.astype(np.float64), D, cfg.hidden)
+            want[t, idx] = v
+            mask[t, idx] = True
+    assert mask.sum() >= 30
+    ctx.compute_gae()
+    ctx.sync()
+    b = ctx.storage("BOOT").cpu().numpy()
+    assert np.all(b[~mask] == 0.0)
+    assert rel(b[mask], want[mask]) < 2e-2
+    assert int(ctx.scalars()["n_to_total"]) == int(mask.sum())
+
+
 def test_curriculum_kernel_bit_exact():
     cfg, ctx, env, _ = make(n_envs=64, T=4, levels=10, cols=5)
     rng = np.random.default_rng(1)

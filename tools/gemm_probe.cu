@@ -306,6 +306,14 @@ int main(int argc, char** argv) {
     probe_dw(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), atoi(argv[6]), atoi(argv[7]), st, true);
     return 0;
   }
+  if (!strcmp(which, "roll")) {  // rollout-size forward GEMMs (M = 4096 envs) at different tile widths
+    const int cfg[][4] = {{4096, 1024, 256, 256}, {4096, 1024, 256, 128}, {4096, 512, 256, 256}, {4096, 512, 256, 128},
+                          {4096, 256, 512, 256}, {4096, 256, 512, 128}, {4096, 256, 512, 64},
+                          {4096, 128, 256, 128}, {4096, 128, 256, 64}, {24576, 1024, 256, 128}, {24576, 256, 512, 128},
+                          {24576, 128, 256, 64}};
+    for (auto& c : cfg) probe_fwd(c[0], c[1], c[2], c[3], st);
+    return 0;
+  }
   if (!strcmp(which, "phases")) {
     probe_dw_phases(1024, 240, 24576, 256, 18, 1, st);   // dW1 (both nets): 8 tiles x 18
     probe_dw_phases(512, 512, 24576, 256, 18, 1, st);    // dW2 both nets as 8 tiles
