@@ -80,7 +80,7 @@ int bn_small(int n, int m_rows, int nz) {
 }
 
 struct DwPlan {
-  int rows, N, bn, n_tiles, m_tiles, kb_total, tiles, S, kb_per_split;
+  int rows, N, bn, n_tiles, m_tiles, kb_total, tiles, S, kb_per_split, pair;
   size_t part_bytes, bytes;
 };
 // Weight-gradient GEMM plan (k_gemm_dw): 128 x bn output tiles; the minibatch (K) is split over S CTAs per
@@ -93,6 +93,10 @@ DwPlan dw_plan(int rows, int N, int K, int nz) {
   p.m_tiles = (rows + 127) / 128;
   p.kb_total = (K + 63) / 64;
   p.tiles = p.n_tiles * p.m_tiles * nz;
+  // CTA pairs (256-row tiles, tcgen05 cta_group::2) when every z has an even number of 128-row tiles:
+  // each SM then receives 2/3 of the operand bytes for the same MMA work
+  // (measured: no gain over single CTAs inside the iteration -- the split-K tail dominates -- so off by default)
+  p.pair = 0;
   // one wave of <= 148 CTAs, and >= 8 k-blocks per CTA (the fp32 partial costs ~3 k-blocks of traffic)
   const int S = std::max(1, std::min(std::max(1, p.kb_total / 8), 148 / std::max(1, p.tiles)));
   p.kb_per_split = (p.kb_total + S - 1) / S;
@@ -841,7 +845,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
     o.row_split = row_split;
     o.payload = ctx->payload;
     Scope sc_(ctx, LG_PROF_GEMM_DW);
-    cudaError_t e = launch_gemm_dw(p.bn, g, o, p.S, ctx->st);
+    cudaError_t e = p.pair ? launch_gemm_dw_pair(p.bn, g, o, p.S, ctx->st) : launch_gemm_dw(p.bn, g, o, p.S, ctx->st);
     if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm_dw: %s", cudaGetErrorString(e));
     return LG_OK;
   };

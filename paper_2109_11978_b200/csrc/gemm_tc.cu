@@ -22,6 +22,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -39,8 +41,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// mbarrier wait: a plain try_wait loop (mode 1). A suspend-time hint (mode 0) lets a waiting thread sleep
+// until the hint expires when the phase is completed from the peer CTA of a pair (multicast tcgen05.commit /
+// the peer's TMA complete_tx): the CTA-pair kernel then crawls. Mode 2 = test_wait spin, 3 = bounded (probe).
 #ifndef LG_MBAR_MODE
-#define LG_MBAR_MODE 0
+#define LG_MBAR_MODE 1
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if LG_MBAR_MODE == 0
@@ -52,6 +57,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680));
+#elif LG_MBAR_MODE == 3
+  // diagnostics build (tools/gemm_probe3): bounded wait that reports the stuck barrier and gives up
+  uint32_t ok = 0;
+  for (long long it = 0; it < (1ll << 22) && !ok; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity));
+  }
+  if (!ok) {
+    uint32_t rk;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rk));
+    printf("mbar timeout: block (%d,%d) rank %u thread %d bar smem 0x%x parity %u\n", blockIdx.x, blockIdx.y, rk,
+           threadIdx.x, smem_u32(bar), parity);
+  }
 #elif LG_MBAR_MODE == 1
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -481,6 +503,102 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (out.dbg && threadIdx.x == 0) out.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (k)] = gtimer(); \
   } while (0)
 
+// The split-K tail shared by the dW kernels: the CTA's fp32 partial (128 rows x RLD, staged in smem `red`) ->
+// the L2 buffer [tile][split][128][RLD] with coalesced 16-B stores; a grid barrier (cooperative launch: all
+// CTAs resident; the counter only grows, the target is the next multiple of the grid size, so no reset is
+// needed between launches); then the whole grid reduces: items (tile, row, column group) are split evenly
+// over the CTAs and each sums its S partials in split order 0..S-1 (deterministic) into the canonical gradient.
+template <int BN>
+__device__ __forceinline__ void dw_partial_barrier_reduce(const GemmArgs& args, const DwOut& out, const float* red,
+                                                          int tile, int split, int S, int ntiles) {
+  constexpr int RLD = BN + 20;
+  const int warp = threadIdx.x >> 5;
+  (void)warp;
+  // partial -> L2 buffer [tile][split][128][RLD]: one bulk async copy (the TMA engine streams the whole
+  // 128 x RLD fp32 tile from shared memory)
+  float* part_me = out.part + ((size_t)tile * S + split) * 128 * RLD;
+  fence_async_smem();  // this thread's smem writes -> visible to the async proxy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(part_me), "r"(smem_u32(red)),
+                 "r"((uint32_t)(128 * RLD * 4))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  // grid barrier (all CTAs resident: cooperative launch); the counter only grows, the target is the next
+  // multiple of the grid size, so no reset is needed between launches
+  __threadfence();
+  __syncthreads();
+  DW_STAMP(4);
+  if (threadIdx.x == 0) {
+    const uint32_t n = gridDim.x * gridDim.y * gridDim.z;
+    const uint32_t old = atomicAdd(reinterpret_cast<uint32_t*>(out.cnt), 1u);
+    const uint32_t target = (old / n + 1u) * n;
+    while ((int32_t)(ld_acquire_gpu(reinterpret_cast<const uint32_t*>(out.cnt)) - target) < 0) __nanosleep(64);
+  }
+  __syncthreads();
+  DW_STAMP(5);
+  
+  // grid-wide reduction: items (tile, row, column group) split evenly over the CTAs, S partials per item
+  constexpr int PER = BN / 4 + 1;  // float4 column groups + the bias group
+  float* const gw0 = out.grad + out.w_off[0];
+  float* const gw1 = out.grad + out.w_off[1];
+  float* const gb0 = out.grad + out.b_off[0];
+  float* const gb1 = out.grad + out.b_off[1];
+  const int row_split = out.row_split, ocols = out.cols;
+
+  const long long n_items = (long long)ntiles * 128 * PER;
+  const int n_cta = gridDim.x * gridDim.y, cid = blockIdx.y * gridDim.x + blockIdx.x;
+  const long long per_cta = (n_items + n_cta - 1) / n_cta;
+  const long long lo = (long long)cid * per_cta, hi = min(n_items, lo + per_cta);
+  bool bad = false;
+  for (long long it = lo + threadIdx.x; it < hi; it += blockDim.x) {
+    const int t = (int)(it / (128 * PER));
+    const int rem = (int)(it - (long long)t * 128 * PER);
+    const int i = rem / PER, g = rem - i * PER;
+    const TileCoord c2 = decode(args, t, args.m_tiles, BN);
+    if (i >= args.M - c2.m0) continue;
+    const int cv = min(BN, ocols - c2.n0);
+    const bool isb = g == BN / 4;
+    if (isb ? c2.ntile != 0 : 4 * g >= cv) continue;
+    const float* src = out.part + ((size_t)t * S * 128 + i) * RLD + 4 * g;
+    // all S partials of the item in flight at once (S <= 24 in one pass), then summed in split order
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < S; s0 += 24) {
+      float4 w[24];
+#pragma unroll
+      for (int q = 0; q < 24; ++q)
+        if (s0 + q < S) w[q] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(s0 + q) * 128 * RLD));
+#pragma unroll
+      for (int q = 0; q < 24; ++q)
+        if (s0 + q < S) {
+          if (s0 + q == 0) v = w[0];
+          else { v.x = v.x + w[q].x; v.y = v.y + w[q].y; v.z = v.z + w[q].z; v.w = v.w + w[q].w; }
+        }
+    }
+    int rr = c2.m0 + i;
+    bool second = c2.z == 1;
+    if (row_split > 0 && rr >= row_split) { second = true; rr -= row_split; }
+    if (isb) {
+      bad |= !isfinite(v.x);
+      (second ? gb1 : gb0)[rr] = v.x;
+    } else {
+      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+      const int c = 4 * g;
+      float* dst = (second ? gw1 : gw0) + (long long)rr * ocols + c2.n0 + c;
+      const int nv = cv - c;
+      dst[0] = v.x;
+      if (nv > 1) dst[1] = v.y;
+      if (nv > 2) dst[2] = v.z;
+      if (nv > 3) dst[3] = v.w;
+    }
+  }
+  if (bad) atomicAdd(out.payload + 4, 1.0f);
+  DW_STAMP(6);
+}
+
 template <int BN>
 struct DwCfg {  // k_gemm_dw: no epilogue staging buffers, the operand ring is reused for the reduction
   static constexpr int BM = 128, BK = 64;
@@ -635,82 +753,253 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   tc_fence_before();
   __syncthreads();
   DW_STAMP(3);
-  // partial -> L2 buffer [tile][split][128][RLD] (rows of 128 consecutive floats per warp pass, coalesced)
-  float* part_me = out.part + ((size_t)tile * S + split) * 128 * RLD;
-  {
-    const int n4 = 128 * RLD / 4;
-    const float4* src = reinterpret_cast<const float4*>(red);
-    float4* dst = reinterpret_cast<float4*>(part_me);
-    for (int k = threadIdx.x; k < n4; k += blockDim.x) __stcg(dst + k, src[k]);
-  }
-  // grid barrier (all CTAs resident: cooperative launch); the counter only grows, the target is the next
-  // multiple of the grid size, so no reset is needed between launches
-  __shared__ uint32_t s_target;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t n = gridDim.x * gridDim.y;
-    const uint32_t old = atomicAdd(reinterpret_cast<uint32_t*>(out.cnt), 1u);
-    const uint32_t target = (old / n + 1u) * n;
-    while ((int32_t)(ld_acquire_gpu(reinterpret_cast<const uint32_t*>(out.cnt)) - target) < 0) __nanosleep(64);
-    s_target = target;
-  }
-  __syncthreads();
-  DW_STAMP(4);
-  // grid-wide reduction: items (tile, row, column group) split evenly over the CTAs, S partials per item
-  constexpr int PER = BN / 4 + 1;  // float4 column groups + the bias group
-  float* const gw0 = out.grad + out.w_off[0];
-  float* const gw1 = out.grad + out.w_off[1];
-  float* const gb0 = out.grad + out.b_off[0];
-  float* const gb1 = out.grad + out.b_off[1];
-  const int row_split = out.row_split, ocols = out.cols;
-  const int ntiles = gridDim.y;
-  const long long n_items = (long long)ntiles * 128 * PER;
-  const int n_cta = gridDim.x * gridDim.y, cid = blockIdx.y * gridDim.x + blockIdx.x;
-  const long long per_cta = (n_items + n_cta - 1) / n_cta;
-  const long long lo = (long long)cid * per_cta, hi = min(n_items, lo + per_cta);
-  bool bad = false;
-  for (long long it = lo + threadIdx.x; it < hi; it += blockDim.x) {
-    const int t = (int)(it / (128 * PER));
-    const int rem = (int)(it - (long long)t * 128 * PER);
-    const int i = rem / PER, g = rem - i * PER;
-    const TileCoord c2 = decode(args, t, args.m_tiles, BN);
-    if (i >= args.M - c2.m0) continue;
-    const int cv = min(BN, ocols - c2.n0);
-    const bool isb = g == BN / 4;
-    if (isb ? c2.ntile != 0 : 4 * g >= cv) continue;
-    const float* src = out.part + ((size_t)t * S * 128 + i) * RLD + 4 * g;
-    float4 v = __ldcg(reinterpret_cast<const float4*>(src));
-    for (int s0 = 1; s0 < S; s0 += 8) {  // splits in order, 8 loads in flight
-      float4 w[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (s0 + q < S) w[q] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(s0 + q) * 128 * RLD));
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (s0 + q < S) { v.x = v.x + w[q].x; v.y = v.y + w[q].y; v.z = v.z + w[q].z; v.w = v.w + w[q].w; }
-    }
-    int rr = c2.m0 + i;
-    bool second = c2.z == 1;
-    if (row_split > 0 && rr >= row_split) { second = true; rr -= row_split; }
-    if (isb) {
-      bad |= !isfinite(v.x);
-      (second ? gb1 : gb0)[rr] = v.x;
-    } else {
-      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
-      const int c = 4 * g;
-      float* dst = (second ? gw1 : gw0) + (long long)rr * ocols + c2.n0 + c;
-      const int nv = cv - c;
-      dst[0] = v.x;
-      if (nv > 1) dst[1] = v.y;
-      if (nv > 2) dst[2] = v.z;
-      if (nv > 3) dst[3] = v.w;
-    }
-  }
-  if (bad) atomicAdd(out.payload + 4, 1.0f);
+  dw_partial_barrier_reduce<BN>(args, out, red, tile, split, S, (int)gridDim.y);
   DW_STAMP(7);
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
-  (void)s_target;
+}
+
+// ------------------------------------------------------------------ dW with a CTA pair (tcgen05 cta_group::2)
+// A thread-block cluster of 2 CTAs (one TPC) computes a 256 x BN output tile for one K-split: CTA r loads its
+// own 128 output rows of A (dZ) and the r-th half of B (the BN/2 activation columns), so each SM receives
+// 2/3 of the bytes of a 128 x BN single-CTA tile for the same MMA work (the per-SM TMA rate, not the tensor
+// core, bounds these skinny GEMMs). Both CTAs' loads complete on the leader's full barrier; the leader alone
+// issues tcgen05.mma.cta_group::2 (M = 256) and multicasts its commits to the empty / accumulator-full
+// barriers of both CTAs; each CTA then drains its own TMEM half (its 128 rows) into the shared split-K tail.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's smem, completing on an mbarrier of either CTA of the pair (shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t mbar_cluster, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `bar` (same offset) in both CTAs
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+
+template <int BN>
+struct Dw2Cfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;        // own 128 rows
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // own half of the columns
+  static constexpr int ONES_BYTES = 16 * 128;
+  static constexpr int FIXED = 1024 + ONES_BYTES + 512;
+  static constexpr int STAGES_FIT = (232448 - FIXED) / (A_BYTES + B_BYTES);
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int ACC_COLS = ((BN + 16) + 31) / 32 * 32;
+  static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : ACC_COLS <= 256 ? 256 : 512;
+  static constexpr int SMEM = FIXED + STAGES * (A_BYTES + B_BYTES);
+};
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw2(const __grid_constant__ GemmArgs args, const DwOut out) {
+  using C = Dw2Cfg<BN>;
+  constexpr int RLD = BN + 20;
+  static_assert(BN % 128 == 0, "each CTA loads whole 64-column atoms of its half");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  float* red = reinterpret_cast<float*>(smem);  // reuses the operand ring after the last MMA
+  uint8_t* sOnes = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
+  static_assert(128 * RLD * 4 <= C::STAGES * (C::A_BYTES + C::B_BYTES), "reduction buffer must fit the ring");
+
+  DW_STAMP(0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int S = gridDim.x / 2;  // splits per pair tile
+  const int split = blockIdx.x >> 1;
+  // pair tile blockIdx.y -> (z, m-pair, n-tile); this CTA's 128-row tile index in decode() order
+  const int n_t = args.n_tiles;
+  const int ntile = blockIdx.y % n_t;
+  const int pr = blockIdx.y / n_t;
+  const int mpairs = args.m_tiles / 2;
+  const int mt = (pr % mpairs) * 2 + (int)rank, z = pr / mpairs;
+  const int tile = (z * args.m_tiles + mt) * n_t + ntile;
+  const int m0 = mt * 128, n0 = ntile * BN;
+  const bool bias_col = ntile == 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tfull[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    uint32_t* o = reinterpret_cast<uint32_t*>(sOnes);
+    for (int k = threadIdx.x; k < C::ONES_BYTES / 4; k += blockDim.x) o[k] = 0x3F803F80u;
+    fence_async_smem();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_barrier();  // both CTAs' barriers initialised and TMEM allocated before any cross-CTA signal
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  DW_STAMP(1);
+  const int kb0 = split * args.kb_per_split;
+  const int nkb = max(0, min(args.kb_per_split, args.kb_total - kb0));
+  const CUtensorMap* tmA = &args.tmA[z];
+  const CUtensorMap* tmB = &args.tmB[z];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        const int k0 = (kb0 + kb) * C::BK;
+        uint8_t* a = sA + stage * C::A_BYTES;
+        uint8_t* b = sB + stage * C::B_BYTES;
+        if (rank == 0) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+        tma_load_2d_pair(tmA, fb, a, m0, k0);
+        tma_load_2d_pair(tmA, fb, a + 8192, m0 + 64, k0);
+#pragma unroll
+        for (int i = 0; i < BN / 128; ++i)
+          tma_load_2d_pair(tmB, fb, b + i * 8192, n0 + (int)rank * (BN / 2) + 64 * i, k0);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(256, BN, true, true);
+      constexpr uint32_t idesc_ones = idesc_bf16(256, 16, true, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k) {
+          const uint64_t ad = sdesc(a0 + k * 2048u, 8192u, 1024u);
+          const uint64_t bd = sdesc(b0 + k * 2048u, 8192u, 1024u);
+          tc_mma_pair(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          if (bias_col) {
+            const uint64_t od = sdesc(smem_u32(sOnes) + k * 32u, 0u, 1024u);
+            tc_mma_pair(tmem + BN, ad, od, idesc_ones, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+        }
+        tc_commit_pair(&empty[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+      }
+      if (nkb > 0) tc_commit_pair(&tfull[0]);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // TMEM (this CTA's 128 rows) -> smem partial (an empty split contributes zeros)
+    const int e = warp - 4, q = e & 3, h = e >> 2;
+    const int row = q * 32 + lane;
+    if (nkb > 0) {
+      mbar_wait(&tfull[0], 0);
+      __syncwarp();
+      tc_fence_after();
+    }
+    if (out.dbg && threadIdx.x == 128) out.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + 2] = gtimer();
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    for (int c = h * (BN / 2); c < (h + 1) * (BN / 2); c += 32) {
+      uint32_t r[32];
+      if (nkb > 0) {
+        tmem_ld32_nowait(tbase + c, r);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) r[k] = 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 32; k += 4)
+        *reinterpret_cast<float4*>(red + row * RLD + c + k) =
+            make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]), __uint_as_float(r[k + 2]), __uint_as_float(r[k + 3]));
+    }
+    if (h == 0) {
+      uint32_t r[32];
+      if (nkb > 0 && bias_col) {
+        tmem_ld32_nowait(tbase + BN, r);
+        tmem_wait_ld();
+      }
+      *reinterpret_cast<float4*>(red + row * RLD + BN) =
+          make_float4((nkb > 0 && bias_col) ? __uint_as_float(r[0]) : 0.0f, 0.0f, 0.0f, 0.0f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  DW_STAMP(3);
+  (void)m0;
+  dw_partial_barrier_reduce<BN>(args, out, red, tile, split, S, args.nz * args.m_tiles * args.n_tiles);
+  DW_STAMP(7);
+  tc_fence_before();
+  cluster_barrier();  // both CTAs are done with the pair's TMEM
+  tc_fence_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+}
+
+template <int BN>
+static cudaError_t launch_dw2_bn(const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
+  using C = Dw2Cfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_dw2<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int pair_tiles = a.nz * (a.m_tiles / 2) * a.n_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * S, pair_tiles, 1);
+  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_gemm_dw2<BN>, a, o);
+}
+
+// CTA-pair variant (requires an even number of 128-row tiles per z and BN in {128, 256}); S = splits per pair
+// tile, 2 * S * pair_tiles <= #SMs
+static int g_dw_max_ctas();
+cudaError_t launch_gemm_dw_pair(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
+  if (S < 1 || (a.m_tiles & 1) || 2 * S * a.nz * (a.m_tiles / 2) * a.n_tiles > g_dw_max_ctas()) return cudaErrorInvalidValue;
+  switch (bn) {
+    case 128: return launch_dw2_bn<128>(a, o, S, st);
+    case 256: return launch_dw2_bn<256>(a, o, S, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // ------------------------------------------------------------------ host side

@@ -82,6 +82,8 @@ struct DwOut {                 // canonical destinations of a weight-gradient GE
 // split-K over S CTAs per output tile in one cooperative wave (S * tiles <= #SMs), deterministic reduction
 // of the S fp32 partials through L2 by the whole grid
 cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);
+// the same with CTA pairs (tcgen05 cta_group::2, 256-row tiles): even m_tiles, bn in {128, 256}
+cudaError_t launch_gemm_dw_pair(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);
 cudaError_t launch_gemm_dw_kmajor(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);  // diagnostics
 
 // ------------------------------------------------------------------ PPO kernels (ppo.cu)

@@ -1,5 +1,5 @@
-"""Build tools/gemm_probe{0,1,2} (diagnostics only): the library's GEMM translation unit compiled with each
-mbarrier wait strategy (LG_MBAR_MODE 0 = try_wait with suspend hint, 1 = try_wait, 2 = test_wait spin)."""
+"""Build tools/gemm_probe{1,3} (diagnostics only): the library's GEMM translation unit compiled with each
+mbarrier wait strategy (LG_MBAR_MODE 1 = try_wait (default), 3 = bounded wait reporting stuck barriers)."""
 import os
 import subprocess
 import sys
@@ -10,7 +10,7 @@ from paper_2109_11978_b200 import build as B  # noqa: E402
 
 inc, _ = B._nccl_dirs()
 rc = 0
-for mode in (0, 1, 2):
+for mode in (1, 3):
     obj = os.path.join(B.BUILD, f"gemm_tc_probe{mode}.o")
     cmd = [B.NVCC, *B.FLAGS, f"-DLG_MBAR_MODE={mode}", "-I", os.path.join(ROOT, "include"), "-c",
            os.path.join(B.CSRC, "gemm_tc.cu"), "-o", obj]

@@ -221,7 +221,8 @@ static void probe_dw_kmajor(int Nout, int Nin, int K, int bn, int S, int G, cuda
 }
 
 // phase timestamps of every CTA of one dW launch (globaltimer ns, relative to the earliest CTA start)
-static void probe_dw_phases(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st, int dmode = 0) {
+static void probe_dw_phases(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st, int dmode = 0,
+                            bool pair = false) {
   __nv_bfloat16 *dZ, *X;
   float *grad, *part;
   int* cnt;
@@ -247,7 +248,15 @@ static void probe_dw_phases(int Nout, int Nin, int K, int bn, int S, int G, cuda
   memset(&o, 0, sizeof(o));
   o.grad = grad; o.b_off[0] = (long long)Nout * Nin; o.cols = Nin; o.payload = grad + (size_t)Nout * Nin + Nout;
   o.G = G; o.part = part; o.cnt = cnt; o.dbg = dbg; o.dbg_mode = dmode;
-  for (int r = 0; r < 4; ++r) CK(launch_gemm_dw(bn, g, o, S, st));
+  for (int r = 0; r < 4; ++r) {
+    if (pair) {
+      GemmArgs gp = g;
+      gp.kb_per_split = (g.kb_total + S - 1) / S;
+      CK(launch_gemm_dw_pair(bn, gp, o, S, st));
+    } else {
+      CK(launch_gemm_dw(bn, g, o, S, st));
+    }
+  }
   CK(cudaStreamSynchronize(st));
   std::vector<unsigned long long> h((size_t)nct * 8);
   CK(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -260,11 +269,69 @@ static void probe_dw_phases(int Nout, int Nin, int K, int bn, int S, int G, cuda
       avg[k] += v / nct;
       mx[k] = std::max(mx[k], v);
     }
-  printf("dw phases Nout=%d Nin=%d K=%d S=%d G=%d ctas=%d kb/cta=%d dbg_mode=%d (us from first CTA start; avg | max):\n",
-         Nout, Nin, K, S, G, nct, g.kb_per_split, dmode);
-  const char* nm[8] = {"start", "tmem alloc", "mma done", "partial->smem", "grid barrier", "-", "-", "reduced"};
+  printf("dw phases%s Nout=%d Nin=%d K=%d S=%d G=%d ctas=%d kb/cta=%d dbg_mode=%d (us from first CTA start; avg | max):\n",
+         pair ? " (CTA pair)" : "", Nout, Nin, K, S, G, nct, g.kb_per_split, dmode);
+  const char* nm[8] = {"start", "tmem alloc", "mma done", "partial->smem", "partial->L2", "grid barrier", "reduced", "end"};
   for (int k = 0; k < 8; ++k) printf("   %-14s %8.2f | %8.2f\n", nm[k], avg[k], mx[k]);
   CK(cudaFree(dZ)); CK(cudaFree(X)); CK(cudaFree(grad)); CK(cudaFree(part)); CK(cudaFree(cnt)); CK(cudaFree(dbg));
+}
+
+// CTA-pair dW (launch_gemm_dw_pair, S splits per 256-row pair tile) vs the single-CTA kernel (2S splits)
+static void probe_dw_pair(int Nout, int Nin, int K, int bn, int S, cudaStream_t st) {
+  __nv_bfloat16 *dZ, *X;
+  float *g1, *g2, *part;
+  int* cnt;
+  const size_t gsz = (size_t)Nout * Nin + Nout + 64;
+  CK(cudaMalloc(&dZ, (size_t)K * Nout * 2)); CK(cudaMalloc(&X, (size_t)K * Nin * 2));
+  CK(cudaMalloc(&g1, gsz * 4)); CK(cudaMalloc(&g2, gsz * 4));
+  fill(dZ, (size_t)K * Nout); fill(X, (size_t)K * Nin);
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  make_tmap_bf16(&g.tmA[0], dZ, K, Nout, Nout, 64);
+  make_tmap_bf16(&g.tmB[0], X, K, Nin, Nin, 64);
+  g.M = Nout; g.N = Nin; g.m_tiles = (Nout + 127) / 128; g.nz = 1;
+  g.kb_total = (K + 63) / 64; g.n_tiles = (Nin + bn - 1) / bn; g.n_splits = 1;
+  const int tiles = g.m_tiles * g.n_tiles;
+  GemmArgs g1a = g, g2a = g;
+  const int S1 = std::min(S, g.kb_total);  // single-CTA: 128-row tiles, same CTA count
+  g1a.kb_per_split = (g.kb_total + S1 - 1) / S1;
+  const int S1e = (g.kb_total + g1a.kb_per_split - 1) / g1a.kb_per_split;
+  g2a.kb_per_split = (g.kb_total + S - 1) / S;
+  const int S2e = (g.kb_total + g2a.kb_per_split - 1) / g2a.kb_per_split;
+  const int Smax = std::max(S1e, S2e);
+  CK(cudaMalloc(&part, (size_t)tiles * Smax * 128 * (bn + 20) * 4));
+  CK(cudaMalloc(&cnt, 256)); CK(cudaMemset(cnt, 0, 256));
+  DwOut o;
+  memset(&o, 0, sizeof(o));
+  o.grad = g1; o.b_off[0] = (long long)Nout * Nin; o.cols = Nin; o.payload = g1 + (size_t)Nout * Nin + Nout;
+  o.G = 1; o.part = part; o.cnt = cnt;
+  DwOut o2 = o;
+  o2.grad = g2; o2.payload = g2 + (size_t)Nout * Nin + Nout;
+  const double fl = 2.0 * Nout * Nin * K;
+  printf("  [pair probe Nout=%d Nin=%d K=%d S=%d] single-CTA timing...\n", Nout, Nin, K, S);
+  float u1 = time_us([&] { CK(launch_gemm_dw(bn, g1a, o, S1e, st)); }, st);
+  printf("  one pair launch...\n");
+  CK(launch_gemm_dw_pair(bn, g2a, o2, S2e, st));
+  CK(cudaStreamSynchronize(st));
+  printf("  pair timing...\n");
+  float u2 = time_us([&] { CK(launch_gemm_dw_pair(bn, g2a, o2, S2e, st)); }, st);
+  printf("dw Nout=%d Nin=%d K=%d bn=%d  single-CTA (%d splits, %d CTAs) %8.2f us (%6.1f TF)  CTA-pair (%d splits, %d CTAs) %8.2f us (%6.1f TF)\n",
+         Nout, Nin, K, bn, S1e, S1e * tiles, u1, fl / u1 * 1e-6, S2e, 2 * S2e * tiles / 2, u2, fl / u2 * 1e-6);
+  CK(cudaMemset(g1, 0, gsz * 4)); CK(cudaMemset(g2, 0, gsz * 4));
+  CK(launch_gemm_dw(bn, g1a, o, S1e, st));
+  CK(launch_gemm_dw_pair(bn, g2a, o2, S2e, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<float> a(gsz), b(gsz);
+  CK(cudaMemcpy(a.data(), g1, gsz * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(b.data(), g2, gsz * 4, cudaMemcpyDeviceToHost));
+  double num = 0, den = 0, mx = 0;
+  for (size_t i = 0; i + 64 < gsz; ++i) {
+    num += (a[i] - b[i]) * (double)(a[i] - b[i]); den += (double)a[i] * a[i];
+    mx = std::max(mx, (double)std::fabs(a[i] - b[i]));
+  }
+  printf("   pair vs single: rel l2 %.3e  max abs %.3e  (bias[0] %g vs %g)\n", std::sqrt(num / den), mx,
+         a[(size_t)Nout * Nin], b[(size_t)Nout * Nin]);
+  CK(cudaFree(dZ)); CK(cudaFree(X)); CK(cudaFree(g1)); CK(cudaFree(g2)); CK(cudaFree(part)); CK(cudaFree(cnt));
 }
 
 static void check_dw(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st) {
@@ -282,6 +349,7 @@ __global__ void k_empty(int* p) {
 }
 
 int main(int argc, char** argv) {
+  setvbuf(stdout, nullptr, _IONBF, 0);
   cudaStream_t st;
   CK(cudaStreamCreate(&st));
   CK(cudaMalloc(&g_flush, 512u << 20));
@@ -315,10 +383,20 @@ int main(int argc, char** argv) {
     return 0;
   }
   if (!strcmp(which, "phases")) {
+    probe_dw_phases(1024, 240, 24576, 256, 18, 1, st, 0, true);
+    probe_dw_phases(512, 512, 24576, 256, 18, 1, st, 0, true);
     probe_dw_phases(1024, 240, 24576, 256, 18, 1, st);   // dW1 (both nets): 8 tiles x 18
     probe_dw_phases(512, 512, 24576, 256, 18, 1, st);    // dW2 both nets as 8 tiles
     probe_dw_phases(256, 256, 24576, 256, 74, 1, st);    // dW3 both nets as 2 tiles
     probe_dw_phases(128, 64, 64, 64, 1, 1, st);
+    return 0;
+  }
+  if (!strcmp(which, "pair")) {
+    probe_dw_pair(256, 128, 640, 256, 2, st);       // small sanity: 1 pair tile, 2 splits
+    probe_dw_pair(1024, 240, 24576, 256, 18, st);   // dW1 (both nets): 4 pair tiles x 18 splits = 144 CTAs
+    probe_dw_pair(512, 512, 24576, 256, 18, st);    // dW2 both nets as 4 pair tiles
+    probe_dw_pair(1024, 240, 24576, 256, 12, st);
+    probe_dw_pair(512, 512, 24576, 256, 12, st);
     return 0;
   }
   if (!strcmp(which, "kmaj")) {
