@@ -165,92 +165,102 @@ __device__ __forceinline__ void fill_obs_rec(const St& s, ObsRec& o) {
   o.px = s.p[0]; o.py = s.p[1]; o.pz = s.p[2];
 }
 
-__device__ __forceinline__ float noise_scale(int e) {
-  if (e < 3) return 0.01f;
-  if (e < 6) return 0.2f;
-  if (e < 9) return 0.05f;
-  if (e < 12) return 0.0f;
-  if (e < 24) return 0.01f;
-  if (e < 36) return 1.5f;
-  if (e < 48) return 0.0f;
-  return 0.1f;
-}
+// Observation rows (DESIGN.md §3.7 step 10): 64 threads per env row (2 rows per 128-thread block, no
+// index division); thread gq owns the items gq, gq+64, ...; item gq = the 4 consecutive elements
+// [4gq, 4gq+4) = one Philox block of noise words
+// (two when a reset shifted the row's first word) and writes them as one 8-byte bf16x4 store. Proprioceptive
+// items (4gq < 48) read one float4 of the record; scan items step through the scan grid incrementally.
+// Blocks [0, ceil(N/2)) write the post-step rows of OBS slot `slot`; with `with_terminal` the next
+// ceil(N/2) blocks write the pre-reset rows of this step's time-outs (records < n_to) into the rollout's
+// compacted time-out buffer (row = the record's destination row).
+__constant__ float c_noise_scale[48] = {0.01f, 0.01f, 0.01f, 0.2f, 0.2f, 0.2f, 0.05f, 0.05f, 0.05f, 0.0f, 0.0f, 0.0f,
+                                        0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f,
+                                        1.5f, 1.5f, 1.5f, 1.5f, 1.5f, 1.5f, 1.5f, 1.5f, 1.5f, 1.5f, 1.5f, 1.5f,
+                                        0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+constexpr int OBS_ROWS_PER_BLOCK = 2;
 
-// one observation element e of record o
-__device__ __forceinline__ float obs_elem(const EnvParams& P, const World& W, const ObsRec& o, int e) {
-  if (e < 48) return o.pro[e];
-  int k = e - 48;
-  int ix = k / P.scan_ny, iy = k - ix * P.scan_ny;
-  float dx = (float)(ix - P.scan_nx / 2) * 0.1f;
-  float dy = (float)(iy - P.scan_ny / 2) * 0.1f;
-  float x = o.px + (o.c * dx - o.s * dy);
-  float y = o.py + (o.s * dx + o.c * dy);
-  return o.pz - h_bilinear(W, x, y);
-}
-
-// Observation rows (DESIGN.md §3.7 step 10): one thread per item = 4 consecutive elements of one row
-// = one Philox block of noise; written as one 8-byte bf16x4 store, so consecutive threads write
-// consecutive bytes of a row. Items [0, N*G) are the post-step rows of OBS slot `slot`; items
-// [N*G, 2*N*G) are the compacted pre-reset rows of time-out envs (rows < n_to, for the bootstrap critic).
-__global__ void __launch_bounds__(256) k_env_obs(EnvParams P, int ev_off, __nv_bfloat16* __restrict__ dst_bf16,
-                                                 float* __restrict__ dst_f32, int with_terminal) {
+__global__ void __launch_bounds__(64 * OBS_ROWS_PER_BLOCK) k_env_obs(EnvParams P, int ev_off,
+                                                                     __nv_bfloat16* __restrict__ dst_bf16,
+                                                                     float* __restrict__ dst_f32, int with_terminal) {
   const int D = P.obs_dim, Dp = P.obs_stride, G = Dp / 4;
   const uint32_t ev = P.scalars->s_base + (uint32_t)ev_off;
-  const int NG = P.N * G;
-  int it = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nb_main = (P.N + OBS_ROWS_PER_BLOCK - 1) / OBS_ROWS_PER_BLOCK;
+  int r = (int)blockIdx.x * OBS_ROWS_PER_BLOCK + (int)(threadIdx.x >> 6);
   const ObsRec* recs = reinterpret_cast<const ObsRec*>(P.recs);
   __nv_bfloat16* dst = dst_bf16;
   float* df = dst_f32;
-  if (it >= NG) {
+  if ((int)blockIdx.x >= nb_main) {
     if (!with_terminal) return;
-    it -= NG;
-    if (it >= P.scalars->n_to * G) return;
+    r -= nb_main * OBS_ROWS_PER_BLOCK;
+    if (r >= P.scalars->n_to) return;
     recs = reinterpret_cast<const ObsRec*>(P.trecs);
     dst = P.term_obs;
     df = nullptr;
+  } else if (r >= P.N) {
+    return;
   }
-  const int r = it / G, gq = it - r * G;
-  const ObsRec& o = recs[r];
-  if (o.row < 0) return;  // time-out beyond the compacted buffer's capacity (not reachable for T <= 1000)
-  World W{P.hf, P.R, P.C, P.inv_cell};
-  Rng rng{P.seed_lo, P.seed_hi};
-  float v[4];
-  U4 nb0, nb1;
-  const bool noise = (P.flags & F_NOISE) != 0;
-  const uint32_t wbase = o.word0 + 4u * (uint32_t)gq;
-  if (noise && 4 * gq < D) {
-    nb0 = rng.block(wbase >> 2, o.g, ev, TAG_OBS);
-    if (wbase & 3u) nb1 = rng.block((wbase >> 2) + 1, o.g, ev, TAG_OBS);
-  }
+  const ObsRec* o = recs + r;
+  const int row = o->row;
+  if (row < 0) return;  // time-out beyond the compacted buffer's capacity (not reachable for T <= 1000)
+  for (int gq = threadIdx.x & 63; gq < G; gq += 64) {
+  const int e0 = 4 * gq;
+  float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  float sc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if (e0 < 48) {
+    const float4 p4 = *reinterpret_cast<const float4*>(o->pro + e0);
+    v[0] = p4.x; v[1] = p4.y; v[2] = p4.z; v[3] = p4.w;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int e = 4 * gq + k;
-    float x = 0.0f;
-    if (e < D) {
-      x = obs_elem(P, W, o, e);
-      if (noise) {
-        const float sc = noise_scale(e);
-        if (sc != 0.0f) {
-          const uint32_t w = wbase + (uint32_t)k;
-          const uint32_t word = ((w >> 2) == (wbase >> 2)) ? pick(nb0, w) : pick(nb1, w);
-          x = x + usym(sc, word);
-        }
+    for (int j = 0; j < 4; ++j) sc[j] = c_noise_scale[e0 + j];
+  } else {
+    World W{P.hf, P.R, P.C, P.inv_cell};
+    const float px = o->px, py = o->py, pz = o->pz, c = o->c, sn = o->s;
+    const int k0 = e0 - 48;
+    int ix = k0 / P.scan_ny, iy = k0 - ix * P.scan_ny;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (e0 + j < D) {
+        const float dx = (float)(ix - P.scan_nx / 2) * 0.1f;
+        const float dy = (float)(iy - P.scan_ny / 2) * 0.1f;
+        const float x = px + (c * dx - sn * dy);
+        const float y = py + (sn * dx + c * dy);
+        v[j] = pz - h_bilinear(W, x, y);
+        sc[j] = 0.1f;
       }
-      if (df) df[(size_t)o.row * D + e] = x;
+      if (++iy == P.scan_ny) { iy = 0; ++ix; }
     }
-    v[k] = x;
+  }
+  if ((P.flags & F_NOISE) && (sc[0] != 0.0f || sc[1] != 0.0f || sc[2] != 0.0f || sc[3] != 0.0f)) {
+    Rng rng{P.seed_lo, P.seed_hi};
+    const uint32_t wbase = o->word0 + 4u * (uint32_t)gq;
+    const U4 nb0 = rng.block(wbase >> 2, o->g, ev, TAG_OBS);
+    U4 nb1 = nb0;
+    if (wbase & 3u) nb1 = rng.block((wbase >> 2) + 1, o->g, ev, TAG_OBS);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (sc[j] != 0.0f) {
+        const uint32_t w = wbase + (uint32_t)j;
+        const uint32_t word = ((w >> 2) == (wbase >> 2)) ? pick(nb0, w) : pick(nb1, w);
+        v[j] = v[j] + usym(sc[j], word);
+      }
+    }
+  }
+  if (df) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (e0 + j < D) df[(size_t)row * D + e0 + j] = v[j];
   }
   __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
   uint2 pk;
   pk.x = *reinterpret_cast<uint32_t*>(&lo);
   pk.y = *reinterpret_cast<uint32_t*>(&hi);
-  *reinterpret_cast<uint2*>(dst + (size_t)o.row * Dp + 4 * gq) = pk;
+  *reinterpret_cast<uint2*>(dst + (size_t)row * Dp + e0) = pk;
+  }
 }
 
 static void launch_obs(const EnvParams& P, int ev_off, __nv_bfloat16* dst, float* f32, int with_terminal,
                        cudaStream_t st) {
-  const long long items = (long long)P.N * (P.obs_stride / 4) * (with_terminal ? 2 : 1);
-  k_env_obs<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(P, ev_off, dst, f32, with_terminal);
+  const int nb_main = (P.N + OBS_ROWS_PER_BLOCK - 1) / OBS_ROWS_PER_BLOCK;
+  k_env_obs<<<nb_main * (with_terminal ? 2 : 1), 64 * OBS_ROWS_PER_BLOCK, 0, st>>>(P, ev_off, dst, f32, with_terminal);
 }
 
 // ------------------------------------------------------------------ kernels
