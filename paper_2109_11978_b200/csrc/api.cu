@@ -71,6 +71,8 @@ Canon canon_of(const Dims& d) {
 }
 
 int bn_for(int n) { return n >= 256 ? 256 : (n > 64 ? 128 : 64); }
+// input-gradient GEMMs (epilogue bound, short K): 256-wide tiles only above 256 columns (measured)
+int bn_dx(int n) { return n > 256 ? 256 : (n > 64 ? 128 : 64); }
 // narrower tiles while the GEMM still fits one wave: small-M (rollout) GEMMs are latency bound, more CTAs win
 int bn_small(int n, int m_rows, int nz) {
   const int mt = (m_rows + 127) / 128;
@@ -471,8 +473,8 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     cmap(&x2.tmC[z], dZ1 + z * d.H0, d.H0, 2 * d.H0);
     x2.aux[z] = H1 + z * d.H0;
   }
-  set_fwd_common(x3, d.Mmb, d.H1, d.H2, bn_for(d.H1), 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
-  set_fwd_common(x2, d.Mmb, d.H0, d.H1, bn_for(d.H0), 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
+  set_fwd_common(x3, d.Mmb, d.H1, d.H2, bn_dx(d.H1), 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
+  set_fwd_common(x2, d.Mmb, d.H0, d.H1, bn_dx(d.H0), 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
   // ---- backward dW (A = dZ MN-major, B = activations MN-major), split-K over the minibatch
   auto dw_setup = [&](GemmArgs& g, const DwPlan& p, int nz) {
     g.M = p.rows; g.N = p.N; g.M_dev = nullptr;
@@ -853,12 +855,12 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
   if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
   GemmArgs x3 = ctx->dx3;
   x3.M = d.Mmb;
-  if ((s = gemm(ctx, GEMM_DX, x3, bn_for(d.H1), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_DX, x3, bn_dx(d.H1), 2)) != LG_OK) return s;
   // layer 2
   if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   GemmArgs x2 = ctx->dx2;
   x2.M = d.Mmb;
-  if ((s = gemm(ctx, GEMM_DX, x2, bn_for(d.H0), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_DX, x2, bn_dx(d.H0), 2)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
   if ((s = dw(ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
   return LG_OK;

@@ -374,10 +374,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
       if (EPI == 2 && active) {
         const int nb = tc.n0 + h * WCOLS;
         const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nb);
+        if (row < M && nb + 64 <= args.N) {  // whole 64-column chunk in range (the common case)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint4 u = (row < M && nb + 8 * j < args.N) ? a4[j] : make_uint4(0, 0, 0, 0);
-          av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+          for (int j = 0; j < 8; ++j) {
+            const uint4 u = __ldg(a4 + j);
+            av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4 u = (row < M && nb + 8 * j < args.N) ? a4[j] : make_uint4(0, 0, 0, 0);
+            av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+          }
         }
       }
       mbar_wait(&tfull[acc], aph);
@@ -438,10 +446,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
               for (int k = 0; k < 64; k += 2) {
                 const uint32_t* rr = k < 32 ? r0 : r1;
                 const int kk = k & 31;
-                uint32_t w = av[k / 2];
-                float2 hf = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w));
-                const float g0 = __uint_as_float(rr[kk]) * (hf.x > 0.0f ? 1.0f : hf.x + 1.0f);
-                const float g1 = __uint_as_float(rr[kk + 1]) * (hf.y > 0.0f ? 1.0f : hf.y + 1.0f);
+                const uint32_t w = av[k / 2];
+                // ELU'(x) from the saved output h = ELU(x) > -1: h > 0 ? 1 : h + 1 == min(h + 1, 1) (h + 1 exact)
+                const float h0 = __uint_as_float(w << 16), h1 = __uint_as_float(w & 0xFFFF0000u);
+                const float g0 = __uint_as_float(rr[kk]) * fminf(h0 + 1.0f, 1.0f);
+                const float g1 = __uint_as_float(rr[kk + 1]) * fminf(h1 + 1.0f, 1.0f);
                 __nv_bfloat162 o = __floats2bfloat162_rn(g0, g1);
                 pk[k / 2] = *reinterpret_cast<uint32_t*>(&o);
               }
@@ -449,10 +458,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
             if (EPI == 2 && c + 64 < (h + 1) * WCOLS) {  // prefetch the next chunk's saved activation
               const int nn = nb + 64;
               const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nn);
+              if (row < M && nn + 64 <= args.N) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                uint4 u = (row < M && nn + 8 * j < args.N) ? a4[j] : make_uint4(0, 0, 0, 0);
-                av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+                for (int j = 0; j < 8; ++j) {
+                  const uint4 u = __ldg(a4 + j);
+                  av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  uint4 u = (row < M && nn + 8 * j < args.N) ? a4[j] : make_uint4(0, 0, 0, 0);
+                  av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+                }
               }
             }
             uint8_t* buf = mybuf + (nst & 1) * C::EPI_BUF;

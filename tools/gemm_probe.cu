@@ -107,6 +107,29 @@ static void probe_fwd(int M, int N, int K, int bn, cudaStream_t st) {
   CK(cudaFree(X)); CK(cudaFree(W)); CK(cudaFree(Y)); CK(cudaFree(bias));
 }
 
+// input gradient: dZp[M][N] = (dZ[M][K] W[K][N]) * ELU'(H[M][N])  (A K-major, B = W[out=K][in=N] MN-major)
+static void probe_dx(int M, int N, int K, int bn, cudaStream_t st, bool once = false) {
+  __nv_bfloat16 *dZ, *W, *H, *Y;
+  CK(cudaMalloc(&dZ, (size_t)M * K * 2)); CK(cudaMalloc(&W, (size_t)K * N * 2));
+  CK(cudaMalloc(&H, (size_t)M * N * 2)); CK(cudaMalloc(&Y, (size_t)M * N * 2));
+  fill(dZ, (size_t)M * K); fill(W, (size_t)K * N); fill(H, (size_t)M * N);
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  make_tmap_bf16(&g.tmA[0], dZ, M, K, K, 128);
+  make_tmap_bf16(&g.tmB[0], W, K, N, N, 64);
+  make_tmap_bf16(&g.tmC[0], Y, M, N, N, 32);
+  g.M = M; g.N = N; g.m_tiles = (M + 127) / 128; g.nz = 1;
+  g.kb_total = (K + 63) / 64; g.kb_per_split = g.kb_total; g.n_tiles = (N + bn - 1) / bn; g.n_splits = 1;
+  g.ldo = N; g.aux[0] = H; g.ld_aux = N;
+  const double fl = 2.0 * M * N * K;
+  for (int probe = 0; probe < (once ? 1 : 3); ++probe) {
+    g.probe = probe;
+    float us = time_us([&] { CK(launch_gemm(GEMM_DX, bn, g, st)); }, st);
+    printf("dx M=%d N=%d K=%d bn=%d probe=%d  %8.2f us  %7.1f TFLOP/s\n", M, N, K, bn, probe, us, fl / us * 1e-6);
+  }
+  CK(cudaFree(dZ)); CK(cudaFree(W)); CK(cudaFree(H)); CK(cudaFree(Y));
+}
+
 // weight gradient: dW[N_out][N_in] = dZ[K][N_out]^T X[K][N_in], split-K over G clusters of S per tile
 static std::vector<float> probe_dw(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st, bool quiet = false) {
   __nv_bfloat16 *dZ, *X;
@@ -355,7 +378,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&g_flush, 512u << 20));
   const char* which = argc > 1 ? argv[1] : "all";
   if (argc > 2 && !strcmp(argv[2], "noflush")) g_do_flush = false;
-  if (!strcmp(which, "one") || !strcmp(which, "onefwd")) g_do_flush = false;
+  if (!strcmp(which, "one") || !strcmp(which, "onefwd") || !strcmp(which, "onedx")) g_do_flush = false;
   if (argc > 2 && !strcmp(argv[2], "batch")) { g_do_flush = false; g_batch = true; }
   printf("L2 flush between reps: %s\n", g_do_flush ? "yes" : "no");
   {
@@ -372,6 +395,18 @@ int main(int argc, char** argv) {
   if (!strcmp(which, "one") && argc >= 9) {  // one dW config: one Nout Nin K bn S G (for ncu)
     g_do_flush = false;
     probe_dw(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), atoi(argv[6]), atoi(argv[7]), st, true);
+    return 0;
+  }
+  if (!strcmp(which, "dx")) {
+    probe_dx(24576, 512, 256, 256, st);   // dX2: dZ1 = dZ2 W2 (per net), K = H1 = 256
+    probe_dx(24576, 512, 256, 128, st);
+    probe_dx(24576, 256, 128, 256, st);   // dX3: dZ2 = dZ3 W3 (per net), K = H2 = 128
+    probe_dx(24576, 256, 128, 128, st);
+    return 0;
+  }
+  if (!strcmp(which, "onedx") && argc >= 6) {
+    g_do_flush = false;
+    probe_dx(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), st, true);
     return 0;
   }
   if (!strcmp(which, "roll")) {  // rollout-size forward GEMMs (M = 4096 envs) at different tile widths
