@@ -203,6 +203,10 @@ struct lg_ctx {
   Canon cn;
   void* buf[LG_NUM_BUFFERS];
   cudaStream_t st;
+  // second stream for the weight-gradient GEMMs: dW_l only reads dZ_l, so it runs beside dX_l (fork/join by
+  // events, captured as graph edges)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork[3] = {nullptr, nullptr, nullptr}, ev_join = nullptr;
   lg_status err = LG_OK;
   std::string msg;
   int world = 1;
@@ -233,16 +237,17 @@ namespace {
 struct Scope {
   lg_ctx* c;
   int cat, a = -1;
-  Scope(lg_ctx* c_, int cat_) : c(c_), cat(cat_) {
+  cudaStream_t s;
+  Scope(lg_ctx* c_, int cat_, cudaStream_t s_ = nullptr) : c(c_), cat(cat_), s(s_ ? s_ : c_->st) {
     if (c->prof && c->evn + 2 <= c->ev.size()) {
       a = (int)c->evn++;
-      cudaEventRecordWithFlags(c->ev[a], c->st, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+      cudaEventRecordWithFlags(c->ev[a], s, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     }
   }
   ~Scope() {
     if (a >= 0) {
       int b = (int)c->evn++;
-      cudaEventRecordWithFlags(c->ev[b], c->st, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+      cudaEventRecordWithFlags(c->ev[b], s, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
       c->pairs.push_back({cat, a, b});
     }
   }
@@ -357,6 +362,18 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   ctx->cn = canon_of(ctx->d);
   for (int i = 0; i < LG_NUM_BUFFERS; ++i) ctx->buf[i] = buffers_h[i];
   ctx->st = reinterpret_cast<cudaStream_t>(stream);
+  {
+    int lo = 0, hi = 0, prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (ctx->st) cudaStreamGetPriority(ctx->st, &prio);
+    bool ok2 = cudaStreamCreateWithPriority(&ctx->st2, cudaStreamNonBlocking, prio) == cudaSuccess;
+    for (int k = 0; k < 3; ++k) ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_fork[k], cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok2) {
+      delete ctx;
+      return LG_ERR_CUDA;
+    }
+  }
   ctx->world = cfg->world_size;
   const Dims& d = ctx->d;
   const Layout& L = ctx->L;
@@ -559,6 +576,9 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
 
 lg_status lg_destroy(lg_ctx* ctx) {
   if (!ctx) return LG_ERR_INVALID_ARG;
+  if (ctx->st2) { cudaStreamSynchronize(ctx->st2); cudaStreamDestroy(ctx->st2); }
+  for (int k = 0; k < 3; ++k) if (ctx->ev_fork[k]) cudaEventDestroy(ctx->ev_fork[k]);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -846,23 +866,35 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
     o.cols = cols;
     o.row_split = row_split;
     o.payload = ctx->payload;
-    Scope sc_(ctx, LG_PROF_GEMM_DW);
-    cudaError_t e = p.pair ? launch_gemm_dw_pair(p.bn, g, o, p.S, ctx->st) : launch_gemm_dw(p.bn, g, o, p.S, ctx->st);
+    Scope sc_(ctx, LG_PROF_GEMM_DW, ctx->st2);
+    cudaError_t e = p.pair ? launch_gemm_dw_pair(p.bn, g, o, p.S, ctx->st2) : launch_gemm_dw(p.bn, g, o, p.S, ctx->st2);
     if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm_dw: %s", cudaGetErrorString(e));
     return LG_OK;
   };
+  // The dW chain runs on st2, forked after dZ_l is written: dW3 beside dX3, dW2 beside dX2, then dW1;
+  // st waits for it before the gradient is reduced / applied.
+  auto fork = [&](int k) -> lg_status {
+    CK(cudaEventRecord(ctx->ev_fork[k], ctx->st));
+    CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork[k], 0));
+    return LG_OK;
+  };
   // layer 3
+  if ((s = fork(0)) != LG_OK) return s;
   if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
   GemmArgs x3 = ctx->dx3;
   x3.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x3, bn_dx(d.H1), 2)) != LG_OK) return s;
   // layer 2
+  if ((s = fork(1)) != LG_OK) return s;
   if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   GemmArgs x2 = ctx->dx2;
   x2.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x2, bn_dx(d.H0), 2)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
+  if ((s = fork(2)) != LG_OK) return s;
   if ((s = dw(ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
+  CK(cudaEventRecord(ctx->ev_join, ctx->st2));
+  CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
   return LG_OK;
 }
 
