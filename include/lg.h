@@ -51,6 +51,9 @@ typedef enum {
 #define LG_F_NOISE 2u      /* observation noise (Table 4) */
 #define LG_F_PUSH 4u       /* pushes every 10 s */
 #define LG_F_BOOTSTRAP 8u  /* time-out bootstrapping */
+/* implementation switch (diagnostics/parity): policy_act uses the per-layer GEMM + head kernels instead of the
+ * fused rollout-policy kernel (same results bit for bit; only the 512-256-128 MLP has a fused kernel) */
+#define LG_F_UNFUSED_POLICY 256u
 
 #define LG_NUM_BUFFERS 20
 /* Buffer slots for lg_required_sizes / lg_create. Layouts are DESIGN.md §4. */

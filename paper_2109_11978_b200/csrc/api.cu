@@ -717,10 +717,37 @@ lg_status curriculum_update(lg_ctx* ctx, int32_t n, const uint8_t* crossed, cons
 }
 
 // ------------------------------------------------------------------ policy
+// the fused rollout policy kernel covers the paper's MLP (512-256-128, observation <= 256 columns)
+static bool fused_policy_ok(const Dims& d) { return d.H0 == 512 && d.H1 == 256 && d.H2 == 128 && d.Dp <= 256; }
+
 lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float* mu, float* value) {
   GUARD();
   const Dims& d = ctx->d;
   if (t < 0 || t >= d.T) return fail(ctx, LG_ERR_RANGE, "policy_act: t=%d out of [0,%d)", t, d.T);
+  if (fused_policy_ok(d) && !(ctx->cfg.flags & LG_F_UNFUSED_POLICY)) {
+    FusedPolicyArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.tmX = ctx->l1_roll[t].tmA[0];
+    fa.tmW1 = ctx->l1_roll[t].tmB[0];
+    fa.tmW2[0] = ctx->l2.tmB[0]; fa.tmW2[1] = ctx->l2.tmB[1];
+    fa.tmW3[0] = ctx->l3.tmB[0]; fa.tmW3[1] = ctx->l3.tmB[1];
+    void* W = ctx->buf[LG_BUF_WEIGHTS];
+    fa.b1 = at<float>(W, ctx->L.w_b1); fa.b2 = at<float>(W, ctx->L.w_b2); fa.b3 = at<float>(W, ctx->L.w_b3);
+    fa.W4a = at<float>(W, ctx->L.w_W4a); fa.b4a = at<float>(W, ctx->L.w_b4a);
+    fa.W4c = at<float>(W, ctx->L.w_W4c); fa.b4c = at<float>(W, ctx->L.w_b4c); fa.logstd = at<float>(W, ctx->L.w_ls);
+    fa.N = d.N; fa.rank = ctx->cfg.rank; fa.t = t; fa.kb1 = (d.Dp + 63) / 64;
+    fa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); fa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
+    fa.scalars = ctx->sc;
+    fa.act = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
+    fa.mu = reinterpret_cast<float*>(ctx->buf[LG_BUF_MU]) + (size_t)t * d.N * 12;
+    fa.logp = reinterpret_cast<float*>(ctx->buf[LG_BUF_LOGP]) + (size_t)t * d.N;
+    fa.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE]) + (size_t)t * d.N;
+    fa.u_act = actions; fa.u_logp = logp; fa.u_mu = mu; fa.u_value = value;
+    Scope sc_(ctx, LG_PROF_GEMM_ROLL);
+    cudaError_t e = launch_policy_fused(fa, ctx->st);
+    if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "policy (fused): %s", cudaGetErrorString(e));
+    return LG_OK;
+  }
   lg_status s = forward_rows(ctx, ctx->l1_roll[t], d.N, LG_PROF_GEMM_ROLL);
   if (s != LG_OK) return s;
   HeadArgs h = head_args(ctx, d.N);

@@ -157,6 +157,30 @@ __device__ __forceinline__ float h_bilinear(const World& w, float x, float y) {
   return fa(fm(fs(1.0f, ty), lo), fm(ty, hi));
 }
 
+// ------------------------------------------------------------------ Gaussian policy arithmetic
+// Written with explicit roundings so every kernel that evaluates them (rollout heads, fused rollout policy,
+// loss head) produces the same bits regardless of the translation unit's contraction choices.
+// log-density term of one action dimension: 0.5 z^2 + log sigma, z = (a - mu) / sigma
+__device__ __forceinline__ float logp_term(float a, float mu, float ls) {
+  const float z = __fmul_rn(__fsub_rn(a, mu), expf(-ls));
+  return __fadd_rn(__fmul_rn(__fmul_rn(0.5f, z), z), ls);
+}
+// action of dimension j from the ACTION Philox block j/4 of env g at event ev: a = mu + sigma * eps,
+// eps = Box-Muller pair (2k, 2k+1), k = j/2 (cos for even j, sin for odd j)
+__device__ __forceinline__ float sample_action_b(const U4& b, int j, float mu, float ls) {  // b = block j/4
+  const int k2 = (j & ~1) & 3;
+  const uint32_t w0 = pick(b, (uint32_t)k2), w1 = pick(b, (uint32_t)k2 + 1u);
+  const float u1 = (float)((w0 >> 8) + 1u) * 0x1p-24f;
+  const float u2 = (float)(w1 >> 8) * 0x1p-24f;
+  const float rr = sqrtf(-2.0f * log_poly(u1));
+  float sn, cs;
+  sincos_poly(0x1.921fb6p2f * u2, sn, cs);
+  return __fadd_rn(mu, __fmul_rn(expf(ls), __fmul_rn(rr, (j & 1) ? sn : cs)));
+}
+__device__ __forceinline__ float sample_action(const Rng& rng, uint32_t g, uint32_t ev, int j, float mu, float ls) {
+  return sample_action_b(rng.block((uint32_t)(j >> 2), g, ev, TAG_ACTION), j, mu, ls);
+}
+
 // ------------------------------------------------------------------ misc
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

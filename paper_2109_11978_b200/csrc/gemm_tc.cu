@@ -1019,6 +1019,329 @@ cudaError_t launch_gemm_dw_pair(int bn, const GemmArgs& a, const DwOut& o, int S
   }
 }
 
+// ------------------------------------------------------------------ fused rollout policy
+// Shared memory: R1 (8 x 16 KB K-major SW128 A-operand blocks: the X tile, then H1, then H2), a 2-stage ring
+// of 32 KB weight chunks, biases, head weights and the cross-thread head exchange.
+namespace fp {
+constexpr int H0 = 512, H1 = 256, H2 = 128, BK = 64;
+constexpr int ABLK = 128 * BK * 2;     // one 128-row x 64-col bf16 A block (16 KB)
+constexpr int R1_BYTES = 8 * ABLK;     // H1 = 8 blocks
+constexpr int STAGE = 256 * BK * 2;    // one 256-row weight chunk (32 KB)
+constexpr int NSTAGE = 2;
+constexpr int OFF_RING = R1_BYTES;
+constexpr int OFF_BIAS = OFF_RING + NSTAGE * STAGE;           // b1 (512) | b2 (256) | b3 (128) fp32
+constexpr int OFF_HW = OFF_BIAS + (H0 + H1 + H2) * 4;          // head weights [13][128] fp32
+constexpr int OFF_XCH = OFF_HW + 13 * H2 * 4;                   // [128 rows][2][13] partial sums per thread
+constexpr int OFF_BAR = OFF_XCH + 128 * 26 * 4;
+constexpr int SMEM = 1024 + OFF_BAR + 16 * 8;
+}  // namespace fp
+
+// bf16 pack of 32 fp32 values after bias + ELU, written into a K-major SW128 A block (row r, columns c..c+31
+// of the layer output = k-block c/64, 16-B chunks (c%64)/8 .. +3)
+__device__ __forceinline__ void store_act_block(uint8_t* R1, int r, int c, const uint32_t* acc, const float* bias) {
+  uint32_t pk[16];
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const float x0 = elu_fast(__uint_as_float(acc[k]) + bias[k]);
+    const float x1 = elu_fast(__uint_as_float(acc[k + 1]) + bias[k + 1]);
+    __nv_bfloat162 o = __floats2bfloat162_rn(x0, x1);
+    pk[k / 2] = *reinterpret_cast<uint32_t*>(&o);
+  }
+  uint8_t* blk = R1 + (c >> 6) * fp::ABLK + r * 128;
+  const int ch0 = (c & 63) >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int ch = ch0 + q;
+    *reinterpret_cast<uint4*>(blk + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  }
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_constant__ FusedPolicyArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* R1 = smem;
+  uint8_t* ring = smem + fp::OFF_RING;
+  float* sB1 = reinterpret_cast<float*>(smem + fp::OFF_BIAS);
+  float* sB2 = sB1 + fp::H0;
+  float* sB3 = sB2 + fp::H1;
+  float* sHW = reinterpret_cast<float*>(smem + fp::OFF_HW);
+  float* sX = reinterpret_cast<float*>(smem + fp::OFF_XCH);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + fp::OFF_BAR);
+  uint64_t* xfull = bars + 0;
+  uint64_t* full = bars + 1;           // [2]
+  uint64_t* empty = bars + 3;          // [2]
+  uint64_t* tfull = bars + 5;          // [3]
+  uint64_t* h1ready = bars + 8;
+  uint64_t* h2ready = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int z = blockIdx.y;
+  const int m0 = blockIdx.x * 128;
+  if (threadIdx.x == 0) {
+    mbar_init(xfull, 1);
+    for (int s2 = 0; s2 < fp::NSTAGE; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
+    for (int s2 = 0; s2 < 3; ++s2) mbar_init(&tfull[s2], 1);
+    mbar_init(h1ready, EPI_WARPS);
+    mbar_init(h2ready, EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int k = threadIdx.x; k < fp::H0; k += blockDim.x) sB1[k] = a.b1[z * fp::H0 + k];
+  for (int k = threadIdx.x; k < fp::H1; k += blockDim.x) sB2[k] = a.b2[z * fp::H1 + k];
+  for (int k = threadIdx.x; k < fp::H2; k += blockDim.x) sB3[k] = a.b3[z * fp::H2 + k];
+  for (int k = threadIdx.x; k < 13 * fp::H2; k += blockDim.x) sHW[k] = k < 12 * fp::H2 ? a.W4a[k] : a.W4c[k - 12 * fp::H2];
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(xfull, a.kb1 * fp::ABLK);
+      for (int kb = 0; kb < a.kb1; ++kb) tma_load_2d(&a.tmX, xfull, R1 + kb * fp::ABLK, kb * fp::BK, m0);
+      int stage = 0;
+      uint32_t phase = 0;
+      auto load = [&](const CUtensorMap* map, int x, int y, uint32_t bytes) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        mbar_expect_tx(&full[stage], bytes);
+        tma_load_2d(map, &full[stage], ring + stage * fp::STAGE, x, y);
+        if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+      };
+      for (int nh = 0; nh < 2; ++nh)
+        for (int kb = 0; kb < a.kb1; ++kb) load(&a.tmW1, kb * fp::BK, z * fp::H0 + nh * 256, fp::STAGE);
+      for (int kb = 0; kb < fp::H0 / fp::BK; ++kb) load(&a.tmW2[z], kb * fp::BK, 0, fp::STAGE);
+      for (int kb = 0; kb < fp::H1 / fp::BK; ++kb) load(&a.tmW3[z], kb * fp::BK, 0, fp::STAGE / 2);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id256 = idesc_bf16(128, 256, false, false);
+      constexpr uint32_t id128 = idesc_bf16(128, 128, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      auto chunk = [&](uint32_t a_base, uint32_t dcol, uint32_t idesc) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t b0 = smem_u32(ring + stage * fp::STAGE);
+        return b0;
+      };
+      mbar_wait(xfull, 0);
+      tc_fence_after();
+      // layer 1: two 256-column halves of this net's 512 outputs, K = kb1 blocks of the observation
+      for (int nh = 0; nh < 2; ++nh)
+        for (int kb = 0; kb < a.kb1; ++kb) {
+          const uint32_t b0 = chunk(0, 0, 0);
+          const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
+#pragma unroll
+          for (int k = 0; k < fp::BK / 16; ++k)
+            tc_mma(tmem + nh * 256, sdesc(a0 + k * 32u, 0u, 1024u), sdesc(b0 + k * 32u, 0u, 1024u), id256,
+                   (kb > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&empty[stage]);
+          if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+        }
+      tc_commit(&tfull[0]);
+      // layer 2: A = H1 (8 blocks in R1), N = 256 into TMEM columns [0, 256)
+      mbar_wait(h1ready, 0);
+      tc_fence_after();
+      for (int kb = 0; kb < fp::H0 / fp::BK; ++kb) {
+        const uint32_t b0 = chunk(0, 0, 0);
+        const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
+#pragma unroll
+        for (int k = 0; k < fp::BK / 16; ++k)
+          tc_mma(tmem, sdesc(a0 + k * 32u, 0u, 1024u), sdesc(b0 + k * 32u, 0u, 1024u), id256, (kb > 0 || k > 0) ? 1u : 0u);
+        tc_commit(&empty[stage]);
+        if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+      }
+      tc_commit(&tfull[1]);
+      // layer 3: A = H2 (4 blocks in R1), N = 128 into TMEM columns [256, 384)
+      mbar_wait(h2ready, 0);
+      tc_fence_after();
+      for (int kb = 0; kb < fp::H1 / fp::BK; ++kb) {
+        const uint32_t b0 = chunk(0, 0, 0);
+        const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
+#pragma unroll
+        for (int k = 0; k < fp::BK / 16; ++k)
+          tc_mma(tmem + 256, sdesc(a0 + k * 32u, 0u, 1024u), sdesc(b0 + k * 32u, 0u, 1024u), id128,
+                 (kb > 0 || k > 0) ? 1u : 0u);
+        tc_commit(&empty[stage]);
+        if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+      }
+      tc_commit(&tfull[2]);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogues
+    const int e = warp - 4, q = e & 3, h = e >> 2;
+    const int r = q * 32 + lane;  // TMEM lane = tile row
+    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+    // layer 1 -> H1 (bias + ELU, bf16) into R1 (the observation tile there is dead once tfull[0] fired)
+    mbar_wait(&tfull[0], 0);
+    __syncwarp();
+    tc_fence_after();
+    for (int c = h * 256; c < h * 256 + 256; c += 32) {
+      uint32_t acc[32];
+      tmem_ld32_nowait(tb + c, acc);
+      tmem_wait_ld();
+      store_act_block(R1, r, c, acc, sB1 + c);
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(h1ready);
+    // layer 2 -> H2 into R1 (H1 is dead once tfull[1] fired)
+    mbar_wait(&tfull[1], 0);
+    __syncwarp();
+    tc_fence_after();
+    for (int c = h * 128; c < h * 128 + 128; c += 32) {
+      uint32_t acc[32];
+      tmem_ld32_nowait(tb + c, acc);
+      tmem_wait_ld();
+      store_act_block(R1, r, c, acc, sB2 + c);
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(h2ready);
+    // layer 3 -> H3 (as stored by the unfused path: bf16-rounded) -> heads. The thread of parity h forms the
+    // partial sums of the warp-per-row head (head_fwd_warp) for the lanes l = 2i + h and combines them in that
+    // butterfly's order (pairs by lane bits 4, 3, 2, 1); the last level (bit 0) adds the two threads' sums.
+    mbar_wait(&tfull[2], 0);
+    __syncwarp();
+    tc_fence_after();
+    const int nval = z == 0 ? 12 : 1;
+    float tot[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) tot[j] = 0.0f;
+    {
+      // this thread's 16 lanes l = 2i + h: columns 4l .. 4l+3 of H3, bf16-rounded as the unfused path stores it
+      float hv[64];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {  // 32-column chunk cc = lanes 8cc .. 8cc+7
+        uint32_t acc[32];
+        tmem_ld32_nowait(tb + 256 + 32 * cc, acc);
+        tmem_wait_ld();
+#pragma unroll
+        for (int li = 0; li < 4; ++li)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int l = 8 * cc + 2 * li + h;
+            const uint32_t av = h ? acc[8 * li + 4 + u] : acc[8 * li + u];
+            const float x = elu_fast(__uint_as_float(av) + sB3[4 * l + u]);
+            hv[4 * (4 * cc + li) + u] = __bfloat162float(__float2bfloat16_rn(x));
+          }
+      }
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        if (j < nval) {
+          const float* wrow = sHW + (z == 0 ? j : 12) * fp::H2;
+          float pl[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float* w = wrow + 4 * (2 * i + h);
+            float s2 = __fmul_rn(w[0], hv[4 * i]);
+            s2 = fmaf(w[1], hv[4 * i + 1], s2);
+            s2 = fmaf(w[2], hv[4 * i + 2], s2);
+            pl[i] = fmaf(w[3], hv[4 * i + 3], s2);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pl[i] = pl[i] + pl[i + 8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pl[i] = pl[i] + pl[i + 4];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) pl[i] = pl[i] + pl[i + 2];
+          tot[j] = pl[0] + pl[1];
+        }
+      }
+    }
+    // exchange the two threads' sums (the butterfly's last level adds them: a + b == b + a), then the two
+    // threads of a row split the action dimensions: h = 0 takes j < 6 (ACTION Philox blocks 0, 1), h = 1 takes
+    // j >= 6 (blocks 1, 2); their log-density terms meet again in smem for the fixed-order sum.
+    const int hs = (warp - 4) >> 2;
+    float* xrow = sX + r * 26;  // [2][13]: the two threads' partial sums
+#pragma unroll
+    for (int j = 0; j < 12; ++j) if (j < nval) xrow[hs * 13 + j] = tot[j];
+    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
+    const int row = m0 + r;
+    if (z == 1) {
+      if (hs == 0 && row < a.N) {
+        const float V = __fadd_rn(tot[0] + xrow[13], __ldg(a.b4c));
+        a.value[row] = V;
+        if (a.u_value) a.u_value[row] = V;
+      }
+    } else {
+      float* trow = xrow;  // reused for the 12 log-density terms after the sums are consumed
+      float tm[6];
+      if (row < a.N) {
+        Rng rng{a.seed_lo, a.seed_hi};
+        const uint32_t gid = (uint32_t)(a.rank * a.N + row);
+        const uint32_t ev = a.scalars->s_base + (uint32_t)a.t + 1u;
+        const U4 blk0 = rng.block((uint32_t)(hs == 0 ? 0 : 1), gid, ev, TAG_ACTION);
+        const U4 blk1 = rng.block((uint32_t)(hs == 0 ? 1 : 2), gid, ev, TAG_ACTION);
+#pragma unroll
+        for (int jj = 0; jj < 6; ++jj) {
+          const int j = 6 * hs + jj;
+          const float other = xrow[(1 - hs) * 13 + j];
+          const float mu = __fadd_rn(tot[j] + other, __ldg(a.b4a + j));
+          const float ls = __ldg(a.logstd + j);
+          const bool first = (j >> 2) == (hs == 0 ? 0 : 1);
+          const float act = sample_action_b(first ? blk0 : blk1, j, mu, ls);
+          tm[jj] = logp_term(act, mu, ls);
+          a.act[(size_t)row * 12 + j] = act;
+          a.mu[(size_t)row * 12 + j] = mu;
+          if (a.u_act) a.u_act[(size_t)row * 12 + j] = act;
+          if (a.u_mu) a.u_mu[(size_t)row * 12 + j] = mu;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));  // all sums read before the terms overwrite them
+#pragma unroll
+      for (int jj = 0; jj < 6; ++jj) trow[6 * hs + jj] = tm[jj];
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
+      if (hs == 0 && row < a.N) {
+        float t[12];
+#pragma unroll
+        for (int j = 0; j < 12; ++j) t[j] = trow[j];
+        // log-probability: dim_sum's butterfly (term j on lane 2j, zeros elsewhere), same additions in order:
+        // offsets 16, 8, 4, 2, 1 pair lanes (2m, 2m+16), (2m, 2m+8), (2m, 2m+4), (0, 2), (0, 1)
+        float e8[8];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) e8[m] = t[m] + t[m + 8];
+#pragma unroll
+        for (int m = 4; m < 8; ++m) e8[m] = t[m] + 0.0f;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) e8[m] = e8[m] + e8[m + 4];
+        e8[0] = e8[0] + e8[2];
+        e8[1] = e8[1] + e8[3];
+        const float k01 = e8[0] + e8[1];
+        const float lp = __fsub_rn(-(k01 + 0.0f), 11.027262398456072f);
+        a.logp[row] = lp;
+        if (a.u_logp) a.u_logp[row] = lp;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+cudaError_t launch_policy_fused(const FusedPolicyArgs& a, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_policy_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (a.kb1 < 1 || a.kb1 > 4) return cudaErrorInvalidValue;
+  dim3 grid((a.N + 127) / 128, 2, 1);
+  k_policy_fused<<<grid, GEMM_THREADS, fp::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static int g_num_sms = 0;

@@ -86,6 +86,27 @@ cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cud
 cudaError_t launch_gemm_dw_pair(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);
 cudaError_t launch_gemm_dw_kmajor(int bn, const GemmArgs& a, const DwOut& o, int S, cudaStream_t st);  // diagnostics
 
+// ------------------------------------------------------------------ fused rollout policy (gemm_tc.cu)
+// One rollout step of the policy for the 512-256-128 MLP: per CTA one 128-row tile of one
+// net (z = 0 actor, 1 critic); three chained tcgen05 GEMMs with the activations kept in shared memory, the
+// heads, and for the actor the Gaussian sample + log-probability (bit-identical to the unfused path).
+struct FusedPolicyArgs {
+  CUtensorMap tmX;           // OBS slot rows [N][Dp] bf16, box {64, 128}
+  CUtensorMap tmW1;          // W1 [2*512][Dp], box {64, 256}
+  CUtensorMap tmW2[2];       // W2[z] [256][512], box {64, 256}
+  CUtensorMap tmW3[2];       // W3[z] [128][256], box {64, 128}
+  const float* b1;           // [2*512]
+  const float* b2;           // [2*256]
+  const float* b3;           // [2*128]
+  const float* W4a; const float* b4a; const float* W4c; const float* b4c; const float* logstd;
+  int N, rank, t, kb1;       // kb1 = K-blocks of layer 1 (Dp / 64 rounded up, <= 4)
+  uint32_t seed_lo, seed_hi;
+  const DevScalars* scalars;
+  float* act; float* mu; float* logp; float* value;              // storage slot t
+  float* u_act; float* u_logp; float* u_mu; float* u_value;      // optional caller copies
+};
+cudaError_t launch_policy_fused(const FusedPolicyArgs& a, cudaStream_t st);
+
 // ------------------------------------------------------------------ PPO kernels (ppo.cu)
 struct NetDims {
   int D, Dp, H0, H1, H2;

@@ -92,8 +92,7 @@ __device__ __forceinline__ float dim_sum(float x, int lane) {
 
 // log N(a | mu, exp(ls)) from the per-dimension lanes
 __device__ __forceinline__ float logp_warp(float a_j, float mu_j, float ls_j, int lane) {
-  const float z = (a_j - mu_j) * expf(-ls_j);
-  return -dim_sum(0.5f * z * z + ls_j, lane) - SIX_LN_2PI;
+  return __fsub_rn(-dim_sum(logp_term(a_j, mu_j, ls_j), lane), SIX_LN_2PI);
 }
 
 constexpr int HEAD_WARPS = 8;      // rollout heads: warps per block
@@ -130,17 +129,7 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) k_heads(HeadArgs a) {
     float act = 0.0f;
     if (dl) {
       Rng rng{a.seed_lo, a.seed_hi};
-      const uint32_t g = (uint32_t)(a.rank * a.N + r);
-      const uint32_t ev = a.scalars->s_base + (uint32_t)a.t + 1u;
-      const U4 b = rng.block((uint32_t)(j >> 2), g, ev, TAG_ACTION);  // words 2k, 2k+1 (k = j/2) lie in block j/4
-      const int k2 = (j & ~1) & 3;
-      const uint32_t w0 = pick(b, (uint32_t)k2), w1 = pick(b, (uint32_t)k2 + 1u);
-      const float u1 = (float)((w0 >> 8) + 1u) * 0x1p-24f;
-      const float u2 = (float)(w1 >> 8) * 0x1p-24f;
-      const float rr = sqrtf(-2.0f * log_poly(u1));
-      float sn, cs;
-      sincos_poly(0x1.921fb6p2f * u2, sn, cs);
-      act = tot + expf(ls) * (rr * ((j & 1) ? sn : cs));
+      act = sample_action(rng, (uint32_t)(a.rank * a.N + r), a.scalars->s_base + (uint32_t)a.t + 1u, j, tot, ls);
     }
     const float lp = logp_warp(act, tot, ls, lane);
     const size_t o = (size_t)r * 12 + j;

@@ -223,6 +223,25 @@ def test_policy_act_rollout_vs_oracle():
         assert gpu_state(ctx).tobytes() == env.state.tobytes()
 
 
+@pytest.mark.parametrize("n_envs", [700, 4096])
+def test_fused_policy_bit_identical_to_unfused(n_envs):
+    """The fused rollout-policy kernel (three chained tcgen05 GEMMs + heads + sampling in one CTA) must give
+    the same bits as the per-layer GEMM + warp-per-row head path (LG_F_UNFUSED_POLICY), over a rollout
+    (ragged last tile for 700 envs), so the first minibatch's probability ratio stays exactly 1."""
+    outs = []
+    for extra in (0, lg.F_UNFUSED_POLICY):
+        cfg, ctx, env, theta = make(n_envs=n_envs, T=3, flags=ALL | extra)
+        ctx.reset()
+        for t in range(cfg.n_steps):
+            ctx.policy_act(t)
+            ctx.env_step(t)
+        ctx.sync()
+        outs.append({k: ctx.storage(k, extra=(12,) if k in ("ACT", "MU") else ()).cpu().numpy().copy()
+                     for k in ("ACT", "MU", "LOGP", "VALUE")})
+    for k in outs[0]:
+        assert outs[0][k].tobytes() == outs[1][k].tobytes(), k
+
+
 # ------------------------------------------------------------------ GAE (fp32 vs fp64 oracle)
 def _rollout(ctx, cfg):
     ctx.reset()
