@@ -1056,6 +1056,11 @@ __device__ __forceinline__ void store_act_block(uint8_t* R1, int r, int c, const
   }
 }
 
+#define FP_STAMP(k)                                                                                        \
+  do {                                                                                                     \
+    if (a.dbg) a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = gtimer();                \
+  } while (0)
+
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_constant__ FusedPolicyArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1078,6 +1083,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = blockIdx.y;
   const int m0 = blockIdx.x * 128;
+  if (threadIdx.x == 0) FP_STAMP(0);
   if (threadIdx.x == 0) {
     mbar_init(xfull, 1);
     for (int s2 = 0; s2 < fp::NSTAGE; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
@@ -1086,10 +1092,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     mbar_init(h2ready, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int k = threadIdx.x; k < fp::H0; k += blockDim.x) sB1[k] = a.b1[z * fp::H0 + k];
-  for (int k = threadIdx.x; k < fp::H1; k += blockDim.x) sB2[k] = a.b2[z * fp::H1 + k];
-  for (int k = threadIdx.x; k < fp::H2; k += blockDim.x) sB3[k] = a.b3[z * fp::H2 + k];
-  for (int k = threadIdx.x; k < 13 * fp::H2; k += blockDim.x) sHW[k] = k < 12 * fp::H2 ? a.W4a[k] : a.W4c[k - 12 * fp::H2];
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -1098,6 +1100,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) FP_STAMP(1);
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -1180,10 +1183,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     const int e = warp - 4, q = e & 3, h = e >> 2;
     const int r = q * 32 + lane;  // TMEM lane = tile row
     const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+    // biases and head weights are staged here, while the producer and the MMA warp run layer 1
+    {
+      const int et = threadIdx.x - 128, nt = EPI_WARPS * 32;
+      for (int k = et; k < fp::H0; k += nt) sB1[k] = __ldg(a.b1 + z * fp::H0 + k);
+      for (int k = et; k < fp::H1; k += nt) sB2[k] = __ldg(a.b2 + z * fp::H1 + k);
+      for (int k = et; k < fp::H2; k += nt) sB3[k] = __ldg(a.b3 + z * fp::H2 + k);
+      for (int k = et; k < 13 * fp::H2; k += nt) sHW[k] = k < 12 * fp::H2 ? __ldg(a.W4a + k) : __ldg(a.W4c + k - 12 * fp::H2);
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
+    }
     // layer 1 -> H1 (bias + ELU, bf16) into R1 (the observation tile there is dead once tfull[0] fired)
     mbar_wait(&tfull[0], 0);
     __syncwarp();
     tc_fence_after();
+    if (threadIdx.x == 128) FP_STAMP(2);
     for (int c = h * 256; c < h * 256 + 256; c += 32) {
       uint32_t acc[32];
       tmem_ld32_nowait(tb + c, acc);
@@ -1194,10 +1207,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(h1ready);
+    if (threadIdx.x == 128) FP_STAMP(3);
     // layer 2 -> H2 into R1 (H1 is dead once tfull[1] fired)
     mbar_wait(&tfull[1], 0);
     __syncwarp();
     tc_fence_after();
+    if (threadIdx.x == 128) FP_STAMP(4);
     for (int c = h * 128; c < h * 128 + 128; c += 32) {
       uint32_t acc[32];
       tmem_ld32_nowait(tb + c, acc);
@@ -1208,12 +1223,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(h2ready);
+    if (threadIdx.x == 128) FP_STAMP(5);
     // layer 3 -> H3 (as stored by the unfused path: bf16-rounded) -> heads. The thread of parity h forms the
     // partial sums of the warp-per-row head (head_fwd_warp) for the lanes l = 2i + h and combines them in that
     // butterfly's order (pairs by lane bits 4, 3, 2, 1); the last level (bit 0) adds the two threads' sums.
     mbar_wait(&tfull[2], 0);
     __syncwarp();
     tc_fence_after();
+    if (threadIdx.x == 128) FP_STAMP(6);
     const int nval = z == 0 ? 12 : 1;
     float tot[12];
 #pragma unroll
@@ -1262,6 +1279,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     // exchange the two threads' sums (the butterfly's last level adds them: a + b == b + a), then the two
     // threads of a row split the action dimensions: h = 0 takes j < 6 (ACTION Philox blocks 0, 1), h = 1 takes
     // j >= 6 (blocks 1, 2); their log-density terms meet again in smem for the fixed-order sum.
+    if (threadIdx.x == 128) FP_STAMP(7);
     const int hs = (warp - 4) >> 2;
     float* xrow = sX + r * 26;  // [2][13]: the two threads' partial sums
 #pragma unroll
@@ -1326,6 +1344,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) FP_STAMP(8);
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 

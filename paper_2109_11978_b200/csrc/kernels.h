@@ -104,6 +104,7 @@ struct FusedPolicyArgs {
   const DevScalars* scalars;
   float* act; float* mu; float* logp; float* value;              // storage slot t
   float* u_act; float* u_logp; float* u_mu; float* u_value;      // optional caller copies
+  unsigned long long* dbg;   // diagnostics only (tools/gemm_probe): per-CTA phase timestamps, else null
 };
 cudaError_t launch_policy_fused(const FusedPolicyArgs& a, cudaStream_t st);
 

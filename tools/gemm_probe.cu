@@ -357,6 +357,55 @@ static void probe_dw_pair(int Nout, int Nin, int K, int bn, int S, cudaStream_t 
   CK(cudaFree(dZ)); CK(cudaFree(X)); CK(cudaFree(g1)); CK(cudaFree(g2)); CK(cudaFree(part)); CK(cudaFree(cnt));
 }
 
+// fused rollout policy on synthetic data: timing and per-CTA phase stamps
+static void probe_fused(int N, cudaStream_t st) {
+  const int Dp = 240, H0 = 512, H1 = 256, H2 = 128;
+  __nv_bfloat16 *X, *W1, *W2, *W3;
+  float *b1, *b2, *b3, *W4a, *b4a, *W4c, *b4c, *ls, *out;
+  unsigned long long* dbg;
+  void* sc;
+  CK(cudaMalloc(&X, (size_t)N * Dp * 2)); CK(cudaMalloc(&W1, (size_t)2 * H0 * Dp * 2));
+  CK(cudaMalloc(&W2, (size_t)2 * H1 * H0 * 2)); CK(cudaMalloc(&W3, (size_t)2 * H2 * H1 * 2));
+  fill(X, (size_t)N * Dp); fill(W1, (size_t)2 * H0 * Dp); fill(W2, (size_t)2 * H1 * H0); fill(W3, (size_t)2 * H2 * H1);
+  CK(cudaMalloc(&b1, 4096 * 4)); CK(cudaMemset(b1, 0, 4096 * 4));
+  b2 = b1 + 1024; b3 = b2 + 512; W4a = b3 + 256; b4a = W4a + 12 * 128; W4c = b4a + 16; b4c = W4c + 128; ls = b4c + 16;
+  CK(cudaMalloc(&out, (size_t)N * 40 * 4));
+  CK(cudaMalloc(&sc, 4096)); CK(cudaMemset(sc, 0, 4096));
+  const int nct = ((N + 127) / 128) * 2;
+  CK(cudaMalloc(&dbg, (size_t)nct * 16 * 8)); CK(cudaMemset(dbg, 0, (size_t)nct * 16 * 8));
+  FusedPolicyArgs a;
+  memset(&a, 0, sizeof(a));
+  make_tmap_bf16(&a.tmX, X, N, Dp, Dp, 128);
+  make_tmap_bf16(&a.tmW1, W1, 2 * H0, Dp, Dp, 256);
+  for (int z = 0; z < 2; ++z) {
+    make_tmap_bf16(&a.tmW2[z], W2 + (size_t)z * H1 * H0, H1, H0, H0, 256);
+    make_tmap_bf16(&a.tmW3[z], W3 + (size_t)z * H2 * H1, H2, H1, H1, 128);
+  }
+  a.b1 = b1; a.b2 = b2; a.b3 = b3; a.W4a = W4a; a.b4a = b4a; a.W4c = W4c; a.b4c = b4c; a.logstd = ls;
+  a.N = N; a.kb1 = 4; a.scalars = reinterpret_cast<const DevScalars*>(sc);
+  a.act = out; a.mu = out + (size_t)N * 12; a.logp = out + (size_t)N * 24; a.value = out + (size_t)N * 25;
+  float us = time_us([&] { CK(launch_policy_fused(a, st)); }, st);
+  printf("fused policy N=%d: %.2f us per launch\n", N, us);
+  a.dbg = dbg;
+  for (int r = 0; r < 3; ++r) CK(launch_policy_fused(a, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> h((size_t)nct * 16);
+  CK(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < nct; ++c) t0 = std::min(t0, h[(size_t)c * 16]);
+  const char* nm[9] = {"start", "prologue", "L1 mma done", "H1 written", "L2 mma done", "H2 written", "L3 mma done",
+                       "head sums", "end"};
+  for (int k = 0; k < 9; ++k) {
+    double avg = 0, mx = 0;
+    for (int c = 0; c < nct; ++c) {
+      const double v = (h[(size_t)c * 16 + k] - t0) * 1e-3;
+      avg += v / nct;
+      mx = std::max(mx, v);
+    }
+    printf("   %-14s %8.2f | %8.2f\n", nm[k], avg, mx);
+  }
+}
+
 static void check_dw(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st) {
   std::vector<float> a = probe_dw(Nout, Nin, K, bn, 1, 1, st, true);  // unsplit K
   std::vector<float> b = probe_dw(Nout, Nin, K, bn, S, G, st, true);
@@ -424,6 +473,11 @@ int main(int argc, char** argv) {
     probe_dw_phases(512, 512, 24576, 256, 18, 1, st);    // dW2 both nets as 8 tiles
     probe_dw_phases(256, 256, 24576, 256, 74, 1, st);    // dW3 both nets as 2 tiles
     probe_dw_phases(128, 64, 64, 64, 1, 1, st);
+    return 0;
+  }
+  if (!strcmp(which, "fused")) {
+    probe_fused(4096, st);
+    probe_fused(1024, st);
     return 0;
   }
   if (!strcmp(which, "pair")) {
