@@ -693,10 +693,9 @@ lg_status env_step_obs_reward(lg_ctx* ctx, int32_t t, const float* actions, floa
   float* act_slot = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
   if (actions && actions != act_slot)
     CK(cudaMemcpyAsync(act_slot, actions, (size_t)d.N * 12 * 4, cudaMemcpyDeviceToDevice, ctx->st));
-  {
+  if (t == 0) {  // a rollout begins (the per-step counters are two slots the env step kernel clears itself)
     Scope sc_(ctx, LG_PROF_MISC);
-    CK(cudaMemsetAsync(&ctx->sc->n_to, 0, 4, ctx->st));
-    if (t == 0) CK(cudaMemsetAsync(&ctx->sc->n_to_total, 0, 4, ctx->st));  // a rollout begins
+    CK(cudaMemsetAsync(&ctx->sc->n_to_total, 0, 4, ctx->st));
   }
   { Scope sc_(ctx, LG_PROF_ENV); launch_env_step(ctx->ep, t, act_slot, obs, reward, terminated, timeout, terms, ctx->st); }
   CKL();
@@ -858,8 +857,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
   GemmArgs l1 = ctx->l1_upd;
   lg_status s = forward_rows(ctx, l1, d.Mmb);
   if (s != LG_OK) return s;
-  { Scope sc_(ctx, LG_PROF_MISC); CK(cudaMemsetAsync(ctx->payload, 0, 16 * 4, ctx->st)); }
-  LossArgs la;
+  LossArgs la;  // (the minibatch's gather kernel zeroed the gradient payload)
   la.nd = NetDims{d.D, d.Dp, d.H0, d.H1, d.H2};
   la.M = d.Mmb;
   la.H3 = at<__nv_bfloat16>(A, L.a_H3);
@@ -940,6 +938,9 @@ static GatherArgs gather_args(lg_ctx* ctx) {
   g.A = reinterpret_cast<const float*>(ctx->buf[LG_BUF_ADV]);
   g.R = reinterpret_cast<const float*>(ctx->buf[LG_BUF_RET]);
   g.sc = ctx->sc;
+  g.bc_slot = -1;
+  g.payload = ctx->payload;
+  g.b1 = ctx->cfg.adam_b1; g.b2 = ctx->cfg.adam_b2;
   g.X = at<__nv_bfloat16>(A, L.a_X);
   g.o_act = at<float>(A, L.a_act); g.o_mu = at<float>(A, L.a_mu); g.o_logp = at<float>(A, L.a_logp);
   g.o_V = at<float>(A, L.a_V); g.o_adv = at<float>(A, L.a_adv); g.o_ret = at<float>(A, L.a_ret);
@@ -1005,6 +1006,7 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
     for (int m = 0; m < d.K; ++m) {
       GatherArgs g = gather_args(ctx);
       g.perm = perm + (size_t)m * d.Mmb;
+      g.bc_slot = e * d.K + m;
       { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
       CKL();
       if ((s = minibatch_gradient(ctx)) != LG_OK) return s;

@@ -22,7 +22,7 @@ struct DevScalars {
   uint32_t iteration;   // PPO iterations completed (shuffle event = iteration*E + epoch)
   int32_t adam_t;       // applied Adam steps
   float alpha;          // Alg. 1 learning rate
-  int32_t n_to;         // compacted time-out rows of the current env step
+  int32_t reserved0;
   int32_t nonfinite_skips;
   int32_t applied;
   int32_t pad0;
@@ -36,6 +36,8 @@ struct DevScalars {
   float alpha_ring[2];
   int32_t adamt_ring[2];
   int32_t n_to_total;   // time-out rows compacted since the rollout began (batched bootstrap)
+  float bc_next[2];     // Adam bias corrections 1 - b^(t+1) for the next applied step (set at the minibatch start)
+  int32_t n_to_slot[2]; // compacted time-out rows of env step event ev in slot ev & 1 (the step clears the other)
 };
 
 // ------------------------------------------------------------------ Philox4x32-10

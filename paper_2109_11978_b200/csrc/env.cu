@@ -171,7 +171,7 @@ __device__ __forceinline__ void fill_obs_rec(const St& s, ObsRec& o) {
 // (two when a reset shifted the row's first word) and writes them as one 8-byte bf16x4 store. Proprioceptive
 // items (4gq < 48) read one float4 of the record; scan items step through the scan grid incrementally.
 // Blocks [0, ceil(N/2)) write the post-step rows of OBS slot `slot`; with `with_terminal` the next
-// ceil(N/2) blocks write the pre-reset rows of this step's time-outs (records < n_to) into the rollout's
+// ceil(N/2) blocks write the pre-reset rows of this step's time-outs (records < n_to_slot[ev & 1]) into the rollout's
 // compacted time-out buffer (row = the record's destination row).
 __constant__ float c_noise_scale[48] = {0.01f, 0.01f, 0.01f, 0.2f, 0.2f, 0.2f, 0.05f, 0.05f, 0.05f, 0.0f, 0.0f, 0.0f,
                                         0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f, 0.01f,
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(64 * OBS_ROWS_PER_BLOCK) k_env_obs(EnvParams P
   if ((int)blockIdx.x >= nb_main) {
     if (!with_terminal) return;
     r -= nb_main * OBS_ROWS_PER_BLOCK;
-    if (r >= P.scalars->n_to) return;
+    if (r >= P.scalars->n_to_slot[ev & 1u]) return;
     recs = reinterpret_cast<const ObsRec*>(P.trecs);
     dst = P.term_obs;
     df = nullptr;
@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
   World W{P.hf, P.R, P.C, P.inv_cell};
   Rng rng{P.seed_lo, P.seed_hi};
   const uint32_t ev = P.scalars->s_base + (uint32_t)t + 1u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.scalars->n_to_slot[(ev + 1u) & 1u] = 0;  // the next step's counter
   const int N = P.N;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = gt >> 2, l = gt & 3;
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
       // record r of this step (k_env_obs writes its observation) -> row grow of the rollout's compacted
       // time-out buffer, evaluated by the critic once after the rollout (storage_compute_gae)
       int row = 0, grow = 0;
-      if (l == 0) { row = atomicAdd(&P.scalars->n_to, 1); grow = atomicAdd(&P.scalars->n_to_total, 1); }
+      if (l == 0) { row = atomicAdd(&P.scalars->n_to_slot[ev & 1u], 1); grow = atomicAdd(&P.scalars->n_to_total, 1); }
       row = __shfl_sync(gm, row, gbase);
       grow = __shfl_sync(gm, grow, gbase);
       ObsRec& tr = reinterpret_cast<ObsRec*>(P.trecs)[row];

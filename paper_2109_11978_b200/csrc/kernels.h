@@ -202,7 +202,10 @@ struct GatherArgs {
   const int32_t* idx;        // alternative explicit indices (parity)
   const __nv_bfloat16* obs;  // [T+1][N][Dp]
   const float* act; const float* mu; const float* logp; const float* V; const float* A; const float* R;
-  const DevScalars* sc;
+  DevScalars* sc;
+  int bc_slot;               // >= 0: also set sc->bc_next for the Adam step of minibatch slot bc_slot (ring m & 1)
+  float* payload;            // zeroed (16 floats) for the minibatch's loss / gradient statistics
+  float b1, b2;
   __nv_bfloat16* X; float* o_act; float* o_mu; float* o_logp; float* o_V; float* o_adv; float* o_ret;
 };
 void launch_gather(const GatherArgs& a, cudaStream_t st);

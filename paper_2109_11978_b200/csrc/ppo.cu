@@ -511,6 +511,12 @@ void launch_perm(const PermArgs& a, cudaStream_t st) { k_perm<<<(a.B + 255) / 25
 // ------------------------------------------------------------------ minibatch gather (warp per row)
 constexpr int GATHER_ROWS = 4;  // rows per warp: the permutation loads and the row copies are all in flight together
 __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
+  if (a.payload && blockIdx.x == 0 && threadIdx.x < 16) a.payload[threadIdx.x] = 0.0f;
+  if (a.bc_slot >= 0 && blockIdx.x == 0 && threadIdx.x == 0) {  // Adam bias corrections for this minibatch
+    const int t = a.sc->adamt_ring[a.bc_slot & 1] + 1;
+    a.sc->bc_next[0] = (float)(1.0 - pow((double)a.b1, (double)t));
+    a.sc->bc_next[1] = (float)(1.0 - pow((double)a.b2, (double)t));
+  }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int r0 = warp * GATHER_ROWS;
   if (r0 >= a.M) return;
@@ -618,8 +624,8 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, 
     }
     s_apply = bad ? 0 : 1;
     s_alpha = alpha;
-    s_bc1 = (float)(1.0 - pow((double)a.b1, (double)t));
-    s_bc2 = (float)(1.0 - pow((double)a.b2, (double)t));
+    s_bc1 = sc->bc_next[0];  // 1 - b1^t for the applied step t (computed by this minibatch's gather)
+    s_bc2 = sc->bc_next[1];
     if (blockIdx.x == 0) {
       sc->alpha_ring[(m + 1) & 1] = alpha;
       sc->adamt_ring[(m + 1) & 1] = t;
