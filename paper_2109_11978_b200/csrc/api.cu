@@ -182,7 +182,7 @@ Layout layout_of(const Dims& d) {
   L.k_dw1 = o; o = al(o + L.dw1.bytes);
   L.k_dw2 = o; o = al(o + L.dw2.bytes);
   L.k_dw3 = o; o = al(o + L.dw3.bytes);
-  L.k_perm = o; o = al(o + (size_t)d.B * 4);
+  L.k_perm = o; o = al(o + (size_t)d.E * d.B * 4);  // all epochs' permutations of an iteration
   L.k_tobs = o; o = al(o + (size_t)d.to_cap * d.Dp * 2);
   L.k_tidx = o; o = al(o + (size_t)d.to_cap * 4);
   L.k_step = o; o = al(o + 16 * 4);
@@ -958,7 +958,7 @@ lg_status ppo_shuffle(lg_ctx* ctx, int32_t epoch, uint32_t* perm) {
   PermArgs pa;
   pa.B = (uint32_t)ctx->d.B; pa.E = ctx->d.E; pa.epoch = epoch; pa.rank = ctx->cfg.rank;
   pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
-  pa.sc = ctx->sc; pa.perm = perm;
+  pa.sc = ctx->sc; pa.perm = perm; pa.n_epochs = 1;
   launch_perm(pa, ctx->st);
   CKL();
   return LG_OK;
@@ -996,16 +996,18 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
   aa.inv_world = 1.0f / (float)ctx->world;
   aa.sc = ctx->sc;
   lg_status s;
-  for (int e = 0; e < d.E; ++e) {
+  {  // the Feistel permutations of all E epochs (P:272 shuffled minibatches), one launch
     PermArgs pa;
-    pa.B = (uint32_t)d.B; pa.E = d.E; pa.epoch = e; pa.rank = ctx->cfg.rank;
+    pa.B = (uint32_t)d.B; pa.E = d.E; pa.epoch = 0; pa.rank = ctx->cfg.rank;
     pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
-    pa.sc = ctx->sc; pa.perm = perm;
+    pa.sc = ctx->sc; pa.perm = perm; pa.n_epochs = d.E;
     { Scope sc_(ctx, LG_PROF_GATHER); launch_perm(pa, ctx->st); }
     CKL();
+  }
+  for (int e = 0; e < d.E; ++e) {
     for (int m = 0; m < d.K; ++m) {
       GatherArgs g = gather_args(ctx);
-      g.perm = perm + (size_t)m * d.Mmb;
+      g.perm = perm + (size_t)e * d.B + (size_t)m * d.Mmb;
       g.bc_slot = e * d.K + m;
       { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
       CKL();

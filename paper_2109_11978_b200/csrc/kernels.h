@@ -193,6 +193,7 @@ void launch_adv_finalize(const double* sum_total, const double* sq_total, double
 
 struct PermArgs {
   uint32_t B; int E; int epoch; int rank; uint32_t seed_lo, seed_hi; const DevScalars* sc; uint32_t* perm;
+  int n_epochs;              // epochs epoch .. epoch + n_epochs - 1, written to perm + k * B
 };
 void launch_perm(const PermArgs& a, cudaStream_t st);
 

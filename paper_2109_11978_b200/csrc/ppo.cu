@@ -481,11 +481,13 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
   return x;
 }
 
+// grid.y = epochs computed by this launch (a.epoch + blockIdx.y), each writing perm + blockIdx.y * B
 __global__ void k_perm(PermArgs a) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= a.B) return;
   Rng rng{a.seed_lo, a.seed_hi};
-  const uint32_t ev = a.sc->iteration * (uint32_t)a.E + (uint32_t)a.epoch;
+  const int epoch = a.epoch + (int)blockIdx.y;
+  const uint32_t ev = a.sc->iteration * (uint32_t)a.E + (uint32_t)epoch;
   U4 K = rng.block(0, (uint32_t)a.rank, ev, TAG_SHUFFLE);
   const uint32_t Ks[4] = {K.x, K.y, K.z, K.w};
   uint32_t k = 0;
@@ -504,9 +506,9 @@ __global__ void k_perm(PermArgs a) {
     }
     x = (L << half) | R;
   } while (x >= a.B);
-  a.perm[j] = x;
+  a.perm[(size_t)blockIdx.y * a.B + j] = x;
 }
-void launch_perm(const PermArgs& a, cudaStream_t st) { k_perm<<<(a.B + 255) / 256, 256, 0, st>>>(a); }
+void launch_perm(const PermArgs& a, cudaStream_t st) { k_perm<<<dim3((a.B + 255) / 256, a.n_epochs), 256, 0, st>>>(a); }
 
 // ------------------------------------------------------------------ minibatch gather (warp per row)
 constexpr int GATHER_ROWS = 4;  // rows per warp: the permutation loads and the row copies are all in flight together
