@@ -183,6 +183,14 @@ __device__ __forceinline__ float sample_action(const Rng& rng, uint32_t g, uint3
   return sample_action_b(rng.block((uint32_t)(j >> 2), g, ev, TAG_ACTION), j, mu, ls);
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels launched with launch_pdl (kernels.h) let their dependent grid start launching as soon as all their
+// CTAs are running (pdl_trigger), and block in pdl_wait until the preceding grid has completed and its memory
+// is visible -- every such kernel calls pdl_wait before touching data a predecessor wrote, so completion stays
+// transitive along the stream. Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ misc
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -182,6 +182,8 @@ constexpr int OBS_ROWS_PER_BLOCK = 2;
 __global__ void __launch_bounds__(64 * OBS_ROWS_PER_BLOCK) k_env_obs(EnvParams P, int ev_off,
                                                                      __nv_bfloat16* __restrict__ dst_bf16,
                                                                      float* __restrict__ dst_f32, int with_terminal) {
+  pdl_trigger();
+  pdl_wait();
   const int D = P.obs_dim, Dp = P.obs_stride, G = Dp / 4;
   const uint32_t ev = P.scalars->s_base + (uint32_t)ev_off;
   const int nb_main = (P.N + OBS_ROWS_PER_BLOCK - 1) / OBS_ROWS_PER_BLOCK;
@@ -260,7 +262,8 @@ __global__ void __launch_bounds__(64 * OBS_ROWS_PER_BLOCK) k_env_obs(EnvParams P
 static void launch_obs(const EnvParams& P, int ev_off, __nv_bfloat16* dst, float* f32, int with_terminal,
                        cudaStream_t st) {
   const int nb_main = (P.N + OBS_ROWS_PER_BLOCK - 1) / OBS_ROWS_PER_BLOCK;
-  k_env_obs<<<nb_main * (with_terminal ? 2 : 1), 64 * OBS_ROWS_PER_BLOCK, 0, st>>>(P, ev_off, dst, f32, with_terminal);
+  launch_pdl(k_env_obs, dim3(nb_main * (with_terminal ? 2 : 1)), dim3(64 * OBS_ROWS_PER_BLOCK), 0, st, P, ev_off, dst, f32,
+             with_terminal);
 }
 
 // ------------------------------------------------------------------ kernels
@@ -401,6 +404,8 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
                                                             float* __restrict__ rew_out,
                                                             uint8_t* __restrict__ term_out, uint8_t* __restrict__ to_out,
                                                             float* __restrict__ terms_out) {
+  pdl_trigger();
+  pdl_wait();
   World W{P.hf, P.R, P.C, P.inv_cell};
   Rng rng{P.seed_lo, P.seed_hi};
   const uint32_t ev = P.scalars->s_base + (uint32_t)t + 1u;
@@ -687,8 +692,8 @@ void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* 
 void launch_env_step(const EnvParams& P, int t, const float* actions, float* obs_f32, float* rew, uint8_t* term,
                      uint8_t* to, float* terms, cudaStream_t st) {
   const long long threads = 4LL * P.N;
-  k_env_step<<<(unsigned)((threads + STEP_THREADS - 1) / STEP_THREADS), STEP_THREADS, 0, st>>>(P, t, actions, rew, term,
-                                                                                               to, terms);
+  launch_pdl(k_env_step, dim3((unsigned)((threads + STEP_THREADS - 1) / STEP_THREADS)), dim3(STEP_THREADS), 0, st, P, t,
+             actions, rew, term, to, terms);
   launch_obs(P, t + 1, P.obs_out + (size_t)(t + 1) * P.N * P.obs_stride, obs_f32, (P.flags & F_BOOTSTRAP) ? 1 : 0,
              st);  // noise event s_base + t + 1
 }

@@ -237,6 +237,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
+  if (args.M_dev) pdl_wait();  // the device-side row count is a predecessor's output
   const int M = args.M_dev ? *args.M_dev : args.M;
   const int m_tiles = args.m_tiles;
   const int total = args.nz * m_tiles * args.n_tiles * args.n_splits;
@@ -265,6 +267,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the prologue above overlapped the preceding kernel; its outputs are read from here on
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -1084,6 +1087,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   const int z = blockIdx.y;
   const int m0 = blockIdx.x * 128;
   if (threadIdx.x == 0) FP_STAMP(0);
+  pdl_trigger();
   if (threadIdx.x == 0) {
     mbar_init(xfull, 1);
     for (int s2 = 0; s2 < fp::NSTAGE; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
@@ -1100,6 +1104,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // observation rows and weights are predecessors' outputs
   if (threadIdx.x == 0) FP_STAMP(1);
 
   if (warp == 0) {
@@ -1357,8 +1362,7 @@ cudaError_t launch_policy_fused(const FusedPolicyArgs& a, cudaStream_t st) {
   }
   if (a.kb1 < 1 || a.kb1 > 4) return cudaErrorInvalidValue;
   dim3 grid((a.N + 127) / 128, 2, 1);
-  k_policy_fused<<<grid, GEMM_THREADS, fp::SMEM, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_policy_fused, grid, dim3(GEMM_THREADS), fp::SMEM, st, a);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1421,8 +1425,7 @@ static cudaError_t launch_one(const GemmArgs& a, cudaStream_t st) {
   }
   const int total = a.nz * a.m_tiles * a.n_tiles * a.n_splits;
   const int grid = total < g_num_sms ? total : g_num_sms;
-  k_gemm_tc<BN, A_MN, B_MN, EPI><<<grid, GEMM_THREADS, C::SMEM, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_gemm_tc<BN, A_MN, B_MN, EPI>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, st, a);
 }
 
 template <bool A_MN, bool B_MN, int EPI>

@@ -99,6 +99,8 @@ constexpr int HEAD_WARPS = 8;      // rollout heads: warps per block
 constexpr int HEAD_ROWS_PER_WARP = 4;
 
 __global__ void __launch_bounds__(HEAD_WARPS * 32) k_heads(HeadArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int M = a.M_dev ? *a.M_dev : a.M;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = (blockIdx.x * HEAD_WARPS + warp) * HEAD_ROWS_PER_WARP;
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) k_heads(HeadArgs a) {
 
 void launch_heads(const HeadArgs& a, cudaStream_t st) {
   const int rows_per_block = HEAD_WARPS * HEAD_ROWS_PER_WARP;
-  k_heads<<<(a.M + rows_per_block - 1) / rows_per_block, HEAD_WARPS * 32, 0, st>>>(a);
+  launch_pdl(k_heads, dim3((a.M + rows_per_block - 1) / rows_per_block), dim3(HEAD_WARPS * 32), 0, st, a);
 }
 
 // ------------------------------------------------------------------ PPO loss head (fwd + bwd)
@@ -166,6 +168,8 @@ int loss_blocks(int M) { return std::max(1, std::min(LOSS_MAX_BLOCKS, (M + LOSS_
 __device__ __forceinline__ float elu_grad_from_out(float h) { return h > 0.0f ? 1.0f : h + 1.0f; }
 
 __global__ void __launch_bounds__(LOSS_WARPS * 32, 1) k_loss_heads(LossArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sacc[];  // [LOSS_WARPS][HP] warp partials, then [LOSS_WARPS][5] fp64 statistics
   const int H2 = a.nd.H2, HP = a.HP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -285,7 +289,7 @@ void launch_loss_heads(const LossArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(k_loss_heads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = smem;
   }
-  k_loss_heads<<<loss_blocks(a.M), LOSS_WARPS * 32, smem, st>>>(a);
+  launch_pdl(k_loss_heads, dim3(loss_blocks(a.M)), dim3(LOSS_WARPS * 32), smem, st, a);
 }
 
 // sums over blocks (fixed order) -> canonical gradient of heads/log-std + stats payload.
@@ -294,6 +298,8 @@ void launch_loss_heads(const LossArgs& a, cudaStream_t st) {
 constexpr int RH_WARPS = 32;
 constexpr int RH_UNROLL = 8;
 __global__ void __launch_bounds__(RH_WARPS * 32) k_reduce_heads(HeadReduceArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float ssum[RH_WARPS][33];
   const int H2 = a.H2;
   const int nval = 13 * H2 + 25;
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(RH_WARPS * 32) k_reduce_heads(HeadReduceArgs a
 
 void launch_reduce_heads(const HeadReduceArgs& a, cudaStream_t st) {
   int n = 13 * a.H2 + 25;
-  k_reduce_heads<<<(n + 31) / 32, RH_WARPS * 32, 0, st>>>(a);
+  launch_pdl(k_reduce_heads, dim3((n + 31) / 32), dim3(RH_WARPS * 32), 0, st, a);
 }
 
 // split-K partials -> canonical W and b gradients. Block = 8 warps x 32 consecutive elements; warp w
@@ -513,6 +519,8 @@ void launch_perm(const PermArgs& a, cudaStream_t st) { k_perm<<<dim3((a.B + 255)
 // ------------------------------------------------------------------ minibatch gather (warp per row)
 constexpr int GATHER_ROWS = 4;  // rows per warp: the permutation loads and the row copies are all in flight together
 __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
+  pdl_trigger();
+  pdl_wait();
   if (a.payload && blockIdx.x == 0 && threadIdx.x < 16) a.payload[threadIdx.x] = 0.0f;
   if (a.bc_slot >= 0 && blockIdx.x == 0 && threadIdx.x == 0) {  // Adam bias corrections for this minibatch
     const int t = a.sc->adamt_ring[a.bc_slot & 1] + 1;
@@ -578,7 +586,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
 }
 void launch_gather(const GatherArgs& a, cudaStream_t st) {
   const long long warps = (a.M + GATHER_ROWS - 1) / GATHER_ROWS;
-  k_gather<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(a);
+  launch_pdl(k_gather, dim3((unsigned)((warps * 32 + 255) / 256)), dim3(256), 0, st, a);
 }
 
 // ------------------------------------------------------------------ Alg. 1 + Adam
@@ -602,6 +610,8 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
 constexpr int ADAM_PER_THREAD = 2;
 __global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, float kl_target, int world, int m,
                                               float* acc) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float s_alpha, s_bc1, s_bc2;
   __shared__ int s_apply;
   // this thread's elements are loaded first, so their latency overlaps the Alg. 1 / bias-correction scalars
@@ -661,7 +671,7 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, 
 void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc, cudaStream_t st) {
   const long long per_block = 256LL * ADAM_PER_THREAD;
   const int nb = (int)((a.sh.P + per_block - 1) / per_block);
-  k_adam<<<nb, 256, 0, st>>>(a, payload, kl_target, world, m, acc);
+  launch_pdl(k_adam, dim3(nb), dim3(256), 0, st, a, payload, kl_target, world, m, acc);
 }
 
 __global__ void k_sync_shadow(ShadowArgs sh, const float* theta) {
