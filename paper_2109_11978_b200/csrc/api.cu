@@ -125,6 +125,8 @@ struct Layout {
   size_t w_W1, w_W2, w_W3, w_b1, w_b2, w_b3, w_W4a, w_b4a, w_W4c, w_b4c, w_ls, w_lso;
   // ACTIV
   size_t a_X, a_H1, a_H2, a_H3, a_dZ1, a_dZ2, a_dZ3, a_act, a_mu, a_logp, a_V, a_adv, a_ret, a_omu, a_oV;
+  // the gathered minibatch (X + per-sample fields) is double-buffered: set b = 0 at a_X.., set 1 at these
+  size_t b_X, b_act, b_mu, b_logp, b_V, b_adv, b_ret;
   // WORK
   size_t k_sc, k_gae, k_var, k_tot, k_lpart, k_spart, k_dw1, k_dw2, k_dw3, k_perm, k_tobs, k_tidx, k_step, k_stats,
       k_ctrl, k_rec, k_trec;
@@ -173,6 +175,13 @@ Layout layout_of(const Dims& d) {
   L.a_V = o; o = al(o + R * 4);
   L.a_adv = o; o = al(o + R * 4);
   L.a_ret = o; o = al(o + R * 4);
+  L.b_X = o; o = al(o + R * d.Dp * 2);
+  L.b_act = o; o = al(o + R * 12 * 4);
+  L.b_mu = o; o = al(o + R * 12 * 4);
+  L.b_logp = o; o = al(o + R * 4);
+  L.b_V = o; o = al(o + R * 4);
+  L.b_adv = o; o = al(o + R * 4);
+  L.b_ret = o; o = al(o + R * 4);
   L.a_omu = o; o = al(o + R * 12 * 4);
   L.a_oV = o; o = al(o + R * 4);
   L.bytes[LG_BUF_ACTIV] = o;
@@ -227,6 +236,7 @@ struct lg_ctx {
   std::vector<GemmArgs> l1_roll;  // per OBS slot 0..T
   GemmArgs l1_upd, l2, l3, l1_boot, l2_boot, l3_boot, l1_vt, dx3, dx2, dw3, dw2, dw1;
   GemmArgs l2r, l3r;        // layers 2, 3 for M <= n_envs rows (rollout): narrower tiles (bn2r, bn3r)
+  GemmArgs l1_upd_b1, dw1_b1;  // layer-1 forward and weight gradient on gathered set 1 (l1_upd / dw1: set 0)
   int bn2r = 0, bn3r = 0;
   EnvParams ep;
   ShadowArgs shadow;
@@ -436,6 +446,8 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   cmap(&u1.tmC[0], H1, 2 * d.H0, 2 * d.H0);
   set_fwd_common(u1, d.Mmb, 2 * d.H0, d.Dp, bn1, 1);
   u1.ldo = 2 * d.H0; u1.bias[0] = b1;
+  ctx->l1_upd_b1 = u1;
+  ok &= make_tmap_bf16(&ctx->l1_upd_b1.tmA[0], bf(A, L.b_X), R, d.Dp, d.Dp, 128);
   // ---- forward, layers 2, 3 (z = net)
   GemmArgs& g2 = ctx->l2;
   memset(&g2, 0, sizeof(g2));
@@ -528,6 +540,8 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   dw_setup(w3, L.dw3, 2);
   dw_setup(w2, L.dw2, 2);
   dw_setup(w1, L.dw1, 1);
+  ctx->dw1_b1 = w1;
+  ok &= make_tmap_bf16(&ctx->dw1_b1.tmB[0], bf(A, L.b_X), Mr, d.Dp, d.Dp, 64);
   if (!ok) {
     delete ctx;
     return LG_ERR_CUDA;
@@ -858,24 +872,31 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
 }
 
 // gradient of one minibatch (rows already gathered into the ACTIV minibatch arrays)
-static lg_status minibatch_gradient(lg_ctx* ctx) {
+static GatherArgs gather_args(lg_ctx* ctx, int b);
+
+// One minibatch's gradient on gathered set b. With next_perm, the gather of the next minibatch (into set
+// 1 - b) is launched on st right after dX2, beside the last weight-gradient GEMM on st2.
+static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_perm) {
   const Dims& d = ctx->d;
   const Layout& L = ctx->L;
   void* W = ctx->buf[LG_BUF_WEIGHTS];
   void* A = ctx->buf[LG_BUF_ACTIV];
   void* K = ctx->buf[LG_BUF_WORK];
   float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
-  GemmArgs l1 = ctx->l1_upd;
+  GemmArgs l1 = b ? ctx->l1_upd_b1 : ctx->l1_upd;
   lg_status s = forward_rows(ctx, l1, d.Mmb);
   if (s != LG_OK) return s;
-  LossArgs la;  // (the minibatch's gather kernel zeroed the gradient payload)
+  LossArgs la;
   la.nd = NetDims{d.D, d.Dp, d.H0, d.H1, d.H2};
   la.M = d.Mmb;
   la.H3 = at<__nv_bfloat16>(A, L.a_H3);
   la.W4a = at<float>(W, L.w_W4a); la.b4a = at<float>(W, L.w_b4a); la.W4c = at<float>(W, L.w_W4c); la.b4c = at<float>(W, L.w_b4c);
   la.logstd = at<float>(W, L.w_ls); la.logstd_old = at<float>(W, L.w_lso);
-  la.act = at<float>(A, L.a_act); la.mu_old = at<float>(A, L.a_mu); la.logp_old = at<float>(A, L.a_logp);
-  la.V_old = at<float>(A, L.a_V); la.adv = at<float>(A, L.a_adv); la.ret = at<float>(A, L.a_ret);
+  la.act = at<float>(A, b ? L.b_act : L.a_act); la.mu_old = at<float>(A, b ? L.b_mu : L.a_mu);
+  la.logp_old = at<float>(A, b ? L.b_logp : L.a_logp);
+  la.V_old = at<float>(A, b ? L.b_V : L.a_V); la.adv = at<float>(A, b ? L.b_adv : L.a_adv);
+  la.ret = at<float>(A, b ? L.b_ret : L.a_ret);
+  la.payload = ctx->payload;
   la.clip = ctx->cfg.clip; la.vclip = ctx->cfg.vclip; la.ent_coef = ctx->cfg.ent_coef; la.vf_coef = ctx->cfg.vf_coef;
   la.dZ3 = at<__nv_bfloat16>(A, L.a_dZ3);
   la.part = at<float>(K, L.k_lpart);
@@ -928,13 +949,19 @@ static lg_status minibatch_gradient(lg_ctx* ctx) {
   if ((s = gemm(ctx, GEMM_DX, x2, bn_dx(d.H0), 2)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
   if ((s = fork(2)) != LG_OK) return s;
-  if ((s = dw(ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
+  if ((s = dw(b ? ctx->dw1_b1 : ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
+  if (next_perm) {  // the next minibatch's gather (set 1 - b) runs beside dW1
+    GatherArgs g = gather_args(ctx, 1 - b);
+    g.perm = next_perm;
+    { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
+    CKL();
+  }
   CK(cudaEventRecord(ctx->ev_join, ctx->st2));
   CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
   return LG_OK;
 }
 
-static GatherArgs gather_args(lg_ctx* ctx) {
+static GatherArgs gather_args(lg_ctx* ctx, int b) {
   const Dims& d = ctx->d;
   void* A = ctx->buf[LG_BUF_ACTIV];
   const Layout& L = ctx->L;
@@ -949,18 +976,18 @@ static GatherArgs gather_args(lg_ctx* ctx) {
   g.A = reinterpret_cast<const float*>(ctx->buf[LG_BUF_ADV]);
   g.R = reinterpret_cast<const float*>(ctx->buf[LG_BUF_RET]);
   g.sc = ctx->sc;
-  g.bc_slot = -1;
-  g.payload = ctx->payload;
-  g.b1 = ctx->cfg.adam_b1; g.b2 = ctx->cfg.adam_b2;
-  g.X = at<__nv_bfloat16>(A, L.a_X);
-  g.o_act = at<float>(A, L.a_act); g.o_mu = at<float>(A, L.a_mu); g.o_logp = at<float>(A, L.a_logp);
-  g.o_V = at<float>(A, L.a_V); g.o_adv = at<float>(A, L.a_adv); g.o_ret = at<float>(A, L.a_ret);
+  g.X = at<__nv_bfloat16>(A, b ? L.b_X : L.a_X);
+  g.o_act = at<float>(A, b ? L.b_act : L.a_act); g.o_mu = at<float>(A, b ? L.b_mu : L.a_mu);
+  g.o_logp = at<float>(A, b ? L.b_logp : L.a_logp);
+  g.o_V = at<float>(A, b ? L.b_V : L.a_V); g.o_adv = at<float>(A, b ? L.b_adv : L.a_adv);
+  g.o_ret = at<float>(A, b ? L.b_ret : L.a_ret);
   return g;
 }
 
 static void iter_begin(lg_ctx* ctx) {
   void* W = ctx->buf[LG_BUF_WEIGHTS];
-  launch_iter_begin(ctx->sc, at<float>(W, ctx->L.w_lso), at<float>(W, ctx->L.w_ls), ctx->step_f + 4, ctx->st);
+  launch_iter_begin(ctx->sc, at<float>(W, ctx->L.w_lso), at<float>(W, ctx->L.w_ls), ctx->step_f + 4, ctx->cfg.adam_b1,
+                    ctx->cfg.adam_b2, ctx->st);
 }
 
 lg_status ppo_shuffle(lg_ctx* ctx, int32_t epoch, uint32_t* perm) {
@@ -981,11 +1008,11 @@ lg_status ppo_minibatch_grad(lg_ctx* ctx, const int32_t* idx, int32_t M_mb) {
   if (!idx || M_mb != d.Mmb) return fail(ctx, LG_ERR_SHAPE, "ppo_minibatch_grad: M_mb must equal N*T/K = %d", d.Mmb);
   iter_begin(ctx);
   CKL();
-  GatherArgs g = gather_args(ctx);
+  GatherArgs g = gather_args(ctx, 0);
   g.idx = idx;
   launch_gather(g, ctx->st);
   CKL();
-  return minibatch_gradient(ctx);
+  return minibatch_gradient(ctx, 0, nullptr);
 }
 
 lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
@@ -1015,19 +1042,30 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
     { Scope sc_(ctx, LG_PROF_GATHER); launch_perm(pa, ctx->st); }
     CKL();
   }
-  for (int e = 0; e < d.E; ++e) {
-    for (int m = 0; m < d.K; ++m) {
-      GatherArgs g = gather_args(ctx);
-      g.perm = perm + (size_t)e * d.B + (size_t)m * d.Mmb;
-      g.bc_slot = e * d.K + m;
+  {  // the first minibatch's gather (later ones are launched inside minibatch_gradient, beside dW1)
+    GatherArgs g = gather_args(ctx, 0);
+    g.perm = perm;
+    { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
+    CKL();
+  }
+  const int n_mb = d.E * d.K;
+  static const bool prefetch = [] {
+    const char* e = getenv("LG_GATHER_PREFETCH");
+    return e && e[0] == '1';
+  }();
+  for (int k = 0; k < n_mb; ++k) {  // minibatch k = epoch k / K, slice k % K of that epoch's permutation
+    const uint32_t* next = k + 1 < n_mb ? perm + (size_t)(k + 1) * d.Mmb : nullptr;
+    if (!prefetch && k > 0) {  // gather on the critical path (measured faster than beside dW1)
+      GatherArgs g = gather_args(ctx, k & 1);
+      g.perm = perm + (size_t)k * d.Mmb;
       { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
       CKL();
-      if ((s = minibatch_gradient(ctx)) != LG_OK) return s;
-      { Scope sc_(ctx, LG_PROF_COMM); if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s; }
-      Scope sc_adam(ctx, LG_PROF_ADAM);
-      launch_adam(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, e * d.K + m, ctx->step_f + 4, ctx->st);
-      CKL();
     }
+    if ((s = minibatch_gradient(ctx, k & 1, prefetch ? next : nullptr)) != LG_OK) return s;
+    { Scope sc_(ctx, LG_PROF_COMM); if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s; }
+    Scope sc_adam(ctx, LG_PROF_ADAM);
+    launch_adam(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, ctx->st);
+    CKL();
   }
   IterEndArgs ie;
   memset(&ie, 0, sizeof(ie));

@@ -36,7 +36,8 @@ struct DevScalars {
   float alpha_ring[2];
   int32_t adamt_ring[2];
   int32_t n_to_total;   // time-out rows compacted since the rollout began (batched bootstrap)
-  float bc_next[2];     // Adam bias corrections 1 - b^(t+1) for the next applied step (set at the minibatch start)
+  float bc_ring[2][2];  // Adam bias corrections {1 - b1^t, 1 - b2^t} for minibatch slot m (read bc_ring[m & 1],
+                        // written for slot m + 1 by Adam of slot m; slot 0 by iter_begin)
   int32_t n_to_slot[2]; // compacted time-out rows of env step event ev in slot ev & 1 (the step clears the other)
 };
 

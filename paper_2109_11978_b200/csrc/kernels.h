@@ -165,6 +165,7 @@ struct LossArgs {
   const float* logstd; const float* logstd_old;
   const float* act; const float* mu_old; const float* logp_old; const float* V_old; const float* adv; const float* ret;
   float clip, vclip, ent_coef, vf_coef;
+  float* payload;            // gradient payload; the loss kernel clears its accumulated slot 4
   __nv_bfloat16* dZ3;        // [M][2*H2] out
   float* part;               // [nblk][HP]
   double* spart;             // [nblk][8]
@@ -224,9 +225,7 @@ struct GatherArgs {
   const __nv_bfloat16* obs;  // [T+1][N][Dp]
   const float* act; const float* mu; const float* logp; const float* V; const float* A; const float* R;
   DevScalars* sc;
-  int bc_slot;               // >= 0: also set sc->bc_next for the Adam step of minibatch slot bc_slot (ring m & 1)
-  float* payload;            // zeroed (16 floats) for the minibatch's loss / gradient statistics
-  float b1, b2;
+
   __nv_bfloat16* X; float* o_act; float* o_mu; float* o_logp; float* o_V; float* o_adv; float* o_ret;
 };
 void launch_gather(const GatherArgs& a, cudaStream_t st);
@@ -259,7 +258,8 @@ struct IterEndArgs {
   DevScalars* sc; void* stats; int n_mb; int T; int n_levels; const uint32_t* state; int N; float entropy_dummy;
   const float* logstd;
 };
-void launch_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, cudaStream_t st);
+void launch_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, float b1, float b2,
+                       cudaStream_t st);
 void launch_iter_end(const IterEndArgs& a, const float* iter_acc, cudaStream_t st);
 void launch_advance_sbase(DevScalars* sc, int T, cudaStream_t st);
 

@@ -170,6 +170,9 @@ __device__ __forceinline__ float elu_grad_from_out(float h) { return h > 0.0f ? 
 __global__ void __launch_bounds__(LOSS_WARPS * 32, 1) k_loss_heads(LossArgs a) {
   pdl_trigger();
   pdl_wait();
+  // first payload writer of the minibatch: clear the atomically accumulated non-finite counter (the other
+  // slots are assigned by k_reduce_heads); the previous minibatch's Adam has consumed the payload already
+  if (a.payload && blockIdx.x == 0 && threadIdx.x == 0) a.payload[4] = 0.0f;
   extern __shared__ float sacc[];  // [LOSS_WARPS][HP] warp partials, then [LOSS_WARPS][5] fp64 statistics
   const int H2 = a.nd.H2, HP = a.HP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -521,12 +524,6 @@ constexpr int GATHER_ROWS = 4;  // rows per warp: the permutation loads and the 
 __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   pdl_trigger();
   pdl_wait();
-  if (a.payload && blockIdx.x == 0 && threadIdx.x < 16) a.payload[threadIdx.x] = 0.0f;
-  if (a.bc_slot >= 0 && blockIdx.x == 0 && threadIdx.x == 0) {  // Adam bias corrections for this minibatch
-    const int t = a.sc->adamt_ring[a.bc_slot & 1] + 1;
-    a.sc->bc_next[0] = (float)(1.0 - pow((double)a.b1, (double)t));
-    a.sc->bc_next[1] = (float)(1.0 - pow((double)a.b2, (double)t));
-  }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int r0 = warp * GATHER_ROWS;
   if (r0 >= a.M) return;
@@ -636,11 +633,13 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, 
     }
     s_apply = bad ? 0 : 1;
     s_alpha = alpha;
-    s_bc1 = sc->bc_next[0];  // 1 - b1^t for the applied step t (computed by this minibatch's gather)
-    s_bc2 = sc->bc_next[1];
+    s_bc1 = sc->bc_ring[m & 1][0];  // 1 - b^t for the applied step t (written by the previous Adam / iter_begin)
+    s_bc2 = sc->bc_ring[m & 1][1];
     if (blockIdx.x == 0) {
       sc->alpha_ring[(m + 1) & 1] = alpha;
       sc->adamt_ring[(m + 1) & 1] = t;
+      sc->bc_ring[(m + 1) & 1][0] = (float)(1.0 - pow((double)a.b1, (double)(t + 1)));
+      sc->bc_ring[(m + 1) & 1][1] = (float)(1.0 - pow((double)a.b2, (double)(t + 1)));
       if (bad) {
         sc->nonfinite_skips += 1;
       } else {
@@ -684,14 +683,21 @@ void launch_sync_shadow(const ShadowArgs& sh, const float* theta, cudaStream_t s
 }
 
 // ------------------------------------------------------------------ iteration bookkeeping
-__global__ void k_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc) {
+__global__ void k_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, float b1,
+                             float b2) {
   const int j = threadIdx.x;
   if (j < 12) logstd_old[j] = logstd[j];
   if (j < 8) iter_acc[j] = 0.0f;
-  if (j == 0) { sc->alpha_ring[0] = sc->alpha; sc->adamt_ring[0] = sc->adam_t; }
+  if (j == 0) {
+    sc->alpha_ring[0] = sc->alpha;
+    sc->adamt_ring[0] = sc->adam_t;
+    sc->bc_ring[0][0] = (float)(1.0 - pow((double)b1, (double)(sc->adam_t + 1)));
+    sc->bc_ring[0][1] = (float)(1.0 - pow((double)b2, (double)(sc->adam_t + 1)));
+  }
 }
-void launch_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, cudaStream_t st) {
-  k_iter_begin<<<1, 32, 0, st>>>(sc, logstd_old, logstd, iter_acc);
+void launch_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, float b1, float b2,
+                       cudaStream_t st) {
+  k_iter_begin<<<1, 32, 0, st>>>(sc, logstd_old, logstd, iter_acc, b1, b2);
 }
 
 __global__ void k_iter_end(IterEndArgs a, const float* acc) {
