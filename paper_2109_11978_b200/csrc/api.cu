@@ -14,16 +14,6 @@
 #include "common.cuh"
 #include "kernels.h"
 
-namespace lg {
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("LG_NO_PDL");
-    return !(e && e[0] == '1');
-  }();
-  return on;
-}
-}  // namespace lg
-
 using namespace lg;
 
 namespace {

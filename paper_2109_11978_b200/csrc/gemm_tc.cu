@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -137,6 +138,42 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---- CTA-pair (tcgen05 cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's smem, completing on an mbarrier of either CTA of the pair (shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t mbar_cluster, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `bar` (same offset) in both CTAs
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+
 // Shared-memory matrix descriptor (SM100 version 1), 128-byte swizzle.
 //  K-major : rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO); LBO unused.
 //  MN-major: rows of 128 B (64 bf16 of M or N) indexed by k; 8-k atoms 1024 B apart (SBO),
@@ -160,11 +197,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool PAIR = false>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // a CTA of a pair holds half of B
   static constexpr int ONES_BYTES = 16 * 128;  // 16 rows x 64 bf16 of 1.0
   static constexpr int EPI_BUF = 4096;         // one 32 x 128-B staging sub-tile
   static constexpr int EPI_NBUF = EPI == 3 ? 1 : 2;
@@ -220,9 +257,14 @@ __device__ __forceinline__ TileCoord decode(const GemmArgs& a, int t, int m_tile
   return c;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// PAIR: a cluster of 2 CTAs computes 256-row tiles with tcgen05.mma.cta_group::2 -- each CTA loads its own
+// 128 rows of A and half of B (so each SM receives 2/3 of the operand bytes of a 128 x BN tile), both CTAs'
+// loads complete on the leader's full barrier, the leader issues the MMAs and multicasts its commits, and the
+// peer's epilogue warps release the accumulator stage on the leader's tempty barrier (remote arrive).
+template <int BN, bool A_MN, bool B_MN, int EPI, bool PAIR = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_constant__ GemmArgs args) {
-  using C = GemmCfg<BN, EPI>;
+  using C = GemmCfg<BN, EPI, PAIR>;
+  static_assert(!PAIR || (EPI != 3 && !A_MN && BN >= 128), "pairs: forward / input-gradient GEMMs only");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -240,17 +282,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   pdl_trigger();
   if (args.M_dev) pdl_wait();  // the device-side row count is a predecessor's output
   const int M = args.M_dev ? *args.M_dev : args.M;
-  const int m_tiles = args.m_tiles;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  // tile loop over (pair) tiles: a pair tile covers 128-row tiles 2u and 2u+1 of the same column block
+  const int m_tiles = PAIR ? (args.m_tiles + 1) / 2 : args.m_tiles;
+  const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ncl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int total = args.nz * m_tiles * args.n_tiles * args.n_splits;
-  {  // CTA-uniform early exit when none of this CTA's tiles has rows (device-sized M, e.g. no time-outs)
+  auto tile_of = [&](int t) {  // (pair) tile -> this CTA's coordinates; skip when the (pair) tile has no rows
+    TileCoord c = decode(args, t, m_tiles, BN);
+    if (PAIR) c.m0 = 2 * c.m0 + (int)rank * 128;
+    return c;
+  };
+  auto skip = [&](const TileCoord& c) { return (PAIR ? c.m0 - (int)rank * 128 : c.m0) >= M; };
+  if (!PAIR) {  // CTA-uniform early exit when none of this CTA's tiles has rows (device-sized M, e.g. no time-outs)
     bool any = false;
-    for (int t = blockIdx.x; t < total && !any; t += gridDim.x) any = decode(args, t, m_tiles, BN).m0 < M;
+    for (int t = cid; t < total && !any; t += ncl) any = !skip(tile_of(t));
     if (!any) return;
   }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], (PAIR ? 2 : 1) * EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (EPI == 3) {  // 16 x 64 bf16 ones (any swizzle of a constant tile is the same tile)
@@ -259,12 +311,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     fence_async_smem();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_barrier();  // the peer's barriers exist before any cross-CTA signal
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // the prologue above overlapped the preceding kernel; its outputs are read from here on
@@ -274,9 +333,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = decode(args, t, m_tiles, BN);
-        if (tc.m0 >= M) continue;
+      for (int t = cid; t < total; t += ncl) {
+        const TileCoord tc = tile_of(t);
+        if (skip(tc)) continue;
         const CUtensorMap* tmA = &args.tmA[tc.z];
         const CUtensorMap* tmB = &args.tmB[tc.z];
         const int kb0 = tc.split * args.kb_per_split;
@@ -286,6 +345,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
           const int k0 = (kb0 + kb) * C::BK;
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
+          if (PAIR) {
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            tma_load_2d_pair(tmA, fb, a, k0, tc.m0);
+            const int nh = tc.n0 + (int)rank * (BN / 2);
+            if (!B_MN) {
+              tma_load_2d_pair(&args.tmBp[tc.z], fb, b, k0, nh);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BN / 128; ++i) tma_load_2d_pair(tmB, fb, b + i * 8192, nh + 64 * i, k0);
+            }
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+            continue;
+          }
           if (args.probe & 2) { mbar_arrive(&full[stage]); if (++stage == C::STAGES) { stage = 0; phase ^= 1u; } continue; }
           mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           if (!A_MN) {
@@ -307,17 +380,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, BN, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, BN, A_MN, B_MN);
       constexpr uint32_t idesc_ones = idesc_bf16(128, 16, A_MN, false);
       const uint32_t a_lbo = A_MN ? 8192u : 0u, b_lbo = B_MN ? 8192u : 0u;
       const uint32_t a_step = A_MN ? 2048u : 32u, b_step = B_MN ? 2048u : 32u;  // bytes per UMMA_K = 16
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = decode(args, t, m_tiles, BN);
-        if (tc.m0 >= M) continue;
+      for (int t = cid; t < total; t += ncl) {
+        const TileCoord tc = tile_of(t);
+        if (skip(tc)) continue;
         const int acc = local % C::ACC_STAGES;
         const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
         ++local;
@@ -336,16 +409,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
           for (int k = 0; k < C::BK / 16; ++k) {
             const uint64_t ad = sdesc(a0 + k * a_step, a_lbo, 1024u);
             const uint64_t bd = sdesc(b0 + k * b_step, b_lbo, 1024u);
-            tc_mma(tacc, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
-            if (bias_col) {
-              const uint64_t od = sdesc(smem_u32(sOnes) + k * 32u, 0u, 1024u);
-              tc_mma(tacc + BN, ad, od, idesc_ones, (kb > 0 || k > 0) ? 1u : 0u);
+            if (PAIR) {
+              tc_mma_pair(tacc, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            } else {
+              tc_mma(tacc, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if (bias_col) {
+                const uint64_t od = sdesc(smem_u32(sOnes) + k * 32u, 0u, 1024u);
+                tc_mma(tacc + BN, ad, od, idesc_ones, (kb > 0 || k > 0) ? 1u : 0u);
+              }
             }
           }
-          tc_commit(&empty[stage]);
+          if (PAIR) tc_commit_pair(&empty[stage]);
+          else tc_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
         }
-        tc_commit(&tfull[acc]);
+        if (PAIR) tc_commit_pair(&tfull[acc]);
+        else tc_commit(&tfull[acc]);
       }
     }
     __syncwarp();
@@ -357,9 +436,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     constexpr int WCOLS = BN >= 128 ? BN / 2 : BN;  // columns handled by this warp
     const bool active = BN >= 128 || h == 0;
     int local = 0, nst = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileCoord tc = decode(args, t, m_tiles, BN);
-      if (tc.m0 >= M) continue;
+    for (int t = cid; t < total; t += ncl) {
+      const TileCoord tc = tile_of(t);
+      if (skip(tc)) continue;
       const int acc = local % C::ACC_STAGES;
       const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
       ++local;
@@ -486,17 +565,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
           }
         }
       }
-      // release the accumulator stage to the MMA warp
+      // release the accumulator stage to the MMA warp (the leader's barrier for a pair)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR && rank != 0) {
+          const uint32_t rb = mapa_shared(smem_u32(&tempty[acc]), 0);
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
+      }
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  if (PAIR) {
+    cluster_barrier();  // both CTAs are done with the pair's TMEM
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  } else {
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  }
 }
 
 // ------------------------------------------------------------------ dW: one-wave split-K with an L2 reduction
@@ -785,41 +876,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
 // core, bounds these skinny GEMMs). Both CTAs' loads complete on the leader's full barrier; the leader alone
 // issues tcgen05.mma.cta_group::2 (M = 256) and multicasts its commits to the empty / accumulator-full
 // barriers of both CTAs; each CTA then drains its own TMEM half (its 128 rows) into the shared split-K tail.
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// TMA load into this CTA's smem, completing on an mbarrier of either CTA of the pair (shared::cluster address)
-__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t mbar_cluster, void* dst, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(x), "r"(y)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `bar` (same offset) in both CTAs
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   smem_u32(bar)),
-               "h"((uint16_t)3)
-               : "memory");
-}
-
 template <int BN>
 struct Dw2Cfg {
   static constexpr int BM = 128, BK = 64;
@@ -1366,6 +1422,14 @@ cudaError_t launch_policy_fused(const FusedPolicyArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ host side
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LG_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static int g_num_sms = 0;
 static int g_dw_max_ctas() {  // one k_gemm_dw CTA per SM (its shared memory allows no more)
@@ -1408,12 +1472,13 @@ bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, rows, cols, ld, 32, box_rows);
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, bool PAIR = false>
 static cudaError_t launch_one(const GemmArgs& a, cudaStream_t st) {
-  using C = GemmCfg<BN, EPI>;
+  using C = GemmCfg<BN, EPI, PAIR>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, A_MN, B_MN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, A_MN, B_MN, EPI, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -1423,6 +1488,25 @@ static cudaError_t launch_one(const GemmArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
+  if (PAIR) {
+    const int total = a.nz * ((a.m_tiles + 1) / 2) * a.n_tiles * a.n_splits;
+    const int pairs = total < g_num_sms / 2 ? total : g_num_sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, A_MN, B_MN, EPI, PAIR>, a);
+  }
   const int total = a.nz * a.m_tiles * a.n_tiles * a.n_splits;
   const int grid = total < g_num_sms ? total : g_num_sms;
   return launch_pdl(k_gemm_tc<BN, A_MN, B_MN, EPI>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, st, a);
@@ -1430,6 +1514,15 @@ static cudaError_t launch_one(const GemmArgs& a, cudaStream_t st) {
 
 template <bool A_MN, bool B_MN, int EPI>
 static cudaError_t dispatch_bn(int bn, const GemmArgs& a, cudaStream_t st) {
+  if constexpr (EPI != 3 && !A_MN) {
+    if (a.pair) {
+      switch (bn) {
+        case 128: return launch_one<128, A_MN, B_MN, EPI, true>(a, st);
+        case 256: return launch_one<256, A_MN, B_MN, EPI, true>(a, st);
+        default: break;
+      }
+    }
+  }
   switch (bn) {
     case 64: return launch_one<64, A_MN, B_MN, EPI>(a, st);
     case 128: return launch_one<128, A_MN, B_MN, EPI>(a, st);

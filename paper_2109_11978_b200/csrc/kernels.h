@@ -81,6 +81,8 @@ struct GemmArgs {
   long long part_zstride, part_sstride;
   int part_rows, part_ld, part_bias_col, bias_col;
   int probe;                 // diagnostics only (tools/gemm_probe): bit0 = skip the MMAs, bit1 = skip the TMA loads
+  int pair;                  // forward / input-gradient GEMMs: CTA pairs (cta_group::2, 256-row tiles)
+  CUtensorMap tmBp[2];       // pair + K-major B: B with a box of BN/2 rows (each CTA loads half of the tile's B)
 };
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);

@@ -406,6 +406,46 @@ static void probe_fused(int N, cudaStream_t st) {
   }
 }
 
+// forward (kind 0) / input-gradient (kind 1) GEMM: CTA pair vs single CTA, timing and element-wise equality
+static void probe_pair_gemm(int kind, int M, int N, int K, int bn, cudaStream_t st) {
+  __nv_bfloat16 *A, *W, *H, *Y1, *Y2;
+  float* bias;
+  CK(cudaMalloc(&A, (size_t)M * K * 2)); CK(cudaMalloc(&W, (size_t)K * N * 2)); CK(cudaMalloc(&H, (size_t)M * N * 2));
+  CK(cudaMalloc(&Y1, (size_t)M * N * 2)); CK(cudaMalloc(&Y2, (size_t)M * N * 2)); CK(cudaMalloc(&bias, N * 4));
+  fill(A, (size_t)M * K); fill(W, (size_t)K * N); fill(H, (size_t)M * N);
+  CK(cudaMemset(bias, 0, N * 4));
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  make_tmap_bf16(&g.tmA[0], A, M, K, K, 128);
+  if (kind == 0) {  // W [N][K] K-major
+    make_tmap_bf16(&g.tmB[0], W, N, K, K, bn);
+    make_tmap_bf16(&g.tmBp[0], W, N, K, K, bn / 2);
+    g.bias[0] = bias;
+  } else {          // W [K][N] read MN-major
+    make_tmap_bf16(&g.tmB[0], W, K, N, N, 64);
+    g.aux[0] = H; g.ld_aux = N;
+  }
+  g.M = M; g.N = N; g.m_tiles = (M + 127) / 128; g.nz = 1;
+  g.kb_total = (K + 63) / 64; g.kb_per_split = g.kb_total; g.n_tiles = (N + bn - 1) / bn; g.n_splits = 1; g.ldo = N;
+  GemmArgs g1 = g, g2 = g;
+  make_tmap_bf16(&g1.tmC[0], Y1, M, N, N, 32);
+  make_tmap_bf16(&g2.tmC[0], Y2, M, N, N, 32);
+  g2.pair = 1;
+  const GemmKind gk = kind == 0 ? GEMM_FWD : GEMM_DX;
+  const double fl = 2.0 * M * N * K;
+  float u1 = time_us([&] { CK(launch_gemm(gk, bn, g1, st)); }, st);
+  float u2 = time_us([&] { CK(launch_gemm(gk, bn, g2, st)); }, st);
+  CK(cudaStreamSynchronize(st));
+  std::vector<uint16_t> y1((size_t)M * N), y2((size_t)M * N);
+  CK(cudaMemcpy(y1.data(), Y1, y1.size() * 2, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(y2.data(), Y2, y2.size() * 2, cudaMemcpyDeviceToHost));
+  size_t diff = 0;
+  for (size_t i = 0; i < y1.size(); ++i) diff += y1[i] != y2[i];
+  printf("%s M=%d N=%d K=%d bn=%d  single %8.2f us (%6.1f TF)  pair %8.2f us (%6.1f TF)  differing outputs %zu of %zu\n",
+         kind == 0 ? "fwd" : "dx ", M, N, K, bn, u1, fl / u1 * 1e-6, u2, fl / u2 * 1e-6, diff, y1.size());
+  CK(cudaFree(A)); CK(cudaFree(W)); CK(cudaFree(H)); CK(cudaFree(Y1)); CK(cudaFree(Y2)); CK(cudaFree(bias));
+}
+
 static void check_dw(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st) {
   std::vector<float> a = probe_dw(Nout, Nin, K, bn, 1, 1, st, true);  // unsplit K
   std::vector<float> b = probe_dw(Nout, Nin, K, bn, S, G, st, true);
@@ -473,6 +513,18 @@ int main(int argc, char** argv) {
     probe_dw_phases(512, 512, 24576, 256, 18, 1, st);    // dW2 both nets as 8 tiles
     probe_dw_phases(256, 256, 24576, 256, 74, 1, st);    // dW3 both nets as 2 tiles
     probe_dw_phases(128, 64, 64, 64, 1, 1, st);
+    return 0;
+  }
+  if (!strcmp(which, "pairgemm")) {
+    probe_pair_gemm(0, 24576, 1024, 256, 256, st);  // L1
+    probe_pair_gemm(0, 24576, 256, 512, 256, st);   // L2 (one net)
+    probe_pair_gemm(0, 24576, 128, 256, 128, st);   // L3 (one net)
+    probe_pair_gemm(1, 24576, 512, 256, 256, st);   // dX2 (one net)
+    probe_pair_gemm(1, 24576, 256, 128, 128, st);   // dX3 (one net)
+    probe_pair_gemm(0, 1000, 256, 256, 256, st);    // odd tile count (8 tiles -> 4 pairs), ragged rows
+    probe_pair_gemm(0, 900, 256, 256, 256, st);     // 8 tiles, ragged
+    probe_pair_gemm(0, 700, 256, 256, 128, st);     // 6 tiles
+    probe_pair_gemm(0, 300, 256, 256, 256, st);     // 3 tiles (odd)
     return 0;
   }
   if (!strcmp(which, "fused")) {
