@@ -901,6 +901,9 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
   { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
   CKL();
+  // the weight-gradient chain runs on st2 beside the dX chain; the profiled pass (lg_profile, timing each
+  // category) keeps everything on st so that every kernel's measured duration is its own
+  cudaStream_t sdw = ctx->prof ? ctx->st : ctx->st2;
   auto dw = [&](const GemmArgs& g, const DwPlan& p, size_t koff, int cols, const long long* woff,
                 const long long* boff, int row_split) -> lg_status {
     DwOut o;
@@ -913,14 +916,15 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
     o.cols = cols;
     o.row_split = row_split;
     o.payload = ctx->payload;
-    Scope sc_(ctx, LG_PROF_GEMM_DW, ctx->st2);
-    cudaError_t e = p.pair ? launch_gemm_dw_pair(p.bn, g, o, p.S, ctx->st2) : launch_gemm_dw(p.bn, g, o, p.S, ctx->st2);
+    Scope sc_(ctx, LG_PROF_GEMM_DW, sdw);
+    cudaError_t e = p.pair ? launch_gemm_dw_pair(p.bn, g, o, p.S, sdw) : launch_gemm_dw(p.bn, g, o, p.S, sdw);
     if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm_dw: %s", cudaGetErrorString(e));
     return LG_OK;
   };
   // The dW chain runs on st2, forked after dZ_l is written: dW3 beside dX3, dW2 beside dX2, then dW1;
   // st waits for it before the gradient is reduced / applied.
   auto fork = [&](int k) -> lg_status {
+    if (sdw == ctx->st) return LG_OK;
     CK(cudaEventRecord(ctx->ev_fork[k], ctx->st));
     CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork[k], 0));
     return LG_OK;
@@ -946,8 +950,10 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
     { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
     CKL();
   }
-  CK(cudaEventRecord(ctx->ev_join, ctx->st2));
-  CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
+  if (sdw != ctx->st) {
+    CK(cudaEventRecord(ctx->ev_join, ctx->st2));
+    CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0));
+  }
   return LG_OK;
 }
 
