@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
       __syncwarp();
       tc_fence_after();
       const uint32_t tbase = tmem + acc * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
-      if (active) {
+      if (active && !(args.probe & 4)) {
         if (EPI == 3) {
           // fp32 split-K partial: 32-column chunks
           const int prow = (tc.z * args.n_splits + tc.split) * args.part_rows + tc.m0 + q * 32;

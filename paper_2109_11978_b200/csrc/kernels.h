@@ -80,7 +80,8 @@ struct GemmArgs {
   float* part;               // EPI 3: split-K partials [z][split][part_rows][part_ld] (bias column direct)
   long long part_zstride, part_sstride;
   int part_rows, part_ld, part_bias_col, bias_col;
-  int probe;                 // diagnostics only (tools/gemm_probe): bit0 = skip the MMAs, bit1 = skip the TMA loads
+  int probe;                 // diagnostics only (tools/gemm_probe): bit0 = skip the MMAs, bit1 = skip the TMA loads,
+                             // bit2 = skip the epilogue
   int pair;                  // forward / input-gradient GEMMs: CTA pairs (cta_group::2, 256-row tiles)
   CUtensorMap tmBp[2];       // pair + K-major B: B with a box of BN/2 rows (each CTA loads half of the tile's B)
 };

@@ -97,7 +97,9 @@ static void probe_fwd(int M, int N, int K, int bn, cudaStream_t st) {
   g.kb_total = (K + 63) / 64; g.kb_per_split = g.kb_total; g.n_tiles = (N + bn - 1) / bn; g.n_splits = 1;
   g.ldo = N; g.bias[0] = bias;
   const double fl = 2.0 * M * N * K;
-  for (int probe = 0; probe < 3; ++probe) {
+  const int probes[4] = {0, 1, 2, 4};
+  for (int pi = 0; pi < 4; ++pi) {
+    const int probe = probes[pi];
     g.probe = probe;
     float us = time_us([&] { CK(launch_gemm(GEMM_FWD, bn, g, st)); }, st);
     const double bytes = ((double)M * K + (double)g.m_tiles * 128.0 * 0 + (double)N * K * g.m_tiles) * 2.0;
@@ -122,7 +124,9 @@ static void probe_dx(int M, int N, int K, int bn, cudaStream_t st, bool once = f
   g.kb_total = (K + 63) / 64; g.kb_per_split = g.kb_total; g.n_tiles = (N + bn - 1) / bn; g.n_splits = 1;
   g.ldo = N; g.aux[0] = H; g.ld_aux = N;
   const double fl = 2.0 * M * N * K;
-  for (int probe = 0; probe < (once ? 1 : 3); ++probe) {
+  const int probes[4] = {0, 1, 2, 4};
+  for (int pi = 0; pi < (once ? 1 : 4); ++pi) {
+    const int probe = probes[pi];
     g.probe = probe;
     float us = time_us([&] { CK(launch_gemm(GEMM_DX, bn, g, st)); }, st);
     printf("dx M=%d N=%d K=%d bn=%d probe=%d  %8.2f us  %7.1f TFLOP/s\n", M, N, K, bn, probe, us, fl / us * 1e-6);
@@ -484,6 +488,14 @@ int main(int argc, char** argv) {
   if (!strcmp(which, "one") && argc >= 9) {  // one dW config: one Nout Nin K bn S G (for ncu)
     g_do_flush = false;
     probe_dw(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), atoi(argv[6]), atoi(argv[7]), st, true);
+    return 0;
+  }
+  if (!strcmp(which, "epi")) {
+    probe_fwd(24576, 1024, 256, 256, st);
+    probe_fwd(24576, 256, 512, 256, st);
+    probe_fwd(24576, 128, 256, 128, st);
+    probe_dx(24576, 512, 256, 256, st);
+    probe_dx(24576, 256, 128, 128, st);
     return 0;
   }
   if (!strcmp(which, "dx")) {
