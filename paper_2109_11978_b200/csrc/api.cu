@@ -75,12 +75,12 @@ int bn_for(int n) { return n >= 256 ? 256 : (n > 64 ? 128 : 64); }
 // input-gradient GEMMs (epilogue bound, short K): 256-wide tiles only above 256 columns (measured)
 int bn_dx(int n) { return n > 256 ? 256 : (n > 64 ? 128 : 64); }
 // narrower tiles while the GEMM still fits one wave: small-M (rollout) GEMMs are latency bound, more CTAs win
-int bn_small(int n, int m_rows, int nz) {
+int bn_fit(int bn, int n, int m_rows, int nz) {
   const int mt = (m_rows + 127) / 128;
-  int bn = bn_for(n);
   while (bn > 64 && (long long)mt * ((n + bn / 2 - 1) / (bn / 2)) * nz <= 148) bn /= 2;
   return bn;
 }
+int bn_small(int n, int m_rows, int nz) { return bn_fit(bn_for(n), n, m_rows, nz); }
 
 struct DwPlan {
   int rows, N, bn, n_tiles, m_tiles, kb_total, tiles, S, kb_per_split, pair;
@@ -88,10 +88,10 @@ struct DwPlan {
 };
 // Weight-gradient GEMM plan (k_gemm_dw): 128 x bn output tiles; the minibatch (K) is split over S CTAs per
 // tile so that tiles * S fills the 148 SMs in one wave; the S fp32 partials are reduced through L2.
-DwPlan dw_plan(int rows, int N, int K, int nz) {
+static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn) {
   DwPlan p;
   p.rows = rows; p.N = N;
-  p.bn = N > 128 ? 256 : (N > 64 ? 128 : 64);  // wide tiles: fewer operand re-reads
+  p.bn = bn;
   p.n_tiles = (N + p.bn - 1) / p.bn;
   p.m_tiles = (rows + 127) / 128;
   p.kb_total = (K + 63) / 64;
@@ -107,6 +107,25 @@ DwPlan dw_plan(int rows, int N, int K, int nz) {
   p.part_bytes = al((size_t)p.tiles * p.S * 128 * (p.bn + 20) * 4);
   p.bytes = p.part_bytes + 256;  // + the grid-barrier counter
   return p;
+}
+// The tile width: the widest tiles (fewest operand re-reads) unless the batch is small (fewer than 8 splits)
+// -- then narrower tiles put more SMs on the same k-blocks. Modelled cost of
+// the busiest CTA: its operand bytes (the per-SM TMA rate bounds these GEMMs) + the split-K partial's round
+// trip through L2; the cheapest wins, ties to the wider tile.
+DwPlan dw_plan(int rows, int N, int K, int nz) {
+  const int widest = N > 128 ? 256 : (N > 64 ? 128 : 64);
+  DwPlan best = dw_plan_bn(rows, N, K, nz, widest);
+  // large minibatches keep the widest tiles: their splits already fill the SMs, and the dW chain shares
+  // them with the concurrent dX chain (measured: narrower dW3 tiles cost ~2% of the C3 iteration)
+  if (best.S >= 8 || best.tiles >= 148) return best;
+  auto cost = [](const DwPlan& p) {
+    return (double)p.kb_per_split * (128 * 64 * 2 + p.bn * 64 * 2) + (p.S > 1 ? 2.0 * 128 * (p.bn + 20) * 4 : 0.0);
+  };
+  for (int bn = widest / 2; bn >= 64; bn /= 2) {
+    const DwPlan q = dw_plan_bn(rows, N, K, nz, bn);
+    if (q.tiles * q.S <= 148 && cost(q) < 0.9 * cost(best)) best = q;
+  }
+  return best;
 }
 
 struct Layout {
@@ -228,6 +247,8 @@ struct lg_ctx {
   GemmArgs l2r, l3r;        // layers 2, 3 for M <= n_envs rows (rollout): narrower tiles (bn2r, bn3r)
   GemmArgs l1_upd_b1, dw1_b1;  // layer-1 forward and weight gradient on gathered set 1 (l1_upd / dw1: set 0)
   int bn2r = 0, bn3r = 0;
+  int bn1u = 0, bn2u = 0, bn3u = 0, bnx3 = 0, bnx2 = 0;  // update GEMMs (minibatch rows; narrower when M is small)
+  CUtensorMap tmW2f[2], tmW3f[2];  // the fused rollout policy's W2 / W3 maps (its fixed boxes, not the update's)
   EnvParams ep;
   ShadowArgs shadow;
   cudaGraph_t graph = nullptr;
@@ -412,7 +433,11 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   float* b2 = at<float>(W, L.w_b2);
   float* b3 = at<float>(W, L.w_b3);
   bool ok = true;
-  const int bn1 = bn_for(2 * d.H0), bn1c = bn_for(d.H0), bn2 = bn_for(d.H1), bn3 = bn_for(d.H2);
+  const int bn1 = bn_for(2 * d.H0), bn1c = bn_for(d.H0);
+  const int bn1u = ctx->bn1u = bn_small(2 * d.H0, d.Mmb, 1);
+  const int bn2 = ctx->bn2u = bn_small(d.H1, d.Mmb, 2), bn3 = ctx->bn3u = bn_small(d.H2, d.Mmb, 2);
+  ctx->bnx3 = bn_fit(bn_dx(d.H1), d.H1, d.Mmb, 2);
+  ctx->bnx2 = bn_fit(bn_dx(d.H0), d.H0, d.Mmb, 2);
   const uint64_t R = d.R;
   // output maps (TMA stores, box 64 x 32, clipped to the per-net column range)
   auto cmap = [&](CUtensorMap* m, const __nv_bfloat16* base, int cols, int ld) {
@@ -432,9 +457,9 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   GemmArgs& u1 = ctx->l1_upd;
   memset(&u1, 0, sizeof(u1));
   ok &= make_tmap_bf16(&u1.tmA[0], X, R, d.Dp, d.Dp, 128);
-  ok &= make_tmap_bf16(&u1.tmB[0], W1, 2 * d.H0, d.Dp, d.Dp, bn1);
+  ok &= make_tmap_bf16(&u1.tmB[0], W1, 2 * d.H0, d.Dp, d.Dp, bn1u);
   cmap(&u1.tmC[0], H1, 2 * d.H0, 2 * d.H0);
-  set_fwd_common(u1, d.Mmb, 2 * d.H0, d.Dp, bn1, 1);
+  set_fwd_common(u1, d.Mmb, 2 * d.H0, d.Dp, bn1u, 1);
   u1.ldo = 2 * d.H0; u1.bias[0] = b1;
   ctx->l1_upd_b1 = u1;
   ok &= make_tmap_bf16(&ctx->l1_upd_b1.tmA[0], bf(A, L.b_X), R, d.Dp, d.Dp, 128);
@@ -455,6 +480,10 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   }
   set_fwd_common(g2, d.Mmb, d.H1, d.H0, bn2, 2); g2.ldo = 2 * d.H1;
   set_fwd_common(g3, d.Mmb, d.H2, d.H1, bn3, 2); g3.ldo = 2 * d.H2;
+  for (int z = 0; z < 2; ++z) {
+    ok &= make_tmap_bf16(&ctx->tmW2f[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, bn_for(d.H1));
+    ok &= make_tmap_bf16(&ctx->tmW3f[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, bn_for(d.H2));
+  }
   ctx->bn2r = bn_small(d.H1, d.N, 2);
   ctx->bn3r = bn_small(d.H2, d.N, 2);
   ctx->l2r = g2;
@@ -503,8 +532,8 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     cmap(&x2.tmC[z], dZ1 + z * d.H0, d.H0, 2 * d.H0);
     x2.aux[z] = H1 + z * d.H0;
   }
-  set_fwd_common(x3, d.Mmb, d.H1, d.H2, bn_dx(d.H1), 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
-  set_fwd_common(x2, d.Mmb, d.H0, d.H1, bn_dx(d.H0), 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
+  set_fwd_common(x3, d.Mmb, d.H1, d.H2, ctx->bnx3, 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
+  set_fwd_common(x2, d.Mmb, d.H0, d.H1, ctx->bnx2, 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
   // ---- backward dW (A = dZ MN-major, B = activations MN-major), split-K over the minibatch
   auto dw_setup = [&](GemmArgs& g, const DwPlan& p, int nz) {
     g.M = p.rows; g.N = p.N; g.M_dev = nullptr;
@@ -576,6 +605,19 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   seg(cn.W4[1], 1, d.H2, 1, at<float>(W, L.w_W4c), d.H2);
   seg(cn.b4[1], 1, 1, 1, at<float>(W, L.w_b4c), 1);
   seg(cn.logstd, 1, 12, 1, at<float>(W, L.w_ls), 12);
+  {  // the segments tile the canonical vector exactly (k_adam visits every parameter through them)
+    long long covered = 0;
+    sh.blk0[0] = 0;
+    for (int k = 0; k < sh.nseg; ++k) {
+      const long long n = (long long)sh.seg[k].rows * sh.seg[k].cols;
+      covered += n;
+      sh.blk0[k + 1] = sh.blk0[k] + (int)((n + ADAM_BLOCK_ELEMS - 1) / ADAM_BLOCK_ELEMS);
+    }
+    if (covered != d.P) {
+      delete ctx;
+      return LG_ERR_SHAPE;
+    }
+  }
   // zero the padded weight columns and the work buffer once (no kernels launched by the caller yet)
   cudaError_t e = cudaMemsetAsync(W, 0, L.bytes[LG_BUF_WEIGHTS], ctx->st);
   if (e == cudaSuccess) e = cudaMemsetAsync(K, 0, L.bytes[LG_BUF_WORK], ctx->st);
@@ -662,7 +704,8 @@ static HeadArgs head_args(lg_ctx* ctx, int M) {
   return h;
 }
 
-static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int M, int cat = LG_PROF_GEMM_FWD) {
+// l1: the layer-1 GEMM (its B map's box is bn1 wide); M <= n_envs rows use the rollout's layer-2/3 tiles
+static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int bn1, int M, int cat = LG_PROF_GEMM_FWD) {
   const Dims& d = ctx->d;
   g_gemm_cat = cat;
   l1.M = M;
@@ -670,9 +713,9 @@ static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int M, int cat = LG_PRO
   GemmArgs g2 = small ? ctx->l2r : ctx->l2, g3 = small ? ctx->l3r : ctx->l3;
   g2.M = M; g3.M = M;
   lg_status s;
-  if ((s = gemm(ctx, GEMM_FWD, l1, bn_for(2 * d.H0), 1)) != LG_OK) return s;
-  if ((s = gemm(ctx, GEMM_FWD, g2, small ? ctx->bn2r : bn_for(d.H1), 2)) != LG_OK) return s;
-  if ((s = gemm(ctx, GEMM_FWD, g3, small ? ctx->bn3r : bn_for(d.H2), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, l1, bn1, 1)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, g2, small ? ctx->bn2r : ctx->bn2u, 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, g3, small ? ctx->bn3r : ctx->bn3u, 2)) != LG_OK) return s;
   return LG_OK;
 }
 
@@ -684,8 +727,8 @@ static lg_status critic_rows(lg_ctx* ctx, GemmArgs& c1, const int* M_dev, int M)
   a.M_dev = b.M_dev = c.M_dev = M_dev;
   lg_status s;
   if ((s = gemm(ctx, GEMM_FWD, a, bn_for(d.H0), 1)) != LG_OK) return s;
-  if ((s = gemm(ctx, GEMM_FWD, b, bn_for(d.H1), 1)) != LG_OK) return s;
-  if ((s = gemm(ctx, GEMM_FWD, c, bn_for(d.H2), 1)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, b, ctx->bn2u, 1)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, c, ctx->bn3u, 1)) != LG_OK) return s;
   return LG_OK;
 }
 
@@ -743,8 +786,8 @@ lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float*
     memset(&fa, 0, sizeof(fa));
     fa.tmX = ctx->l1_roll[t].tmA[0];
     fa.tmW1 = ctx->l1_roll[t].tmB[0];
-    fa.tmW2[0] = ctx->l2.tmB[0]; fa.tmW2[1] = ctx->l2.tmB[1];
-    fa.tmW3[0] = ctx->l3.tmB[0]; fa.tmW3[1] = ctx->l3.tmB[1];
+    fa.tmW2[0] = ctx->tmW2f[0]; fa.tmW2[1] = ctx->tmW2f[1];
+    fa.tmW3[0] = ctx->tmW3f[0]; fa.tmW3[1] = ctx->tmW3f[1];
     void* W = ctx->buf[LG_BUF_WEIGHTS];
     fa.b1 = at<float>(W, ctx->L.w_b1); fa.b2 = at<float>(W, ctx->L.w_b2); fa.b3 = at<float>(W, ctx->L.w_b3);
     fa.W4a = at<float>(W, ctx->L.w_W4a); fa.b4a = at<float>(W, ctx->L.w_b4a);
@@ -762,7 +805,7 @@ lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float*
     if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "policy (fused): %s", cudaGetErrorString(e));
     return LG_OK;
   }
-  lg_status s = forward_rows(ctx, ctx->l1_roll[t], d.N, LG_PROF_GEMM_ROLL);
+  lg_status s = forward_rows(ctx, ctx->l1_roll[t], bn_for(2 * d.H0), d.N, LG_PROF_GEMM_ROLL);
   if (s != LG_OK) return s;
   HeadArgs h = head_args(ctx, d.N);
   h.mode = 0;
@@ -783,7 +826,7 @@ lg_status policy_forward(lg_ctx* ctx, const void* x, int32_t M, float* mu, float
   if (!x || !mu || !value || M < 1 || M > d.R) return fail(ctx, LG_ERR_INVALID_ARG, "policy_forward: bad arguments");
   GemmArgs l1 = ctx->l1_upd;
   if (!make_tmap_bf16(&l1.tmA[0], x, M, d.Dp, d.Dp, 128)) return fail(ctx, LG_ERR_CUDA, "tensor map");
-  lg_status s = forward_rows(ctx, l1, M);
+  lg_status s = forward_rows(ctx, l1, ctx->bn1u, M);
   if (s != LG_OK) return s;
   HeadArgs h = head_args(ctx, M);
   h.mode = 2;
@@ -874,7 +917,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   void* K = ctx->buf[LG_BUF_WORK];
   float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
   GemmArgs l1 = b ? ctx->l1_upd_b1 : ctx->l1_upd;
-  lg_status s = forward_rows(ctx, l1, d.Mmb);
+  lg_status s = forward_rows(ctx, l1, ctx->bn1u, d.Mmb);
   if (s != LG_OK) return s;
   LossArgs la;
   la.nd = NetDims{d.D, d.Dp, d.H0, d.H1, d.H2};
@@ -934,13 +977,13 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
   GemmArgs x3 = ctx->dx3;
   x3.M = d.Mmb;
-  if ((s = gemm(ctx, GEMM_DX, x3, bn_dx(d.H1), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_DX, x3, ctx->bnx3, 2)) != LG_OK) return s;
   // layer 2
   if ((s = fork(1)) != LG_OK) return s;
   if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   GemmArgs x2 = ctx->dx2;
   x2.M = d.Mmb;
-  if ((s = gemm(ctx, GEMM_DX, x2, bn_dx(d.H0), 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_DX, x2, ctx->bnx2, 2)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
   if ((s = fork(2)) != LG_OK) return s;
   if ((s = dw(b ? ctx->dw1_b1 : ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;

@@ -614,17 +614,73 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (out.dbg && threadIdx.x == 0) out.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (k)] = gtimer(); \
   } while (0)
 
-// The split-K tail shared by the dW kernels: the CTA's fp32 partial (128 rows x RLD, staged in smem `red`) ->
-// the L2 buffer [tile][split][128][RLD] with coalesced 16-B stores; a grid barrier (cooperative launch: all
-// CTAs resident; the counter only grows, the target is the next multiple of the grid size, so no reset is
-// needed between launches); then the whole grid reduces: items (tile, row, column group) are split evenly
-// over the CTAs and each sums its S partials in split order 0..S-1 (deterministic) into the canonical gradient.
+// One reduced output item (tile t, row i, float4 column group g; g == BN/4 is the bias column) -> its
+// canonical gradient destination, or !ok when it lies outside the real output (ragged rows / columns).
+struct DwItem {
+  float* dst;
+  int nv;     // valid columns of the group (1..4)
+  bool isb;   // bias item
+  bool ok;
+};
+template <int BN>
+__device__ __forceinline__ DwItem dw_item(const GemmArgs& args, const DwOut& out, int t, int i, int g) {
+  DwItem d;
+  d.ok = false; d.dst = nullptr; d.nv = 0; d.isb = false;
+  const TileCoord c2 = decode(args, t, args.m_tiles, BN);
+  if (i >= args.M - c2.m0) return d;
+  const int cv = min(BN, out.cols - c2.n0);
+  d.isb = g == BN / 4;
+  if (d.isb ? c2.ntile != 0 : 4 * g >= cv) return d;
+  int rr = c2.m0 + i;
+  bool second = c2.z == 1;
+  if (out.row_split > 0 && rr >= out.row_split) { second = true; rr -= out.row_split; }
+  if (d.isb) {
+    d.dst = out.grad + (second ? out.b_off[1] : out.b_off[0]) + rr;
+    d.nv = 1;
+  } else {
+    d.dst = out.grad + (second ? out.w_off[1] : out.w_off[0]) + (long long)rr * out.cols + c2.n0 + 4 * g;
+    d.nv = min(4, cv - 4 * g);
+  }
+  d.ok = true;
+  return d;
+}
+__device__ __forceinline__ bool dw_emit(const DwItem& d, const float4& v) {
+  if (d.isb) {
+    d.dst[0] = v.x;
+    return isfinite(v.x);
+  }
+  d.dst[0] = v.x;
+  if (d.nv > 1) d.dst[1] = v.y;
+  if (d.nv > 2) d.dst[2] = v.z;
+  if (d.nv > 3) d.dst[3] = v.w;
+  return isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+}
+
+// The split-K tail shared by the dW kernels. S == 1: the CTA holds its whole tile, which it writes straight
+// from shared memory into the canonical gradient (no partial, no barrier). S > 1: the CTA's fp32 partial
+// (128 rows x RLD, staged in smem `red`) -> the L2 buffer [tile][split][128][RLD] with one bulk copy; a grid
+// barrier (cooperative launch: all CTAs resident; the counter only grows, the target is the next multiple of
+// the grid size, so no reset is needed between launches); then the whole grid reduces: items (tile, row,
+// column group) are split evenly over the CTAs and each sums its S partials in split order 0..S-1
+// (deterministic) into the canonical gradient. Small S keeps several items' partial loads in flight per
+// thread (the reduction is load-latency bound when the grid is small).
 template <int BN>
 __device__ __forceinline__ void dw_partial_barrier_reduce(const GemmArgs& args, const DwOut& out, const float* red,
                                                           int tile, int split, int S, int ntiles) {
   constexpr int RLD = BN + 20;
-  const int warp = threadIdx.x >> 5;
-  (void)warp;
+  constexpr int PER = BN / 4 + 1;  // float4 column groups + the bias group
+  bool bad = false;
+  if (S == 1) {
+    for (int it = threadIdx.x; it < 128 * PER; it += blockDim.x) {
+      const int i = it / PER, g = it - i * PER;
+      const DwItem d = dw_item<BN>(args, out, tile, i, g);
+      if (!d.ok) continue;
+      bad |= !dw_emit(d, *reinterpret_cast<const float4*>(red + i * RLD + 4 * g));
+    }
+    if (bad) atomicAdd(out.payload + 4, 1.0f);
+    DW_STAMP(6);
+    return;
+  }
   // partial -> L2 buffer [tile][split][128][RLD]: one bulk async copy (the TMA engine streams the whole
   // 128 x RLD fp32 tile from shared memory)
   float* part_me = out.part + ((size_t)tile * S + split) * 128 * RLD;
@@ -638,8 +694,6 @@ __device__ __forceinline__ void dw_partial_barrier_reduce(const GemmArgs& args, 
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
-  // grid barrier (all CTAs resident: cooperative launch); the counter only grows, the target is the next
-  // multiple of the grid size, so no reset is needed between launches
   __threadfence();
   __syncthreads();
   DW_STAMP(4);
@@ -651,59 +705,71 @@ __device__ __forceinline__ void dw_partial_barrier_reduce(const GemmArgs& args, 
   }
   __syncthreads();
   DW_STAMP(5);
-  
-  // grid-wide reduction: items (tile, row, column group) split evenly over the CTAs, S partials per item
-  constexpr int PER = BN / 4 + 1;  // float4 column groups + the bias group
-  float* const gw0 = out.grad + out.w_off[0];
-  float* const gw1 = out.grad + out.w_off[1];
-  float* const gb0 = out.grad + out.b_off[0];
-  float* const gb1 = out.grad + out.b_off[1];
-  const int row_split = out.row_split, ocols = out.cols;
 
   const long long n_items = (long long)ntiles * 128 * PER;
   const int n_cta = gridDim.x * gridDim.y, cid = blockIdx.y * gridDim.x + blockIdx.x;
   const long long per_cta = (n_items + n_cta - 1) / n_cta;
   const long long lo = (long long)cid * per_cta, hi = min(n_items, lo + per_cta);
-  bool bad = false;
-  for (long long it = lo + threadIdx.x; it < hi; it += blockDim.x) {
+  auto src_of = [&](long long it) {
     const int t = (int)(it / (128 * PER));
     const int rem = (int)(it - (long long)t * 128 * PER);
     const int i = rem / PER, g = rem - i * PER;
-    const TileCoord c2 = decode(args, t, args.m_tiles, BN);
-    if (i >= args.M - c2.m0) continue;
-    const int cv = min(BN, ocols - c2.n0);
-    const bool isb = g == BN / 4;
-    if (isb ? c2.ntile != 0 : 4 * g >= cv) continue;
-    const float* src = out.part + ((size_t)t * S * 128 + i) * RLD + 4 * g;
-    // all S partials of the item in flight at once (S <= 24 in one pass), then summed in split order
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < S; s0 += 24) {
-      float4 w[24];
+    return out.part + ((size_t)t * S * 128 + i) * RLD + 4 * g;
+  };
+  auto item_of = [&](long long it) {
+    const int t = (int)(it / (128 * PER));
+    const int rem = (int)(it - (long long)t * 128 * PER);
+    const int i = rem / PER, g = rem - i * PER;
+    return dw_item<BN>(args, out, t, i, g);
+  };
+  if (S <= 6) {
+    // 4 items per thread per pass, all 4*S partial loads in flight, each item summed in split order
+    constexpr int J = 4;
+    for (long long base = lo + threadIdx.x; base < hi; base += (long long)J * blockDim.x) {
+      float4 w[J][6];
+      DwItem d[J];
 #pragma unroll
-      for (int q = 0; q < 24; ++q)
-        if (s0 + q < S) w[q] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(s0 + q) * 128 * RLD));
+      for (int j = 0; j < J; ++j) {
+        const long long it = base + (long long)j * blockDim.x;
+        d[j].ok = false;
+        if (it < hi) d[j] = item_of(it);
+        if (d[j].ok) {
+          const float* src = src_of(it);
 #pragma unroll
-      for (int q = 0; q < 24; ++q)
-        if (s0 + q < S) {
-          if (s0 + q == 0) v = w[0];
-          else { v.x = v.x + w[q].x; v.y = v.y + w[q].y; v.z = v.z + w[q].z; v.w = v.w + w[q].w; }
+          for (int q = 0; q < 6; ++q)
+            if (q < S) w[j][q] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)q * 128 * RLD));
         }
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        if (!d[j].ok) continue;
+        float4 v = w[j][0];
+#pragma unroll
+        for (int q = 1; q < 6; ++q)
+          if (q < S) { v.x = v.x + w[j][q].x; v.y = v.y + w[j][q].y; v.z = v.z + w[j][q].z; v.w = v.w + w[j][q].w; }
+        bad |= !dw_emit(d[j], v);
+      }
     }
-    int rr = c2.m0 + i;
-    bool second = c2.z == 1;
-    if (row_split > 0 && rr >= row_split) { second = true; rr -= row_split; }
-    if (isb) {
-      bad |= !isfinite(v.x);
-      (second ? gb1 : gb0)[rr] = v.x;
-    } else {
-      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
-      const int c = 4 * g;
-      float* dst = (second ? gw1 : gw0) + (long long)rr * ocols + c2.n0 + c;
-      const int nv = cv - c;
-      dst[0] = v.x;
-      if (nv > 1) dst[1] = v.y;
-      if (nv > 2) dst[2] = v.z;
-      if (nv > 3) dst[3] = v.w;
+  } else {
+    for (long long it = lo + threadIdx.x; it < hi; it += blockDim.x) {
+      const DwItem d = item_of(it);
+      if (!d.ok) continue;
+      const float* src = src_of(it);
+      // all S partials of the item in flight at once (S <= 24 in one pass), then summed in split order
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s0 = 0; s0 < S; s0 += 24) {
+        float4 w[24];
+#pragma unroll
+        for (int q = 0; q < 24; ++q)
+          if (s0 + q < S) w[q] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(s0 + q) * 128 * RLD));
+#pragma unroll
+        for (int q = 0; q < 24; ++q)
+          if (s0 + q < S) {
+            if (s0 + q == 0) v = w[0];
+            else { v.x = v.x + w[q].x; v.y = v.y + w[q].y; v.z = v.z + w[q].z; v.w = v.w + w[q].w; }
+          }
+      }
+      bad |= !dw_emit(d, v);
     }
   }
   if (bad) atomicAdd(out.payload + 4, 1.0f);

@@ -245,7 +245,9 @@ struct ShadowArgs {
   int nseg;
   Segment seg[MAX_SEG];
   long long P;
+  int blk0[MAX_SEG + 1];     // k_adam: first block of each segment (ADAM_BLOCK_ELEMS elements per block)
 };
+constexpr int ADAM_BLOCK_ELEMS = 512;  // k_adam: 256 threads x 2 elements, every block inside one segment
 
 struct AdamArgs {
   ShadowArgs sh;

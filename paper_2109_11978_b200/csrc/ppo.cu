@@ -604,20 +604,27 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
   }
 }
 
-constexpr int ADAM_PER_THREAD = 2;
-__global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, float kl_target, int world, int m,
-                                              float* acc) {
+// Grid: the parameter segments (ShadowArgs, one per weight / bias tensor) each get ceil(n / 512) blocks, so a
+// block's 512 elements lie in one segment: its canonical range and its bf16 / fp32 GEMM shadow are found once.
+constexpr int ADAM_PER_THREAD = ADAM_BLOCK_ELEMS / 256;
+__global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a, const float* payload, float kl_target,
+                                              int world, int m, float* acc) {
   pdl_trigger();
   pdl_wait();
   __shared__ float s_alpha, s_bc1, s_bc2;
   __shared__ int s_apply;
+  int sg = 0;
+  while (sg + 1 < a.sh.nseg && (int)blockIdx.x >= a.sh.blk0[sg + 1]) ++sg;  // block-uniform
+  const Segment& G = a.sh.seg[sg];
+  const int n = G.rows * G.cols;
+  const int l0 = ((int)blockIdx.x - a.sh.blk0[sg]) * ADAM_BLOCK_ELEMS + threadIdx.x;
   // this thread's elements are loaded first, so their latency overlaps the Alg. 1 / bias-correction scalars
-  const long long i0 = (blockIdx.x * (long long)blockDim.x) * ADAM_PER_THREAD + threadIdx.x;
   float g[ADAM_PER_THREAD], mo[ADAM_PER_THREAD], vo[ADAM_PER_THREAD], tho[ADAM_PER_THREAD];
 #pragma unroll
   for (int u = 0; u < ADAM_PER_THREAD; ++u) {
-    const long long i = i0 + (long long)u * blockDim.x;
-    if (i < a.sh.P) { g[u] = a.grad[i]; mo[u] = a.m[i]; vo[u] = a.v[i]; tho[u] = a.theta[i]; }
+    const int l = l0 + u * 256;
+    const long long i = G.off + l;
+    if (l < n) { g[u] = a.grad[i]; mo[u] = a.m[i]; vo[u] = a.v[i]; tho[u] = a.theta[i]; }
   }
   if (threadIdx.x == 0) {
     DevScalars* sc = a.sc;
@@ -654,8 +661,9 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, 
   const float alpha = s_alpha, bc1 = s_bc1, bc2 = s_bc2;
 #pragma unroll
   for (int u = 0; u < ADAM_PER_THREAD; ++u) {
-    const long long i = i0 + (long long)u * blockDim.x;
-    if (i >= a.sh.P) break;
+    const int l = l0 + u * 256;
+    if (l >= n) break;
+    const long long i = G.off + l;
     const float gg = g[u] * a.inv_world;
     const float mm = a.b1 * mo[u] + (1.0f - a.b1) * gg;
     const float v = a.b2 * vo[u] + (1.0f - a.b2) * gg * gg;
@@ -664,13 +672,13 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a, const float* payload, 
     const float mh = mm / bc1, vh = v / bc2;
     const float th = tho[u] - alpha * mh / (sqrtf(vh) + a.eps);
     a.theta[i] = th;
-    write_shadow(a.sh, i, th);
+    const int r = l / G.cols, c = l - r * G.cols;
+    if (G.kind == 0) reinterpret_cast<__nv_bfloat16*>(G.dst)[(size_t)r * G.dst_ld + c] = __float2bfloat16_rn(th);
+    else reinterpret_cast<float*>(G.dst)[(size_t)r * G.dst_ld + c] = th;
   }
 }
 void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc, cudaStream_t st) {
-  const long long per_block = 256LL * ADAM_PER_THREAD;
-  const int nb = (int)((a.sh.P + per_block - 1) / per_block);
-  launch_pdl(k_adam, dim3(nb), dim3(256), 0, st, a, payload, kl_target, world, m, acc);
+  launch_pdl(k_adam, dim3((unsigned)a.sh.blk0[a.sh.nseg]), dim3(256), 0, st, a, payload, kl_target, world, m, acc);
 }
 
 __global__ void k_sync_shadow(ShadowArgs sh, const float* theta) {

@@ -302,8 +302,12 @@ def _grad_tensors(g, D, hidden):
     return {k: v for k, v in learn.unpack(np.asarray(g, np.float64), D, hidden).items()}
 
 
+# minibatch rows 3072 (dW split S = 6), 384 (S = 1: the tile written straight from shared memory),
+# 600 (ragged 128-row tail), 12288 (S = 18, wide and narrow dW tiles)
 @pytest.mark.parametrize("hidden,scan,N,T,K", [((512, 256, 128), (17, 11), 512, 24, 4),
-                                               ((128, 64, 32), (0, 0), 64, 24, 4)])
+                                               ((128, 64, 32), (0, 0), 64, 24, 4),
+                                               ((512, 256, 128), (17, 11), 100, 24, 4),
+                                               ((512, 256, 128), (17, 11), 1024, 24, 2)])
 def test_minibatch_gradient_vs_oracle(hidden, scan, N, T, K):
     cfg, ctx, env, theta = make(n_envs=N, T=T, hidden=hidden, scan=scan, rough=scan[0] > 0, K=K,
                                 levels=4 if scan[0] else 1, cols=5 if scan[0] else 1)
