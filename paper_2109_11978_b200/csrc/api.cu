@@ -461,6 +461,7 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   cmap(&u1.tmC[0], H1, 2 * d.H0, 2 * d.H0);
   set_fwd_common(u1, d.Mmb, 2 * d.H0, d.Dp, bn1u, 1);
   u1.ldo = 2 * d.H0; u1.bias[0] = b1;
+  u1.ws = 1;  // weight-stationary where the resident block fits (measured gains: layers 1, 3 and dX2)
   ctx->l1_upd_b1 = u1;
   ok &= make_tmap_bf16(&ctx->l1_upd_b1.tmA[0], bf(A, L.b_X), R, d.Dp, d.Dp, 128);
   // ---- forward, layers 2, 3 (z = net)
@@ -480,6 +481,7 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   }
   set_fwd_common(g2, d.Mmb, d.H1, d.H0, bn2, 2); g2.ldo = 2 * d.H1;
   set_fwd_common(g3, d.Mmb, d.H2, d.H1, bn3, 2); g3.ldo = 2 * d.H2;
+  g3.ws = 1;
   for (int z = 0; z < 2; ++z) {
     ok &= make_tmap_bf16(&ctx->tmW2f[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, bn_for(d.H1));
     ok &= make_tmap_bf16(&ctx->tmW3f[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, bn_for(d.H2));
@@ -488,6 +490,7 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   ctx->bn3r = bn_small(d.H2, d.N, 2);
   ctx->l2r = g2;
   ctx->l3r = g3;
+  ctx->l3r.ws = 0;
   for (int z = 0; z < 2; ++z) {
     ok &= make_tmap_bf16(&ctx->l2r.tmB[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, ctx->bn2r);
     ok &= make_tmap_bf16(&ctx->l3r.tmB[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, ctx->bn3r);
@@ -534,6 +537,7 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   }
   set_fwd_common(x3, d.Mmb, d.H1, d.H2, ctx->bnx3, 2); x3.ldo = 2 * d.H1; x3.ld_aux = 2 * d.H1;
   set_fwd_common(x2, d.Mmb, d.H0, d.H1, ctx->bnx2, 2); x2.ldo = 2 * d.H0; x2.ld_aux = 2 * d.H0;
+  x2.ws = 1;
   // ---- backward dW (A = dZ MN-major, B = activations MN-major), split-K over the minibatch
   auto dw_setup = [&](GemmArgs& g, const DwPlan& p, int nz) {
     g.M = p.rows; g.N = p.N; g.M_dev = nullptr;
@@ -942,6 +946,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   hr.part = la.part; hr.spart = la.spart; hr.grad = grad;
   hr.off_W4a = ctx->cn.W4[0]; hr.off_b4a = ctx->cn.b4[0]; hr.off_W4c = ctx->cn.W4[1]; hr.off_b4c = ctx->cn.b4[1];
   hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
+  // (measured: on the dW stream instead, the reduction delays dW3 -> dW1 by more than it saves here)
   { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
   CKL();
   // the weight-gradient chain runs on st2 beside the dX chain; the profiled pass (lg_profile, timing each

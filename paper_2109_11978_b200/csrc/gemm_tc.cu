@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -31,7 +32,6 @@
 namespace lg {
 
 // ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -110,6 +110,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -197,23 +198,26 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
 
-template <int BN, int EPI, bool PAIR = false>
+template <int BN, int EPI, bool PAIR = false, int WSKB = 0>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // a CTA of a pair holds half of B
-  static constexpr int ONES_BYTES = 16 * 128;  // 16 rows x 64 bf16 of 1.0
+  static constexpr int ONES_BYTES = EPI == 3 ? 16 * 128 : 0;  // 16 rows x 64 bf16 of 1.0 (bias column)
   static constexpr int EPI_BUF = 4096;         // one 32 x 128-B staging sub-tile
-  static constexpr int EPI_NBUF = EPI == 3 ? 1 : 2;
+  static constexpr int EPI_NBUF = (EPI == 3 || WSKB) ? 1 : 2;
   static constexpr int BIAS_BYTES = EPI == 0 ? EPI_WARPS * 128 * 4 : 0;
-  static constexpr int FIXED = 1024 + ONES_BYTES + EPI_WARPS * EPI_NBUF * EPI_BUF + BIAS_BYTES + 512;
-  static constexpr int STAGES_FIT = (232448 - FIXED) / (A_BYTES + B_BYTES);
+  static constexpr int BRES = WSKB * B_BYTES;  // weight-stationary: the resident column block of B
+  static constexpr int FIXED = 1024 + ONES_BYTES + EPI_WARPS * EPI_NBUF * EPI_BUF + BIAS_BYTES + 512 + BRES;
+  static constexpr int STAGE_BYTES = WSKB ? A_BYTES : A_BYTES + B_BYTES;
+  static constexpr int STAGES_FIT = (232448 - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int ACC_COLS = ((BN + (EPI == 3 ? 16 : 0)) + 31) / 32 * 32;
   static constexpr int ACC_STAGES = 2 * ACC_COLS <= 512 ? 2 : 1;
   static constexpr int TMEM_NEED = ACC_STAGES * ACC_COLS;
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
-  static constexpr int SMEM = FIXED + STAGES * (A_BYTES + B_BYTES);
+  static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
+  static_assert(STAGES >= 2, "operand ring");
 };
 
 // ELU(x) = x > 0 ? x : e^x - 1, with e^x = 2^(x log2 e) from ex2.approx.ftz (one MUFU op, no subnormal
@@ -261,22 +265,27 @@ __device__ __forceinline__ TileCoord decode(const GemmArgs& a, int t, int m_tile
 // 128 rows of A and half of B (so each SM receives 2/3 of the operand bytes of a 128 x BN tile), both CTAs'
 // loads complete on the leader's full barrier, the leader issues the MMAs and multicasts its commits, and the
 // peer's epilogue warps release the accumulator stage on the leader's tempty barrier (remote arrive).
-template <int BN, bool A_MN, bool B_MN, int EPI, bool PAIR = false>
+// WSKB > 0 (weight-stationary, EPI 0 / 2): the grid is split into column blocks ("slices": n_tiles x nz); a CTA
+// serves one slice, loads that slice's B (<= WSKB k-blocks) into shared memory once and streams only A tiles of
+// its rows -- B is not re-read from L2 for every tile, so the operand traffic per tile drops to the A tile.
+template <int BN, bool A_MN, bool B_MN, int EPI, bool PAIR = false, int WSKB = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_constant__ GemmArgs args) {
-  using C = GemmCfg<BN, EPI, PAIR>;
+  using C = GemmCfg<BN, EPI, PAIR, WSKB>;
   static_assert(!PAIR || (EPI != 3 && !A_MN && BN >= 128), "pairs: forward / input-gradient GEMMs only");
+  static_assert(!WSKB || (!PAIR && EPI != 3), "weight-stationary: single-CTA forward / input-gradient GEMMs");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
-  uint8_t* sEpi = sB + C::STAGES * C::B_BYTES;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;                       // ring B stages, or the resident slice (WSKB)
+  uint8_t* sEpi = sB + (WSKB ? C::BRES : C::STAGES * C::B_BYTES);
   uint8_t* sOnes = sEpi + EPI_WARPS * C::EPI_NBUF * C::EPI_BUF;
   float* sBias = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES + C::BIAS_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;  // WSKB: the resident B slice has landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
@@ -293,16 +302,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     if (PAIR) c.m0 = 2 * c.m0 + (int)rank * 128;
     return c;
   };
+  // weight-stationary schedule: slice = cid % nsl (fixed column block of B), row tiles mi, mi + cps, ...
+  const int nsl = args.n_tiles * args.nz;
+  const int cps = WSKB ? (int)gridDim.x / nsl : 1;
+  const int wslice = WSKB ? cid % nsl : 0;
+  // the it-th tile of this CTA (false when there is none)
+  auto tile_at = [&](int it, TileCoord& c) -> bool {
+    if (WSKB) {
+      const int m = cid / nsl + it * cps;
+      if (m >= m_tiles) return false;
+      c.z = wslice / args.n_tiles; c.ntile = wslice - c.z * args.n_tiles; c.n0 = c.ntile * BN; c.split = 0;
+      c.m0 = m * 128;
+      return true;
+    }
+    const int t = cid + it * ncl;
+    if (t >= total) return false;
+    c = tile_of(t);
+    return true;
+  };
   auto skip = [&](const TileCoord& c) { return (PAIR ? c.m0 - (int)rank * 128 : c.m0) >= M; };
   if (!PAIR) {  // CTA-uniform early exit when none of this CTA's tiles has rows (device-sized M, e.g. no time-outs)
     bool any = false;
-    for (int t = cid; t < total && !any; t += ncl) any = !skip(tile_of(t));
+    TileCoord c0;
+    for (int it = 0; !any && tile_at(it, c0); ++it) any = !skip(c0);
     if (!any) return;
   }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], (PAIR ? 2 : 1) * EPI_WARPS); }
+    mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (EPI == 3) {  // 16 x 64 bf16 ones (any swizzle of a constant tile is the same tile)
@@ -333,8 +362,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < total; t += ncl) {
-        const TileCoord tc = tile_of(t);
+      if (WSKB) {  // the slice's B column block, once (kb_total <= WSKB k-blocks, checked by the host)
+        TileCoord c0;
+        tile_at(0, c0);
+        const CUtensorMap* tmB = &args.tmB[c0.z];
+        mbar_expect_tx(bfull, args.kb_total * C::B_BYTES);
+        for (int kb = 0; kb < args.kb_total; ++kb) {
+          uint8_t* b = sB + kb * C::B_BYTES;
+          if (!B_MN) {
+            tma_load_2d(tmB, bfull, b, kb * C::BK, c0.n0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) tma_load_2d(tmB, bfull, b + i * 8192, c0.n0 + 64 * i, kb * C::BK);
+          }
+        }
+      }
+      TileCoord tc;
+      for (int it = 0; tile_at(it, tc); ++it) {
         if (skip(tc)) continue;
         const CUtensorMap* tmA = &args.tmA[tc.z];
         const CUtensorMap* tmB = &args.tmB[tc.z];
@@ -345,6 +389,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
           const int k0 = (kb0 + kb) * C::BK;
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
+          if (WSKB) {
+            mbar_expect_tx(&full[stage], C::A_BYTES);
+            if (!A_MN) {
+              tma_load_2d(tmA, &full[stage], a, k0, tc.m0);
+            } else {
+              tma_load_2d(tmA, &full[stage], a, tc.m0, k0);
+              tma_load_2d(tmA, &full[stage], a + 8192, tc.m0 + 64, k0);
+            }
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1u; }
+            continue;
+          }
           if (PAIR) {
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -388,8 +443,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = cid; t < total; t += ncl) {
-        const TileCoord tc = tile_of(t);
+      if (WSKB) {
+        mbar_wait(bfull, 0);
+        tc_fence_after();
+      }
+      TileCoord tc;
+      for (int it = 0; tile_at(it, tc); ++it) {
         if (skip(tc)) continue;
         const int acc = local % C::ACC_STAGES;
         const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
@@ -404,7 +463,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (args.probe & 1) { mbar_arrive(&empty[stage]); if (++stage == C::STAGES) { stage = 0; phase ^= 1u; } continue; }
-          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES), b0 = smem_u32(sB + stage * C::B_BYTES);
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + (WSKB ? kb0 + kb : stage) * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k) {
             const uint64_t ad = sdesc(a0 + k * a_step, a_lbo, 1024u);
@@ -436,8 +496,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     constexpr int WCOLS = BN >= 128 ? BN / 2 : BN;  // columns handled by this warp
     const bool active = BN >= 128 || h == 0;
     int local = 0, nst = 0;
-    for (int t = cid; t < total; t += ncl) {
-      const TileCoord tc = tile_of(t);
+    TileCoord tc;
+    for (int it = 0; tile_at(it, tc); ++it) {
       if (skip(tc)) continue;
       const int acc = local % C::ACC_STAGES;
       const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
@@ -554,8 +614,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
                 }
               }
             }
-            uint8_t* buf = mybuf + (nst & 1) * C::EPI_BUF;
-            if (lane == 0) bulk_wait_read1();
+            uint8_t* buf = mybuf + (C::EPI_NBUF == 2 ? (nst & 1) * C::EPI_BUF : 0);
+            if (lane == 0) {
+              if (C::EPI_NBUF == 2) bulk_wait_read1();
+              else bulk_wait_read0();
+            }
             __syncwarp();
             stage_row(buf, lane, pk);
             fence_async_smem();
@@ -1538,13 +1601,13 @@ bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, rows, cols, ld, 32, box_rows);
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI, bool PAIR = false>
+template <int BN, bool A_MN, bool B_MN, int EPI, bool PAIR = false, int WSKB = 0>
 static cudaError_t launch_one(const GemmArgs& a, cudaStream_t st) {
-  using C = GemmCfg<BN, EPI, PAIR>;
+  using C = GemmCfg<BN, EPI, PAIR, WSKB>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, A_MN, B_MN, EPI, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, A_MN, B_MN, EPI, PAIR, WSKB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -1573,14 +1636,39 @@ static cudaError_t launch_one(const GemmArgs& a, cudaStream_t st) {
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, A_MN, B_MN, EPI, PAIR>, a);
   }
+  if (WSKB) {  // cps CTAs per column block (slice), every CTA of a slice takes every cps-th row tile
+    const int nsl = a.n_tiles * a.nz;
+    const int cps = std::min(a.m_tiles, g_num_sms / nsl);
+    return launch_pdl(k_gemm_tc<BN, A_MN, B_MN, EPI, false, WSKB>, dim3(cps * nsl), dim3(GEMM_THREADS), C::SMEM, st, a);
+  }
   const int total = a.nz * a.m_tiles * a.n_tiles * a.n_splits;
   const int grid = total < g_num_sms ? total : g_num_sms;
   return launch_pdl(k_gemm_tc<BN, A_MN, B_MN, EPI>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, st, a);
 }
 
+// weight-stationary eligibility: one split, the slice count fits the grid, the resident block fits WSKB
+static bool ws_ok(const GemmArgs& a) {
+  static const bool off = [] { const char* e = getenv("LG_NO_WS"); return e && e[0] == '1'; }();
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return !off && a.ws && !a.pair && !a.M_dev && a.n_splits == 1 && a.kb_per_split == a.kb_total &&
+         a.n_tiles * a.nz <= g_num_sms / 2;
+}
+
 template <bool A_MN, bool B_MN, int EPI>
 static cudaError_t dispatch_bn(int bn, const GemmArgs& a, cudaStream_t st) {
   if constexpr (EPI != 3 && !A_MN) {
+    if (ws_ok(a)) {  // resident B: <= 128 KB (BN 256: 4 k-blocks, BN 128: 8); smaller blocks leave a deeper A ring
+      const int kb = a.kb_total;
+      if (bn == 256 && kb <= 2) return launch_one<256, A_MN, B_MN, EPI, false, 2>(a, st);
+      if (bn == 256 && kb <= 4) return launch_one<256, A_MN, B_MN, EPI, false, 4>(a, st);
+      if (bn == 128 && kb <= 4) return launch_one<128, A_MN, B_MN, EPI, false, 4>(a, st);
+      if (bn == 128 && kb <= 8) return launch_one<128, A_MN, B_MN, EPI, false, 8>(a, st);
+    }
     if (a.pair) {
       switch (bn) {
         case 128: return launch_one<128, A_MN, B_MN, EPI, true>(a, st);

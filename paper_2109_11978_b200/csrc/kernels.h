@@ -84,6 +84,8 @@ struct GemmArgs {
                              // bit2 = skip the epilogue
   int pair;                  // forward / input-gradient GEMMs: CTA pairs (cta_group::2, 256-row tiles)
   CUtensorMap tmBp[2];       // pair + K-major B: B with a box of BN/2 rows (each CTA loads half of the tile's B)
+  int ws;                    // forward / input-gradient GEMMs: weight-stationary schedule (each CTA keeps one column
+                             // block of B resident in shared memory and streams only A), when the block fits
 };
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);

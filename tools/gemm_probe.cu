@@ -450,6 +450,51 @@ static void probe_pair_gemm(int kind, int M, int N, int K, int bn, cudaStream_t 
   CK(cudaFree(A)); CK(cudaFree(W)); CK(cudaFree(H)); CK(cudaFree(Y1)); CK(cudaFree(Y2)); CK(cudaFree(bias));
 }
 
+// forward (kind 0) / input-gradient (kind 1) GEMM: weight-stationary vs the tile-order schedule (timing and
+// element-wise equality; nz = 2 column groups like the per-net layers)
+static void probe_ws_gemm(int kind, int M, int N, int K, int bn, int nz, cudaStream_t st) {
+  __nv_bfloat16 *A, *W, *H, *Y1, *Y2;
+  float* bias;
+  CK(cudaMalloc(&A, (size_t)M * K * 2 * nz)); CK(cudaMalloc(&W, (size_t)K * N * 2 * nz));
+  CK(cudaMalloc(&H, (size_t)M * N * 2 * nz));
+  CK(cudaMalloc(&Y1, (size_t)M * N * 2 * nz)); CK(cudaMalloc(&Y2, (size_t)M * N * 2 * nz)); CK(cudaMalloc(&bias, N * 4 * nz));
+  fill(A, (size_t)M * K * nz); fill(W, (size_t)K * N * nz); fill(H, (size_t)M * N * nz);
+  CK(cudaMemset(bias, 0, N * 4 * nz));
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  for (int z = 0; z < nz; ++z) {
+    make_tmap_bf16(&g.tmA[z], A + (size_t)z * K, M, K, (size_t)K * nz, 128);
+    if (kind == 0) {
+      make_tmap_bf16(&g.tmB[z], W + (size_t)z * N * K, N, K, K, bn);
+      g.bias[z] = bias + z * N;
+    } else {
+      make_tmap_bf16(&g.tmB[z], W + (size_t)z * K * N, K, N, N, 64);
+      g.aux[z] = H + (size_t)z * N; g.ld_aux = N * nz;
+    }
+  }
+  g.M = M; g.N = N; g.m_tiles = (M + 127) / 128; g.nz = nz;
+  g.kb_total = (K + 63) / 64; g.kb_per_split = g.kb_total; g.n_tiles = (N + bn - 1) / bn; g.n_splits = 1; g.ldo = N * nz;
+  GemmArgs g1 = g, g2 = g;
+  for (int z = 0; z < nz; ++z) {
+    make_tmap_bf16(&g1.tmC[z], Y1 + (size_t)z * N, M, N, (size_t)N * nz, 32);
+    make_tmap_bf16(&g2.tmC[z], Y2 + (size_t)z * N, M, N, (size_t)N * nz, 32);
+  }
+  g2.ws = 1;
+  const GemmKind gk = kind == 0 ? GEMM_FWD : GEMM_DX;
+  const double fl = 2.0 * M * N * K * nz;
+  float u1 = time_us([&] { CK(launch_gemm(gk, bn, g1, st)); }, st);
+  float u2 = time_us([&] { CK(launch_gemm(gk, bn, g2, st)); }, st);
+  CK(cudaStreamSynchronize(st));
+  std::vector<uint16_t> y1((size_t)M * N * nz), y2((size_t)M * N * nz);
+  CK(cudaMemcpy(y1.data(), Y1, y1.size() * 2, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(y2.data(), Y2, y2.size() * 2, cudaMemcpyDeviceToHost));
+  size_t diff = 0;
+  for (size_t i = 0; i < y1.size(); ++i) diff += y1[i] != y2[i];
+  printf("%s M=%d N=%d K=%d nz=%d bn=%d  tile-order %8.2f us (%6.1f TF)  weight-stationary %8.2f us (%6.1f TF)  differing %zu of %zu\n",
+         kind == 0 ? "fwd" : "dx ", M, N, K, nz, bn, u1, fl / u1 * 1e-6, u2, fl / u2 * 1e-6, diff, y1.size());
+  CK(cudaFree(A)); CK(cudaFree(W)); CK(cudaFree(H)); CK(cudaFree(Y1)); CK(cudaFree(Y2)); CK(cudaFree(bias));
+}
+
 static void check_dw(int Nout, int Nin, int K, int bn, int S, int G, cudaStream_t st) {
   std::vector<float> a = probe_dw(Nout, Nin, K, bn, 1, 1, st, true);  // unsplit K
   std::vector<float> b = probe_dw(Nout, Nin, K, bn, S, G, st, true);
@@ -537,6 +582,18 @@ int main(int argc, char** argv) {
     probe_pair_gemm(0, 900, 256, 256, 256, st);     // 8 tiles, ragged
     probe_pair_gemm(0, 700, 256, 256, 128, st);     // 6 tiles
     probe_pair_gemm(0, 300, 256, 256, 256, st);     // 3 tiles (odd)
+    return 0;
+  }
+  if (!strcmp(which, "ws")) {
+    probe_ws_gemm(0, 24576, 1024, 256, 256, 1, st);  // L1 (both nets), K = Dp padded
+    probe_ws_gemm(0, 24576, 256, 512, 256, 2, st);   // L2 per net: tile order only (B 256 KB)
+    probe_ws_gemm(0, 24576, 256, 512, 128, 2, st);   // L2 per net, 128-column blocks
+    probe_ws_gemm(0, 24576, 128, 256, 128, 2, st);   // L3 per net
+    probe_ws_gemm(1, 24576, 512, 256, 256, 2, st);   // dX2 per net
+    probe_ws_gemm(1, 24576, 256, 128, 256, 2, st);   // dX3 per net
+    probe_ws_gemm(1, 24576, 256, 128, 128, 2, st);
+    probe_ws_gemm(0, 1000, 1024, 256, 256, 1, st);   // ragged rows
+    probe_ws_gemm(1, 700, 512, 256, 256, 2, st);
     return 0;
   }
   if (!strcmp(which, "fused")) {
