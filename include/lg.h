@@ -134,6 +134,14 @@ const char* lg_last_error(const lg_ctx* ctx);
 lg_status lg_params_set(lg_ctx* ctx, const float* theta);
 /* Refresh the GEMM-layout shadow from LG_BUF_THETA (after the caller wrote θ directly). */
 lg_status lg_params_sync(lg_ctx* ctx);
+/* Checkpoint / resume. Every piece of training state lives in the caller-owned
+ * buffers (θ, Adam moments, α and the Adam step on device, the environment state, OBS slot 0 = o_0 of the
+ * next iteration, the step counter s_base), so a checkpoint is a byte copy of all LG_NUM_BUFFERS buffers
+ * taken between iterations (stream idle). After the caller restores such a copy into the buffers of a
+ * context created with the same configuration, lg_resume marks the environment as initialised (instead
+ * of env_reset, which would redraw o_0) and refreshes the GEMM shadow from θ; the continued run is
+ * bit-identical to the uninterrupted one. No validation of the buffer contents is possible. */
+lg_status lg_resume(lg_ctx* ctx);
 
 /* --- Environment (SPEC env module S:237-323; PAPER §3) --- */
 /* Reset envs (mask u8 [N], NULL = all; `init` != 0 also assigns column g mod n_cols and level 0,

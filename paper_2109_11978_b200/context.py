@@ -203,6 +203,27 @@ class Context:
     def sync(self):
         self.stream.synchronize()
 
+    # ---- checkpoint / resume (lg_resume): all training state is in the caller-owned buffers --------------
+    def checkpoint(self):
+        """Host copy of every buffer (take it between iterations). Returns {"config": ..., "buffers": [...]}."""
+        self.sync()
+        return {"config": {f.name: getattr(self.cfg, f.name) for f in fields(self.cfg)},
+                "buffers": [b.cpu() for b in self.bufs]}
+
+    def restore(self, ckpt):
+        """Load a checkpoint of a context with the same configuration and continue from it."""
+        cur = {f.name: getattr(self.cfg, f.name) for f in fields(self.cfg)}
+        if {k: (tuple(v) if isinstance(v, (list, tuple)) else v) for k, v in ckpt["config"].items()} != \
+                {k: (tuple(v) if isinstance(v, (list, tuple)) else v) for k, v in cur.items()}:
+            raise ValueError("checkpoint was taken with a different configuration")
+        self.sync()
+        for b, h in zip(self.bufs, ckpt["buffers"]):
+            if b.numel() != h.numel():
+                raise ValueError("checkpoint buffer sizes differ")
+            b.copy_(h.to(self.device))
+        torch.cuda.synchronize(self.device)
+        self._ck(lg.lg_resume(self.ctx), "lg_resume")
+
     def close(self):
         if getattr(self, "ctx", None):
             lg.lg_destroy(self.ctx)

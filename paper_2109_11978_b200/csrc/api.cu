@@ -678,6 +678,14 @@ lg_status lg_params_sync(lg_ctx* ctx) {
   return LG_OK;
 }
 
+lg_status lg_resume(lg_ctx* ctx) {
+  GUARD();
+  launch_sync_shadow(ctx->shadow, reinterpret_cast<const float*>(ctx->buf[LG_BUF_THETA]), ctx->st);
+  CKL();
+  ctx->reset_done = true;
+  return LG_OK;
+}
+
 // ------------------------------------------------------------------ MLP helpers
 static int g_gemm_cat = LG_PROF_GEMM_FWD;  // category of the next GEMM launches (profiling only)
 

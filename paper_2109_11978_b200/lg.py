@@ -47,7 +47,7 @@ class lg_update_stats(ctypes.Structure):
 
 
 EXPORTS = ["lg_num_params", "lg_obs_dim", "lg_obs_stride", "lg_required_sizes", "lg_create", "lg_destroy",
-           "lg_last_error", "lg_params_set", "lg_params_sync", "env_reset", "env_step_obs_reward", "policy_act",
+           "lg_last_error", "lg_params_set", "lg_params_sync", "lg_resume", "env_reset", "env_step_obs_reward", "policy_act",
            "policy_forward", "storage_compute_gae", "ppo_update", "ppo_shuffle", "ppo_minibatch_grad", "curriculum_update",
            "lg_nccl_unique_id", "lg_set_nccl", "lg_broadcast_params", "lg_iterate_host",
            "lg_graph_capture_iteration", "lg_graph_launch", "lg_device_scalars", "lg_profile", "lg_profile_read", "lg_graph_kernel_count"]
@@ -70,6 +70,7 @@ _sig = {
     "lg_last_error": (ctypes.c_char_p, [P]),
     "lg_params_set": (I32, [P, P]),
     "lg_params_sync": (I32, [P]),
+    "lg_resume": (I32, [P]),
     "env_reset": (I32, [P, P, I32, P]),
     "env_step_obs_reward": (I32, [P, I32, P, P, P, P, P, P]),
     "policy_act": (I32, [P, I32, P, P, P, P]),
@@ -155,6 +156,10 @@ def lg_params_set(ctx, theta):
 
 def lg_params_sync(ctx):
     return _lib.lg_params_sync(ctx)
+
+
+def lg_resume(ctx):
+    return _lib.lg_resume(ctx)
 
 
 def env_reset(ctx, mask=None, init=1, obs=None):

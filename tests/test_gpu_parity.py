@@ -401,3 +401,57 @@ def test_iterate_host_stats_finite():
         assert np.isfinite(d[k])
     assert np.float32(1e-5) <= d["lr"] <= np.float32(1e-2)
     assert sum(d["level_hist"]) == cfg.n_envs
+
+
+# ------------------------------------------------------------------ checkpoint / resume, ablation arms
+def test_checkpoint_resume_bit_exact():
+    """lg_resume: a run restored from a checkpoint continues bit-identically."""
+    cfg, ctx, env, theta = make(n_envs=256, T=8, seed=9)
+    ctx.reset()
+    ctx.capture()
+    for _ in range(2):
+        ctx.replay()
+    ck = ctx.checkpoint()
+    for _ in range(3):
+        ctx.replay()
+    ctx.sync()
+    names = ("THETA", "ADAM_M", "ADAM_V", "STATE", "OBS", "ADV", "RET")
+    ref = {k: ctx.bufs[lg.BUF[k]].cpu() for k in names}
+    sc_ref = ctx.scalars()
+    hf = synth.make_world(4, 5, seed=3, rough=True)
+    ctx2 = Context(cfg, hf)
+    ctx2.restore(ck)
+    ctx2.capture()
+    for _ in range(3):
+        ctx2.replay()
+    ctx2.sync()
+    for k in names:
+        assert torch.equal(ctx2.bufs[lg.BUF[k]].cpu(), ref[k]), k
+    assert ctx2.scalars() == sc_ref
+    bad = dict(ck, config=dict(ck["config"], n_steps=9))
+    with pytest.raises(ValueError):
+        ctx2.restore(bad)
+
+
+def test_bootstrap_arms_identical_until_a_timeout():
+    """NEXT-1 pin (time-out bootstrapping): the bootstrap-on and -off arms of a paired run are
+    bit-identical while no episode times out, and differ in θ once time-outs occur (episode step 1000)."""
+    res = {}
+    for arm, fl in (("on", ALL), ("off", ALL & ~lg.F_BOOTSTRAP)):
+        cfg, ctx, env, theta = make(n_envs=256, T=8, seed=5, flags=fl)
+        ctx.reset()
+        ctx.capture()
+        for _ in range(2):
+            ctx.replay()
+        ctx.sync()
+        before = ctx.theta.cpu().numpy().copy()
+        st = gpu_state(ctx)
+        st["ep_step"][:96] = 995  # these episodes reach 1000 steps (time-out) at step 4 of the next iteration
+        set_gpu_state(ctx, st)
+        ctx.replay()
+        ctx.sync()
+        res[arm] = (before, ctx.theta.cpu().numpy().copy(), ctx.scalars(), gpu_state(ctx).tobytes())
+    assert np.array_equal(res["on"][0], res["off"][0])
+    assert res["on"][2]["n_to_total"] > 0 and res["off"][2]["n_to_total"] == 0
+    assert res["on"][3] == res["off"][3]                 # the environment does not depend on the flag
+    assert not np.array_equal(res["on"][1], res["off"][1])
