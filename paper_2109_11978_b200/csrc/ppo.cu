@@ -193,12 +193,34 @@ __global__ void __launch_bounds__(LOSS_WARPS * 32, 1) k_loss_heads(LossArgs a) {
   gWc[0] = gWc[1] = gWc[2] = gWc[3] = 0.0f;
   float gb = 0.0f, gls = 0.0f, gbv = 0.0f;           // lanes 2j: db4a_j, dlogstd_j; lane 0: db4c
   double st0 = 0.0, st1 = 0.0, st2 = 0.0, st3 = 0.0, st4 = 0.0;
+  // the next row's inputs are loaded while this row is computed (software pipelining: the row loop is
+  // otherwise bound by the latency of its own loads)
+  uint2 nua = make_uint2(0u, 0u), nuc = make_uint2(0u, 0u);
+  float nact = 0.0f, nmuo = 0.0f, nlpo = 0.0f, nadv = 0.0f, nVo = 0.0f, nret = 0.0f;
+  auto fetch = [&](int r) {
+    if (r >= a.M) return;
+    const __nv_bfloat16* hrow = a.H3 + (size_t)r * 2 * H2;
+    if (4 * lane < H2) {
+      nua = __ldg(reinterpret_cast<const uint2*>(hrow + 4 * lane));
+      nuc = __ldg(reinterpret_cast<const uint2*>(hrow + H2 + 4 * lane));
+    }
+    nact = dl ? __ldg(a.act + (size_t)r * 12 + j) : 0.0f;
+    nmuo = dl ? __ldg(a.mu_old + (size_t)r * 12 + j) : 0.0f;
+    nlpo = __ldg(a.logp_old + r); nadv = __ldg(a.adv + r); nVo = __ldg(a.V_old + r); nret = __ldg(a.ret + r);
+  };
+  fetch(gw);
   for (int r = gw; r < a.M; r += TW) {
+    const uint2 ua = nua, uc = nuc;
+    const float act = nact, muo = nmuo, lpo = nlpo, adv = nadv, Vo = nVo, ret = nret;
+    fetch(r + TW);
     float ha[4], hc[4];
-    load_h3(a.H3 + (size_t)r * 2 * H2, H2, lane, ha, hc);
-    const float act = dl ? __ldg(a.act + (size_t)r * 12 + j) : 0.0f;
-    const float muo = dl ? __ldg(a.mu_old + (size_t)r * 12 + j) : 0.0f;
-    const float lpo = __ldg(a.logp_old + r), adv = __ldg(a.adv + r), Vo = __ldg(a.V_old + r), ret = __ldg(a.ret + r);
+    {
+      float2 t2;
+      t2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ua.x)); ha[0] = t2.x; ha[1] = t2.y;
+      t2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ua.y)); ha[2] = t2.x; ha[3] = t2.y;
+      t2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uc.x)); hc[0] = t2.x; hc[1] = t2.y;
+      t2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uc.y)); hc[2] = t2.x; hc[3] = t2.y;
+    }
     const float tot = head_fwd_warp(w, ha, hc, lane) + bias;
     const float V = __shfl_sync(0xffffffffu, tot, 24);
     const float lp = logp_warp(act, tot, ls, lane);
