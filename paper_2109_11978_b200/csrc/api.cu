@@ -907,9 +907,7 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
   launch_sum_partials(vp, ctx->L.nblk_var, tot + 1, ctx->st);
   CKL();
   if ((s = allreduce_d(ctx, tot + 1, 1)) != LG_OK) return s;
-  launch_adv_finalize(tot, tot + 1, count, ctx->sc, ctx->st);
-  CKL();
-  launch_advance_sbase(ctx->sc, d.T, ctx->st);
+  launch_adv_finalize(tot, tot + 1, count, ctx->sc, d.T, ctx->st);  // (also advances s_base by T)
   CKL();
   if (adv) CK(cudaMemcpyAsync(adv, g.A, (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));
   if (ret) CK(cudaMemcpyAsync(ret, g.R, (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));

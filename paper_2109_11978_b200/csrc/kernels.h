@@ -215,7 +215,9 @@ int gae_blocks(int N);
 void launch_sum_partials(const double* part, int n, double* out, cudaStream_t st);
 void launch_var_partials(const float* A, int n, const double* mean_total, double count, double* part, cudaStream_t st);
 int var_blocks(int n);
-void launch_adv_finalize(const double* sum_total, const double* sq_total, double count, DevScalars* sc, cudaStream_t st);
+// also advances the step counter s_base by T (the rollout's events are consumed)
+void launch_adv_finalize(const double* sum_total, const double* sq_total, double count, DevScalars* sc, int T,
+                         cudaStream_t st);
 
 struct PermArgs {
   uint32_t B; int E; int epoch; int rank; uint32_t seed_lo, seed_hi; const DevScalars* sc; uint32_t* perm;
@@ -268,6 +270,5 @@ struct IterEndArgs {
 void launch_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, float b1, float b2,
                        cudaStream_t st);
 void launch_iter_end(const IterEndArgs& a, const float* iter_acc, cudaStream_t st);
-void launch_advance_sbase(DevScalars* sc, int T, cudaStream_t st);
 
 }  // namespace lg

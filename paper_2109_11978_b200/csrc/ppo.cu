@@ -447,18 +447,36 @@ __global__ void __launch_bounds__(GAE_BLOCK) k_gae(GaeArgs a) {
   double local = 0.0;
   if (i < a.N) {
     float nextA = 0.0f, nextV = a.VT[i];
-    for (int t = a.T - 1; t >= 0; --t) {
-      const size_t k = (size_t)t * a.N + i;
-      const float nd = (a.flags[k] & 3u) ? 0.0f : 1.0f;
-      const float rt = a.bootstrap ? a.r[k] + a.gamma * a.b[k] : a.r[k];
-      const float v = a.V[k];
-      const float delta = rt + a.gamma * nd * nextV - v;
-      const float A = delta + a.gamma * a.lam * nd * nextA;
-      a.A[k] = A;
-      a.R[k] = A + v;
-      local += (double)A;
-      nextA = A;
-      nextV = v;
+    // the recurrence runs backwards in t; the inputs of GAE_PF steps are loaded before it consumes them
+    constexpr int GAE_PF = 8;
+    for (int t1 = a.T - 1; t1 >= 0; t1 -= GAE_PF) {
+      float rr[GAE_PF], bb[GAE_PF], vv[GAE_PF];
+      uint8_t ff[GAE_PF];
+#pragma unroll
+      for (int u = 0; u < GAE_PF; ++u) {
+        const int t = t1 - u;
+        if (t >= 0) {
+          const size_t k = (size_t)t * a.N + i;
+          rr[u] = __ldg(a.r + k); bb[u] = a.bootstrap ? __ldg(a.b + k) : 0.0f; vv[u] = __ldg(a.V + k);
+          ff[u] = __ldg(a.flags + k);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GAE_PF; ++u) {
+        const int t = t1 - u;
+        if (t < 0) break;
+        const size_t k = (size_t)t * a.N + i;
+        const float nd = (ff[u] & 3u) ? 0.0f : 1.0f;
+        const float rt = a.bootstrap ? rr[u] + a.gamma * bb[u] : rr[u];
+        const float v = vv[u];
+        const float delta = rt + a.gamma * nd * nextV - v;
+        const float A = delta + a.gamma * a.lam * nd * nextA;
+        a.A[k] = A;
+        a.R[k] = A + v;
+        local += (double)A;
+        nextA = A;
+        nextV = v;
+      }
     }
   }
   double s = block_sum_d(local, sred);
@@ -496,14 +514,16 @@ void launch_var_partials(const float* A, int n, const double* mean_total, double
   k_var_partials<<<var_blocks(n), VAR_BLOCK, 0, st>>>(A, n, mean_total, count, part);
 }
 
-__global__ void k_adv_finalize(const double* sum_total, const double* sq_total, double count, DevScalars* sc) {
+__global__ void k_adv_finalize(const double* sum_total, const double* sq_total, double count, DevScalars* sc, int T) {
   const double mean = *sum_total / count;
   const double var = count > 1.0 ? *sq_total / (count - 1.0) : 0.0;
   sc->adv_mean = mean;
   sc->adv_inv_std = 1.0 / (sqrt(var) + 1e-8);
+  sc->s_base += (uint32_t)T;  // the rollout's T steps are consumed: the next rollout's events follow them
 }
-void launch_adv_finalize(const double* sum_total, const double* sq_total, double count, DevScalars* sc, cudaStream_t st) {
-  k_adv_finalize<<<1, 1, 0, st>>>(sum_total, sq_total, count, sc);
+void launch_adv_finalize(const double* sum_total, const double* sq_total, double count, DevScalars* sc, int T,
+                         cudaStream_t st) {
+  k_adv_finalize<<<1, 1, 0, st>>>(sum_total, sq_total, count, sc, T);
 }
 
 // ------------------------------------------------------------------ Feistel shuffle
@@ -514,13 +534,18 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
 
 // grid.y = epochs computed by this launch (a.epoch + blockIdx.y), each writing perm + blockIdx.y * B
 __global__ void k_perm(PermArgs a) {
+  __shared__ uint32_t sKey[4];
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.B) return;
-  Rng rng{a.seed_lo, a.seed_hi};
   const int epoch = a.epoch + (int)blockIdx.y;
-  const uint32_t ev = a.sc->iteration * (uint32_t)a.E + (uint32_t)epoch;
-  U4 K = rng.block(0, (uint32_t)a.rank, ev, TAG_SHUFFLE);
-  const uint32_t Ks[4] = {K.x, K.y, K.z, K.w};
+  if (threadIdx.x == 0) {  // the epoch's round keys: one Philox block per thread block
+    Rng rng{a.seed_lo, a.seed_hi};
+    const uint32_t ev = a.sc->iteration * (uint32_t)a.E + (uint32_t)epoch;
+    const U4 K = rng.block(0, (uint32_t)a.rank, ev, TAG_SHUFFLE);
+    sKey[0] = K.x; sKey[1] = K.y; sKey[2] = K.z; sKey[3] = K.w;
+  }
+  __syncthreads();
+  if (j >= a.B) return;
+  const uint32_t Ks[4] = {sKey[0], sKey[1], sKey[2], sKey[3]};
   uint32_t k = 0;
   while ((1u << k) < a.B) ++k;
   if (k & 1u) ++k;
@@ -734,9 +759,14 @@ __global__ void k_iter_end(IterEndArgs a, const float* acc) {
   __shared__ int hist[16];
   if (threadIdx.x < 16) hist[threadIdx.x] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < a.N; i += blockDim.x) {
-    int lv = (int)a.state[(size_t)S_LEVEL * a.N + i];
-    atomicAdd(&hist[min(max(lv, 0), 15)], 1);
+  for (int i0 = 0; i0 < a.N; i0 += blockDim.x) {  // per warp: one ballot per level bin
+    const int i = i0 + (int)threadIdx.x;
+    const int lv = i < a.N ? min(max((int)a.state[(size_t)S_LEVEL * a.N + i], 0), 15) : -1;
+#pragma unroll
+    for (int bnum = 0; bnum < 16; ++bnum) {
+      const int c = __popc(__ballot_sync(0xffffffffu, lv == bnum));
+      if ((threadIdx.x & 31) == 0 && c) atomicAdd(&hist[bnum], c);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -773,7 +803,5 @@ void launch_iter_end(const IterEndArgs& a, const float* iter_acc, cudaStream_t s
   k_iter_end<<<1, 256, 0, st>>>(a, iter_acc);
 }
 
-__global__ void k_advance_sbase(DevScalars* sc, int T) { sc->s_base += (uint32_t)T; }
-void launch_advance_sbase(DevScalars* sc, int T, cudaStream_t st) { k_advance_sbase<<<1, 1, 0, st>>>(sc, T); }
 
 }  // namespace lg
