@@ -1105,16 +1105,16 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
   }();
   for (int k = 0; k < n_mb; ++k) {  // minibatch k = epoch k / K, slice k % K of that epoch's permutation
     const uint32_t* next = k + 1 < n_mb ? perm + (size_t)(k + 1) * d.Mmb : nullptr;
-    if (!prefetch && k > 0) {  // gather on the critical path (measured faster than beside dW1)
-      GatherArgs g = gather_args(ctx, k & 1);
-      g.perm = perm + (size_t)k * d.Mmb;
-      { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
-      CKL();
-    }
     if ((s = minibatch_gradient(ctx, k & 1, prefetch ? next : nullptr)) != LG_OK) return s;
     { Scope sc_(ctx, LG_PROF_COMM); if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s; }
     Scope sc_adam(ctx, LG_PROF_ADAM);
-    launch_adam(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, ctx->st);
+    if (next && !prefetch) {  // Adam of minibatch k and the gather of minibatch k + 1 (other set) in one launch
+      GatherArgs g = gather_args(ctx, (k + 1) & 1);
+      g.perm = next;
+      launch_adam_gather(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, g, ctx->st);
+    } else {
+      launch_adam(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, ctx->st);
+    }
     CKL();
   }
   IterEndArgs ie;

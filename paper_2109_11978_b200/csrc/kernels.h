@@ -261,6 +261,9 @@ struct AdamArgs {
 };
 void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc,
                  cudaStream_t st);
+// Adam of minibatch m together with the gather of the next minibatch (one launch, disjoint block ranges)
+void launch_adam_gather(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc,
+                        const GatherArgs& g, cudaStream_t st);
 void launch_sync_shadow(const ShadowArgs& sh, const float* theta, cudaStream_t st);
 
 struct IterEndArgs {

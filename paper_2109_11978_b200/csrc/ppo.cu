@@ -568,10 +568,8 @@ void launch_perm(const PermArgs& a, cudaStream_t st) { k_perm<<<dim3((a.B + 255)
 
 // ------------------------------------------------------------------ minibatch gather (warp per row)
 constexpr int GATHER_ROWS = 4;  // rows per warp: the permutation loads and the row copies are all in flight together
-__global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
-  pdl_trigger();
-  pdl_wait();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void gather_body(const GatherArgs& a, int bid) {
+  const int warp = (bid * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int r0 = warp * GATHER_ROWS;
   if (r0 >= a.M) return;
   const int nr = min(GATHER_ROWS, a.M - r0);
@@ -628,9 +626,17 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     else a.o_ret[w] = sv[pss][0];
   }
 }
+__global__ void __launch_bounds__(256) k_gather(const __grid_constant__ GatherArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  gather_body(a, blockIdx.x);
+}
+static int gather_blocks(int M) {
+  const long long warps = (M + GATHER_ROWS - 1) / GATHER_ROWS;
+  return (int)((warps * 32 + 255) / 256);
+}
 void launch_gather(const GatherArgs& a, cudaStream_t st) {
-  const long long warps = (a.M + GATHER_ROWS - 1) / GATHER_ROWS;
-  launch_pdl(k_gather, dim3((unsigned)((warps * 32 + 255) / 256)), dim3(256), 0, st, a);
+  launch_pdl(k_gather, dim3((unsigned)gather_blocks(a.M)), dim3(256), 0, st, a);
 }
 
 // ------------------------------------------------------------------ Alg. 1 + Adam
@@ -654,17 +660,15 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
 // Grid: the parameter segments (ShadowArgs, one per weight / bias tensor) each get ceil(n / 512) blocks, so a
 // block's 512 elements lie in one segment: its canonical range and its bf16 / fp32 GEMM shadow are found once.
 constexpr int ADAM_PER_THREAD = ADAM_BLOCK_ELEMS / 256;
-__global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a, const float* payload, float kl_target,
-                                              int world, int m, float* acc) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payload, float kl_target, int world, int m,
+                                          float* acc, int bid) {
   __shared__ float s_alpha, s_bc1, s_bc2;
   __shared__ int s_apply;
   int sg = 0;
-  while (sg + 1 < a.sh.nseg && (int)blockIdx.x >= a.sh.blk0[sg + 1]) ++sg;  // block-uniform
+  while (sg + 1 < a.sh.nseg && bid >= a.sh.blk0[sg + 1]) ++sg;  // block-uniform
   const Segment& G = a.sh.seg[sg];
   const int n = G.rows * G.cols;
-  const int l0 = ((int)blockIdx.x - a.sh.blk0[sg]) * ADAM_BLOCK_ELEMS + threadIdx.x;
+  const int l0 = (bid - a.sh.blk0[sg]) * ADAM_BLOCK_ELEMS + threadIdx.x;
   // this thread's elements are loaded first, so their latency overlaps the Alg. 1 / bias-correction scalars
   float g[ADAM_PER_THREAD], mo[ADAM_PER_THREAD], vo[ADAM_PER_THREAD], tho[ADAM_PER_THREAD];
 #pragma unroll
@@ -689,7 +693,7 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
     s_alpha = alpha;
     s_bc1 = sc->bc_ring[m & 1][0];  // 1 - b^t for the applied step t (written by the previous Adam / iter_begin)
     s_bc2 = sc->bc_ring[m & 1][1];
-    if (blockIdx.x == 0) {
+    if (bid == 0) {
       sc->alpha_ring[(m + 1) & 1] = alpha;
       sc->adamt_ring[(m + 1) & 1] = t;
       sc->bc_ring[(m + 1) & 1][0] = (float)(1.0 - pow((double)a.b1, (double)(t + 1)));
@@ -724,8 +728,31 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
     else reinterpret_cast<float*>(G.dst)[(size_t)r * G.dst_ld + c] = th;
   }
 }
+__global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a, const float* payload, float kl_target,
+                                              int world, int m, float* acc) {
+  pdl_trigger();
+  pdl_wait();
+  adam_body(a, payload, kl_target, world, m, acc, blockIdx.x);
+}
+// Adam of minibatch m and the gather of minibatch m + 1 in one launch (blocks [0, nadam) update θ, the rest
+// gather; both are memory bound, independent, and run side by side instead of as two dependent launches)
+__global__ void __launch_bounds__(256) k_adam_gather(const __grid_constant__ AdamArgs a, const float* payload,
+                                                     float kl_target, int world, int m, float* acc,
+                                                     const __grid_constant__ GatherArgs g, int nadam) {
+  pdl_trigger();
+  pdl_wait();
+  if ((int)blockIdx.x < nadam) adam_body(a, payload, kl_target, world, m, acc, blockIdx.x);
+  else gather_body(g, (int)blockIdx.x - nadam);
+}
+
 void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc, cudaStream_t st) {
   launch_pdl(k_adam, dim3((unsigned)a.sh.blk0[a.sh.nseg]), dim3(256), 0, st, a, payload, kl_target, world, m, acc);
+}
+void launch_adam_gather(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc,
+                        const GatherArgs& g, cudaStream_t st) {
+  const int nadam = a.sh.blk0[a.sh.nseg];
+  launch_pdl(k_adam_gather, dim3((unsigned)(nadam + gather_blocks(g.M))), dim3(256), 0, st, a, payload, kl_target,
+             world, m, acc, g, nadam);
 }
 
 __global__ void k_sync_shadow(ShadowArgs sh, const float* theta) {
