@@ -97,8 +97,8 @@ static void probe_fwd(int M, int N, int K, int bn, cudaStream_t st) {
   g.kb_total = (K + 63) / 64; g.kb_per_split = g.kb_total; g.n_tiles = (N + bn - 1) / bn; g.n_splits = 1;
   g.ldo = N; g.bias[0] = bias;
   const double fl = 2.0 * M * N * K;
-  const int probes[4] = {0, 1, 2, 4};
-  for (int pi = 0; pi < 4; ++pi) {
+  const int probes[6] = {0, 1, 2, 4, 5, 6};  // 5: loads only, 6: MMAs only
+  for (int pi = 0; pi < 6; ++pi) {
     const int probe = probes[pi];
     g.probe = probe;
     float us = time_us([&] { CK(launch_gemm(GEMM_FWD, bn, g, st)); }, st);
