@@ -110,7 +110,8 @@ def main(rep, rnd="r01"):
                         "k_env_step": "transition, reward, flags, curriculum, reset", "k_env_obs": "observation + height scan + noise",
                         "k_heads": "value scatter (time-out bootstrap)", "k_gae": "GAE reverse scan",
                         "k_perm": "Feistel shuffle (5 epochs)", "k_gather": "minibatch gather", "k_loss_heads": "heads + PPO loss + dZ3",
-                        "k_reduce_heads": "head-gradient reduction", "k_adam": "Alg. 1 + Adam + weight shadows"}.get(e["name"], "")
+                        "k_reduce_heads": "head-gradient reduction", "k_adam": "Alg. 1 + Adam + weight shadows",
+                        "k_adam_gather": "Alg. 1 + Adam + shadows, with the next minibatch's gather"}.get(e["name"], "")
         dram_pct = gbs / hbm_peak * 100
         if bound == "tensor" and e["tens"] >= 15:
             lim = "tensor / epilogue traffic"
