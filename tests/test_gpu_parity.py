@@ -455,3 +455,110 @@ def test_bootstrap_arms_identical_until_a_timeout():
     assert res["on"][2]["n_to_total"] > 0 and res["off"][2]["n_to_total"] == 0
     assert res["on"][3] == res["off"][3]                 # the environment does not depend on the flag
     assert not np.array_equal(res["on"][1], res["off"][1])
+
+
+# ------------------------------------------------------------------ BASELINE configs[2] full size (C3)
+def test_env_full_size_c3_bit_exact():
+    """4096 envs x 24 steps on the C3 world (10 levels x 20 columns, 187-point scan, curriculum, noise, pushes),
+    teacher-forced with random actions: state, observation, reward and flags bit-exact at every step, in the
+    launch configuration bench.py times (same kernels, same grid shapes)."""
+    cfg, ctx, env, _ = make(n_envs=4096, T=24, levels=10, cols=20, seed=1234)
+    N = cfg.n_envs
+    obs_g = torch.zeros(N, cfg.obs_dim, device="cuda")
+    ctx.reset(obs=obs_g)
+    o0 = env.reset()
+    ctx.sync()
+    assert gpu_state(ctx).tobytes() == env.state.tobytes() and np.array_equal(obs_g.cpu().numpy(), o0)
+    st = env.state.copy()
+    st["ep_step"][::97] = 990        # time-outs during the rollout
+    st["push_timer"][1::53] = 495    # pushes
+    st["level"][2::41] = 9           # top-level promotions loop back
+    st["crossed"][2::41] = 1
+    st["ep_step"][2::41] = 995
+    env.state[:] = st
+    set_gpu_state(ctx, st)
+    rng = np.random.default_rng(3)
+    rew_g = torch.zeros(N, device="cuda")
+    term_g = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    to_g = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    n_to = 0
+    for t in range(cfg.n_steps):
+        a = (rng.standard_normal((N, 12)) * 0.5).astype(np.float32)
+        ctx.env_step(t, actions=torch.from_numpy(a).cuda(), obs=obs_g, reward=rew_g, terminated=term_g, timeout=to_g)
+        o, r, te, to, _, _ = env.step(a)
+        ctx.sync()
+        assert gpu_state(ctx).tobytes() == env.state.tobytes(), t
+        assert np.array_equal(o, obs_g.cpu().numpy()), t
+        assert np.array_equal(r, rew_g.cpu().numpy()), t
+        assert np.array_equal(te, term_g.cpu().numpy()) and np.array_equal(to, to_g.cpu().numpy()), t
+        n_to += int(to.sum())
+    assert n_to >= 40
+
+
+def test_rollout_gae_and_minibatch_gradient_full_size_c3():
+    """The full C3 rollout through the GPU path (fused policy, env kernels), GAE with time-out bootstrap over
+    98,304 samples against the oracle (1e-5), and one full-size minibatch (M = 24,576) gradient against the
+    fp64 oracle (bf16 MLP tolerance 2e-2)."""
+    cfg, ctx, env, theta = make(n_envs=4096, T=24, levels=10, cols=20, seed=1234)
+    ctx.reset()
+    st = gpu_state(ctx)
+    st["ep_step"][::61] = 990         # time-outs inside the rollout exercise the bootstrap path
+    set_gpu_state(ctx, st)
+    for t in range(cfg.n_steps):
+        ctx.policy_act(t)
+        ctx.env_step(t)
+    ctx.compute_gae()
+    ctx.sync()
+    bt = _batch_from_gpu(ctx, cfg)
+    assert bt["timeout"].sum() >= 60
+    A_o, R_o = learn.gae(bt["r"], bt["V"], bt["V_T"], bt["b"], bt["term"], bt["timeout"])
+    assert close_mixed(ctx.storage("ADV").cpu().numpy(), A_o, 1e-5)
+    assert close_mixed(ctx.storage("RET").cpu().numpy(), R_o, 1e-5)
+    # bootstrap values: the critic on the pre-reset observation of every time-out
+    to_idx = np.argwhere(bt["timeout"] > 0)
+    assert np.all(bt["b"][bt["timeout"] == 0] == 0.0)
+    B = cfg.n_envs * cfg.n_steps
+    M = B // cfg.n_minibatches
+    idx = np.random.default_rng(11).permutation(B)[:M].astype(np.int32)
+    ctx.minibatch_grad(torch.from_numpy(idx).cuda())
+    ctx.sync()
+    g_gpu = ctx.grad[:ctx.P].cpu().numpy()
+    An = learn.normalize_adv(A_o).reshape(B)
+    D = cfg.obs_dim
+    obs = bt["obs"].reshape(B, -1)[:, :D]
+    p = learn.unpack(theta.astype(np.float64), D, cfg.hidden)
+    g_o, _ = learn.ppo_minibatch(p, obs[idx], bt["act"].reshape(B, 12)[idx], bt["logp"].reshape(B)[idx],
+                                 bt["V"].reshape(B)[idx], An[idx], R_o.reshape(B)[idx], bt["mu"].reshape(B, 12)[idx],
+                                 bt["logstd_old"].astype(np.float64))
+    G = _grad_tensors(g_gpu, D, cfg.hidden)
+    for k, ref in g_o.items():
+        assert rel(G[k], ref) < 2e-2, (k, rel(G[k], ref))
+    assert len(to_idx) == int(bt["timeout"].sum())
+
+
+def test_ppo_update_drift_full_size_c3():
+    """All 5 x 4 minibatches of one C3 iteration (M = 24,576): parameter drift after the update against the
+    oracle with the GPU's bf16 rounding points <= 1e-3 relative (BASELINE north_star), Alg. 1 state equal."""
+    cfg, ctx, env, theta = make(n_envs=4096, T=24, levels=10, cols=20, seed=1234)
+    _rollout(ctx, cfg)
+    ctx.compute_gae()
+    ctx.sync()
+    bt = _batch_from_gpu(ctx, cfg)
+    B = cfg.n_envs * cfg.n_steps
+    perms = []
+    pt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    for e in range(cfg.n_epochs):
+        ctx.shuffle(e, pt)
+        ctx.sync()
+        perms.append(pt.cpu().numpy().view(np.uint32).copy())
+    stats = torch.zeros(64, dtype=torch.int32, device="cuda")
+    ctx.update(stats)
+    ctx.sync()
+    th_gpu = ctx.theta.cpu().numpy().astype(np.float64)
+    z = np.zeros(theta.size)
+    th_q, m, v, t, alpha, st = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms,
+                                                cfg.obs_dim, cfg.hidden, quant="bf16")
+    sc = ctx.scalars()
+    assert sc["adam_t"] == t == 20
+    assert abs(sc["alpha"] - alpha) <= 1e-6 * alpha
+    assert rel(th_gpu, th_q) <= 1e-3
