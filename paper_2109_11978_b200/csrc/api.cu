@@ -789,24 +789,31 @@ lg_status curriculum_update(lg_ctx* ctx, int32_t n, const uint8_t* crossed, cons
 // the fused rollout policy kernel covers the paper's MLP (512-256-128, observation <= 256 columns)
 static bool fused_policy_ok(const Dims& d) { return d.H0 == 512 && d.H1 == 256 && d.H2 == 128 && d.Dp <= 256; }
 
+// the fused rollout policy kernel on OBS slot t (slot T: the critic alone gives V(o_T))
+static FusedPolicyArgs fused_args(lg_ctx* ctx, int t) {
+  const Dims& d = ctx->d;
+  FusedPolicyArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.tmX = ctx->l1_roll[t].tmA[0];
+  fa.tmW1 = ctx->l1_roll[t].tmB[0];
+  fa.tmW2[0] = ctx->tmW2f[0]; fa.tmW2[1] = ctx->tmW2f[1];
+  fa.tmW3[0] = ctx->tmW3f[0]; fa.tmW3[1] = ctx->tmW3f[1];
+  void* W = ctx->buf[LG_BUF_WEIGHTS];
+  fa.b1 = at<float>(W, ctx->L.w_b1); fa.b2 = at<float>(W, ctx->L.w_b2); fa.b3 = at<float>(W, ctx->L.w_b3);
+  fa.W4a = at<float>(W, ctx->L.w_W4a); fa.b4a = at<float>(W, ctx->L.w_b4a);
+  fa.W4c = at<float>(W, ctx->L.w_W4c); fa.b4c = at<float>(W, ctx->L.w_b4c); fa.logstd = at<float>(W, ctx->L.w_ls);
+  fa.N = d.N; fa.rank = ctx->cfg.rank; fa.t = t; fa.kb1 = (d.Dp + 63) / 64;
+  fa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); fa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
+  fa.scalars = ctx->sc;
+  return fa;
+}
+
 lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float* mu, float* value) {
   GUARD();
   const Dims& d = ctx->d;
   if (t < 0 || t >= d.T) return fail(ctx, LG_ERR_RANGE, "policy_act: t=%d out of [0,%d)", t, d.T);
   if (fused_policy_ok(d) && !(ctx->cfg.flags & LG_F_UNFUSED_POLICY)) {
-    FusedPolicyArgs fa;
-    memset(&fa, 0, sizeof(fa));
-    fa.tmX = ctx->l1_roll[t].tmA[0];
-    fa.tmW1 = ctx->l1_roll[t].tmB[0];
-    fa.tmW2[0] = ctx->tmW2f[0]; fa.tmW2[1] = ctx->tmW2f[1];
-    fa.tmW3[0] = ctx->tmW3f[0]; fa.tmW3[1] = ctx->tmW3f[1];
-    void* W = ctx->buf[LG_BUF_WEIGHTS];
-    fa.b1 = at<float>(W, ctx->L.w_b1); fa.b2 = at<float>(W, ctx->L.w_b2); fa.b3 = at<float>(W, ctx->L.w_b3);
-    fa.W4a = at<float>(W, ctx->L.w_W4a); fa.b4a = at<float>(W, ctx->L.w_b4a);
-    fa.W4c = at<float>(W, ctx->L.w_W4c); fa.b4c = at<float>(W, ctx->L.w_b4c); fa.logstd = at<float>(W, ctx->L.w_ls);
-    fa.N = d.N; fa.rank = ctx->cfg.rank; fa.t = t; fa.kb1 = (d.Dp + 63) / 64;
-    fa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); fa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
-    fa.scalars = ctx->sc;
+    FusedPolicyArgs fa = fused_args(ctx, t);
     fa.act = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
     fa.mu = reinterpret_cast<float*>(ctx->buf[LG_BUF_MU]) + (size_t)t * d.N * 12;
     fa.logp = reinterpret_cast<float*>(ctx->buf[LG_BUF_LOGP]) + (size_t)t * d.N;
@@ -874,14 +881,24 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
     { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(hb, ctx->st); }
     CKL();
   }
-  // V(o_T): critic on OBS slot T
-  lg_status s = critic_rows(ctx, ctx->l1_vt, nullptr, d.N);
-  if (s != LG_OK) return s;
-  HeadArgs h = head_args(ctx, d.N);
-  h.mode = 1;
-  h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE_T]);
-  { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(h, ctx->st); }
-  CKL();
+  // V(o_T): critic on OBS slot T (the fused kernel's critic half when it applies: one launch, bit-identical)
+  lg_status s = LG_OK;
+  if (fused_policy_ok(d) && !(ctx->cfg.flags & LG_F_UNFUSED_POLICY)) {
+    FusedPolicyArgs fa = fused_args(ctx, d.T);
+    fa.z0 = 1;
+    fa.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE_T]);
+    Scope sc_(ctx, LG_PROF_GEMM_ROLL);
+    cudaError_t e = launch_policy_fused(fa, ctx->st);
+    if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "V(o_T) (fused): %s", cudaGetErrorString(e));
+  } else {
+    s = critic_rows(ctx, ctx->l1_vt, nullptr, d.N);
+    if (s != LG_OK) return s;
+    HeadArgs h = head_args(ctx, d.N);
+    h.mode = 1;
+    h.value = reinterpret_cast<float*>(ctx->buf[LG_BUF_VALUE_T]);
+    { Scope sc_(ctx, LG_PROF_HEADS); launch_heads(h, ctx->st); }
+    CKL();
+  }
   GaeArgs g;
   g.N = d.N; g.T = d.T;
   g.r = reinterpret_cast<const float*>(ctx->buf[LG_BUF_REWARD]);

@@ -1269,7 +1269,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int z = blockIdx.y;
+  const int z = a.z0 + (int)blockIdx.y;
   const int m0 = blockIdx.x * 128;
   if (threadIdx.x == 0) FP_STAMP(0);
   pdl_trigger();
@@ -1546,7 +1546,8 @@ cudaError_t launch_policy_fused(const FusedPolicyArgs& a, cudaStream_t st) {
     attr_set = true;
   }
   if (a.kb1 < 1 || a.kb1 > 4) return cudaErrorInvalidValue;
-  dim3 grid((a.N + 127) / 128, 2, 1);
+  if (a.z0 < 0 || a.z0 > 1) return cudaErrorInvalidValue;
+  dim3 grid((a.N + 127) / 128, 2 - a.z0, 1);
   return launch_pdl(k_policy_fused, grid, dim3(GEMM_THREADS), fp::SMEM, st, a);
 }
 

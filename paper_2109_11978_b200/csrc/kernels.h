@@ -125,6 +125,7 @@ struct FusedPolicyArgs {
   const float* b3;           // [2*128]
   const float* W4a; const float* b4a; const float* W4c; const float* b4c; const float* logstd;
   int N, rank, t, kb1;       // kb1 = K-blocks of layer 1 (Dp / 64 rounded up, <= 4)
+  int z0;                    // first net: 0 = actor and critic (grid.y = 2), 1 = critic only (V(o_T))
   uint32_t seed_lo, seed_hi;
   const DevScalars* scalars;
   float* act; float* mu; float* logp; float* value;              // storage slot t

@@ -796,32 +796,41 @@ __global__ void k_iter_end(IterEndArgs a, const float* acc) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    DevScalars* sc = a.sc;
-    sc->alpha = sc->alpha_ring[a.n_mb & 1];
+  // the statistics fields are written by separate threads (independent loads, no serial chain through
+  // one thread); the counters are reset only after every thread has read them
+  DevScalars* sc = a.sc;
+  lg_update_stats_dev* s = a.stats ? reinterpret_cast<lg_update_stats_dev*>(a.stats) : nullptr;
+  const int k = threadIdx.x;
+  float alpha = 0.0f;
+  if (k == 0) {
+    alpha = sc->alpha_ring[a.n_mb & 1];
+    sc->alpha = alpha;
     sc->adam_t = sc->adamt_ring[a.n_mb & 1];
-    if (a.stats) {
-      lg_update_stats_dev* s = reinterpret_cast<lg_update_stats_dev*>(a.stats);
+    if (s) s->lr = alpha;
+  }
+  if (s) {
+    if (k == 1) {
       const float n = fmaxf(acc[4], 1.0f);
-      s->surrogate_loss = acc[0] / n;
-      s->value_loss = acc[1] / n;
+      s->surrogate_loss = acc[0] / n; s->value_loss = acc[1] / n; s->mean_kl = acc[2] / n;
+      s->clip_fraction = acc[3] / n; s->minibatches_applied = (int)acc[4];
+    } else if (k == 2) {
       float H = 0.0f;
       for (int j = 0; j < 12; ++j) H += 0.5f + HALF_LN_2PI + a.logstd[j];
       s->entropy = H;
-      s->mean_kl = acc[2] / n;
-      s->lr = sc->alpha;
-      s->clip_fraction = acc[3] / n;
-      s->nonfinite_skips = sc->nonfinite_skips;
-      s->minibatches_applied = (int)acc[4];
+    } else if (k == 3) {
       const int ne = sc->episodes;
       s->mean_episode_return = ne > 0 ? sc->ep_return_sum / (float)ne : 0.0f;
       s->mean_episode_length = ne > 0 ? sc->ep_len_sum / (float)ne : 0.0f;
       s->episodes = ne;
-      s->promotions = sc->promotions;
-      s->demotions = sc->demotions;
-      s->reserved = (int)sc->iteration + 1;
-      for (int k = 0; k < 16; ++k) s->level_hist[k] = hist[k];
+    } else if (k == 4) {
+      s->promotions = sc->promotions; s->demotions = sc->demotions;
+      s->nonfinite_skips = sc->nonfinite_skips; s->reserved = (int)sc->iteration + 1;
+    } else if (k >= 32 && k < 48) {
+      s->level_hist[k - 32] = hist[k - 32];
     }
+  }
+  __syncthreads();
+  if (k == 0) {
     sc->ep_return_sum = 0.0f; sc->ep_len_sum = 0.0f; sc->episodes = 0; sc->promotions = 0; sc->demotions = 0;
     sc->iteration += 1;
   }
