@@ -412,10 +412,15 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
   if (blockIdx.x == 0 && threadIdx.x == 0) P.scalars->n_to_slot[(ev + 1u) & 1u] = 0;  // the next step's counter
   const int N = P.N;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = gt >> 2, l = gt & 3;
-  if (i >= N) return;  // whole groups leave together (4 | blockDim)
+  if ((gt & ~31) >= 4 * N) return;  // whole warps beyond the last env leave
+  // every lane of a live warp runs the step (lanes past the last env shadow env N-1 and write nothing), so
+  // the per-env group sums are full-warp shuffles: a shuffle with a 4-lane member mask compiles to a
+  // vote / branch loop that cost ~25 % of the kernel's issue slots in branch resolution
+  const bool live = (gt >> 2) < N;
+  const int i = live ? gt >> 2 : N - 1, l = gt & 3;
   const int lane = threadIdx.x & 31, gbase = lane & ~3;
-  const unsigned gm = 0xFu << gbase;
+  const unsigned gm = 0xFu << gbase;  // the group's lanes (shuffles inside group-divergent branches)
+  constexpr unsigned FULL = 0xffffffffu;
   Com c;
   Leg g;
   load_com(P.state, N, i, c);
@@ -468,14 +473,14 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
       qdd[2] = ((tau[2] + tc2) - C_J * g.qd[2]) / J_J;
       cross3(r, f, rf);
     }
-    const uint32_t contact = (__ballot_sync(gm, touch) >> gbase) & 0xFu;
+    const uint32_t contact = (__ballot_sync(FULL, touch) >> gbase) & 0xFu;
     float F[3] = {0.0f, 0.0f, 0.0f}, Tw[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
     for (int L = 0; L < 4; ++L)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        F[k] = F[k] + __shfl_sync(gm, f[k], gbase + L);
-        Tw[k] = Tw[k] + __shfl_sync(gm, rf[k], gbase + L);
+        F[k] = F[k] + __shfl_sync(FULL, f[k], gbase + L);
+        Tw[k] = Tw[k] + __shfl_sync(FULL, rf[k], gbase + L);
       }
     F[2] = F[2] - M_BASE * GRAV;
     float tb[3], Iw[3], gy[3], wdot[3];
@@ -507,10 +512,10 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
       float term = 0.0f;
       if (td) { term = g.tair - 0.5f; g.tair = 0.0f; }
       else if (!cn) g.tair = g.tair + DT_SIM;
-      const uint32_t tds = (__ballot_sync(gm, td) >> gbase) & 0xFu;
+      const uint32_t tds = (__ballot_sync(FULL, td) >> gbase) & 0xFu;
 #pragma unroll
       for (int L = 0; L < 4; ++L) {
-        const float tL = __shfl_sync(gm, term, gbase + L);
+        const float tL = __shfl_sync(FULL, term, gbase + L);
         if ((tds >> L) & 1u) airsum = airsum + tL;
       }
     }
@@ -526,7 +531,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
     mv(R, kb, r);
     float kx = c.p[0] + r[0], ky = c.p[1] + r[1], kz = c.p[2] + r[2];
     const bool kin = h_plate(W, kx, ky) - kz > 0.0f;
-    n_c = __popc((__ballot_sync(gm, kin) >> gbase) & 0xFu);
+    n_c = __popc((__ballot_sync(FULL, kin) >> gbase) & 0xFu);
   }
   c.ep_step += 1;
   c.push_timer += 1;
@@ -538,7 +543,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
   for (int k = 0; k < 3; ++k) fin = fin && isfinite(c.p[k]) && isfinite(c.v[k]) && isfinite(c.w[k]);
   for (int k = 0; k < 4; ++k) fin = fin && isfinite(c.quat[k]);
   for (int k = 0; k < 3; ++k) fin = fin && isfinite(g.q[k]) && isfinite(g.qd[k]);
-  const bool finite = ((__ballot_sync(gm, fin) >> gbase) & 0xFu) == 0xFu;
+  const bool finite = ((__ballot_sync(FULL, fin) >> gbase) & 0xFu) == 0xFu;
   // reward
   float rt[9];
   {
@@ -558,18 +563,18 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
     rt[3] = (-0.05f * DT) * (wh0 * wh0 + wh1 * wh1);
     float x3[3];
     for (int k = 0; k < 3; ++k) x3[k] = qdd[k] * qdd[k];
-    const float sa = joint_sum(x3, gbase, gm);
+    const float sa = joint_sum(x3, gbase, FULL);
     for (int k = 0; k < 3; ++k) x3[k] = g.qd[k] * g.qd[k];
-    const float sb = joint_sum(x3, gbase, gm);
+    const float sb = joint_sum(x3, gbase, FULL);
     rt[4] = (-0.001f * DT) * (sa + sb);
     for (int k = 0; k < 3; ++k) x3[k] = tau[k] * tau[k];
-    rt[5] = (-0.00002f * DT) * joint_sum(x3, gbase, gm);
+    rt[5] = (-0.00002f * DT) * joint_sum(x3, gbase, FULL);
     for (int k = 0; k < 3; ++k) {
       float qprev = c_qdef[3 * l + k] + 0.5f * g.aprev[k];
       float d = (qstar[k] - qprev) / DT;
       x3[k] = d * d;
     }
-    rt[6] = (-0.25f * DT) * joint_sum(x3, gbase, gm);
+    rt[6] = (-0.25f * DT) * joint_sum(x3, gbase, FULL);
     rt[7] = (-0.001f * DT) * (float)n_c;
     rt[8] = (2.0f * DT) * airsum;
   }
@@ -581,6 +586,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
   const bool to = (c.ep_step >= 1000) && !terminated;
   const bool done = terminated || to;
   for (int k = 0; k < 3; ++k) g.aprev[k] = a[k];
+  if (!live) return;  // shadow lanes past the last env: no stores (no shuffles follow outside the group)
   const size_t ti = (size_t)t * N + i;
   if (l == 0) {
     P.reward[ti] = r;
