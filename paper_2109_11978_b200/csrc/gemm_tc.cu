@@ -1373,13 +1373,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     const int e = warp - 4, q = e & 3, h = e >> 2;
     const int r = q * 32 + lane;  // TMEM lane = tile row
     const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
-    // biases and head weights are staged here, while the producer and the MMA warp run layer 1
+    // biases and head weights are staged here, while the producer and the MMA warp run layer 1: 16-B cp.async
+    // chunks, all in flight at once (a load-then-store loop serialised ~10 global latencies per thread)
     {
       const int et = threadIdx.x - 128, nt = EPI_WARPS * 32;
-      for (int k = et; k < fp::H0; k += nt) sB1[k] = __ldg(a.b1 + z * fp::H0 + k);
-      for (int k = et; k < fp::H1; k += nt) sB2[k] = __ldg(a.b2 + z * fp::H1 + k);
-      for (int k = et; k < fp::H2; k += nt) sB3[k] = __ldg(a.b3 + z * fp::H2 + k);
-      for (int k = et; k < 13 * fp::H2; k += nt) sHW[k] = k < 12 * fp::H2 ? __ldg(a.W4a + k) : __ldg(a.W4c + k - 12 * fp::H2);
+      constexpr int C1 = fp::H0 / 4, C2 = C1 + fp::H1 / 4, C3 = C2 + fp::H2 / 4, C4 = C3 + 12 * fp::H2 / 4,
+                    C5 = C4 + fp::H2 / 4;
+      for (int k = et; k < C5; k += nt) {
+        const float* src;
+        float* dst;
+        if (k < C1) { src = a.b1 + z * fp::H0 + 4 * k; dst = sB1 + 4 * k; }
+        else if (k < C2) { src = a.b2 + z * fp::H1 + 4 * (k - C1); dst = sB2 + 4 * (k - C1); }
+        else if (k < C3) { src = a.b3 + z * fp::H2 + 4 * (k - C2); dst = sB3 + 4 * (k - C2); }
+        else if (k < C4) { src = a.W4a + 4 * (k - C3); dst = sHW + 4 * (k - C3); }
+        else { src = a.W4c + 4 * (k - C4); dst = sHW + 12 * fp::H2 + 4 * (k - C4); }
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
     }
     // layer 1 -> H1 (bias + ELU, bf16) into R1 (the observation tile there is dead once tfull[0] fired)
