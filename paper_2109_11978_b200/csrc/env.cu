@@ -17,6 +17,24 @@ constexpr float KP = 80.0f, KD = 2.0f, TAU_MAX = 80.0f, J_J = 0.25f, C_J = 0.5f;
 constexpr float K_N = 5000.0f, C_N = 100.0f, C_T = 60.0f, R_B = 0.25f, DT_SIM = 0.005f, DT = 0.02f;
 
 __constant__ float c_inertia[3] = {0.5f, 1.7f, 2.0f};
+__constant__ float c_inertia_rc[3] = {(float)(1.0 / 0.5), (float)(1.0 / (double)1.7f), (float)(1.0 / 2.0)};
+
+// x / c for the transition model's constant divisors (J_J, M_BASE, the inertias, 0.25, DT): q0 = RN(x rc),
+// one fma residual and one fma correction (rc = RN(1/c)). On 2^-100 <= |x| <= 2^100 this equals the IEEE
+// quotient RN(x / c) bit for bit for each of these c -- checked over all 2^32 inputs by tools/div_check.cu;
+// +-0 keep their sign through q0 = x rc; everything else (denormals, huge, inf, NaN) takes the IEEE division.
+// Same result as the oracle's plain x / c, without the division's slow-path branch.
+__device__ __forceinline__ float div_const(float x, float c, float rc) {
+  const float ax = fabsf(x);
+  const float q0 = __fmul_rn(x, rc);
+  const float r = __fmaf_rn(-q0, c, x);
+  const float q = __fmaf_rn(r, rc, q0);
+  if (ax == 0.0f) return q0;
+  if (ax >= 0x1p-100f && ax <= 0x1p100f) return q;
+  return __fdiv_rn(x, c);
+}
+constexpr float RC_J = (float)(1.0 / (double)J_J), RC_M = (float)(1.0 / (double)M_BASE),
+                RC_DT = (float)(1.0 / (double)DT), RC_Q = (float)(1.0 / 0.25);
 __constant__ float c_hip[4][3] = {{0.30f, 0.15f, 0.0f}, {0.30f, -0.15f, 0.0f}, {-0.30f, 0.15f, 0.0f}, {-0.30f, -0.15f, 0.0f}};
 __constant__ float c_slat[4] = {1.0f, -1.0f, 1.0f, -1.0f};
 __constant__ float c_qdef[12] = {0.0f, 0.7f, -1.4f, 0.0f, 0.7f, -1.4f, 0.0f, -0.7f, 1.4f, 0.0f, -0.7f, 1.4f};
@@ -468,9 +486,9 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
       float fbb[3];
       mtv(R, f, fbb);
       float tc0 = dot3(J[0], fbb), tc1 = dot3(J[1], fbb), tc2 = dot3(J[2], fbb);
-      qdd[0] = ((tau[0] + tc0) - C_J * g.qd[0]) / J_J;
-      qdd[1] = ((tau[1] + tc1) - C_J * g.qd[1]) / J_J;
-      qdd[2] = ((tau[2] + tc2) - C_J * g.qd[2]) / J_J;
+      qdd[0] = div_const((tau[0] + tc0) - C_J * g.qd[0], J_J, RC_J);
+      qdd[1] = div_const((tau[1] + tc1) - C_J * g.qd[1], J_J, RC_J);
+      qdd[2] = div_const((tau[2] + tc2) - C_J * g.qd[2], J_J, RC_J);
       cross3(r, f, rf);
     }
     const uint32_t contact = (__ballot_sync(FULL, touch) >> gbase) & 0xFu;
@@ -487,8 +505,8 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
     mtv(R, Tw, tb);
     for (int k = 0; k < 3; ++k) Iw[k] = c_inertia[k] * c.w[k];
     cross3(c.w, Iw, gy);
-    for (int k = 0; k < 3; ++k) wdot[k] = (tb[k] - gy[k]) / c_inertia[k];
-    for (int k = 0; k < 3; ++k) c.v[k] = c.v[k] + DT_SIM * (F[k] / M_BASE);
+    for (int k = 0; k < 3; ++k) wdot[k] = div_const(tb[k] - gy[k], c_inertia[k], c_inertia_rc[k]);
+    for (int k = 0; k < 3; ++k) c.v[k] = c.v[k] + DT_SIM * div_const(F[k], M_BASE, RC_M);
     for (int k = 0; k < 3; ++k) c.w[k] = c.w[k] + DT_SIM * wdot[k];
 #pragma unroll
     for (int k = 0; k < 3; ++k) g.qd[k] = g.qd[k] + DT_SIM * qdd[k];
@@ -557,8 +575,8 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
     float wh1 = -sn * wv[0] + cc * wv[1];
     float wh2 = wv[2];
     float ex = c.cmd[0] - vh0, ey = c.cmd[1] - vh1, ez = c.cmd[2] - wh2;
-    rt[0] = (1.0f * DT) * exp_poly(-((ex * ex + ey * ey) / 0.25f));
-    rt[1] = (0.5f * DT) * exp_poly(-((ez * ez) / 0.25f));
+    rt[0] = (1.0f * DT) * exp_poly(-div_const(ex * ex + ey * ey, 0.25f, RC_Q));
+    rt[1] = (0.5f * DT) * exp_poly(-div_const(ez * ez, 0.25f, RC_Q));
     rt[2] = (-4.0f * DT) * (vh2 * vh2);
     rt[3] = (-0.05f * DT) * (wh0 * wh0 + wh1 * wh1);
     float x3[3];
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
     rt[5] = (-0.00002f * DT) * joint_sum(x3, gbase, FULL);
     for (int k = 0; k < 3; ++k) {
       float qprev = c_qdef[3 * l + k] + 0.5f * g.aprev[k];
-      float d = (qstar[k] - qprev) / DT;
+      float d = div_const(qstar[k] - qprev, DT, RC_DT);
       x3[k] = d * d;
     }
     rt[6] = (-0.25f * DT) * joint_sum(x3, gbase, FULL);
