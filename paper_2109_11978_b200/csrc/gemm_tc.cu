@@ -1261,12 +1261,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   float* sX = reinterpret_cast<float*>(smem + fp::OFF_XCH);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + fp::OFF_BAR);
   uint64_t* xfull = bars + 0;
-  uint64_t* full = bars + 1;           // [2]
-  uint64_t* empty = bars + 3;          // [2]
-  uint64_t* tfull = bars + 5;          // [3]
-  uint64_t* h1ready = bars + 8;
-  uint64_t* h2ready = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* full = bars + 1;           // [4]
+  uint64_t* empty = bars + 5;          // [4]
+  uint64_t* tfull = bars + 9;          // [3]
+  uint64_t* h1ready = bars + 12;
+  uint64_t* h2ready = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  // weight-chunk slots: 0, 1 = the ring; 2, 3 = R1 blocks 4-5 and 6-7, free while layer 1 runs (the
+  // observation tile occupies blocks 0..kb1-1 <= 3, H1 is written only after every layer-1 MMA completed),
+  // so layer 1 streams W1 four chunks deep; layers 2 and 3 use the ring
+  auto slot_ptr = [&](int sl) { return sl < 2 ? ring + sl * fp::STAGE : R1 + (4 + 2 * (sl - 2)) * fp::ABLK; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = a.z0 + (int)blockIdx.y;
@@ -1275,7 +1279,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   pdl_trigger();
   if (threadIdx.x == 0) {
     mbar_init(xfull, 1);
-    for (int s2 = 0; s2 < fp::NSTAGE; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
+    for (int s2 = 0; s2 < 4; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
     for (int s2 = 0; s2 < 3; ++s2) mbar_init(&tfull[s2], 1);
     mbar_init(h1ready, EPI_WARPS);
     mbar_init(h2ready, EPI_WARPS);
@@ -1297,18 +1301,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     if (lane == 0) {
       mbar_expect_tx(xfull, a.kb1 * fp::ABLK);
       for (int kb = 0; kb < a.kb1; ++kb) tma_load_2d(&a.tmX, xfull, R1 + kb * fp::ABLK, kb * fp::BK, m0);
-      int stage = 0;
-      uint32_t phase = 0;
-      auto load = [&](const CUtensorMap* map, int x, int y, uint32_t bytes) {
-        mbar_wait(&empty[stage], phase ^ 1u);
-        mbar_expect_tx(&full[stage], bytes);
-        tma_load_2d(map, &full[stage], ring + stage * fp::STAGE, x, y);
-        if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+      uint32_t ph = 0;  // bit sl: phase parity of slot sl
+      auto load = [&](int sl, const CUtensorMap* map, int x, int y, uint32_t bytes) {
+        mbar_wait(&empty[sl], ((ph >> sl) & 1u) ^ 1u);
+        mbar_expect_tx(&full[sl], bytes);
+        tma_load_2d(map, &full[sl], slot_ptr(sl), x, y);
+        ph ^= 1u << sl;
       };
+      int g = 0;
       for (int nh = 0; nh < 2; ++nh)
-        for (int kb = 0; kb < a.kb1; ++kb) load(&a.tmW1, kb * fp::BK, z * fp::H0 + nh * 256, fp::STAGE);
-      for (int kb = 0; kb < fp::H0 / fp::BK; ++kb) load(&a.tmW2[z], kb * fp::BK, 0, fp::STAGE);
-      for (int kb = 0; kb < fp::H1 / fp::BK; ++kb) load(&a.tmW3[z], kb * fp::BK, 0, fp::STAGE / 2);
+        for (int kb = 0; kb < a.kb1; ++kb, ++g) load(g & 3, &a.tmW1, kb * fp::BK, z * fp::H0 + nh * 256, fp::STAGE);
+      int rr = 0;
+      for (int kb = 0; kb < fp::H0 / fp::BK; ++kb, ++rr) load(rr & 1, &a.tmW2[z], kb * fp::BK, 0, fp::STAGE);
+      for (int kb = 0; kb < fp::H1 / fp::BK; ++kb, ++rr) load(rr & 1, &a.tmW3[z], kb * fp::BK, 0, fp::STAGE / 2);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -1316,54 +1321,58 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     if (lane == 0) {
       constexpr uint32_t id256 = idesc_bf16(128, 256, false, false);
       constexpr uint32_t id128 = idesc_bf16(128, 128, false, false);
-      int stage = 0;
-      uint32_t phase = 0;
-      auto chunk = [&](uint32_t a_base, uint32_t dcol, uint32_t idesc) {
-        mbar_wait(&full[stage], phase);
+      uint32_t ph = 0;  // bit sl: phase parity of slot sl (the producer's schedule)
+      auto take = [&](int sl) {
+        mbar_wait(&full[sl], (ph >> sl) & 1u);
         tc_fence_after();
-        const uint32_t b0 = smem_u32(ring + stage * fp::STAGE);
-        return b0;
+        return smem_u32(slot_ptr(sl));
+      };
+      auto release = [&](int sl) {
+        tc_commit(&empty[sl]);
+        ph ^= 1u << sl;
       };
       mbar_wait(xfull, 0);
       tc_fence_after();
       // layer 1: two 256-column halves of this net's 512 outputs, K = kb1 blocks of the observation
+      int g = 0;
       for (int nh = 0; nh < 2; ++nh)
-        for (int kb = 0; kb < a.kb1; ++kb) {
-          const uint32_t b0 = chunk(0, 0, 0);
+        for (int kb = 0; kb < a.kb1; ++kb, ++g) {
+          const int sl = g & 3;
+          const uint32_t b0 = take(sl);
           const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
 #pragma unroll
           for (int k = 0; k < fp::BK / 16; ++k)
             tc_mma(tmem + nh * 256, sdesc(a0 + k * 32u, 0u, 1024u), sdesc(b0 + k * 32u, 0u, 1024u), id256,
                    (kb > 0 || k > 0) ? 1u : 0u);
-          tc_commit(&empty[stage]);
-          if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+          release(sl);
         }
       tc_commit(&tfull[0]);
       // layer 2: A = H1 (8 blocks in R1), N = 256 into TMEM columns [0, 256)
       mbar_wait(h1ready, 0);
       tc_fence_after();
-      for (int kb = 0; kb < fp::H0 / fp::BK; ++kb) {
-        const uint32_t b0 = chunk(0, 0, 0);
+      int rr = 0;
+      for (int kb = 0; kb < fp::H0 / fp::BK; ++kb, ++rr) {
+        const int sl = rr & 1;
+        const uint32_t b0 = take(sl);
         const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
 #pragma unroll
         for (int k = 0; k < fp::BK / 16; ++k)
           tc_mma(tmem, sdesc(a0 + k * 32u, 0u, 1024u), sdesc(b0 + k * 32u, 0u, 1024u), id256, (kb > 0 || k > 0) ? 1u : 0u);
-        tc_commit(&empty[stage]);
-        if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+        release(sl);
       }
       tc_commit(&tfull[1]);
       // layer 3: A = H2 (4 blocks in R1), N = 128 into TMEM columns [256, 384)
       mbar_wait(h2ready, 0);
       tc_fence_after();
-      for (int kb = 0; kb < fp::H1 / fp::BK; ++kb) {
-        const uint32_t b0 = chunk(0, 0, 0);
+      for (int kb = 0; kb < fp::H1 / fp::BK; ++kb, ++rr) {
+        const int sl = rr & 1;
+        const uint32_t b0 = take(sl);
         const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
 #pragma unroll
         for (int k = 0; k < fp::BK / 16; ++k)
           tc_mma(tmem + 256, sdesc(a0 + k * 32u, 0u, 1024u), sdesc(b0 + k * 32u, 0u, 1024u), id128,
                  (kb > 0 || k > 0) ? 1u : 0u);
-        tc_commit(&empty[stage]);
-        if (++stage == fp::NSTAGE) { stage = 0; phase ^= 1u; }
+        release(sl);
       }
       tc_commit(&tfull[2]);
     }
