@@ -1229,11 +1229,14 @@ constexpr int SMEM = 1024 + OFF_BAR + 16 * 8;
 __device__ __forceinline__ void store_act_block(uint8_t* R1, int r, int c, const uint32_t* acc, const float* bias) {
   uint32_t pk[16];
 #pragma unroll
-  for (int k = 0; k < 32; k += 2) {
-    const float x0 = elu_fast(__uint_as_float(acc[k]) + bias[k]);
-    const float x1 = elu_fast(__uint_as_float(acc[k + 1]) + bias[k + 1]);
-    __nv_bfloat162 o = __floats2bfloat162_rn(x0, x1);
-    pk[k / 2] = *reinterpret_cast<uint32_t*>(&o);
+  for (int k = 0; k < 32; k += 4) {
+    const float4 b4 = *reinterpret_cast<const float4*>(bias + k);  // 16-B aligned: c is a multiple of 32
+    __nv_bfloat162 o0 = __floats2bfloat162_rn(elu_fast(__uint_as_float(acc[k]) + b4.x),
+                                              elu_fast(__uint_as_float(acc[k + 1]) + b4.y));
+    __nv_bfloat162 o1 = __floats2bfloat162_rn(elu_fast(__uint_as_float(acc[k + 2]) + b4.z),
+                                              elu_fast(__uint_as_float(acc[k + 3]) + b4.w));
+    pk[k / 2] = *reinterpret_cast<uint32_t*>(&o0);
+    pk[k / 2 + 1] = *reinterpret_cast<uint32_t*>(&o1);
   }
   uint8_t* blk = R1 + (c >> 6) * fp::ABLK + r * 128;
   const int ch0 = (c & 63) >> 3;
@@ -1470,11 +1473,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
           float pl[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float* w = wrow + 4 * (2 * i + h);
-            float s2 = __fmul_rn(w[0], hv[4 * i]);
-            s2 = fmaf(w[1], hv[4 * i + 1], s2);
-            s2 = fmaf(w[2], hv[4 * i + 2], s2);
-            pl[i] = fmaf(w[3], hv[4 * i + 3], s2);
+            const float4 w = *reinterpret_cast<const float4*>(wrow + 4 * (2 * i + h));  // one broadcast LDS.128
+            float s2 = __fmul_rn(w.x, hv[4 * i]);
+            s2 = fmaf(w.y, hv[4 * i + 1], s2);
+            s2 = fmaf(w.z, hv[4 * i + 2], s2);
+            pl[i] = fmaf(w.w, hv[4 * i + 3], s2);
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i) pl[i] = pl[i] + pl[i + 8];
