@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "csrc", "libleggedrl.so")
+# LG_LIB: another build of the same library (A/B timing of two builds in one process launch; diagnostics)
+LIB_PATH = os.environ.get("LG_LIB") or os.path.join(HERE, "csrc", "libleggedrl.so")
 NUM_BUFFERS = 20
 BUF = dict(HEIGHTFIELD=0, STATE=1, OBS=2, ACT=3, MU=4, LOGP=5, VALUE=6, REWARD=7, BOOT=8, FLAGS=9, ADV=10, RET=11,
            VALUE_T=12, THETA=13, ADAM_M=14, ADAM_V=15, GRAD=16, WEIGHTS=17, ACTIV=18, WORK=19)
