@@ -96,14 +96,17 @@ static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn) {
   p.m_tiles = (rows + 127) / 128;
   p.kb_total = (K + 63) / 64;
   p.tiles = p.n_tiles * p.m_tiles * nz;
-  // CTA pairs (256-row tiles, tcgen05 cta_group::2) when every z has an even number of 128-row tiles:
-  // each SM then receives 2/3 of the operand bytes for the same MMA work
-  // (measured: no gain over single CTAs inside the iteration -- the split-K tail dominates -- so off by default)
+  // CTA pairs (256-row tiles, tcgen05 cta_group::2: each CTA loads its 128 rows of dZ and half of the activation
+  // tile, so the pair reads the activations once for 256 output rows) when every net has an even number of
+  // 128-row tiles; bit-identical to single CTAs (tools/gemm_probe pair), -0.6 % per iteration measured on
+  // the same box (LG_DW_PAIR=0 switches them off)
+  static const bool pair_env = [] { const char* e = getenv("LG_DW_PAIR"); return !(e && e[0] == '0'); }();
   p.pair = 0;
   // one wave of <= 148 CTAs, and >= 8 k-blocks per CTA (the fp32 partial costs ~3 k-blocks of traffic)
   const int S = std::max(1, std::min(std::max(1, p.kb_total / 8), 148 / std::max(1, p.tiles)));
   p.kb_per_split = (p.kb_total + S - 1) / S;
   p.S = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  if (pair_env && (p.m_tiles % 2 == 0) && p.bn >= 128) p.pair = 1;
   p.part_bytes = al((size_t)p.tiles * p.S * 128 * (p.bn + 20) * 4);
   p.bytes = p.part_bytes + 256;  // + the grid-barrier counter
   return p;
