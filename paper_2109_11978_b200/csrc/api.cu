@@ -87,8 +87,14 @@ struct DwPlan {
   size_t part_bytes, bytes;
 };
 // Weight-gradient GEMM plan (k_gemm_dw): 128 x bn output tiles; the minibatch (K) is split over S CTAs per
-// tile so that tiles * S fills the 148 SMs in one wave; the S fp32 partials are reduced through L2.
-static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn) {
+// tile (one wave); the S fp32 partials are reduced through L2.
+//  * critical (dW1: nothing else runs beside it, Adam waits for it): tiles * S fills the 148 SMs;
+//  * background (dW2, dW3: they run on the second stream beside dX2 / dX3, which are on the critical path,
+//    and are needed only by Adam): at most 12 splits and 2/3 of the SMs, so that the dX kernel keeps most
+//    SMs while the weight gradient is accumulated alongside. Measured on one box (C3): 5.09 ms with every
+//    dW at 144 CTAs, 4.89 ms with dW2 at 96 CTAs and dW3 at 24 (S = 12 both); S = 6..16 per layer around
+//    that point are all slower; a k-block-based rule (>= 32 per CTA) slowed the smaller minibatches.
+static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn, bool background) {
   DwPlan p;
   p.rows = rows; p.N = N;
   p.bn = bn;
@@ -102,8 +108,12 @@ static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn) {
   // the same box (LG_DW_PAIR=0 switches them off)
   static const bool pair_env = [] { const char* e = getenv("LG_DW_PAIR"); return !(e && e[0] == '0'); }();
   p.pair = 0;
-  // one wave of <= 148 CTAs, and >= 8 k-blocks per CTA (the fp32 partial costs ~3 k-blocks of traffic)
-  const int S = std::max(1, std::min(std::max(1, p.kb_total / 8), 148 / std::max(1, p.tiles)));
+  // one wave of <= 148 CTAs (background: <= 98), and >= 8 (background: 32) k-blocks per CTA (the fp32
+  // partial costs ~3 k-blocks of traffic)
+  constexpr int BG_SPLITS = 12;
+  const int max_ctas = background ? 98 : 148;
+  int S = std::max(1, std::min(std::max(1, p.kb_total / 8), max_ctas / std::max(1, p.tiles)));
+  if (background) S = std::min(S, BG_SPLITS);
   p.kb_per_split = (p.kb_total + S - 1) / S;
   p.S = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
   if (pair_env && (p.m_tiles % 2 == 0) && p.bn >= 128) p.pair = 1;
@@ -115,9 +125,9 @@ static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn) {
 // -- then narrower tiles put more SMs on the same k-blocks. Modelled cost of
 // the busiest CTA: its operand bytes (the per-SM TMA rate bounds these GEMMs) + the split-K partial's round
 // trip through L2; the cheapest wins, ties to the wider tile.
-DwPlan dw_plan(int rows, int N, int K, int nz) {
+DwPlan dw_plan(int rows, int N, int K, int nz, bool background) {
   const int widest = N > 128 ? 256 : (N > 64 ? 128 : 64);
-  DwPlan best = dw_plan_bn(rows, N, K, nz, widest);
+  DwPlan best = dw_plan_bn(rows, N, K, nz, widest, background);
   // large minibatches keep the widest tiles: their splits already fill the SMs, and the dW chain shares
   // them with the concurrent dX chain (measured: narrower dW3 tiles cost ~2% of the C3 iteration)
   if (best.S >= 8 || best.tiles >= 148) return best;
@@ -125,7 +135,7 @@ DwPlan dw_plan(int rows, int N, int K, int nz) {
     return (double)p.kb_per_split * (128 * 64 * 2 + p.bn * 64 * 2) + (p.S > 1 ? 2.0 * 128 * (p.bn + 20) * 4 : 0.0);
   };
   for (int bn = widest / 2; bn >= 64; bn /= 2) {
-    const DwPlan q = dw_plan_bn(rows, N, K, nz, bn);
+    const DwPlan q = dw_plan_bn(rows, N, K, nz, bn, background);
     if (q.tiles * q.S <= 148 && cost(q) < 0.9 * cost(best)) best = q;
   }
   return best;
@@ -201,9 +211,9 @@ Layout layout_of(const Dims& d) {
   L.nblk_loss = loss_blocks(d.R);
   L.nblk_gae = gae_blocks(d.N);
   L.nblk_var = var_blocks(d.B);
-  L.dw1 = dw_plan(2 * d.H0, d.Dp, d.Mmb, 1);
-  L.dw2 = dw_plan(d.H1, d.H0, d.Mmb, 2);
-  L.dw3 = dw_plan(d.H2, d.H1, d.Mmb, 2);
+  L.dw1 = dw_plan(2 * d.H0, d.Dp, d.Mmb, 1, false);
+  L.dw2 = dw_plan(d.H1, d.H0, d.Mmb, 2, true);
+  L.dw3 = dw_plan(d.H2, d.H1, d.Mmb, 2, true);
   o = 0;
   L.k_sc = o; o = al(o + sizeof(DevScalars));
   L.k_gae = o; o = al(o + (size_t)L.nblk_gae * 8);
