@@ -1013,6 +1013,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
     CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork[k], 0));
     return LG_OK;
   };
+  // launch order inside a layer (measured, same box): dW3 before dX3, dX2 before dW2 (-0.3 %)
   // layer 3
   if ((s = fork(0)) != LG_OK) return s;
   if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
@@ -1021,10 +1022,10 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   if ((s = gemm(ctx, GEMM_DX, x3, ctx->bnx3, 2)) != LG_OK) return s;
   // layer 2
   if ((s = fork(1)) != LG_OK) return s;
-  if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   GemmArgs x2 = ctx->dx2;
   x2.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x2, ctx->bnx2, 2)) != LG_OK) return s;
+  if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
   if ((s = fork(2)) != LG_OK) return s;
   if ((s = dw(b ? ctx->dw1_b1 : ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
