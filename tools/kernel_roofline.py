@@ -5,8 +5,9 @@ usage: python tools/kernel_roofline.py REP [ROUND] > profiles/ROUND_roofline.md
 
 Achieved rates use ncu's serialised per-launch duration (clock-control none, caches flushed between
 launches, so DRAM bytes are cold-cache figures). GEMM FLOPs are the algorithmic 2*M*N*K of the launch,
-identified by its position in the minibatch (gather, L1, L2, L3, loss, reduce, dW3, dX3, dW2, dX2, dW1, adam)
-or in the post-rollout critic sequence. Peaks: MEASURED_PEAKS.json (bf16 sustained, HBM copy)."""
+identified by its position in the minibatch (gather, L1, L2, L3, loss, reduce, dW3, dX3, dX2, dW2, dW1,
+Adam + next gather); the GEMMs before the minibatch are the time-out bootstrap critic (V(o_T) is the fused
+policy kernel's critic half). Peaks: MEASURED_PEAKS.json (bf16 sustained, HBM copy)."""
 import csv
 import io
 import json
@@ -69,20 +70,19 @@ def main(rep, rnd="r01"):
         l2 = val(d, u, "lts__throughput.avg.pct_of_peak_sustained_elapsed")
         issue = val(d, u, "smsp__issue_active.avg.pct_of_peak_sustained_active")
         out.append(dict(name=name, grid=d["Grid Size"], t=t, dram=dram, tens=tens, l2=l2, issue=issue))
-    # label GEMMs by position: the minibatch starts after k_gather, the critic sequence before k_gae
+    # label GEMMs by position: the minibatch starts after k_gather
     labels = [""] * len(out)
     for i, e in enumerate(out):
         if e["name"].startswith("k_gather"):
-            order = ["L1", "L2", "L3", None, None, "dW3", "dX3", "dW2", "dX2", "dW1"]
+            order = ["L1", "L2", "L3", None, None, "dW3", "dX3", "dX2", "dW2", "dW1"]
             for k, lab in enumerate(order, start=1):
                 if i + k < len(out) and lab:
                     labels[i + k] = lab
             break
-    gem = [i for i, e in enumerate(out) if e["name"].startswith("k_gemm_tc") and not labels[i]]
-    for i, lab in zip(gem[-3:], ["cL1", "cL2", "cL3"]):
-        labels[i] = lab
-    for i in gem[:-3]:
-        labels[i] = "boot"
+    # GEMMs before the minibatch: the time-out bootstrap critic chain (V(o_T) runs in the fused policy kernel)
+    for i, e in enumerate(out):
+        if e["name"].startswith("k_gemm_tc") and not labels[i]:
+            labels[i] = "boot"
     print(f"# {rnd}: per-kernel roofline fractions (`ncu --set full --clock-control none`, one launch of each kernel)\n")
     print(f"Peaks: bf16 dense {tc_peak:.0f} TFLOP/s sustained, HBM {hbm_peak:.0f} GB/s ({src}). Durations are ncu's "
           "serialised, cold-cache launch times (shares agree with the bench's in-graph times; absolutes are higher).\n")
