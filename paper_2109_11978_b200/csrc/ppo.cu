@@ -786,14 +786,20 @@ __global__ void k_iter_end(IterEndArgs a, const float* acc) {
   __shared__ int hist[16];
   if (threadIdx.x < 16) hist[threadIdx.x] = 0;
   __syncthreads();
-  for (int i0 = 0; i0 < a.N; i0 += blockDim.x) {  // per warp: one ballot per level bin
-    const int i = i0 + (int)threadIdx.x;
-    const int lv = i < a.N ? min(max((int)a.state[(size_t)S_LEVEL * a.N + i], 0), 15) : -1;
+  for (int i0 = 0; i0 < a.N; i0 += 4 * blockDim.x) {  // 4 level loads in flight per thread, then one ballot per bin
+    int lv[4];
 #pragma unroll
-    for (int bnum = 0; bnum < 16; ++bnum) {
-      const int c = __popc(__ballot_sync(0xffffffffu, lv == bnum));
-      if ((threadIdx.x & 31) == 0 && c) atomicAdd(&hist[bnum], c);
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x + (int)threadIdx.x;
+      lv[u] = i < a.N ? min(max((int)__ldg(a.state + (size_t)S_LEVEL * a.N + i), 0), 15) : -1;
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int bnum = 0; bnum < 16; ++bnum) {
+        const int c = __popc(__ballot_sync(0xffffffffu, lv[u] == bnum));
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&hist[bnum], c);
+      }
   }
   __syncthreads();
   // the statistics fields are written by separate threads (independent loads, no serial chain through
@@ -836,7 +842,7 @@ __global__ void k_iter_end(IterEndArgs a, const float* acc) {
   }
 }
 void launch_iter_end(const IterEndArgs& a, const float* iter_acc, cudaStream_t st) {
-  k_iter_end<<<1, 256, 0, st>>>(a, iter_acc);
+  k_iter_end<<<1, 1024, 0, st>>>(a, iter_acc);
 }
 
 
