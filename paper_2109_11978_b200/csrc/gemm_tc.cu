@@ -249,6 +249,33 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const uint32_t
 struct TileCoord {
   int z, m0, n0, split, ntile;
 };
+
+// dX epilogue: the saved activation H (for ELU'(x) = min(H + 1, 1)) of a warp's 32 rows x 64 columns,
+// loaded with coalesced 16-B cp.async (8 lanes per 128-B row, 4 rows per instruction) into the warp's staging
+// buffer in the swizzled layout stage_row writes (chunk j of row r at r * 128 + ((j ^ (r & 7)) << 4)), then
+// read back row-per-lane. Thread-per-row global loads touch 32 lines per instruction; this touches 4.
+__device__ __forceinline__ void aux_issue(uint8_t* buf, const __nv_bfloat16* aux, int ld, int row0, int M, int nb,
+                                          int N, int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + (lane >> 3), ch = lane & 7;
+    const bool ok = row0 + r < M && nb + 8 * ch < N;
+    const __nv_bfloat16* src = aux + (size_t)(ok ? row0 + r : 0) * ld + (ok ? nb + 8 * ch : 0);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(buf + r * 128 + ((ch ^ (r & 7)) << 4))),
+                 "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void aux_read(const uint8_t* buf, uint32_t* av, int lane) {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 u = *reinterpret_cast<const uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+    av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
+  }
+}
 __device__ __forceinline__ TileCoord decode(const GemmArgs& a, int t, int m_tiles, int BN) {
   TileCoord c;
   c.ntile = t % a.n_tiles;
@@ -513,7 +540,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
         }
         __syncwarp();
       }
-      if (EPI == 2 && active) {
+      constexpr bool AUX_STAGED = EPI == 2 && C::EPI_NBUF == 2;
+      if (AUX_STAGED && active) {  // this tile's first chunk of H into the staging buffer it will be stored from
+        if (lane == 0) bulk_wait_read1();  // that buffer's previous store (two chunks ago) has been read out
+        __syncwarp();
+        aux_issue(mybuf + (nst & 1) * C::EPI_BUF, args.aux[tc.z], args.ld_aux, tc.m0 + q * 32, M, tc.n0 + h * WCOLS,
+                  args.N, lane);
+      }
+      if (EPI == 2 && !AUX_STAGED && active) {
         const int nb = tc.n0 + h * WCOLS;
         const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nb);
         if (row < M && nb + 64 <= args.N) {  // whole 64-column chunk in range (the common case)
@@ -584,6 +618,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
                 pk[k / 2 + 1] = *reinterpret_cast<uint32_t*>(&o1);
               }
             } else {
+              if (AUX_STAGED) {
+                aux_read(mybuf + (nst & 1) * C::EPI_BUF, av, lane);
+                if (c + 64 < (h + 1) * WCOLS) {  // the next chunk's H into the other buffer (its store is done)
+                  if (lane == 0) bulk_wait_read0();
+                  __syncwarp();
+                  aux_issue(mybuf + ((nst + 1) & 1) * C::EPI_BUF, args.aux[tc.z], args.ld_aux, tc.m0 + q * 32, M,
+                            nb + 64, args.N, lane);
+                }
+              }
 #pragma unroll
               for (int k = 0; k < 64; k += 2) {
                 const uint32_t* rr = k < 32 ? r0 : r1;
@@ -597,7 +640,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
                 pk[k / 2] = *reinterpret_cast<uint32_t*>(&o);
               }
             }
-            if (EPI == 2 && c + 64 < (h + 1) * WCOLS) {  // prefetch the next chunk's saved activation
+            if (EPI == 2 && !AUX_STAGED && c + 64 < (h + 1) * WCOLS) {  // prefetch the next chunk's saved activation
               const int nn = nb + 64;
               const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nn);
               if (row < M && nn + 64 <= args.N) {
@@ -615,9 +658,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
               }
             }
             uint8_t* buf = mybuf + (C::EPI_NBUF == 2 ? (nst & 1) * C::EPI_BUF : 0);
-            if (lane == 0) {
-              if (C::EPI_NBUF == 2) bulk_wait_read1();
-              else bulk_wait_read0();
+            if (!AUX_STAGED) {  // (staged H: the buffer was freed before its H was loaded, and H is consumed)
+              if (lane == 0) {
+                if (C::EPI_NBUF == 2) bulk_wait_read1();
+                else bulk_wait_read0();
+              }
             }
             __syncwarp();
             stage_row(buf, lane, pk);
