@@ -70,7 +70,15 @@ def lib():
         _lib.or_curriculum_level.restype = ctypes.c_int32
         _lib.or_feistel_perm.argtypes = [ctypes.c_uint32, u32p, u32p]
         _lib.or_leg_fk.argtypes = [ctypes.c_int, f32p, ctypes.c_float, f32p, ctypes.c_void_p]
+        _lib.or_terrain_generate.argtypes = [f32p, ctypes.c_int, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32]
     return _lib
+
+
+def terrain_generate(n_levels: int, n_cols: int, seed: int) -> np.ndarray:
+    """The world heightfield [80 L][80 C] fp32 of DESIGN.md §3.12 (reading R27)."""
+    hf = np.zeros((80 * n_levels, 80 * n_cols), np.float32)
+    lib().or_terrain_generate(hf, n_levels, n_cols, seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    return hf
 
 
 def _ptr(a):

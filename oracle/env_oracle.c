@@ -619,3 +619,65 @@ void or_transition(const or_env_cfg* cfg, const float* hf, or_state* st, const f
   transition_one(cfg, hf, st, a, g, s, qstar, tau, qdd, airsum, crash, n_c);
   *fz = g_last_fz;
 }
+
+/* ---------------- DESIGN.md §3.12  terrain generation (NEXT-4; reading R27) ----------------
+ * The world of n_levels x n_cols tiles of 80 x 80 cells (8 m at 0.1 m): level l
+ * along x (rows), column c along y; kind = c mod 5 (0 flat, 1 slope pyramid, 2 rough, 3 obstacles, 4 stairs
+ * pyramid); difficulty d = l / (L - 1) (0 when L = 1). Written out cell by cell, in the definition's order.
+ * Random words: Philox key = seed, counter (w / 4, tile id l * n_cols + c, 0, tag 8), word w mod 4. */
+#define OR_TAG_TERRAIN 8u
+static uint32_t terrain_word(uint32_t k0, uint32_t k1, uint32_t tile, uint32_t w) {
+  uint32_t ctr[4] = {w / 4u, tile, 0u, OR_TAG_TERRAIN}, out[4];
+  or_philox(k0, k1, ctr, out);
+  return out[w % 4u];
+}
+
+void or_terrain_generate(float* hf, int n_levels, int n_cols, uint32_t seed_lo, uint32_t seed_hi) {
+  const int C = n_cols * 80;
+  for (int l = 0; l < n_levels; ++l) {
+    const float d = n_levels > 1 ? (float)l / (float)(n_levels - 1) : 0.0f;
+    /* slope: tan(25 deg * d), evaluated in double and rounded once */
+    const float slope = (float)tan(25.0 * (3.14159265358979323846 / 180.0) * (double)d);
+    const float rough_half = 0.5f * (0.05f * (1.0f + d)); /* rough: U(-a/2, a/2), a = 0.05 (1 + d) */
+    const float hmax = 0.05f + 0.15f * d;                 /* obstacle heights U(-hmax, hmax) */
+    const float riser = 0.05f + 0.15f * d;                /* stair riser */
+    for (int c = 0; c < n_cols; ++c) {
+      const int kind = c % 5;
+      const uint32_t tile = (uint32_t)(l * n_cols + c);
+      /* obstacles: 8 boxes, words 5b .. 5b+4 = width, length, x0, y0, height */
+      int bi0[8], bi1[8], bj0[8], bj1[8];
+      float bh[8];
+      for (int b = 0; b < 8; ++b) {
+        const float w = 0.5f + 1.5f * u01(terrain_word(seed_lo, seed_hi, tile, 5u * b + 0u));
+        const float len = 0.5f + 1.5f * u01(terrain_word(seed_lo, seed_hi, tile, 5u * b + 1u));
+        const float x0 = 8.0f * u01(terrain_word(seed_lo, seed_hi, tile, 5u * b + 2u));
+        const float y0 = 8.0f * u01(terrain_word(seed_lo, seed_hi, tile, 5u * b + 3u));
+        bh[b] = usym(hmax, terrain_word(seed_lo, seed_hi, tile, 5u * b + 4u));
+        bi0[b] = (int)(x0 * 10.0f);
+        bi1[b] = (int)(fminf(8.0f, x0 + w) * 10.0f);
+        bj0[b] = (int)(y0 * 10.0f);
+        bj1[b] = (int)(fminf(8.0f, y0 + len) * 10.0f);
+      }
+      for (int i = 0; i < 80; ++i) {
+        for (int j = 0; j < 80; ++j) {
+          const float xc = (float)(2 * i + 1) * 0.05f, yc = (float)(2 * j + 1) * 0.05f; /* cell centre */
+          const float e = fminf(fminf(xc, 8.0f - xc), fminf(yc, 8.0f - yc));           /* to the border */
+          const float ep = fminf(e, 3.0f);                                              /* 2 m plateau */
+          float h = 0.0f;
+          if (kind == 1) {
+            h = slope * ep;
+          } else if (kind == 2) {
+            h = usym(rough_half, terrain_word(seed_lo, seed_hi, tile, (uint32_t)(i * 80 + j)));
+          } else if (kind == 3) {
+            for (int b = 0; b < 8; ++b)
+              if (i >= bi0[b] && i < bi1[b] && j >= bj0[b] && j < bj1[b]) h = bh[b];
+            if (e >= 3.0f) h = 0.0f;
+          } else if (kind == 4) {
+            h = riser * floorf(ep / 0.3f);
+          }
+          hf[(size_t)(l * 80 + i) * C + (size_t)(c * 80 + j)] = h;
+        }
+      }
+    }
+  }
+}
