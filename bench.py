@@ -112,8 +112,8 @@ def measured_traffic(cat):
         except (OSError, ValueError):
             continue
         if d.get("kernel") == CAT_KERNEL.get(cat):
-            return {"bytes_per_launch": d["traffic_bytes_per_launch"], "source": "profiles/" + os.path.basename(f)}
-    return None
+            return d["traffic_bytes_per_launch"], "profiles/" + os.path.basename(f)
+    return None, None
 
 
 def algorithmic(cfg, w):
@@ -296,8 +296,7 @@ def main():
     if dom in gemm_cats:
         ach = alg[dom] / (per_iter[dom]["ms"] * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": f"tcgen05 GEMM ({dom})", "achieved": ach, "peak": pk["bf16_sus"],
-                "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"], "traffic": measured_traffic(dom),
-                "peak_src": pk["src"] + " bf16 sustained"}
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"], "peak_src": pk["src"] + " bf16 sustained"}
     else:
         if dom == "env":
             nb = alg["env_bytes_per_step"] * cfg.n_steps
@@ -305,7 +304,8 @@ def main():
             nb = None
         ach = (nb / (per_iter[dom]["ms"] * 1e-3) / 1e9) if nb else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm"], "unit": "GB/s",
-                "frac": (ach / pk["hbm"]) if ach else None, "traffic": measured_traffic(dom), "peak_src": pk["src"]}
+                "frac": (ach / pk["hbm"]) if ach else None, "peak_src": pk["src"]}
+    roof["traffic"], roof["traffic_src"] = measured_traffic(dom)  # DRAM bytes per launch (ncu --set full) or None
     roof["all_gemms"] = {"achieved": gflops / (gms * 1e-3) / 1e12 if gms else None, "unit": "TFLOP/s",
                          "frac": (gflops / (gms * 1e-3) / 1e12) / pk["bf16_sus"] if gms else None}
     roof["step_roofline_ms"] = alg["total_flops"] / (pk["bf16_sus"] * 1e12) * 1e3

@@ -196,6 +196,19 @@ lg_status lg_set_nccl(lg_ctx* ctx, const uint8_t id_h[128]);
 /* Broadcast θ from rank 0 (then lg_params_sync semantics). */
 lg_status lg_broadcast_params(lg_ctx* ctx);
 
+/* --- World generation (reading R27) --- */
+/* Writes the tiled world heightfield into HEIGHTFIELD (device, fp32 [80*n_levels][80*n_cols], row-major;
+ * level l along x = rows, column c along y), enqueued on `stream` (a cudaStream_t; NULL = legacy default):
+ * 8 m x 8 m tiles of 0.1 m cells, terrain kind = c mod 5 -- flat, slope pyramid (gradient
+ * tan(25 deg * d)), rough (U(+-a/2), a = 0.05 (1 + d)), 8 random box obstacles (heights U(+-(0.05 + 0.15 d)),
+ * 2 m x 2 m flat spawn plateau), stairs pyramid (0.3 m treads, riser 0.05 + 0.15 d) -- with difficulty
+ * d = l / (n_levels - 1) rising along the curriculum's level axis (Fig. 2 caption P:62).
+ * Random draws: Philox key = seed, counter (word / 4, tile id l * n_cols + c, 0, 8). Bit-identical to the
+ * oracle's definition. Context-free (generate before lg_create, which borrows the buffer read-only).
+ * Errors: LG_ERR_INVALID_ARG (null buffer, n_levels or n_cols < 1), LG_ERR_RANGE (n_levels > 64),
+ * LG_ERR_UNSUPPORTED (no sm_100 device), LG_ERR_CUDA (launch failure). */
+lg_status lg_terrain_generate(float* heightfield, int32_t n_levels, int32_t n_cols, uint64_t seed, void* stream);
+
 /* --- Whole iteration through host buffers (end-to-end metric) --- */
 /* Copies the 16-byte control block ctrl_h (reserved, zeros) to the device, runs one full iteration,
  * copies lg_update_stats back into stats_h and synchronises the stream. */

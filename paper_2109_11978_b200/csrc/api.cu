@@ -1166,6 +1166,28 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
 }
 
 // ------------------------------------------------------------------ multi-GPU
+lg_status lg_terrain_generate(float* heightfield, int32_t n_levels, int32_t n_cols, uint64_t seed, void* stream) {
+  if (!heightfield || n_levels < 1 || n_cols < 1) return LG_ERR_INVALID_ARG;
+  if (n_levels > TERRAIN_MAX_LEVELS) return LG_ERR_RANGE;
+  {
+    int dev = 0;
+    cudaDeviceProp prop;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
+      return LG_ERR_UNSUPPORTED;
+  }
+  TerrainArgs t;
+  memset(&t, 0, sizeof(t));
+  t.hf = heightfield;
+  t.n_levels = n_levels; t.n_cols = n_cols;
+  t.seed_lo = (uint32_t)(seed & 0xFFFFFFFFu); t.seed_hi = (uint32_t)(seed >> 32);
+  for (int l = 0; l < n_levels; ++l) {  // slope pyramid gradient tan(25 deg * d_l), in double, rounded once
+    const float d = n_levels > 1 ? (float)l / (float)(n_levels - 1) : 0.0f;
+    t.slope[l] = (float)tan(25.0 * (3.14159265358979323846 / 180.0) * (double)d);
+  }
+  launch_terrain(t, reinterpret_cast<cudaStream_t>(stream));
+  return cudaGetLastError() == cudaSuccess ? LG_OK : LG_ERR_CUDA;
+}
+
 lg_status lg_nccl_unique_id(uint8_t id_h[128]) {
   if (!id_h) return LG_ERR_INVALID_ARG;
   ncclUniqueId id;

@@ -9,7 +9,8 @@ namespace lg {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 constexpr int NW = 66;  // state words per env
-constexpr uint32_t TAG_RESET = 1u, TAG_OBS = 2u, TAG_ACTION = 3u, TAG_PUSH = 4u, TAG_CURR = 5u, TAG_SHUFFLE = 6u;
+constexpr uint32_t TAG_RESET = 1u, TAG_OBS = 2u, TAG_ACTION = 3u, TAG_PUSH = 4u, TAG_CURR = 5u, TAG_SHUFFLE = 6u,
+                   TAG_TERRAIN = 8u;
 constexpr uint32_t F_CURRICULUM = 1u, F_NOISE = 2u, F_PUSH = 4u, F_BOOTSTRAP = 8u;
 
 // state word indices

@@ -707,7 +707,61 @@ __global__ void k_action_eps(int N, int rank, uint32_t seed_lo, uint32_t seed_hi
   action_eps(rng, (uint32_t)(rank * N + i), sc->s_base + (uint32_t)t + 1u, eps + (size_t)i * 12);
 }
 
+// World heightfield (reading R27): block (i, c, l) writes row i
+// of tile (level l, column c), one thread per cell j; the obstacle boxes of the tile (10 Philox blocks) are
+// drawn once per block into shared memory. fp32 with explicit rounding (this file is built -fmad=false).
+__global__ void __launch_bounds__(128) k_terrain(const __grid_constant__ TerrainArgs a) {
+  const int i = blockIdx.x, c = blockIdx.y, l = blockIdx.z, j = threadIdx.x;
+  const int kind = c % 5;
+  const uint32_t tile = (uint32_t)(l * a.n_cols + c);
+  const Rng rng{a.seed_lo, a.seed_hi};
+  const float d = a.n_levels > 1 ? __fdiv_rn((float)l, (float)(a.n_levels - 1)) : 0.0f;
+  __shared__ int bi0[8], bi1[8], bj0[8], bj1[8];
+  __shared__ float bh[8];
+  if (kind == 3 && j < 8) {  // box b = j: words 5b .. 5b+4 = width, length, x0, y0, height
+    uint32_t w[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t wi = 5u * (uint32_t)j + (uint32_t)k;
+      w[k] = pick(rng.block(wi >> 2, tile, 0u, TAG_TERRAIN), wi);
+    }
+    const float wd = __fadd_rn(0.5f, __fmul_rn(1.5f, u01(w[0])));
+    const float ln = __fadd_rn(0.5f, __fmul_rn(1.5f, u01(w[1])));
+    const float x0 = __fmul_rn(8.0f, u01(w[2]));
+    const float y0 = __fmul_rn(8.0f, u01(w[3]));
+    bh[j] = usym(__fadd_rn(0.05f, __fmul_rn(0.15f, d)), w[4]);
+    bi0[j] = (int)__fmul_rn(x0, 10.0f);
+    bi1[j] = (int)__fmul_rn(fminf(8.0f, __fadd_rn(x0, wd)), 10.0f);
+    bj0[j] = (int)__fmul_rn(y0, 10.0f);
+    bj1[j] = (int)__fmul_rn(fminf(8.0f, __fadd_rn(y0, ln)), 10.0f);
+  }
+  __syncthreads();
+  if (j >= 80) return;
+  const float xc = __fmul_rn((float)(2 * i + 1), 0.05f), yc = __fmul_rn((float)(2 * j + 1), 0.05f);
+  const float e = fminf(fminf(xc, __fsub_rn(8.0f, xc)), fminf(yc, __fsub_rn(8.0f, yc)));
+  const float ep = fminf(e, 3.0f);
+  float h = 0.0f;
+  if (kind == 1) {
+    h = __fmul_rn(a.slope[l], ep);
+  } else if (kind == 2) {
+    const uint32_t wi = (uint32_t)(i * 80 + j);
+    const float half = __fmul_rn(0.5f, __fmul_rn(0.05f, __fadd_rn(1.0f, d)));
+    h = usym(half, pick(rng.block(wi >> 2, tile, 0u, TAG_TERRAIN), wi));
+  } else if (kind == 3) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (i >= bi0[b] && i < bi1[b] && j >= bj0[b] && j < bj1[b]) h = bh[b];
+    if (e >= 3.0f) h = 0.0f;
+  } else if (kind == 4) {
+    h = __fmul_rn(__fadd_rn(0.05f, __fmul_rn(0.15f, d)), floorf(__fdiv_rn(ep, 0.3f)));
+  }
+  a.hf[(size_t)(l * 80 + i) * (size_t)(a.n_cols * 80) + (size_t)(c * 80 + j)] = h;
+}
+
 // ------------------------------------------------------------------ launchers
+void launch_terrain(const TerrainArgs& a, cudaStream_t st) {
+  k_terrain<<<dim3(80, a.n_cols, a.n_levels), 128, 0, st>>>(a);
+}
 void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* obs_f32, cudaStream_t st) {
   int nb = (P.N + ENV_BLOCK - 1) / ENV_BLOCK;
   k_env_reset<<<nb, ENV_BLOCK, 0, st>>>(P, mask, init);

@@ -57,6 +57,15 @@ struct EnvParams {
 void launch_env_reset(const EnvParams& P, const uint8_t* mask, int init, float* obs_f32, cudaStream_t st);
 void launch_env_step(const EnvParams& P, int t, const float* actions, float* obs_f32, float* rew, uint8_t* term,
                      uint8_t* to, float* terms, cudaStream_t st);
+// world heightfield (reading R27): fp32 [80 L][80 C]; slope[l] = fp32(tan(25 deg * d_l))
+constexpr int TERRAIN_MAX_LEVELS = 64;
+struct TerrainArgs {
+  float* hf;
+  int n_levels, n_cols;
+  uint32_t seed_lo, seed_hi;
+  float slope[TERRAIN_MAX_LEVELS];
+};
+void launch_terrain(const TerrainArgs& a, cudaStream_t st);
 void launch_curriculum(int n, int n_levels, const uint8_t* crossed, const float* disp, const float* cmd,
                        const int32_t* ep, const uint32_t* words, int32_t* level, cudaStream_t st);
 void launch_action_eps(int N, int rank, uint32_t s0, uint32_t s1, const DevScalars* sc, int t, float* eps,

@@ -51,7 +51,8 @@ EXPORTS = ["lg_num_params", "lg_obs_dim", "lg_obs_stride", "lg_required_sizes", 
            "lg_last_error", "lg_params_set", "lg_params_sync", "lg_resume", "env_reset", "env_step_obs_reward", "policy_act",
            "policy_forward", "storage_compute_gae", "ppo_update", "ppo_shuffle", "ppo_minibatch_grad", "curriculum_update",
            "lg_nccl_unique_id", "lg_set_nccl", "lg_broadcast_params", "lg_iterate_host",
-           "lg_graph_capture_iteration", "lg_graph_launch", "lg_device_scalars", "lg_profile", "lg_profile_read", "lg_graph_kernel_count"]
+           "lg_graph_capture_iteration", "lg_graph_launch", "lg_device_scalars", "lg_profile", "lg_profile_read", "lg_graph_kernel_count",
+           "lg_terrain_generate"]
 PROF_CATS = ["env", "gemm_roll", "gemm_fwd", "gemm_dx", "gemm_dw", "heads", "loss", "reduce", "gather", "adam", "gae",
              "comm", "misc"]
 
@@ -91,6 +92,7 @@ _sig = {
     "lg_profile": (I32, [P, I32]),
     "lg_graph_kernel_count": (I32, [P, ctypes.POINTER(I32)]),
     "lg_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32]),
+    "lg_terrain_generate": (I32, [P, I32, I32, ctypes.c_uint64, P]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -128,6 +130,14 @@ def lg_obs_dim(cfg):
 
 def lg_obs_stride(cfg):
     return _lib.lg_obs_stride(ctypes.byref(cfg))
+
+
+def lg_terrain_generate(hf, n_levels, n_cols, seed, stream=None):
+    """World heightfield into the fp32 device tensor hf [80 L][80 C] (include/lg.h)."""
+    if tuple(hf.shape) != (80 * n_levels, 80 * n_cols) or not hf.is_contiguous() or str(hf.dtype) != "torch.float32":
+        raise LgError("lg_terrain_generate: hf must be a contiguous fp32 [80 L][80 C] device tensor")
+    check(_lib.lg_terrain_generate(_p(hf), n_levels, n_cols, seed & 0xFFFFFFFFFFFFFFFF, stream), None,
+          "lg_terrain_generate")
 
 
 def lg_required_sizes(cfg):

@@ -72,3 +72,14 @@ def test_create_without_gpu_fails_loudly(lgmod):
     bufs = [256 * (i + 1) for i in range(lgmod.NUM_BUFFERS)]  # fake aligned addresses; never dereferenced
     st, ctx = lgmod.lg_create(_cfg(lgmod), bufs, 0)
     assert st == 7  # LG_ERR_UNSUPPORTED: no silent CPU fallback
+
+
+def test_terrain_generate_validation_and_no_cpu_fallback(lgmod):
+    import torch
+    f = lgmod._lib.lg_terrain_generate
+    assert f(None, 10, 20, 0, None) == 1          # LG_ERR_INVALID_ARG: no buffer
+    assert f(4096, 0, 20, 0, None) == 1           # no levels
+    assert f(4096, 10, 0, 0, None) == 1           # no columns
+    assert f(4096, 65, 20, 0, None) == 2          # LG_ERR_RANGE: more levels than the kernel's slope table
+    if not torch.cuda.is_available():
+        assert f(4096, 10, 20, 0, None) == 7      # LG_ERR_UNSUPPORTED: no device, no CPU fallback

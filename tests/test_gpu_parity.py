@@ -57,6 +57,39 @@ def close_mixed(a, b, tol):
     return np.all(np.abs(a - b) <= tol * np.maximum(np.abs(b), 1.0))
 
 
+# ------------------------------------------------------------------ world generation (bit-exact)
+@pytest.mark.parametrize("levels,cols,seed", [(10, 20, 0), (2, 7, (1 << 40) + 5), (1, 3, 9)])
+def test_terrain_generate_bit_exact(levels, cols, seed):
+    hf = torch.full((80 * levels, 80 * cols), float("nan"), device="cuda")
+    lg.lg_terrain_generate(hf, levels, cols, seed)
+    torch.cuda.synchronize()
+    assert np.array_equal(hf.cpu().numpy(), oracle.terrain_generate(levels, cols, seed))
+
+
+def test_terrain_world_runs_through_the_path():
+    """A generated world serves as the env's heightfield: a short teacher-forced rollout stays bit-exact."""
+    levels, cols = 4, 5
+    hf_g = torch.empty((80 * levels, 80 * cols), device="cuda")
+    lg.lg_terrain_generate(hf_g, levels, cols, 21)
+    torch.cuda.synchronize()
+    hf = hf_g.cpu().numpy()
+    cfg = Config.make(n_envs=96, n_steps=8, scan_nx=17, scan_ny=11, n_levels=levels, n_cols=cols, flags=ALL, seed=4)
+    ctx = Context(cfg, hf)
+    ctx.params_set(synth.init_params(cfg.obs_dim, cfg.hidden, seed=4))
+    env = oracle.Env(96, hf, levels, cols, seed=4, flags=ALL)
+    obs_g = torch.zeros(96, cfg.obs_dim, device="cuda")
+    ctx.reset(obs=obs_g)
+    assert np.array_equal(obs_g.cpu().numpy(), env.reset())
+    rng = np.random.default_rng(2)
+    for t in range(8):
+        a = (0.5 * rng.standard_normal((96, 12))).astype(np.float32)
+        ctx.env_step(t, actions=torch.from_numpy(a).cuda(), obs=obs_g)
+        o = env.step(a)[0]
+        ctx.sync()
+        assert np.array_equal(o, obs_g.cpu().numpy()), t
+    assert gpu_state(ctx).tobytes() == env.state.tobytes()
+
+
 # ------------------------------------------------------------------ environment (bit-exact)
 @pytest.mark.parametrize("scan,rough,flags", [((17, 11), True, ALL), ((0, 0), False, ALL & ~lg.F_CURRICULUM)])
 def test_env_teacher_forced_bit_exact(scan, rough, flags):
