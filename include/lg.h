@@ -51,6 +51,10 @@ typedef enum {
 #define LG_F_NOISE 2u      /* observation noise (Table 4) */
 #define LG_F_PUSH 4u       /* pushes every 10 s */
 #define LG_F_BOOTSTRAP 8u  /* time-out bootstrapping */
+/* evaluation: policy_act takes the mean action a = mu (no Gaussian draw; logp is evaluated at a = mu) --
+ * the deterministic policy of the traversability tests ("robustness and traversability tests";
+ * SURVEY §8(f) NEXT-4) */
+#define LG_F_DETERMINISTIC 32u
 /* implementation switch (diagnostics/parity): policy_act uses the per-layer GEMM + head kernels instead of the
  * fused rollout-policy kernel (same results bit for bit; only the 512-256-128 MLP has a fused kernel) */
 #define LG_F_UNFUSED_POLICY 256u

@@ -816,6 +816,7 @@ static FusedPolicyArgs fused_args(lg_ctx* ctx, int t) {
   fa.W4a = at<float>(W, ctx->L.w_W4a); fa.b4a = at<float>(W, ctx->L.w_b4a);
   fa.W4c = at<float>(W, ctx->L.w_W4c); fa.b4c = at<float>(W, ctx->L.w_b4c); fa.logstd = at<float>(W, ctx->L.w_ls);
   fa.N = d.N; fa.rank = ctx->cfg.rank; fa.t = t; fa.kb1 = (d.Dp + 63) / 64;
+  fa.deterministic = (ctx->cfg.flags & LG_F_DETERMINISTIC) ? 1 : 0;
   fa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); fa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
   fa.scalars = ctx->sc;
   return fa;
@@ -841,6 +842,7 @@ lg_status policy_act(lg_ctx* ctx, int32_t t, float* actions, float* logp, float*
   if (s != LG_OK) return s;
   HeadArgs h = head_args(ctx, d.N);
   h.mode = 0;
+  h.deterministic = (ctx->cfg.flags & LG_F_DETERMINISTIC) ? 1 : 0;
   h.t = t;
   h.act = reinterpret_cast<float*>(ctx->buf[LG_BUF_ACT]) + (size_t)t * d.N * 12;
   h.mu = reinterpret_cast<float*>(ctx->buf[LG_BUF_MU]) + (size_t)t * d.N * 12;

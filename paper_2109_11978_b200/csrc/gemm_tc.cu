@@ -1566,7 +1566,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
           const float mu = __fadd_rn(tot[j] + other, __ldg(a.b4a + j));
           const float ls = __ldg(a.logstd + j);
           const bool first = (j >> 2) == (hs == 0 ? 0 : 1);
-          const float act = sample_action_b(first ? blk0 : blk1, j, mu, ls);
+          const float act = a.deterministic ? mu : sample_action_b(first ? blk0 : blk1, j, mu, ls);
           tm[jj] = logp_term(act, mu, ls);
           a.act[(size_t)row * 12 + j] = act;
           a.mu[(size_t)row * 12 + j] = mu;

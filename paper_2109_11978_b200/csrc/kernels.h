@@ -135,6 +135,7 @@ struct FusedPolicyArgs {
   const float* W4a; const float* b4a; const float* W4c; const float* b4c; const float* logstd;
   int N, rank, t, kb1;       // kb1 = K-blocks of layer 1 (Dp / 64 rounded up, <= 4)
   int z0;                    // first net: 0 = actor and critic (grid.y = 2), 1 = critic only (V(o_T))
+  int deterministic;         // a = mu (LG_F_DETERMINISTIC, evaluation)
   uint32_t seed_lo, seed_hi;
   const DevScalars* scalars;
   float* act; float* mu; float* logp; float* value;              // storage slot t
@@ -160,6 +161,7 @@ struct HeadArgs {
   const int* M_dev;          // optional device row count
   // ACT mode
   int mode;                  // 0 = act (sample), 1 = value scatter, 2 = forward (mu, V)
+  int deterministic;         // mode 0: a = mu (LG_F_DETERMINISTIC, evaluation)
   int t, N, rank;
   uint32_t seed_lo, seed_hi;
   const DevScalars* scalars;

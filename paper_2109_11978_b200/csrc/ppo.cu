@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) k_heads(HeadArgs a) {
     float act = 0.0f;
     if (dl) {
       Rng rng{a.seed_lo, a.seed_hi};
-      act = sample_action(rng, (uint32_t)(a.rank * a.N + r), a.scalars->s_base + (uint32_t)a.t + 1u, j, tot, ls);
+      act = a.deterministic ? tot
+                            : sample_action(rng, (uint32_t)(a.rank * a.N + r), a.scalars->s_base + (uint32_t)a.t + 1u,
+                                            j, tot, ls);
     }
     const float lp = logp_warp(act, tot, ls, lane);
     const size_t o = (size_t)r * 12 + j;

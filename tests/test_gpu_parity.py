@@ -275,6 +275,28 @@ def test_fused_policy_bit_identical_to_unfused(n_envs):
         assert outs[0][k].tobytes() == outs[1][k].tobytes(), k
 
 
+def test_deterministic_policy_takes_the_mean_action():
+    """LG_F_DETERMINISTIC (evaluation, NEXT-4): a = mu on both policy paths; the first step's mu equals the
+    stochastic policy's (same weights, same reset), and logp is the density at the mean, -(sum ls + 6 ln 2pi)."""
+    mus = []
+    for extra in (lg.F_DETERMINISTIC, lg.F_DETERMINISTIC | lg.F_UNFUSED_POLICY, 0):
+        cfg, ctx, env, theta = make(n_envs=300, T=2, flags=lg.F_NOISE | extra)
+        ctx.reset()
+        ctx.policy_act(0)
+        ctx.sync()
+        act = ctx.storage("ACT", extra=(12,))[0].cpu().numpy()
+        mu = ctx.storage("MU", extra=(12,))[0].cpu().numpy()
+        if extra:
+            assert np.array_equal(act, mu)
+            lp = ctx.storage("LOGP")[0].cpu().numpy()
+            ls = theta[-12:].astype(np.float64)
+            assert np.allclose(lp, -(ls.sum() + 6.0 * np.log(2.0 * np.pi)), rtol=1e-6, atol=1e-5)
+        else:
+            assert not np.array_equal(act, mu)
+        mus.append(mu)
+    assert mus[0].tobytes() == mus[1].tobytes() == mus[2].tobytes()
+
+
 # ------------------------------------------------------------------ GAE (fp32 vs fp64 oracle)
 def _rollout(ctx, cfg):
     ctx.reset()
