@@ -125,8 +125,15 @@ def algorithmic(cfg, w):
     E = 5
     f_fwd = 2 * 2 * (D * H0 + H0 * H1 + H1 * H2)          # hidden layers, actor + critic, per sample
     f_dx = 2 * 2 * (H0 * H1 + H1 * H2)                     # input gradients of layers 2, 3
+    Dp = (D + 7) // 8 * 8
+    # bf16 operand bytes per sample that the update GEMMs must read and write (activations H_l and
+    # gradients dZ_l of both nets; weights and fp32 partials are not counted)
+    b_fwd = 2 * (Dp + 2 * H0 + 2 * H1) + 2 * (2 * H0 + 2 * H1 + 2 * H2)
+    b_dx = 2 * (2 * H2 + 2 * H1 + 2 * H1) + 2 * (2 * H1 + 2 * H0 + 2 * H0)
+    b_dw = 2 * ((Dp + 2 * H0) + (2 * H0 + 2 * H1) + (2 * H1 + 2 * H2))
     return dict(gemm_roll=T * N * f_fwd + N * f_fwd / 2, gemm_fwd=E * B * f_fwd, gemm_dw=E * B * f_fwd,
                 gemm_dx=E * B * f_dx,
+                bytes_gemm_fwd=E * B * b_fwd, bytes_gemm_dx=E * B * b_dx, bytes_gemm_dw=E * B * b_dw,
                 env_bytes_per_step=N * (66 * 4 * 2 + 48 + (D + 7) // 8 * 8 * 2 + 9 + (216 + 36) * 4),
                 total_flops=T * N * f_fwd + N * f_fwd / 2 + E * B * (2 * f_fwd + f_dx))
 
@@ -295,8 +302,21 @@ def main():
     gms = sum(per_iter.get(k, {"ms": 0})["ms"] for k in gemm_cats)
     if dom in gemm_cats:
         ach = alg[dom] / (per_iter[dom]["ms"] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": f"tcgen05 GEMM ({dom})", "achieved": ach, "peak": pk["bf16_sus"],
-                "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"], "peak_src": pk["src"] + " bf16 sustained"}
+        tensor = {"bound": "tensor", "kernel": f"tcgen05 GEMM ({dom})", "achieved": ach, "peak": pk["bf16_sus"],
+                  "unit": "TFLOP/s", "frac": ach / pk["bf16_sus"], "peak_src": pk["src"] + " bf16 sustained"}
+        roof = tensor
+        if "bytes_" + dom in alg:
+            # the same launches against the HBM roofline: their bf16 activation / gradient operands (175 MB per
+            # minibatch at C3) exceed the 126 MB L2, and moving them takes longer at peak HBM bandwidth than the
+            # FLOPs take at peak tensor rate -- the binding roofline is the primary one, the other is kept
+            gbs = alg["bytes_" + dom] / (per_iter[dom]["ms"] * 1e-3) / 1e9
+            hbm = {"bound": "hbm", "kernel": f"tcgen05 GEMM ({dom})", "achieved": gbs, "peak": pk["hbm"],
+                   "unit": "GB/s", "frac": gbs / pk["hbm"], "peak_src": pk["src"] + " HBM copy",
+                   "algorithmic_bytes_per_iter": alg["bytes_" + dom]}
+            if alg["bytes_" + dom] / (pk["hbm"] * 1e9) > alg[dom] / (pk["bf16_sus"] * 1e12):
+                roof = dict(hbm, tensor_view={k: tensor[k] for k in ("achieved", "peak", "unit", "frac")})
+            else:
+                roof = dict(tensor, hbm_view={k: hbm[k] for k in ("achieved", "peak", "unit", "frac")})
     else:
         if dom == "env":
             nb = alg["env_bytes_per_step"] * cfg.n_steps
