@@ -427,10 +427,14 @@ def test_ppo_update_parameter_drift_vs_oracle():
 
 
 # ------------------------------------------------------------------ whole iteration, graph replay
-def test_iteration_graph_replay_matches_eager():
+@pytest.mark.parametrize("n_envs,T,levels,cols", [(256, 8, 4, 5), (4096, 24, 10, 20), (16384, 50, 10, 20)])
+def test_iteration_graph_replay_matches_eager(n_envs, T, levels, cols):
+    """The launch configuration bench.py times (one CUDA graph per iteration, dW on the second stream) gives
+    the same bits as the eager C-ABI calls, at a small size, at the full C3 size (4096 x 24) and at the
+    sweep's largest batch (16384 x 50)."""
     cfgs = []
     for mode in ("eager", "graph"):
-        cfg, ctx, env, theta = make(n_envs=256, T=8, seed=21)
+        cfg, ctx, env, theta = make(n_envs=n_envs, T=T, seed=21, levels=levels, cols=cols)
         ctx.reset()
         if mode == "eager":
             for _ in range(3):
