@@ -664,10 +664,14 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
 constexpr int ADAM_PER_THREAD = ADAM_BLOCK_ELEMS / 256;
 __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payload, float kl_target, int world, int m,
                                           float* acc, int bid) {
-  __shared__ float s_alpha, s_bc1, s_bc2;
+  __shared__ float s_step, s_ibc2;
   __shared__ int s_apply;
-  int sg = 0;
-  while (sg + 1 < a.sh.nseg && bid >= a.sh.blk0[sg + 1]) ++sg;  // block-uniform
+  int sg = 0;  // the block's segment: the last sg with blk0[sg] <= bid (block-uniform binary search)
+  for (int hi = a.sh.nseg - 1; sg < hi;) {
+    const int mid = (sg + hi + 1) >> 1;
+    if (a.sh.blk0[mid] <= bid) sg = mid;
+    else hi = mid - 1;
+  }
   const Segment& G = a.sh.seg[sg];
   const int n = G.rows * G.cols;
   const int l0 = (bid - a.sh.blk0[sg]) * ADAM_BLOCK_ELEMS + threadIdx.x;
@@ -692,9 +696,11 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payloa
       t = t + 1;
     }
     s_apply = bad ? 0 : 1;
-    s_alpha = alpha;
-    s_bc1 = sc->bc_ring[m & 1][0];  // 1 - b^t for the applied step t (written by the previous Adam / iter_begin)
-    s_bc2 = sc->bc_ring[m & 1][1];
+    // alpha * m_hat / (sqrt(v_hat) + eps) = (alpha / bc1) * m / (sqrt(v / bc2) + eps), bc = 1 - b^t of the
+    // applied step t (written by the previous Adam / iter_begin): the per-block scalars, one division left
+    // per element
+    s_step = alpha / sc->bc_ring[m & 1][0];
+    s_ibc2 = 1.0f / sc->bc_ring[m & 1][1];
     if (bid == 0) {
       sc->alpha_ring[(m + 1) & 1] = alpha;
       sc->adamt_ring[(m + 1) & 1] = t;
@@ -711,7 +717,8 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payloa
   }
   __syncthreads();
   if (!s_apply) return;
-  const float alpha = s_alpha, bc1 = s_bc1, bc2 = s_bc2;
+  const float step = s_step, ibc2 = s_ibc2;
+  const bool dense = G.dst_ld == G.cols;  // shadow rows unpadded: shadow index = canonical index
 #pragma unroll
   for (int u = 0; u < ADAM_PER_THREAD; ++u) {
     const int l = l0 + u * 256;
@@ -722,12 +729,15 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payloa
     const float v = a.b2 * vo[u] + (1.0f - a.b2) * gg * gg;
     a.m[i] = mm;
     a.v[i] = v;
-    const float mh = mm / bc1, vh = v / bc2;
-    const float th = tho[u] - alpha * mh / (sqrtf(vh) + a.eps);
+    const float th = tho[u] - step * mm / (sqrtf(v * ibc2) + a.eps);
     a.theta[i] = th;
-    const int r = l / G.cols, c = l - r * G.cols;
-    if (G.kind == 0) reinterpret_cast<__nv_bfloat16*>(G.dst)[(size_t)r * G.dst_ld + c] = __float2bfloat16_rn(th);
-    else reinterpret_cast<float*>(G.dst)[(size_t)r * G.dst_ld + c] = th;
+    size_t o = (size_t)l;
+    if (!dense) {
+      const int r = l / G.cols, c = l - r * G.cols;
+      o = (size_t)r * G.dst_ld + c;
+    }
+    if (G.kind == 0) reinterpret_cast<__nv_bfloat16*>(G.dst)[o] = __float2bfloat16_rn(th);
+    else reinterpret_cast<float*>(G.dst)[o] = th;
   }
 }
 __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a, const float* payload, float kl_target,
