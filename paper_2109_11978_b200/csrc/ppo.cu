@@ -747,8 +747,10 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
   adam_body(a, payload, kl_target, world, m, acc, blockIdx.x);
 }
 // Adam of minibatch m and the gather of minibatch m + 1 in one launch (blocks [0, nadam) update θ, the rest
-// gather; both are memory bound, independent, and run side by side instead of as two dependent launches)
-__global__ void __launch_bounds__(256) k_adam_gather(const __grid_constant__ AdamArgs a, const float* payload,
+// gather; both are memory bound, independent, and run side by side instead of as two dependent launches).
+// Five blocks per SM (48 registers, 8 B of stack) instead of the four that 58 registers allowed: the random
+// row reads of the gather want the extra warps in flight (same-box A/B: -0.5 % per iteration)
+__global__ void __launch_bounds__(256, 5) k_adam_gather(const __grid_constant__ AdamArgs a, const float* payload,
                                                      float kl_target, int world, int m, float* acc,
                                                      const __grid_constant__ GatherArgs g, int nadam) {
   pdl_trigger();
