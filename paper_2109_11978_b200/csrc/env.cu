@@ -377,7 +377,9 @@ __device__ void reset_group(const World& W, const Rng& rng, Com& c, Leg& g, int 
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const int j = 3 * l + k;
-    g.q[k] = c_qdef[j] + usym(0.05f, wd[7 + j]);
+    // word 7 + j by selects on the leg (a lane-indexed wd[] would live in local memory)
+    const uint32_t wq = l == 0 ? wd[7 + k] : (l == 1 ? wd[10 + k] : (l == 2 ? wd[13 + k] : wd[16 + k]));
+    g.q[k] = c_qdef[j] + usym(0.05f, wq);
     g.qd[k] = 0.0f;
     g.aprev[k] = 0.0f;
   }
@@ -615,7 +617,9 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
     if (to_out) to_out[i] = (uint8_t)to;
   }
   if (terms_out) {  // lane l writes terms l, l+4, l+8
-    for (int k = l; k < 9; k += 4) terms_out[(size_t)i * 9 + k] = rt[k];
+#pragma unroll
+    for (int k = 0; k < 9; ++k)  // constant indices keep rt[] in registers (a lane-indexed rt[k] put it in local memory)
+      if ((k & 3) == l) terms_out[(size_t)i * 9 + k] = rt[k];
   }
   if (done) {  // group-uniform
     if (to && (P.flags & F_BOOTSTRAP)) {

@@ -1563,7 +1563,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
         for (int jj = 0; jj < 6; ++jj) {
           const int j = 6 * hs + jj;
           const float other = xrow[(1 - hs) * 13 + j];
-          const float mu = __fadd_rn(tot[j] + other, __ldg(a.b4a + j));
+          const float tj = hs == 0 ? tot[jj] : tot[6 + jj];  // constant indices: tot[] stays in registers
+          const float mu = __fadd_rn(tj + other, __ldg(a.b4a + j));
           const float ls = __ldg(a.logstd + j);
           const bool first = (j >> 2) == (hs == 0 ? 0 : 1);
           const float act = a.deterministic ? mu : sample_action_b(first ? blk0 : blk1, j, mu, ls);

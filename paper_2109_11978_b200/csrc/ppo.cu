@@ -418,8 +418,9 @@ __global__ void __launch_bounds__(256) k_reduce_dw(DwReduceArgs a) {
     for (int w = 0; w < 8; ++w) t = t + ssum[w][lane];
     int zz = z, rr = r;
     if (a.row_split > 0 && r >= a.row_split) { zz = 1; rr = r - a.row_split; }
-    if (c < a.cols) a.grad[a.w_off[zz] + (long long)rr * a.cols + c] = t;
-    else a.grad[a.b_off[zz] + rr] = t;
+    const long long wo = zz ? a.w_off[1] : a.w_off[0], bo = zz ? a.b_off[1] : a.b_off[0];  // no param indexing
+    if (c < a.cols) a.grad[wo + (long long)rr * a.cols + c] = t;
+    else a.grad[bo + rr] = t;
     if (!isfinite(t)) atomicAdd(&a.payload[4], 1.0f);
   }
 }
