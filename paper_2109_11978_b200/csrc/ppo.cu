@@ -570,7 +570,7 @@ __global__ void k_perm(PermArgs a) {
 void launch_perm(const PermArgs& a, cudaStream_t st) { k_perm<<<dim3((a.B + 255) / 256, a.n_epochs), 256, 0, st>>>(a); }
 
 // ------------------------------------------------------------------ minibatch gather (warp per row)
-constexpr int GATHER_ROWS = 4;  // rows per warp: the permutation loads and the row copies are all in flight together
+constexpr int GATHER_ROWS = 2;  // rows per warp (even: the scalar fields go two rows per pass); see k_adam_gather
 __device__ __forceinline__ void gather_body(const GatherArgs& a, int bid) {
   const int warp = (bid * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int r0 = warp * GATHER_ROWS;
@@ -749,9 +749,10 @@ __global__ void __launch_bounds__(256) k_adam(const __grid_constant__ AdamArgs a
 }
 // Adam of minibatch m and the gather of minibatch m + 1 in one launch (blocks [0, nadam) update θ, the rest
 // gather; both are memory bound, independent, and run side by side instead of as two dependent launches).
-// Five blocks per SM (48 registers, 8 B of stack) instead of the four that 58 registers allowed: the random
-// row reads of the gather want the extra warps in flight (same-box A/B: -0.5 % per iteration)
-__global__ void __launch_bounds__(256, 5) k_adam_gather(const __grid_constant__ AdamArgs a, const float* payload,
+// Two rows per gather warp (45 registers, five blocks per SM, no spills): the random row reads want many
+// warps in flight more than many rows per warp (same-box A/B per iteration: 4 rows at 58 registers = base,
+// 4 rows capped at 48 registers -0.5 %, 2 rows -1.2 %, 8 rows +1.6 %)
+__global__ void __launch_bounds__(256) k_adam_gather(const __grid_constant__ AdamArgs a, const float* payload,
                                                      float kl_target, int world, int m, float* acc,
                                                      const __grid_constant__ GatherArgs g, int nadam) {
   pdl_trigger();
