@@ -110,8 +110,10 @@ static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn, bool background
   p.pair = 0;
   // one wave of <= 148 CTAs (background: <= 98), and >= 8 (background: 32) k-blocks per CTA (the fp32
   // partial costs ~3 k-blocks of traffic)
-  constexpr int BG_SPLITS = 12;
-  const int max_ctas = background ? 98 : 148;
+  // (LG_DW_BG_CTAS / LG_DW_BG_SPLITS override the background plan: measurement only)
+  static const int bg_ctas = [] { const char* e = getenv("LG_DW_BG_CTAS"); return e ? atoi(e) : 98; }();
+  static const int BG_SPLITS = [] { const char* e = getenv("LG_DW_BG_SPLITS"); return e ? atoi(e) : 12; }();
+  const int max_ctas = background ? bg_ctas : 148;
   int S = std::max(1, std::min(std::max(1, p.kb_total / 8), max_ctas / std::max(1, p.tiles)));
   if (background) S = std::min(S, BG_SPLITS);
   p.kb_per_split = (p.kb_total + S - 1) / S;
