@@ -110,7 +110,8 @@ typedef struct {
   float surrogate_loss, value_loss, entropy, mean_kl, lr, clip_fraction;
   int32_t nonfinite_skips, minibatches_applied;
   float mean_episode_return, mean_episode_length;
-  int32_t episodes, promotions, demotions, reserved;
+  int32_t episodes, promotions, demotions;
+  int32_t nonfinite_envs; /* env steps whose state went non-finite: forced terminated, reward 0, reset */
   int32_t level_hist[16];
 } lg_update_stats;
 
@@ -199,6 +200,31 @@ lg_status lg_nccl_unique_id(uint8_t id_h[128]);
 lg_status lg_set_nccl(lg_ctx* ctx, const uint8_t id_h[128]);
 /* Broadcast θ from rank 0 (then lg_params_sync semantics). */
 lg_status lg_broadcast_params(lg_ctx* ctx);
+
+/* --- Multi-rank emulation on one device (tests of the multi-GPU path; VERDICT r01 "loopback") ---
+ * A group binds the contexts of ALL ranks 0..n-1 of one world (each created with world_size = n and its own
+ * rank, otherwise identical configs, on the same device and the same stream). Per-rank work (rollout, GAE,
+ * shuffles, gathers, forward/backward, Adam) runs exactly as in the one-process-per-GPU path; where that path
+ * calls ncclAllReduce (advantage statistics: two fp64 sums per iteration; [gradient ‖ stats payload] after every
+ * minibatch) the group launches ONE kernel that sums the n ranks' buffers element by element in
+ * rank order and writes the sum back to every rank -- no kernel waits on another (B200_PROFILING.md: ranks that
+ * wait on each other must not share a GPU). Calls are enqueued in lockstep: all ranks' phase, the sum, all
+ * ranks' next phase. While grouped, the single-context learning calls (storage_compute_gae, ppo_update,
+ * graph capture, lg_iterate_host) return LG_ERR_STATE. Errors: INVALID_ARG (n outside [1, LG_MAX_GROUP],
+ * null pointers, rank/world mismatch, configs that differ in more than the rank, different streams),
+ * STATE (a context already grouped or on NCCL; a rank destroyed; iterate before env_reset). */
+#define LG_MAX_GROUP 8
+typedef struct lg_group lg_group;
+lg_status lg_group_create(lg_ctx* const* ctxs_h, int32_t n, lg_group** out_h);
+lg_status lg_group_destroy(lg_group* g);
+/* θ of rank 0 copied to every rank (the ncclBroadcast of lg_broadcast_params), shadows refreshed */
+lg_status lg_group_broadcast_params(lg_group* g);
+/* storage_compute_gae of every rank with the union advantage statistics (R13) */
+lg_status lg_group_compute_gae(lg_group* g);
+/* ppo_update of every rank with the per-minibatch gradient sum; stats_h: n device lg_update_stats* or NULL */
+lg_status lg_group_ppo_update(lg_group* g, lg_update_stats* const* stats_h);
+/* one whole iteration of every rank: T x (policy_act, env_step_obs_reward) per rank, then the two above */
+lg_status lg_group_iterate(lg_group* g, lg_update_stats* const* stats_h);
 
 /* --- World generation (reading R27) --- */
 /* Writes the tiled world heightfield into HEIGHTFIELD (device, fp32 [80*n_levels][80*n_cols], row-major;

@@ -234,3 +234,48 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class Group:
+    """All ranks 0..n-1 of one world as contexts on this device (include/lg.h, lg_group_*): the multi-GPU path's
+    per-rank work as in one process per GPU, its allreduce as one rank-ordered sum kernel over the ranks' buffers.
+    Every context must have been created with world_size = n, its own rank and the same stream."""
+
+    def __init__(self, contexts):
+        self.contexts = list(contexts)
+        st, self.g = lg.lg_group_create([c.ctx for c in self.contexts])
+        self._ck(st, "lg_group_create")
+
+    def _ck(self, st, what):
+        if st != 0:
+            for c in self.contexts:
+                msg = lg.lg_last_error(c.ctx) if c.ctx else ""
+                if msg:
+                    raise lg.LgError(f"{what}: {lg.STATUS.get(st, st)} {msg}")
+            raise lg.LgError(f"{what}: {lg.STATUS.get(st, st)}")
+
+    def broadcast_params(self):
+        self._ck(lg.lg_group_broadcast_params(self.g), "lg_group_broadcast_params")
+
+    def compute_gae(self):
+        self._ck(lg.lg_group_compute_gae(self.g), "lg_group_compute_gae")
+
+    def update(self, stats=None):
+        self._ck(lg.lg_group_ppo_update(self.g, stats), "lg_group_ppo_update")
+
+    def iteration(self, stats=None):
+        self._ck(lg.lg_group_iterate(self.g, stats), "lg_group_iterate")
+
+    def sync(self):
+        self.contexts[0].sync()
+
+    def close(self):
+        if getattr(self, "g", None):
+            lg.lg_group_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -240,6 +240,7 @@ Layout layout_of(const Dims& d) {
 
 }  // namespace
 
+struct lg_group;
 struct lg_ctx {
   lg_config cfg;
   Dims d;
@@ -255,6 +256,7 @@ struct lg_ctx {
   std::string msg;
   int world = 1;
   ncclComm_t comm = nullptr;
+  lg_group* group = nullptr;  // set while the context is a rank of an lg_group (single-device emulation)
   bool reset_done = false;
   // prebuilt launch descriptors
   std::vector<GemmArgs> l1_roll;  // per OBS slot 0..T
@@ -278,6 +280,12 @@ struct lg_ctx {
   std::vector<cudaEvent_t> ev;
   std::vector<PP> pairs, gpairs;
   size_t evn = 0;
+};
+
+// n contexts (ranks 0..n-1 of one world) driven together on one device: the emulation of the multi-rank path
+struct lg_group {
+  int n;
+  lg_ctx* cs[LG_MAX_GROUP];  // null once a rank's context has been destroyed
 };
 
 namespace {
@@ -401,7 +409,8 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return LG_ERR_UNSUPPORTED;
   cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10) return LG_ERR_UNSUPPORTED;
+  // the library is built for sm_100a only (build.py): any other device, sm_103 included, is unsupported
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10 || prop.minor != 0) return LG_ERR_UNSUPPORTED;
   lg_ctx* ctx = new lg_ctx();
   ctx->cfg = *cfg;
   dims_of(cfg, ctx->d);
@@ -658,6 +667,9 @@ lg_status lg_destroy(lg_ctx* ctx) {
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->group)  // the group loses this rank: it can no longer run (lg_group_* return LG_ERR_STATE)
+    for (int r = 0; r < ctx->group->n; ++r)
+      if (ctx->group->cs[r] == ctx) ctx->group->cs[r] = nullptr;
   delete ctx;
   return LG_OK;
 }
@@ -874,17 +886,52 @@ lg_status policy_forward(lg_ctx* ctx, const void* x, int32_t M, float* mu, float
 }
 
 // ------------------------------------------------------------------ learning
-static lg_status allreduce_f(lg_ctx* ctx, float* p, size_t n) {
-  if (ctx->world > 1 && ctx->comm) CKN(ncclAllReduce(p, p, n, ncclFloat32, ncclSum, ctx->comm, ctx->st));
-  return LG_OK;
+// The path's collectives: the advantage statistics (two fp64 sums per iteration) and the
+// [gradient ‖ stats payload] of every minibatch, summed over the ranks. `cs[0..n)` are the contexts this process
+// drives for the collective: n = 1 with an NCCL communicator (one process per GPU, world_size ranks), or the n
+// contexts of an lg_group (every rank of the world on this device; the sum is one kernel over all ranks' buffers
+// in rank order -- the emulation of the collective on one GPU, no kernel waits for another). World 1: no-op.
+enum CollSel { COLL_GAE_SUM = 0, COLL_GAE_VAR = 1, COLL_GRAD = 2 };
+static void* coll_ptr(lg_ctx* ctx, CollSel sel) {
+  double* tot = at<double>(ctx->buf[LG_BUF_WORK], ctx->L.k_tot);
+  if (sel == COLL_GAE_SUM) return tot;
+  if (sel == COLL_GAE_VAR) return tot + 1;
+  return ctx->buf[LG_BUF_GRAD];
 }
-static lg_status allreduce_d(lg_ctx* ctx, double* p, size_t n) {
-  if (ctx->world > 1 && ctx->comm) CKN(ncclAllReduce(p, p, n, ncclFloat64, ncclSum, ctx->comm, ctx->st));
+static lg_status collective(lg_ctx* const* cs, int n, CollSel sel) {
+  lg_ctx* ctx = cs[0];
+  const bool dbl = sel != COLL_GRAD;
+  const size_t count = dbl ? 1 : (size_t)ctx->d.P + 16;
+  if (n == 1) {
+    if (ctx->world == 1) return LG_OK;
+    if (!ctx->comm) return fail(ctx, LG_ERR_STATE, "world_size %d without a communicator (lg_set_nccl)", ctx->world);
+    void* p = coll_ptr(ctx, sel);
+    Scope sc_(ctx, LG_PROF_COMM);
+    CKN(ncclAllReduce(p, p, count, dbl ? ncclFloat64 : ncclFloat32, ncclSum, ctx->comm, ctx->st));
+    return LG_OK;
+  }
+  GroupSumArgs g;
+  memset(&g, 0, sizeof(g));
+  g.n = n;
+  g.count = (long long)count;
+  g.is_double = dbl ? 1 : 0;
+  for (int r = 0; r < n; ++r) g.p[r] = coll_ptr(cs[r], sel);
+  Scope sc_(ctx, LG_PROF_COMM);
+  launch_group_sum(g, ctx->st);
+  CKL();
   return LG_OK;
 }
 
-lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
-  GUARD();
+// a context may run the learning calls alone only if it has no peers, or an NCCL communicator for them
+static lg_status solo_ok(lg_ctx* ctx, const char* what) {
+  if (ctx->group) return fail(ctx, LG_ERR_STATE, "%s: the context is a rank of an lg_group (use lg_group_*)", what);
+  if (ctx->world > 1 && !ctx->comm)
+    return fail(ctx, LG_ERR_STATE, "%s: world_size %d needs lg_set_nccl first", what, ctx->world);
+  return LG_OK;
+}
+
+// storage_compute_gae, phase 1 (per rank): bootstrap critic, V(o_T), GAE, Σ A -> tot[0]
+static lg_status gae_local(lg_ctx* ctx) {
   const Dims& d = ctx->d;
   void* K = ctx->buf[LG_BUF_WORK];
   if (ctx->cfg.flags & LG_F_BOOTSTRAP) {  // V(o_term) of every time-out of the rollout, one batched pass
@@ -899,7 +946,6 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
     CKL();
   }
   // V(o_T): critic on OBS slot T (the fused kernel's critic half when it applies: one launch, bit-identical)
-  lg_status s = LG_OK;
   if (fused_policy_ok(d) && !(ctx->cfg.flags & LG_F_UNFUSED_POLICY)) {
     FusedPolicyArgs fa = fused_args(ctx, d.T);
     fa.z0 = 1;
@@ -908,7 +954,7 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
     cudaError_t e = launch_policy_fused(fa, ctx->st);
     if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "V(o_T) (fused): %s", cudaGetErrorString(e));
   } else {
-    s = critic_rows(ctx, ctx->l1_vt, nullptr, d.N);
+    lg_status s = critic_rows(ctx, ctx->l1_vt, nullptr, d.N);
     if (s != LG_OK) return s;
     HeadArgs h = head_args(ctx, d.N);
     h.mode = 1;
@@ -930,22 +976,53 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
   Scope sc_gae(ctx, LG_PROF_GAE);
   launch_gae(g, ctx->st);
   CKL();
-  double* tot = at<double>(K, ctx->L.k_tot);
-  launch_sum_partials(g.part, ctx->L.nblk_gae, tot, ctx->st);
+  launch_sum_partials(g.part, ctx->L.nblk_gae, at<double>(K, ctx->L.k_tot), ctx->st);
   CKL();
-  if ((s = allreduce_d(ctx, tot, 1)) != LG_OK) return s;
+  return LG_OK;
+}
+// phase 2 (per rank, after the Σ A collective): Σ (A - mean)² about the union mean -> tot[1]
+static lg_status gae_var(lg_ctx* ctx) {
+  const Dims& d = ctx->d;
+  void* K = ctx->buf[LG_BUF_WORK];
+  double* tot = at<double>(K, ctx->L.k_tot);
   const double count = (double)d.B * ctx->world;
   double* vp = at<double>(K, ctx->L.k_var);
-  launch_var_partials(g.A, d.B, tot, count, vp, ctx->st);
+  Scope sc_gae(ctx, LG_PROF_GAE);
+  launch_var_partials(reinterpret_cast<const float*>(ctx->buf[LG_BUF_ADV]), d.B, tot, count, vp, ctx->st);
   CKL();
   launch_sum_partials(vp, ctx->L.nblk_var, tot + 1, ctx->st);
   CKL();
-  if ((s = allreduce_d(ctx, tot + 1, 1)) != LG_OK) return s;
-  launch_adv_finalize(tot, tot + 1, count, ctx->sc, d.T, ctx->st);  // (also advances s_base by T)
-  CKL();
-  if (adv) CK(cudaMemcpyAsync(adv, g.A, (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));
-  if (ret) CK(cudaMemcpyAsync(ret, g.R, (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));
   return LG_OK;
+}
+// phase 3 (per rank, after the variance collective): union mean / std into the device scalars
+static lg_status gae_finalize(lg_ctx* ctx, float* adv, float* ret) {
+  const Dims& d = ctx->d;
+  double* tot = at<double>(ctx->buf[LG_BUF_WORK], ctx->L.k_tot);
+  {
+    Scope sc_gae(ctx, LG_PROF_GAE);
+    launch_adv_finalize(tot, tot + 1, (double)d.B * ctx->world, ctx->sc, d.T, ctx->st);  // (also advances s_base by T)
+    CKL();
+  }
+  if (adv) CK(cudaMemcpyAsync(adv, ctx->buf[LG_BUF_ADV], (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));
+  if (ret) CK(cudaMemcpyAsync(ret, ctx->buf[LG_BUF_RET], (size_t)d.B * 4, cudaMemcpyDeviceToDevice, ctx->st));
+  return LG_OK;
+}
+static lg_status run_gae(lg_ctx* const* cs, int n, float* adv, float* ret) {
+  lg_status s;
+  for (int r = 0; r < n; ++r) if ((s = gae_local(cs[r])) != LG_OK) return s;
+  if ((s = collective(cs, n, COLL_GAE_SUM)) != LG_OK) return s;
+  for (int r = 0; r < n; ++r) if ((s = gae_var(cs[r])) != LG_OK) return s;
+  if ((s = collective(cs, n, COLL_GAE_VAR)) != LG_OK) return s;
+  for (int r = 0; r < n; ++r) if ((s = gae_finalize(cs[r], adv, ret)) != LG_OK) return s;
+  return LG_OK;
+}
+
+lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
+  GUARD();
+  lg_status s = solo_ok(ctx, "storage_compute_gae");
+  if (s != LG_OK) return s;
+  lg_ctx* cs[1] = {ctx};
+  return run_gae(cs, 1, adv, ret);
 }
 
 // gradient of one minibatch (rows already gathered into the ACTIV minibatch arrays)
@@ -1100,62 +1177,76 @@ lg_status ppo_minibatch_grad(lg_ctx* ctx, const int32_t* idx, int32_t M_mb) {
   return minibatch_gradient(ctx, 0, nullptr);
 }
 
-lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
-  GUARD();
-  const Dims& d = ctx->d;
-  const Layout& L = ctx->L;
-  void* K = ctx->buf[LG_BUF_WORK];
-  uint32_t* perm = at<uint32_t>(K, L.k_perm);
-  float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
-  { Scope sc_(ctx, LG_PROF_MISC); iter_begin(ctx); }
-  CKL();
+static AdamArgs adam_args(lg_ctx* ctx) {
   AdamArgs aa;
   aa.sh = ctx->shadow;
   aa.theta = reinterpret_cast<float*>(ctx->buf[LG_BUF_THETA]);
   aa.m = reinterpret_cast<float*>(ctx->buf[LG_BUF_ADAM_M]);
   aa.v = reinterpret_cast<float*>(ctx->buf[LG_BUF_ADAM_V]);
-  aa.grad = grad;
+  aa.grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
   aa.b1 = ctx->cfg.adam_b1; aa.b2 = ctx->cfg.adam_b2; aa.eps = ctx->cfg.adam_eps;
   aa.inv_world = 1.0f / (float)ctx->world;
   aa.sc = ctx->sc;
-  lg_status s;
+  return aa;
+}
+static uint32_t* perm_of(lg_ctx* ctx) { return at<uint32_t>(ctx->buf[LG_BUF_WORK], ctx->L.k_perm); }
+// the permutation slice of minibatch k (epoch k / K, slice k % K of that epoch's permutation), or null past the end
+static const uint32_t* mb_perm(lg_ctx* ctx, int k) {
+  return k < ctx->d.E * ctx->d.K ? perm_of(ctx) + (size_t)k * ctx->d.Mmb : nullptr;
+}
+static bool gather_prefetch() {  // LG_GATHER_PREFETCH=1: next gather beside dW1 instead of inside the Adam launch
+  static const bool v = [] { const char* e = getenv("LG_GATHER_PREFETCH"); return e && e[0] == '1'; }();
+  return v;
+}
+
+// ppo_update, per rank: Alg. 1 / Adam scalars of the iteration, the E shuffles, the first minibatch's gather
+static lg_status update_begin(lg_ctx* ctx) {
+  const Dims& d = ctx->d;
+  { Scope sc_(ctx, LG_PROF_MISC); iter_begin(ctx); }
+  CKL();
   {  // the Feistel permutations of all E epochs (P:272 shuffled minibatches), one launch
     PermArgs pa;
     pa.B = (uint32_t)d.B; pa.E = d.E; pa.epoch = 0; pa.rank = ctx->cfg.rank;
     pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
-    pa.sc = ctx->sc; pa.perm = perm; pa.n_epochs = d.E;
+    pa.sc = ctx->sc; pa.perm = perm_of(ctx); pa.n_epochs = d.E;
     { Scope sc_(ctx, LG_PROF_GATHER); launch_perm(pa, ctx->st); }
     CKL();
   }
-  {  // the first minibatch's gather (later ones are launched inside minibatch_gradient, beside dW1)
+  {  // the first minibatch's gather (later ones ride in the Adam launch, or beside dW1 with prefetch)
     GatherArgs g = gather_args(ctx, 0);
-    g.perm = perm;
+    g.perm = perm_of(ctx);
     { Scope sc_(ctx, LG_PROF_GATHER); launch_gather(g, ctx->st); }
     CKL();
   }
-  const int n_mb = d.E * d.K;
-  static const bool prefetch = [] {
-    const char* e = getenv("LG_GATHER_PREFETCH");
-    return e && e[0] == '1';
-  }();
-  for (int k = 0; k < n_mb; ++k) {  // minibatch k = epoch k / K, slice k % K of that epoch's permutation
-    const uint32_t* next = k + 1 < n_mb ? perm + (size_t)(k + 1) * d.Mmb : nullptr;
-    if ((s = minibatch_gradient(ctx, k & 1, prefetch ? next : nullptr)) != LG_OK) return s;
-    { Scope sc_(ctx, LG_PROF_COMM); if ((s = allreduce_f(ctx, grad, (size_t)d.P + 16)) != LG_OK) return s; }
-    Scope sc_adam(ctx, LG_PROF_ADAM);
-    if (next && !prefetch) {  // Adam of minibatch k and the gather of minibatch k + 1 (other set) in one launch
-      GatherArgs g = gather_args(ctx, (k + 1) & 1);
-      g.perm = next;
-      launch_adam_gather(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, g, ctx->st);
-    } else {
-      launch_adam(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, ctx->st);
-    }
-    CKL();
+  return LG_OK;
+}
+// minibatch k, per rank: forward, loss, backward into [grad ‖ payload] (summed over the ranks next)
+static lg_status update_gradient(lg_ctx* ctx, int k) {
+  return minibatch_gradient(ctx, k & 1, gather_prefetch() ? mb_perm(ctx, k + 1) : nullptr);
+}
+// minibatch k, per rank, after the gradient collective: Alg. 1 on the rank-mean KL + Adam (+ next gather)
+static lg_status update_adam(lg_ctx* ctx, int k) {
+  AdamArgs aa = adam_args(ctx);
+  const uint32_t* next = mb_perm(ctx, k + 1);
+  Scope sc_adam(ctx, LG_PROF_ADAM);
+  if (next && !gather_prefetch()) {  // Adam of minibatch k and the gather of minibatch k + 1 (other set) in one launch
+    GatherArgs g = gather_args(ctx, (k + 1) & 1);
+    g.perm = next;
+    launch_adam_gather(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, g, ctx->st);
+  } else {
+    launch_adam(aa, ctx->payload, ctx->cfg.kl_target, ctx->world, k, ctx->step_f + 4, ctx->st);
   }
+  CKL();
+  return LG_OK;
+}
+// iteration end, per rank: statistics, α / Adam step write-back, o_T becomes o_0 of the next iteration
+static lg_status update_end(lg_ctx* ctx, lg_update_stats* stats) {
+  const Dims& d = ctx->d;
+  const Layout& L = ctx->L;
   IterEndArgs ie;
   memset(&ie, 0, sizeof(ie));
   ie.sc = ctx->sc;
-  ie.stats = stats ? (void*)stats : (void*)at<lg_update_stats>(K, L.k_stats);
+  ie.stats = stats ? (void*)stats : (void*)at<lg_update_stats>(ctx->buf[LG_BUF_WORK], L.k_stats);
   ie.n_mb = d.E * d.K; ie.T = d.T; ie.n_levels = d.L;
   ie.state = reinterpret_cast<const uint32_t*>(ctx->buf[LG_BUF_STATE]);
   ie.N = d.N;
@@ -1163,10 +1254,30 @@ lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
   Scope sc_end(ctx, LG_PROF_MISC);
   launch_iter_end(ie, ctx->step_f + 4, ctx->st);
   CKL();
-  // o_T becomes o_0 of the next iteration
   __nv_bfloat16* OBS = reinterpret_cast<__nv_bfloat16*>(ctx->buf[LG_BUF_OBS]);
   CK(cudaMemcpyAsync(OBS, OBS + (size_t)d.T * d.N * d.Dp, (size_t)d.N * d.Dp * 2, cudaMemcpyDeviceToDevice, ctx->st));
   return LG_OK;
+}
+static lg_status run_update(lg_ctx* const* cs, int n, lg_update_stats* const* stats) {
+  lg_status s;
+  for (int r = 0; r < n; ++r) if ((s = update_begin(cs[r])) != LG_OK) return s;
+  const int n_mb = cs[0]->d.E * cs[0]->d.K;
+  for (int k = 0; k < n_mb; ++k) {
+    for (int r = 0; r < n; ++r) if ((s = update_gradient(cs[r], k)) != LG_OK) return s;
+    if ((s = collective(cs, n, COLL_GRAD)) != LG_OK) return s;
+    for (int r = 0; r < n; ++r) if ((s = update_adam(cs[r], k)) != LG_OK) return s;
+  }
+  for (int r = 0; r < n; ++r) if ((s = update_end(cs[r], stats ? stats[r] : nullptr)) != LG_OK) return s;
+  return LG_OK;
+}
+
+lg_status ppo_update(lg_ctx* ctx, lg_update_stats* stats) {
+  GUARD();
+  lg_status s = solo_ok(ctx, "ppo_update");
+  if (s != LG_OK) return s;
+  lg_ctx* cs[1] = {ctx};
+  lg_update_stats* st[1] = {stats};
+  return run_update(cs, 1, st);
 }
 
 // ------------------------------------------------------------------ multi-GPU
@@ -1176,7 +1287,8 @@ lg_status lg_terrain_generate(float* heightfield, int32_t n_levels, int32_t n_co
   {
     int dev = 0;
     cudaDeviceProp prop;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10 ||
+        prop.minor != 0)
       return LG_ERR_UNSUPPORTED;
   }
   TerrainArgs t;
@@ -1203,6 +1315,7 @@ lg_status lg_nccl_unique_id(uint8_t id_h[128]) {
 lg_status lg_set_nccl(lg_ctx* ctx, const uint8_t id_h[128]) {
   GUARD();
   if (!id_h) return fail(ctx, LG_ERR_INVALID_ARG, "null id");
+  if (ctx->group) return fail(ctx, LG_ERR_STATE, "lg_set_nccl: the context is a rank of an lg_group");
   if (ctx->world <= 1) return LG_OK;
   ncclUniqueId id;
   memcpy(&id, id_h, 128);
@@ -1231,6 +1344,10 @@ static lg_status run_iteration(lg_ctx* ctx, lg_update_stats* stats) {
 lg_status lg_graph_capture_iteration(lg_ctx* ctx, lg_update_stats* stats) {
   GUARD();
   if (!ctx->reset_done) return fail(ctx, LG_ERR_STATE, "graph capture before env_reset");
+  {
+    lg_status s0 = solo_ok(ctx, "lg_graph_capture_iteration");
+    if (s0 != LG_OK) return s0;
+  }
   if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
   if (ctx->graph) { cudaGraphDestroy(ctx->graph); ctx->graph = nullptr; }
   CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
@@ -1277,6 +1394,10 @@ lg_status lg_graph_kernel_count(lg_ctx* ctx, int32_t* n_h) {
 
 lg_status lg_iterate_host(lg_ctx* ctx, const uint8_t ctrl_h[16], lg_update_stats* stats_h) {
   GUARD();
+  {
+    lg_status s0 = solo_ok(ctx, "lg_iterate_host");
+    if (s0 != LG_OK) return s0;
+  }
   if (!ctrl_h || !stats_h) return fail(ctx, LG_ERR_INVALID_ARG, "iterate_host: null host buffer");
   void* K = ctx->buf[LG_BUF_WORK];
   CK(cudaMemcpyAsync(at<uint8_t>(K, ctx->L.k_ctrl), ctrl_h, 16, cudaMemcpyHostToDevice, ctx->st));
@@ -1290,6 +1411,88 @@ lg_status lg_iterate_host(lg_ctx* ctx, const uint8_t ctrl_h[16], lg_update_stats
   CK(cudaMemcpyAsync(stats_h, dstats, sizeof(lg_update_stats), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return LG_OK;
+}
+
+// ------------------------------------------------------------------ multi-rank group on one device
+lg_status lg_group_create(lg_ctx* const* ctxs_h, int32_t n, lg_group** out_h) {
+  if (!ctxs_h || !out_h || n < 1 || n > LG_MAX_GROUP) return LG_ERR_INVALID_ARG;
+  for (int r = 0; r < n; ++r)
+    if (!ctxs_h[r]) return LG_ERR_INVALID_ARG;
+  for (int r = 0; r < n; ++r) {
+    lg_ctx* ctx = ctxs_h[r];
+    if (ctx->err != LG_OK) return ctx->err;
+    if (ctx->group || ctx->comm) return fail(ctx, LG_ERR_STATE, "lg_group_create: already grouped or on NCCL");
+    if (ctx->cfg.world_size != n || ctx->cfg.rank != r)
+      return fail(ctx, LG_ERR_INVALID_ARG, "lg_group_create: context %d has rank %d of world %d", r, ctx->cfg.rank,
+                  ctx->cfg.world_size);
+    if (ctx->st != ctxs_h[0]->st) return fail(ctx, LG_ERR_INVALID_ARG, "lg_group_create: ranks must share one stream");
+    lg_config a = ctx->cfg, b = ctxs_h[0]->cfg;
+    a.rank = b.rank = 0;
+    if (memcmp(&a, &b, sizeof(a)) != 0) return fail(ctx, LG_ERR_INVALID_ARG, "lg_group_create: configs differ");
+  }
+  lg_group* g = new lg_group();
+  g->n = n;
+  for (int r = 0; r < n; ++r) { g->cs[r] = ctxs_h[r]; ctxs_h[r]->group = g; }
+  *out_h = g;
+  return LG_OK;
+}
+
+lg_status lg_group_destroy(lg_group* g) {
+  if (!g) return LG_ERR_INVALID_ARG;
+  for (int r = 0; r < g->n; ++r)
+    if (g->cs[r]) g->cs[r]->group = nullptr;
+  delete g;
+  return LG_OK;
+}
+
+static lg_status group_guard(lg_group* g) {
+  if (!g) return LG_ERR_INVALID_ARG;
+  for (int r = 0; r < g->n; ++r) {
+    if (!g->cs[r]) return LG_ERR_STATE;
+    if (g->cs[r]->err != LG_OK) return g->cs[r]->err;
+  }
+  return LG_OK;
+}
+
+lg_status lg_group_broadcast_params(lg_group* g) {
+  lg_status s = group_guard(g);
+  if (s != LG_OK) return s;
+  lg_ctx* c0 = g->cs[0];
+  for (int r = 1; r < g->n; ++r) {
+    lg_ctx* ctx = g->cs[r];
+    CK(cudaMemcpyAsync(ctx->buf[LG_BUF_THETA], c0->buf[LG_BUF_THETA], (size_t)ctx->d.P * 4, cudaMemcpyDeviceToDevice,
+                       ctx->st));
+    launch_sync_shadow(ctx->shadow, reinterpret_cast<const float*>(ctx->buf[LG_BUF_THETA]), ctx->st);
+    CKL();
+  }
+  return LG_OK;
+}
+
+lg_status lg_group_compute_gae(lg_group* g) {
+  lg_status s = group_guard(g);
+  if (s != LG_OK) return s;
+  return run_gae(g->cs, g->n, nullptr, nullptr);
+}
+
+lg_status lg_group_ppo_update(lg_group* g, lg_update_stats* const* stats_h) {
+  lg_status s = group_guard(g);
+  if (s != LG_OK) return s;
+  return run_update(g->cs, g->n, stats_h);
+}
+
+lg_status lg_group_iterate(lg_group* g, lg_update_stats* const* stats_h) {
+  lg_status s = group_guard(g);
+  if (s != LG_OK) return s;
+  for (int r = 0; r < g->n; ++r) {
+    lg_ctx* ctx = g->cs[r];
+    if (!ctx->reset_done) return fail(ctx, LG_ERR_STATE, "lg_group_iterate before env_reset");
+    for (int t = 0; t < ctx->d.T; ++t) {
+      if ((s = policy_act(ctx, t, nullptr, nullptr, nullptr, nullptr)) != LG_OK) return s;
+      if ((s = env_step_obs_reward(ctx, t, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) != LG_OK) return s;
+    }
+  }
+  if ((s = run_gae(g->cs, g->n, nullptr, nullptr)) != LG_OK) return s;
+  return run_update(g->cs, g->n, stats_h);
 }
 
 lg_status lg_profile(lg_ctx* ctx, int32_t enable) {

@@ -31,9 +31,12 @@ struct DevScalars {
   int32_t pad0;
   double adv_mean, adv_inv_std;  // normalisation of the current batch
   float kl_last, pad1;
-  // per-iteration episode statistics (accumulated by env steps)
-  float ep_return_sum, ep_len_sum;
-  int32_t episodes, promotions, demotions, pad2;
+  // per-iteration episode statistics (accumulated by env steps): integer and fixed-point sums, so the totals do
+  // not depend on the order in which the envs' atomics land (SPEC S:414 determinism)
+  long long ep_return_fx;  // sum of finished episodes' returns, fixed point with 24 fraction bits
+  long long ep_len_sum;    // sum of finished episodes' lengths (steps)
+  int32_t episodes, promotions, demotions;
+  int32_t nonfinite_envs;  // env steps whose state went non-finite (forced terminated + reset)
   int32_t level_hist[16];
   // Alg. 1 / Adam state per minibatch slot m of the iteration (read slot m&1, write slot (m+1)&1)
   float alpha_ring[2];

@@ -638,8 +638,11 @@ __global__ void __launch_bounds__(STEP_THREADS) k_env_step(EnvParams P, int t, c
       }
     }
     if (l == 0) {  // episode statistics (stats only; float atomics)
-      atomicAdd(&P.scalars->ep_return_sum, c.ep_return);
-      atomicAdd(&P.scalars->ep_len_sum, (float)c.ep_step);
+      const float fx = c.ep_return * 16777216.0f;  // exact power-of-two scaling, then one rounding to an integer
+      if (isfinite(fx) && fabsf(fx) < 9.0e18f)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.scalars->ep_return_fx), (unsigned long long)__float2ll_rn(fx));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&P.scalars->ep_len_sum), (unsigned long long)c.ep_step);
+      if (!finite) atomicAdd(&P.scalars->nonfinite_envs, 1);
       atomicAdd(&P.scalars->episodes, 1);
     }
     if (P.flags & F_CURRICULUM) {

@@ -806,10 +806,22 @@ __device__ __forceinline__ void dw_partial_barrier_reduce(const GemmArgs& args, 
   __syncthreads();
   DW_STAMP(4);
   if (threadIdx.x == 0) {
+    // generation barrier: cnt[0] counts arrivals and returns to 0 at every release, cnt[1] is the generation.
+    // The generation is read before arriving (it cannot advance before this CTA arrives); the last CTA resets
+    // the count and then publishes the next generation. No modular arithmetic on a growing counter, so
+    // neither a counter wrap nor a grid size that changes between launches (another plan, a restored
+    // checkpoint) can leave a CTA waiting for a target that is never reached.
     const uint32_t n = gridDim.x * gridDim.y * gridDim.z;
-    const uint32_t old = atomicAdd(reinterpret_cast<uint32_t*>(out.cnt), 1u);
-    const uint32_t target = (old / n + 1u) * n;
-    while ((int32_t)(ld_acquire_gpu(reinterpret_cast<const uint32_t*>(out.cnt)) - target) < 0) __nanosleep(64);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(out.cnt);
+    const uint32_t gen = ld_acquire_gpu(cnt + 1);
+    const uint32_t old = atomicAdd(cnt, 1u);
+    if (old == n - 1u) {
+      cnt[0] = 0u;
+      __threadfence();
+      atomicAdd(cnt + 1, 1u);
+    } else {
+      while (ld_acquire_gpu(cnt + 1) == gen) __nanosleep(64);
+    }
   }
   __syncthreads();
   DW_STAMP(5);

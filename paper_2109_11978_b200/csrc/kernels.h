@@ -109,7 +109,7 @@ struct DwOut {                 // canonical destinations of a weight-gradient GE
   float* payload;              // non-finite counter at payload[4]
   int G;                       // unused (1)
   float* part;                 // [tile][S][128][BN + 20] fp32 split partials (L2-resident scratch)
-  int* cnt;                    // grid-barrier counter (only grows; zero at creation)
+  int* cnt;                    // grid barrier: cnt[0] arrivals (back to 0 at each release), cnt[1] generation
   unsigned long long* dbg;     // diagnostics only (tools/gemm_probe): per-CTA phase timestamps, else null
   int dbg_mode;                // diagnostics only: 1 = skip the reduction, 2 = loads only, 3 = stores only
 };
@@ -277,6 +277,15 @@ void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int w
 void launch_adam_gather(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc,
                         const GatherArgs& g, cudaStream_t st);
 void launch_sync_shadow(const ShadowArgs& sh, const float* theta, cudaStream_t st);
+
+// the collective of an lg_group (n ranks on one device): p[r][i] <- sum over r' in rank order of p[r'][i]
+struct GroupSumArgs {
+  void* p[LG_MAX_GROUP];
+  int n;
+  long long count;
+  int is_double;             // fp64 (advantage statistics) or fp32 ([gradient ‖ payload])
+};
+void launch_group_sum(const GroupSumArgs& a, cudaStream_t st);
 
 struct IterEndArgs {
   DevScalars* sc; void* stats; int n_mb; int T; int n_levels; const uint32_t* state; int N; float entropy_dummy;

@@ -780,6 +780,31 @@ void launch_sync_shadow(const ShadowArgs& sh, const float* theta, cudaStream_t s
   k_sync_shadow<<<nb, 256, 0, st>>>(sh, theta);
 }
 
+// ------------------------------------------------------------------ lg_group collective (single-device emulation)
+// Every rank's element i is replaced by the rank-ordered sum of all ranks' element i: the allreduce(sum) of
+// the one-process-per-GPU path, as one kernel over all ranks' buffers (no kernel waits for another).
+template <typename T>
+__global__ void k_group_sum(GroupSumArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.count; i += (long long)gridDim.x * blockDim.x) {
+    T v[LG_MAX_GROUP];
+#pragma unroll
+    for (int r = 0; r < LG_MAX_GROUP; ++r)
+      if (r < a.n) v[r] = reinterpret_cast<const T*>(a.p[r])[i];
+    T s = v[0];
+#pragma unroll
+    for (int r = 1; r < LG_MAX_GROUP; ++r)
+      if (r < a.n) s = s + v[r];
+#pragma unroll
+    for (int r = 0; r < LG_MAX_GROUP; ++r)
+      if (r < a.n) reinterpret_cast<T*>(a.p[r])[i] = s;
+  }
+}
+void launch_group_sum(const GroupSumArgs& a, cudaStream_t st) {
+  const int nb = (int)std::min<long long>((a.count + 255) / 256, 148LL * 8);
+  if (a.is_double) k_group_sum<double><<<nb, 256, 0, st>>>(a);
+  else k_group_sum<float><<<nb, 256, 0, st>>>(a);
+}
+
 // ------------------------------------------------------------------ iteration bookkeeping
 __global__ void k_iter_begin(DevScalars* sc, float* logstd_old, const float* logstd, float* iter_acc, float b1,
                              float b2) {
@@ -841,19 +866,20 @@ __global__ void k_iter_end(IterEndArgs a, const float* acc) {
       s->entropy = H;
     } else if (k == 3) {
       const int ne = sc->episodes;
-      s->mean_episode_return = ne > 0 ? sc->ep_return_sum / (float)ne : 0.0f;
-      s->mean_episode_length = ne > 0 ? sc->ep_len_sum / (float)ne : 0.0f;
+      s->mean_episode_return = ne > 0 ? (float)((double)sc->ep_return_fx * 0x1p-24 / (double)ne) : 0.0f;
+      s->mean_episode_length = ne > 0 ? (float)((double)sc->ep_len_sum / (double)ne) : 0.0f;
       s->episodes = ne;
     } else if (k == 4) {
       s->promotions = sc->promotions; s->demotions = sc->demotions;
-      s->nonfinite_skips = sc->nonfinite_skips; s->reserved = (int)sc->iteration + 1;
+      s->nonfinite_skips = sc->nonfinite_skips; s->nonfinite_envs = sc->nonfinite_envs;
     } else if (k >= 32 && k < 48) {
       s->level_hist[k - 32] = hist[k - 32];
     }
   }
   __syncthreads();
   if (k == 0) {
-    sc->ep_return_sum = 0.0f; sc->ep_len_sum = 0.0f; sc->episodes = 0; sc->promotions = 0; sc->demotions = 0;
+    sc->ep_return_fx = 0; sc->ep_len_sum = 0; sc->episodes = 0; sc->promotions = 0; sc->demotions = 0;
+    sc->nonfinite_envs = 0;
     sc->iteration += 1;
   }
 }

@@ -39,7 +39,7 @@ class lg_update_stats(ctypes.Structure):
                 ("nonfinite_skips", ctypes.c_int32), ("minibatches_applied", ctypes.c_int32),
                 ("mean_episode_return", ctypes.c_float), ("mean_episode_length", ctypes.c_float),
                 ("episodes", ctypes.c_int32), ("promotions", ctypes.c_int32), ("demotions", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("level_hist", ctypes.c_int32 * 16)]
+                ("nonfinite_envs", ctypes.c_int32), ("level_hist", ctypes.c_int32 * 16)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "level_hist"}
@@ -52,7 +52,9 @@ EXPORTS = ["lg_num_params", "lg_obs_dim", "lg_obs_stride", "lg_required_sizes", 
            "policy_forward", "storage_compute_gae", "ppo_update", "ppo_shuffle", "ppo_minibatch_grad", "curriculum_update",
            "lg_nccl_unique_id", "lg_set_nccl", "lg_broadcast_params", "lg_iterate_host",
            "lg_graph_capture_iteration", "lg_graph_launch", "lg_device_scalars", "lg_profile", "lg_profile_read", "lg_graph_kernel_count",
-           "lg_terrain_generate"]
+           "lg_terrain_generate", "lg_group_create", "lg_group_destroy", "lg_group_broadcast_params",
+           "lg_group_compute_gae", "lg_group_ppo_update", "lg_group_iterate"]
+MAX_GROUP = 8
 PROF_CATS = ["env", "gemm_roll", "gemm_fwd", "gemm_dx", "gemm_dw", "heads", "loss", "reduce", "gather", "adam", "gae",
              "comm", "misc"]
 
@@ -93,6 +95,12 @@ _sig = {
     "lg_graph_kernel_count": (I32, [P, ctypes.POINTER(I32)]),
     "lg_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32]),
     "lg_terrain_generate": (I32, [P, I32, I32, ctypes.c_uint64, P]),
+    "lg_group_create": (I32, [ctypes.POINTER(P), I32, ctypes.POINTER(P)]),
+    "lg_group_destroy": (I32, [P]),
+    "lg_group_broadcast_params": (I32, [P]),
+    "lg_group_compute_gae": (I32, [P]),
+    "lg_group_ppo_update": (I32, [P, ctypes.POINTER(P)]),
+    "lg_group_iterate": (I32, [P, ctypes.POINTER(P)]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(_lib, _n)
@@ -259,3 +267,36 @@ def lg_graph_kernel_count(ctx):
     n = I32()
     st = _lib.lg_graph_kernel_count(ctx, ctypes.byref(n))
     return st, n.value
+
+
+def lg_group_create(ctxs):
+    arr = (P * len(ctxs))(*[c.value if isinstance(c, P) else c for c in ctxs])
+    out = P()
+    st = _lib.lg_group_create(arr, len(ctxs), ctypes.byref(out))
+    return st, out
+
+
+def lg_group_destroy(g):
+    return _lib.lg_group_destroy(g)
+
+
+def lg_group_broadcast_params(g):
+    return _lib.lg_group_broadcast_params(g)
+
+
+def lg_group_compute_gae(g):
+    return _lib.lg_group_compute_gae(g)
+
+
+def _stats_arr(stats):
+    if stats is None:
+        return None
+    return (P * len(stats))(*[_p(s) for s in stats])
+
+
+def lg_group_ppo_update(g, stats=None):
+    return _lib.lg_group_ppo_update(g, _stats_arr(stats))
+
+
+def lg_group_iterate(g, stats=None):
+    return _lib.lg_group_iterate(g, _stats_arr(stats))

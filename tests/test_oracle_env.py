@@ -157,16 +157,6 @@ def test_pd_torque_examples_and_free_fall():
     vz = env.state["v"][0][2]
     assert abs(vz - (-4 * 9.81 * 0.005)) < 1e-6                 # 4 substeps of Δv_z = −0.04905
     assert np.all(env.state["v"][0][:2] == 0.0)
-    # Kp·0.1 = 5 N·m (first substep): q* - q = 0.1 via the action (a = 0.2 -> 0.5a = 0.1)
-    _place(env, 0, 5.0)
-    a = np.zeros(12, np.float32)
-    a[1] = 0.2
-    env.state["q"][0][1] = np.float32(0.7)
-    tau, *_ = env.transition_single(0, a)
-    # last-substep τ differs from 5 because q moved; check the first-substep value directly:
-    _place(env, 0, 5.0)
-    qs = np.float32(0.7) + np.float32(0.5) * np.float32(0.2)
-    assert abs(np.float32(50.0) * (qs - np.float32(0.7)) - 5.0) < 1e-5
     # saturation: q* - q = 10 -> τ = τ_max = 80 exactly
     _place(env, 0, 5.0)
     a = np.zeros(12, np.float32)
@@ -418,3 +408,123 @@ def test_feistel_is_bijection(B):
     assert np.array_equal(np.sort(p), np.arange(B, dtype=np.uint32))
     if B > 1000:
         assert np.mean(p[:-1] < p[1:]) < 0.6                     # actually shuffled
+
+
+def test_pd_joint_through_the_transition_kp80():
+    """PD law through the oracle's transition (DESIGN §3.5 with R24's Kp = 80): a robot in the air (no
+    contact, so the joint is decoupled from the base) gets q* - q = 0.1 on one joint.  Four semi-implicit Euler
+    substeps of the scalar joint model J q̈ = Kp(q* - q) - Kd q̇ - c_j q̇ (J = 0.25, Kd = 2, c_j = 0.5, dt = 5 ms),
+    evaluated here in fp64, fix the last substep's τ and q̈ the transition reports and the joint state it leaves.
+    The first substep's torque is Kp·0.1 = 8 N·m; Kp = 50 would give 5 and a different trajectory."""
+    env = _env()
+    env.reset()
+    for j, qs in ((1, 0.1), (8, -0.1), (3, 0.1)):
+        _place(env, 0, 5.0)
+        a = np.zeros(12, np.float32)
+        a[j] = np.float32(2.0 * qs)                       # q* = q_def + 0.5 a  ->  q* - q = qs
+        q, qd, taus = 0.0, 0.0, []
+        for _ in range(4):
+            tau = max(-80.0, min(80.0, 80.0 * (qs - q) - 2.0 * qd))
+            taus.append(tau)
+            qdd = (tau - 0.5 * qd) / 0.25
+            qd += 0.005 * qdd
+            q += 0.005 * qd
+        assert abs(taus[0] - 80.0 * qs) < 1e-12           # 8 N·m in the first substep
+        tau_o, qdd_o, *_ = env.transition_single(0, a)
+        assert abs(tau_o[j] - taus[-1]) < 2e-4, (tau_o[j], taus[-1])
+        assert abs(qdd_o[j] - qdd) < 1e-3
+        assert abs((env.state["q"][0][j] - QDEF[j]) - q) < 1e-6
+        assert abs(env.state["qd"][0][j] - qd) < 1e-5
+        others = [k for k in range(12) if k != j]
+        assert np.all(tau_o[others] == 0.0) and np.all(qdd_o[others] == 0.0)
+
+
+def _ramp_world(a, b, levels=2, cols=2):
+    """Heightfield of a plane: node (i, j) -- at the cell centre ((i+1/2)·0.1, (j+1/2)·0.1) -- holds a·i + b·j."""
+    i = np.arange(80 * levels, dtype=np.float64)[:, None]
+    j = np.arange(80 * cols, dtype=np.float64)[None, :]
+    return (a * i + b * j).astype(np.float32)
+
+
+def _yaw_pitch_quat(yaw, pitch=0.0):
+    """(w, x, y, z) of R = R_z(yaw) R_y(pitch)."""
+    cy, sy, cp, sp = math.cos(yaw / 2), math.sin(yaw / 2), math.cos(pitch / 2), math.sin(pitch / 2)
+    return np.array([cy * cp, -sy * sp, cy * sp, sy * cp])
+
+
+def _rotmat(q):
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+@pytest.mark.parametrize("yaw", [0.0, math.pi / 2, 0.7])
+def test_height_scan_on_a_ramp_rotates_with_heading(yaw):
+    """R1-R3: bilinear interpolation is exact on a plane, so on the ramp world
+    h(x, y) = a·(10x - 1/2) + b·(10y - 1/2) and scan point k = 11·ix + iy at offset ((ix-8)·0.1, (iy-5)·0.1)
+    rotated by the heading ψ must read p_z - h(p + R_z(ψ)·offset).  a != b, so a transposed layout, a wrong
+    rotation sense or a swapped axis fails at yaw π/2 and 0.7."""
+    a, b = 0.013, 0.029
+    hf = _ramp_world(a, b)
+    env = oracle.Env(1, hf, 2, 2, seed=1, scan=(17, 11), flags=0)
+    env.reset()
+    px, py, pz = 8.05, 7.9, 5.0
+    env.state["p"][0] = (px, py, pz)
+    env.state["quat"][0] = _yaw_pitch_quat(yaw)
+    obs = env.observe()[0]
+    c, s = math.cos(yaw), math.sin(yaw)
+    want = np.zeros(187)
+    for ix in range(17):
+        for iy in range(11):
+            dx, dy = (ix - 8) * 0.1, (iy - 5) * 0.1
+            x, y = px + c * dx - s * dy, py + s * dx + c * dy
+            want[11 * ix + iy] = pz - (a * (10 * x - 0.5) + b * (10 * y - 0.5))
+    got = obs[48:].astype(np.float64)
+    assert np.max(np.abs(got - want)) < 2e-5, np.max(np.abs(got - want))
+    # and the layout really matters here: the transposed reading (k = 17·iy + ix) is far off
+    assert np.max(np.abs(got.reshape(17, 11).T.reshape(-1)[:187] - want)) > 1e-2
+
+
+def test_reward_heading_frame_at_yaw_pi_over_2():
+    """R6 ('the z axis is aligned with gravity'): the tracking terms use the velocity in the heading frame.
+    A robot yawed by π/2 moving along world +y at 0.7 m/s, commanded (0.7, 0) in its own frame, tracks perfectly:
+    r1 = 1·dt·φ(0) = 0.02, r2 = 0.5·dt = 0.01 (Table 2).  With the frame rotated the wrong way, or not at all,
+    the error would be √2·0.7 or 0.7·|(1, -1)| and r1 < 0.0004."""
+    z12 = np.zeros(12, np.float32)
+    rec = _rec(v=(0.0, 0.7, 0.0), w=(0.0, 0.0, 0.0), cmd=(0.7, 0.0, 0.0))
+    rec["quat"] = _yaw_pitch_quat(math.pi / 2)
+    terms, _ = oracle.reward_terms(rec, z12, z12, z12, 0.0, 0)
+    assert abs(terms[0] - 0.02) < 1e-6 and abs(terms[1] - 0.01) < 1e-6
+    rec["v"] = (0.7, 0.0, 0.0)                            # moving along world x = sideways for this robot
+    terms, _ = oracle.reward_terms(rec, z12, z12, z12, 0.0, 0)
+    assert abs(terms[0] - 0.02 * math.exp(-(0.49 + 0.49) / 0.25)) < 1e-6
+    # yaw rate: ω_b = (0, 0, 0.4) at yaw π/2 -> heading-frame ω_z = 0.4 (z is shared), command 0.4 -> r2 = 0.01
+    rec["v"] = (0.0, 0.7, 0.0)
+    rec["w"] = (0.0, 0.0, 0.4)
+    rec["cmd"] = (0.7, 0.0, 0.4)
+    terms, _ = oracle.reward_terms(rec, z12, z12, z12, 0.0, 0)
+    assert abs(terms[1] - 0.01) < 1e-6
+
+
+@pytest.mark.parametrize("yaw,pitch", [(0.9, 0.3), (-2.2, -0.45), (math.pi / 2, 0.2)])
+def test_observation_body_frame_at_pitched_yawed_pose(yaw, pitch):
+    """S:247 / SURVEY O-O: obs[0:3] = Rᵀ v (base-frame linear velocity), obs[3:6] = ω_b, obs[6:9] = Rᵀ (0, 0, -1)
+    (projected gravity), with R from the base quaternion -- checked against a numpy rotation at a pitched and
+    yawed pose (a transposed R, a wrong quaternion convention or world-frame values fail)."""
+    env = _env(flags=0)
+    env.reset()
+    _place(env, 0, 3.0)
+    q = _yaw_pitch_quat(yaw, pitch)
+    env.state["quat"][0] = q
+    v = np.array([0.6, -0.3, 0.25])
+    w = np.array([0.2, 0.5, -0.7])
+    env.state["v"][0] = v
+    env.state["w"][0] = w
+    obs = env.observe()[0].astype(np.float64)
+    R = _rotmat(q.astype(np.float32).astype(np.float64))
+    assert np.max(np.abs(obs[0:3] - R.T @ v)) < 2e-6
+    assert np.max(np.abs(obs[3:6] - w)) < 1e-7
+    assert np.max(np.abs(obs[6:9] - R.T @ np.array([0.0, 0.0, -1.0]))) < 2e-6
+    # sanity of the fixture itself: pitch tilts gravity into the body x axis
+    assert abs(obs[6] - math.sin(pitch)) < 1e-5
