@@ -256,6 +256,10 @@ lg_status lg_graph_kernel_count(lg_ctx* ctx, int32_t* n_h);
  * time-outs compacted since the current rollout began, non-finite skips, applied updates, last KL (fp32 bits)} */
 lg_status lg_device_scalars(lg_ctx* ctx, int32_t* out8_h);
 
+/* Debug/introspection: the advantage normalisation of the current batch (R13: union over the ranks, unbiased
+ * std, ε = 1e-8), written by storage_compute_gae: Â = (A - mean) * inv_std with inv_std = 1 / (std + 1e-8). */
+lg_status lg_adv_normalization(lg_ctx* ctx, double* mean_h, double* inv_std_h);
+
 /* Per-category device timing (measurement only). enable != 0: every later launch is bracketed by a
  * CUDA event pair on the context stream (also inside lg_graph_capture_iteration, as event-record
  * nodes). lg_profile_read (after the stream is idle) adds the elapsed ms and launch counts of all

@@ -242,3 +242,48 @@ def ppo_update(theta, m, v, t_adam, alpha, batch: dict, perms, obs_dim, hidden=(
             st["alpha"] = alpha
             stats.append(st)
     return theta, m, v, t_adam, alpha, stats
+
+
+def ppo_update_union(theta, m, v, t_adam, alpha, batches: list, perms: list, obs_dim, hidden=(512, 256, 128),
+                     n_epochs=5, n_minibatches=4, gamma=0.99, lam=0.95, bootstrap=True, kl_target=0.01, quant=None):
+    """One PPO update over W ranks' batches with the multi-rank semantics of SURVEY §8(c).1 O-M:
+    GAE per rank; advantages normalised over the union of all ranks' samples (R13); the global minibatch (e, k)
+    is the union, in rank order, of every rank's minibatch k of epoch e under that rank's own permutation
+    perms[r][e]; the gradient is that of the union minibatch's mean loss and the KL its mean (so Alg. 1 and
+    Adam act identically on every replica).  batches[r] / perms[r] as in ppo_update.  With W = 1 this is
+    ppo_update.  Returns (theta, m, v, t_adam, alpha, stats list)."""
+    W = len(batches)
+    T, N = batches[0]["r"].shape
+    B = T * N
+    cols = {k: [] for k in ("obs", "act", "mu", "logp", "V", "A", "R")}
+    for bt in batches:
+        A, Ret = gae(bt["r"], bt["V"], bt["V_T"], bt["b"], bt["term"], bt["timeout"], gamma, lam, bootstrap)
+        cols["A"].append(A.reshape(B))
+        cols["R"].append(Ret.reshape(B))
+        cols["obs"].append(np.asarray(bt["obs"], np.float64).reshape(B, -1)[:, :obs_dim])
+        cols["act"].append(np.asarray(bt["act"], np.float64).reshape(B, -1))
+        cols["mu"].append(np.asarray(bt["mu"], np.float64).reshape(B, -1))
+        cols["logp"].append(np.asarray(bt["logp"], np.float64).reshape(B))
+        cols["V"].append(np.asarray(bt["V"], np.float64).reshape(B))
+    An = normalize_adv(np.concatenate(cols["A"])).reshape(W, B)  # union statistics
+    ls_old = np.asarray(batches[0]["logstd_old"], np.float64)
+    Mb = B // n_minibatches
+    theta = np.asarray(theta, np.float64).copy()
+    stats = []
+    for e in range(n_epochs):
+        for k in range(n_minibatches):
+            idx = [np.asarray(perms[r][e], np.int64)[k * Mb:(k + 1) * Mb] for r in range(W)]
+            u = lambda name: np.concatenate([cols[name][r][idx[r]] for r in range(W)])  # noqa: E731
+            adv = np.concatenate([An[r][idx[r]] for r in range(W)])
+            p = unpack(theta, obs_dim, hidden)
+            g, st = ppo_minibatch(p, u("obs"), u("act"), u("logp"), u("V"), adv, u("R"), u("mu"), ls_old, quant=quant)
+            gflat = pack(g, obs_dim, hidden)
+            if not (np.isfinite(st["loss"]) and np.all(np.isfinite(gflat))):
+                st["skipped"] = True
+                stats.append(st)
+                continue
+            alpha = alg1(st["kl"], alpha, kl_target)
+            theta, m, v, t_adam = adam_step(theta, gflat, m, v, t_adam, alpha)
+            st["alpha"] = alpha
+            stats.append(st)
+    return theta, m, v, t_adam, alpha, stats

@@ -192,6 +192,11 @@ class Context:
         return dict(s_base=v[0], iteration=v[1], adam_t=v[2], alpha=alpha, n_to_total=v[4], nonfinite_skips=v[5],
                     applied=v[6], kl_last=kl)
 
+    def adv_normalization(self):
+        st, mean, inv_std = lg.lg_adv_normalization(self.ctx)
+        self._ck(st, "lg_adv_normalization")
+        return mean, inv_std
+
     def profile(self, enable=True):
         self._ck(lg.lg_profile(self.ctx, enable), "lg_profile")
 

@@ -1418,17 +1418,16 @@ lg_status lg_group_create(lg_ctx* const* ctxs_h, int32_t n, lg_group** out_h) {
   if (!ctxs_h || !out_h || n < 1 || n > LG_MAX_GROUP) return LG_ERR_INVALID_ARG;
   for (int r = 0; r < n; ++r)
     if (!ctxs_h[r]) return LG_ERR_INVALID_ARG;
+  // validation only returns a status: a refused grouping leaves the contexts usable (no sticky error)
   for (int r = 0; r < n; ++r) {
     lg_ctx* ctx = ctxs_h[r];
     if (ctx->err != LG_OK) return ctx->err;
-    if (ctx->group || ctx->comm) return fail(ctx, LG_ERR_STATE, "lg_group_create: already grouped or on NCCL");
-    if (ctx->cfg.world_size != n || ctx->cfg.rank != r)
-      return fail(ctx, LG_ERR_INVALID_ARG, "lg_group_create: context %d has rank %d of world %d", r, ctx->cfg.rank,
-                  ctx->cfg.world_size);
-    if (ctx->st != ctxs_h[0]->st) return fail(ctx, LG_ERR_INVALID_ARG, "lg_group_create: ranks must share one stream");
+    if (ctx->group || ctx->comm) return LG_ERR_STATE;
+    if (ctx->cfg.world_size != n || ctx->cfg.rank != r) return LG_ERR_INVALID_ARG;
+    if (ctx->st != ctxs_h[0]->st) return LG_ERR_INVALID_ARG;
     lg_config a = ctx->cfg, b = ctxs_h[0]->cfg;
     a.rank = b.rank = 0;
-    if (memcmp(&a, &b, sizeof(a)) != 0) return fail(ctx, LG_ERR_INVALID_ARG, "lg_group_create: configs differ");
+    if (memcmp(&a, &b, sizeof(a)) != 0) return LG_ERR_INVALID_ARG;
   }
   lg_group* g = new lg_group();
   g->n = n;
@@ -1518,6 +1517,17 @@ lg_status lg_profile_read(lg_ctx* ctx, float* ms_h, int32_t* count_h, int32_t n)
     if (p.cat < n) { ms_h[p.cat] += ms; count_h[p.cat] += 1; }
   }
   if (eager) { ctx->pairs.clear(); ctx->evn = 0; }
+  return LG_OK;
+}
+
+lg_status lg_adv_normalization(lg_ctx* ctx, double* mean_h, double* inv_std_h) {
+  GUARD();
+  if (!mean_h || !inv_std_h) return fail(ctx, LG_ERR_INVALID_ARG, "null output");
+  DevScalars s;
+  CK(cudaMemcpyAsync(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  *mean_h = s.adv_mean;
+  *inv_std_h = s.adv_inv_std;
   return LG_OK;
 }
 

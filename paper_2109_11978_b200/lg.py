@@ -53,7 +53,7 @@ EXPORTS = ["lg_num_params", "lg_obs_dim", "lg_obs_stride", "lg_required_sizes", 
            "lg_nccl_unique_id", "lg_set_nccl", "lg_broadcast_params", "lg_iterate_host",
            "lg_graph_capture_iteration", "lg_graph_launch", "lg_device_scalars", "lg_profile", "lg_profile_read", "lg_graph_kernel_count",
            "lg_terrain_generate", "lg_group_create", "lg_group_destroy", "lg_group_broadcast_params",
-           "lg_group_compute_gae", "lg_group_ppo_update", "lg_group_iterate"]
+           "lg_group_compute_gae", "lg_group_ppo_update", "lg_group_iterate", "lg_adv_normalization"]
 MAX_GROUP = 8
 PROF_CATS = ["env", "gemm_roll", "gemm_fwd", "gemm_dx", "gemm_dw", "heads", "loss", "reduce", "gather", "adam", "gae",
              "comm", "misc"]
@@ -95,6 +95,7 @@ _sig = {
     "lg_graph_kernel_count": (I32, [P, ctypes.POINTER(I32)]),
     "lg_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(I32), I32]),
     "lg_terrain_generate": (I32, [P, I32, I32, ctypes.c_uint64, P]),
+    "lg_adv_normalization": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "lg_group_create": (I32, [ctypes.POINTER(P), I32, ctypes.POINTER(P)]),
     "lg_group_destroy": (I32, [P]),
     "lg_group_broadcast_params": (I32, [P]),
@@ -300,3 +301,9 @@ def lg_group_ppo_update(g, stats=None):
 
 def lg_group_iterate(g, stats=None):
     return _lib.lg_group_iterate(g, _stats_arr(stats))
+
+
+def lg_adv_normalization(ctx):
+    m, i = ctypes.c_double(), ctypes.c_double()
+    st = _lib.lg_adv_normalization(ctx, ctypes.byref(m), ctypes.byref(i))
+    return st, m.value, i.value

@@ -1,0 +1,267 @@
+"""GPU: the multi-rank path of the library through the C ABI, on one device.
+
+Every rank of a world of W is its own lg context (world_size = W, its rank, one shared stream) bound into an
+lg_group: per-rank rollout, GAE, shuffle, gather, forward/backward and Adam run exactly as in the
+one-process-per-GPU path; the allreduces (advantage statistics, [gradient ‖ stats] per minibatch) are one
+rank-ordered sum kernel over all ranks' buffers (no kernel waits on another -- B200_PROFILING.md).  Checked:
+rank r's rollout equals rows [rN, (r+1)N) of a single-context rollout over W·N envs bit for bit (RNG keyed by
+global env id), θ is bit-identical on every rank after each iteration, and θ matches the oracle's union-
+minibatch update (O-M).  Also the runtime conditions of SPEC S:287 / S:428 (fault injection) and the
+world_size > 1 guard."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+from oracle import learn  # noqa: E402
+import synth  # noqa: E402
+from paper_2109_11978_b200 import lg  # noqa: E402
+from paper_2109_11978_b200.context import Config, Context, Group  # noqa: E402
+
+ALL = lg.F_CURRICULUM | lg.F_NOISE | lg.F_PUSH | lg.F_BOOTSTRAP
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+def _cfg(N, T, rank=0, world=1, seed=17, flags=ALL, E=5, K=4):
+    return Config.make(n_envs=N, n_steps=T, n_levels=4, n_cols=5, flags=flags, seed=seed, rank=rank,
+                       world_size=world, n_epochs=E, n_minibatches=K)
+
+
+def _batch(ctx):
+    T, N = ctx.T, ctx.N
+    flags = ctx.storage("FLAGS", torch.uint8).cpu().numpy()
+    return dict(obs=ctx.obs[:T].float().cpu().numpy(), act=ctx.storage("ACT", extra=(12,)).cpu().numpy(),
+                mu=ctx.storage("MU", extra=(12,)).cpu().numpy(), logp=ctx.storage("LOGP").cpu().numpy(),
+                V=ctx.storage("VALUE").cpu().numpy(), r=ctx.storage("REWARD").cpu().numpy(),
+                b=ctx.storage("BOOT").cpu().numpy(), term=flags & 1, timeout=(flags >> 1) & 1,
+                V_T=ctx.view("VALUE_T", torch.float32, (N,)).cpu().numpy(), logstd_old=ctx.theta[-12:].cpu().numpy())
+
+
+def _perms(ctx):
+    B = ctx.N * ctx.T
+    pt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    out = []
+    for e in range(ctx.cfg.n_epochs):
+        ctx.shuffle(e, pt)
+        ctx.sync()
+        out.append(pt.cpu().numpy().view(np.uint32).copy())
+    return out
+
+
+@pytest.mark.parametrize("W,N,T", [(2, 256, 8), (4, 128, 12)])
+def test_group_rollout_update_vs_single_context_and_union_oracle(W, N, T):
+    hf = synth.make_world(4, 5, seed=3, rough=True)
+    cfg1 = _cfg(W * N, T)
+    theta = synth.init_params(cfg1.obs_dim, cfg1.hidden, seed=17)
+    single = Context(cfg1, hf)
+    single.params_set(theta)
+    stream = torch.cuda.Stream()
+    ranks = [Context(_cfg(N, T, r, W), hf, stream=stream) for r in range(W)]
+    for c in ranks:
+        c.params_set(theta)
+    grp = Group(ranks)
+    # --- rollout: rank r == rows [rN, (r+1)N) of the single W·N-env context, bit for bit
+    single.reset()
+    for c in ranks:
+        c.reset()
+    for t in range(T):
+        single.policy_act(t)
+        single.env_step(t)
+        for c in ranks:
+            c.policy_act(t)
+            c.env_step(t)
+    single.sync()
+    grp.sync()
+    whole_state = single.state_words.cpu().numpy()
+    for r, c in enumerate(ranks):
+        sl = slice(r * N, (r + 1) * N)
+        assert np.array_equal(c.state_words.cpu().numpy(), whole_state[:, sl]), r
+        assert torch.equal(c.obs.cpu(), single.obs[:, sl].cpu()), r
+        for name, ex in (("ACT", (12,)), ("MU", (12,)), ("LOGP", ()), ("VALUE", ()), ("REWARD", ()), ("BOOT", ())):
+            assert torch.equal(c.storage(name, extra=ex).cpu(), single.storage(name, extra=ex)[:, sl].cpu()), (r, name)
+        assert torch.equal(c.storage("FLAGS", torch.uint8).cpu(), single.storage("FLAGS", torch.uint8)[:, sl].cpu())
+    # --- GAE: per env, so equal to the single context's columns; the union statistics are the group's
+    grp.compute_gae()
+    single.compute_gae()
+    grp.sync()
+    single.sync()
+    for r, c in enumerate(ranks):
+        sl = slice(r * N, (r + 1) * N)
+        for name in ("ADV", "RET", "BOOT"):
+            assert torch.equal(c.storage(name).cpu(), single.storage(name)[:, sl].cpu()), (r, name)
+        assert torch.equal(c.view("VALUE_T", torch.float32, (N,)).cpu(),
+                          single.view("VALUE_T", torch.float32, (W * N,))[sl].cpu())
+    batches = [_batch(c) for c in ranks]
+    perms = [_perms(c) for c in ranks]
+    # --- update with the per-minibatch gradient sum; replicas bit-identical; union oracle (O-M)
+    stats = [torch.zeros(64, dtype=torch.int32, device="cuda") for _ in range(W)]
+    grp.update(stats)
+    grp.sync()
+    th = [c.theta.cpu().numpy() for c in ranks]
+    for r in range(1, W):
+        assert np.array_equal(th[r], th[0]), r
+    sc = [c.scalars() for c in ranks]
+    assert all(s == sc[0] for s in sc)
+    z = np.zeros(theta.size)
+    th_q, _, _, t_q, a_q, _ = learn.ppo_update_union(theta.astype(np.float64), z, z.copy(), 0, 1e-3, batches, perms,
+                                                     cfg1.obs_dim, cfg1.hidden, quant="bf16")
+    th_x, _, _, t_x, a_x, _ = learn.ppo_update_union(theta.astype(np.float64), z, z.copy(), 0, 1e-3, batches, perms,
+                                                     cfg1.obs_dim, cfg1.hidden)
+    assert sc[0]["adam_t"] == t_q == t_x == 20
+    assert abs(sc[0]["alpha"] - a_q) <= 1e-6 * a_q
+    d_q, d_x, d_ox = rel(th[0], th_q), rel(th[0], th_x), rel(th_q, th_x)
+    print(f"W={W}: drift vs union oracle at the GPU rounding points {d_q:.3e}, vs fp64 union oracle {d_x:.3e} "
+          f"(oracle bf16-vs-fp64 {d_ox:.3e})")
+    assert d_q <= 1e-3
+    assert d_x <= d_ox + 1e-3                              # DESIGN R28
+    # --- a second iteration through the whole-iteration group call keeps the replicas identical
+    grp.iteration(stats)
+    grp.sync()
+    th2 = [c.theta.cpu().numpy() for c in ranks]
+    for r in range(1, W):
+        assert np.array_equal(th2[r], th2[0])
+    assert not np.array_equal(th2[0], th[0])
+    for s in stats:
+        d = lg.lg_update_stats.from_buffer_copy(s.cpu().numpy().tobytes())
+        assert d.minibatches_applied == 20 and d.nonfinite_skips == 0
+    grp.close()
+
+
+def test_group_rejects_mismatched_ranks_and_solo_calls():
+    hf = synth.make_world(4, 5, seed=3, rough=True)
+    stream = torch.cuda.Stream()
+    a = Context(_cfg(64, 4, 0, 2), hf, stream=stream)
+    b = Context(_cfg(64, 4, 0, 2), hf, stream=stream)       # rank 0 twice
+    with pytest.raises(lg.LgError):
+        Group([a, b])
+    c = Context(_cfg(64, 4, 1, 2), hf, stream=torch.cuda.Stream())   # rank 1 on another stream
+    with pytest.raises(lg.LgError):
+        Group([a, c])
+    g = Group([a, Context(_cfg(64, 4, 1, 2), hf, stream=stream)])      # a refused grouping left `a` usable
+    with pytest.raises(lg.LgError, match="LG_ERR_STATE"):
+        a.compute_gae()                                                 # grouped: the solo call refuses
+    g.close()
+    # world_size 2 without a communicator or group: the learning calls refuse to run (no silent 1/W scaling)
+    e = Context(_cfg(64, 4, 0, 2), hf)
+    e.params_set(synth.init_params(e.cfg.obs_dim, e.cfg.hidden, seed=1))
+    e.reset()
+    for t in range(4):
+        e.policy_act(t)
+        e.env_step(t)
+    with pytest.raises(lg.LgError, match="LG_ERR_STATE"):
+        e.compute_gae()
+
+
+# ------------------------------------------------------------------ runtime conditions (fault injection)
+def _gpu_state(ctx):
+    return ctx.state_words.t().contiguous().cpu().numpy().view(oracle.STATE_DTYPE).reshape(-1)
+
+
+def _set_gpu_state(ctx, st):
+    w = np.ascontiguousarray(st).view(np.int32).reshape(len(st), 66)
+    ctx.state_words.copy_(torch.from_numpy(np.ascontiguousarray(w.T)).cuda())
+    torch.cuda.synchronize()
+
+
+def test_nonfinite_env_state_forces_terminated_reset_and_is_counted():
+    """SPEC S:287 (env.step errors): non-finite dynamics -> forced reset with the terminated flag and zero
+    reward, counted (lg_update_stats.nonfinite_envs).  A NaN velocity is injected into one env on both sides;
+    the whole state, observation, reward and flags stay bit-exact with the oracle through the incident."""
+    N, T = 96, 6
+    cfg = _cfg(N, T)
+    hf = synth.make_world(4, 5, seed=3, rough=True)
+    ctx = Context(cfg, hf)
+    ctx.params_set(synth.init_params(cfg.obs_dim, cfg.hidden, seed=2))
+    env = oracle.Env(N, hf, 4, 5, seed=cfg.seed, flags=ALL)
+    ctx.reset()
+    env.reset()
+    ctx.sync()
+    rng = np.random.default_rng(4)
+    obs_g = torch.zeros(N, cfg.obs_dim, device="cuda")
+    rew_g = torch.zeros(N, device="cuda")
+    term_g = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    for t in range(T):
+        if t == 2:
+            st = env.state.copy()
+            st["v"][5][0] = np.float32(np.nan)
+            st["qd"][40][7] = np.float32(np.inf)
+            env.state[:] = st
+            _set_gpu_state(ctx, st)
+        a = (0.3 * rng.standard_normal((N, 12))).astype(np.float32)
+        ctx.env_step(t, actions=torch.from_numpy(a).cuda(), obs=obs_g, reward=rew_g, terminated=term_g)
+        o, r, te, to, _, _ = env.step(a)
+        ctx.sync()
+        assert _gpu_state(ctx).tobytes() == env.state.tobytes(), t
+        assert np.array_equal(o, obs_g.cpu().numpy()) and np.array_equal(r, rew_g.cpu().numpy()), t
+        assert np.array_equal(te, term_g.cpu().numpy()), t
+        if t == 2:
+            assert te[5] == 1 and te[40] == 1 and r[5] == 0.0 and r[40] == 0.0
+            st = env.state
+            assert st["ep_step"][5] == 0 and st["ep_step"][40] == 0          # reset in place
+            assert np.all(np.isfinite(st["v"][5])) and np.all(np.isfinite(st["qd"][40]))
+    ctx.compute_gae()
+    stats = torch.zeros(64, dtype=torch.int32, device="cuda")
+    ctx.update(stats)
+    ctx.sync()
+    s = lg.lg_update_stats.from_buffer_copy(stats.cpu().numpy().tobytes())
+    assert s.nonfinite_envs == 2 and s.nonfinite_skips == 0
+
+
+def test_nonfinite_advantage_skips_its_minibatches_on_gpu_and_oracle():
+    """SPEC S:428 (ppo.update errors): a non-finite loss skips the minibatch (no Alg. 1 step, no Adam step, no
+    step count) and records it.  One sample's advantage is set to NaN after GAE: it lies in exactly one
+    minibatch per epoch, so E of the E·K minibatches are skipped.  The oracle takes the same rule (a non-finite
+    sample in the same minibatches) and the updates agree within the drift bound."""
+    N, T, E, K = 256, 8, 5, 4
+    cfg = _cfg(N, T, E=E, K=K)
+    hf = synth.make_world(4, 5, seed=3, rough=True)
+    ctx = Context(cfg, hf)
+    theta = synth.init_params(cfg.obs_dim, cfg.hidden, seed=6)
+    ctx.params_set(theta)
+    ctx.reset()
+    for t in range(T):
+        ctx.policy_act(t)
+        ctx.env_step(t)
+    ctx.compute_gae()
+    ctx.sync()
+    bt = _batch(ctx)
+    perms = _perms(ctx)
+    t_bad, i_bad = 3, 77
+    adv = ctx.storage("ADV")
+    adv[t_bad, i_bad] = float("nan")
+    torch.cuda.synchronize()
+    stats = torch.zeros(64, dtype=torch.int32, device="cuda")
+    ctx.update(stats)
+    ctx.sync()
+    s = lg.lg_update_stats.from_buffer_copy(stats.cpu().numpy().tobytes())
+    sc = ctx.scalars()
+    assert s.nonfinite_skips == E and s.minibatches_applied == E * K - E
+    assert sc["adam_t"] == E * K - E and sc["nonfinite_skips"] == E
+    th = ctx.theta.cpu().numpy()
+    assert np.all(np.isfinite(th))
+    # the oracle: the same sample made non-finite (its observation), the same skip rule
+    bo = dict(bt)
+    bo["obs"] = bt["obs"].copy()
+    bo["obs"][t_bad, i_bad, 0] = np.nan
+    z = np.zeros(theta.size)
+    with np.errstate(invalid="ignore"):
+        th_q, _, _, t_q, a_q, st_q = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bo, perms,
+                                                      cfg.obs_dim, cfg.hidden, quant="bf16")
+    assert sum(1 for x in st_q if x.get("skipped")) == E and t_q == sc["adam_t"]
+    b_flat = t_bad * N + i_bad
+    M = N * T // K
+    for e in range(E):                                   # the skipped minibatch of each epoch holds the sample
+        k = int(np.nonzero(perms[e] == b_flat)[0][0]) // M
+        assert st_q[e * K + k].get("skipped")
+    assert abs(sc["alpha"] - a_q) <= 1e-6 * a_q
+    assert rel(th, th_q) <= 1e-3

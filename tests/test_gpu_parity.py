@@ -51,6 +51,25 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
+def assert_bf16_close(a, ref, what=""):
+    """SURVEY §8(c).4 bf16 MLP outputs and gradients: ‖Δ‖/‖ref‖ <= 2e-2 per tensor AND elementwise
+    |Δ| <= 2e-2·(|ref| + rms(ref))."""
+    a = np.asarray(a, np.float64)
+    ref = np.asarray(ref, np.float64)
+    r = rel(a, ref)
+    assert r <= 2e-2, (what, r)
+    bound = 2e-2 * (np.abs(ref) + np.sqrt(np.mean(ref ** 2)))
+    worst = np.max(np.abs(a - ref) / np.maximum(bound, 1e-300)) if ref.size else 0.0
+    assert worst <= 1.0, (what, worst)
+
+
+def per_tensor_drift(th, ref, D, hidden):
+    """‖Δθ‖ / ‖θ_ref‖ per parameter tensor and overall."""
+    pt = learn.unpack(np.asarray(th, np.float64) - ref, D, hidden)
+    nr = np.linalg.norm(ref)
+    return {k: np.linalg.norm(v) / nr for k, v in pt.items()}
+
+
 def close_mixed(a, b, tol):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
@@ -170,7 +189,7 @@ def test_timeout_bootstrap_values_vs_oracle():
     ctx.sync()
     b = ctx.storage("BOOT").cpu().numpy()
     assert np.all(b[~mask] == 0.0)
-    assert rel(b[mask], want[mask]) < 2e-2
+    assert_bf16_close(b[mask], want[mask], "BOOT")
     assert int(ctx.scalars()["n_to_total"]) == int(mask.sum())
 
 
@@ -227,8 +246,8 @@ def test_policy_forward_vs_oracle(hidden, scan, M):
     ctx.sync()
     mu_o, v_o = _oracle_forward(theta, xb.float().cpu().numpy()[:, :cfg.obs_dim], cfg.obs_dim, hidden)
     mg, vg = mu.cpu().numpy(), v.cpu().numpy()
-    assert rel(mg, mu_o) < 2e-2 and rel(vg, v_o) < 2e-2
-    assert np.all(np.abs(mg - mu_o) <= 2e-2 * (np.abs(mu_o) + np.sqrt(np.mean(mu_o ** 2))))
+    assert_bf16_close(mg, mu_o, "mu")
+    assert_bf16_close(vg, v_o, "V")
 
 
 def test_policy_act_rollout_vs_oracle():
@@ -245,7 +264,8 @@ def test_policy_act_rollout_vs_oracle():
         val = ctx.storage("VALUE")[t].cpu().numpy()
         x = ctx.obs[t].float().cpu().numpy()[:, :cfg.obs_dim]
         mu_o, v_o = _oracle_forward(theta, x, cfg.obs_dim, cfg.hidden)
-        assert rel(mu, mu_o) < 2e-2 and rel(val, v_o) < 2e-2
+        assert_bf16_close(mu, mu_o, "mu")
+        assert_bf16_close(val, v_o, "V")
         eps = env.action_eps(s=t + 1)                         # Box-Muller noise is bit-defined
         assert np.max(np.abs((act - mu) - eps)) <= 4e-6 * np.max(np.abs(act) + 1)
         lp_o = learn.logp_gauss(act.astype(np.float64), mu.astype(np.float64), np.zeros(12))
@@ -333,7 +353,14 @@ def test_gae_vs_oracle_and_bootstrap_value():
     # V(o_T) is the critic on OBS slot T
     _, v_o = _oracle_forward(theta, ctx.obs[cfg.n_steps].float().cpu().numpy()[:, :cfg.obs_dim], cfg.obs_dim,
                              cfg.hidden)
-    assert rel(bt["V_T"], v_o) < 2e-2
+    assert_bf16_close(bt["V_T"], v_o, "V_T")
+    # the normalisation statistics (R13: whole batch, unbiased std) against the oracle's fp64 definition
+    mean, inv_std = ctx.adv_normalization()
+    assert abs(mean - A_o.mean()) <= 1e-6 * max(1.0, abs(A_o.mean()))
+    assert abs(inv_std * (A_o.std(ddof=1) + 1e-8) - 1.0) <= 1e-6
+    An = learn.normalize_adv(A_o)
+    An_gpu = (A.astype(np.float64) - mean) * inv_std
+    assert np.max(np.abs(An_gpu - An)) <= 1e-5 * max(1.0, np.max(np.abs(An)))
 
 
 def test_gae_synthetic_flags_vs_oracle():
@@ -362,7 +389,8 @@ def _grad_tensors(g, D, hidden):
 @pytest.mark.parametrize("hidden,scan,N,T,K", [((512, 256, 128), (17, 11), 512, 24, 4),
                                                ((128, 64, 32), (0, 0), 64, 24, 4),
                                                ((512, 256, 128), (17, 11), 100, 24, 4),
-                                               ((512, 256, 128), (17, 11), 1024, 24, 2)])
+                                               ((512, 256, 128), (17, 11), 1024, 24, 2),
+                                               ((512, 256, 128), (0, 0), 512, 24, 4)])
 def test_minibatch_gradient_vs_oracle(hidden, scan, N, T, K):
     cfg, ctx, env, theta = make(n_envs=N, T=T, hidden=hidden, scan=scan, rough=scan[0] > 0, K=K,
                                 levels=4 if scan[0] else 1, cols=5 if scan[0] else 1)
@@ -386,14 +414,21 @@ def test_minibatch_gradient_vs_oracle(hidden, scan, N, T, K):
                                   bt["logstd_old"].astype(np.float64))
     G = _grad_tensors(g_gpu, D, hidden)
     for k, ref in g_o.items():
-        assert rel(G[k], ref) < 2e-2, (k, rel(G[k], ref))
+        assert_bf16_close(G[k], ref, k)
     pay = ctx.grad[ctx.P:].cpu().numpy()
     assert abs(pay[0] - st["kl"]) <= 2e-2 * max(abs(st["kl"]), 1e-4)
     assert abs(pay[2] - st["value_loss"]) <= 2e-2 * abs(st["value_loss"])
 
 
-def test_ppo_update_parameter_drift_vs_oracle():
-    cfg, ctx, env, theta = make(n_envs=512, T=24)
+@pytest.mark.parametrize("scan,rough", [((17, 11), True), ((0, 0), False)])
+def test_ppo_update_parameter_drift_vs_oracle(scan, rough):
+    """One complete update (5 x 4 minibatches) against the oracle, rough (C3 network) and flat (C2 network).
+    DESIGN R28: the north_star bound (drift <= 1e-3) holds against the oracle evaluated at the GPU's bf16
+    operand rounding points (SURVEY §8(c).1's switch); against the exact fp64 oracle the GPU may drift by no
+    more than the oracle's own bf16-vs-fp64 gap plus 1e-3 (tools/drift_precision.py: bf16 rounding at any one
+    point alone moves an Adam update by ~2e-3)."""
+    cfg, ctx, env, theta = make(n_envs=512, T=24, scan=scan, rough=rough, levels=4 if rough else 1,
+                                cols=5 if rough else 1)
     _rollout(ctx, cfg)
     ctx.compute_gae()
     ctx.sync()
@@ -410,20 +445,21 @@ def test_ppo_update_parameter_drift_vs_oracle():
     ctx.sync()
     th_gpu = ctx.theta.cpu().numpy().astype(np.float64)
     z = np.zeros(theta.size)
-    # reference with the GPU's documented bf16 rounding points (SURVEY §8(c).1 diagnostic switch, DESIGN R26)
     th_q, m, v, t, alpha, st = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms,
                                                 cfg.obs_dim, cfg.hidden, quant="bf16")
-    # exact fp64 reference
     th_x, *_ = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms, cfg.obs_dim, cfg.hidden)
     sc = ctx.scalars()
     assert sc["adam_t"] == t == 20
     assert abs(sc["alpha"] - alpha) <= 1e-6 * alpha
-    drift_q = rel(th_gpu, th_q)
-    drift_x = rel(th_gpu, th_x)
-    step = rel(th_x, theta)
-    print(f"drift vs bf16-point oracle {drift_q:.3e}; vs exact fp64 oracle {drift_x:.3e}; update size {step:.3e}")
+    drift_q, drift_x, gap = rel(th_gpu, th_q), rel(th_gpu, th_x), rel(th_q, th_x)
+    per = per_tensor_drift(th_gpu, th_x, cfg.obs_dim, cfg.hidden)
+    print(f"drift vs bf16-point oracle {drift_q:.3e}; vs exact fp64 oracle {drift_x:.3e} (oracle gap {gap:.3e}); "
+          f"update size {rel(th_x, theta):.3e}; per tensor vs fp64: " +
+          " ".join(f"{k}:{v:.1e}" for k, v in sorted(per.items(), key=lambda kv: -kv[1])[:6]))
     assert drift_q <= 1e-3
-    assert drift_x <= 1e-2
+    assert drift_x <= gap + 1e-3
+    for k, d in per_tensor_drift(th_gpu, th_q, cfg.obs_dim, cfg.hidden).items():
+        assert d <= 1e-3, k
 
 
 # ------------------------------------------------------------------ whole iteration, graph replay
@@ -591,13 +627,14 @@ def test_rollout_gae_and_minibatch_gradient_full_size_c3():
                                  bt["logstd_old"].astype(np.float64))
     G = _grad_tensors(g_gpu, D, cfg.hidden)
     for k, ref in g_o.items():
-        assert rel(G[k], ref) < 2e-2, (k, rel(G[k], ref))
+        assert_bf16_close(G[k], ref, k)
     assert len(to_idx) == int(bt["timeout"].sum())
 
 
 def test_ppo_update_drift_full_size_c3():
     """All 5 x 4 minibatches of one C3 iteration (M = 24,576): parameter drift after the update against the
-    oracle with the GPU's bf16 rounding points <= 1e-3 relative (BASELINE north_star), Alg. 1 state equal."""
+    oracle with the GPU's bf16 rounding points <= 1e-3 relative (BASELINE north_star), against the exact fp64
+    oracle <= the oracle's own rounding-point gap + 1e-3 (DESIGN R28); Alg. 1 state equal."""
     cfg, ctx, env, theta = make(n_envs=4096, T=24, levels=10, cols=20, seed=1234)
     _rollout(ctx, cfg)
     ctx.compute_gae()
@@ -617,7 +654,11 @@ def test_ppo_update_drift_full_size_c3():
     z = np.zeros(theta.size)
     th_q, m, v, t, alpha, st = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms,
                                                 cfg.obs_dim, cfg.hidden, quant="bf16")
+    th_x, *_ = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bt, perms, cfg.obs_dim, cfg.hidden)
     sc = ctx.scalars()
     assert sc["adam_t"] == t == 20
     assert abs(sc["alpha"] - alpha) <= 1e-6 * alpha
-    assert rel(th_gpu, th_q) <= 1e-3
+    drift_q, drift_x, gap = rel(th_gpu, th_q), rel(th_gpu, th_x), rel(th_q, th_x)
+    print(f"C3 drift vs bf16-point oracle {drift_q:.3e}; vs exact fp64 oracle {drift_x:.3e} (oracle gap {gap:.3e})")
+    assert drift_q <= 1e-3
+    assert drift_x <= gap + 1e-3                          # DESIGN R28

@@ -259,3 +259,28 @@ def test_round_bf16_definition():
     assert np.all(np.abs(q - r) <= 2.0 ** -8 * np.abs(r))          # within half a bf16 ulp (rel 2^-8)
     torch = pytest.importorskip("torch")
     assert np.array_equal(q, torch.from_numpy(r.astype(np.float32)).bfloat16().double().numpy())
+
+
+def test_union_update_single_rank_is_ppo_update_and_union_gradient_is_rank_mean():
+    """O-M: with W = 1 the union update is the single-rank update bit for bit; with W = 2 and
+    identical rank batches and permutations, the union minibatch holds every row twice, so its mean-loss
+    gradient and KL equal the single-rank ones, and the update equals ppo_update on one copy."""
+    rng = np.random.default_rng(0)
+    D, hid = 48, (32, 32, 32)
+    T, N = 4, 24
+    bt = synth.synthetic_storage(T, N, D, seed=5, p_term=0.1, p_timeout=0.05)
+    theta = synth.init_params(D, hid, seed=2).astype(np.float64)
+    perms = [rng.permutation(T * N) for _ in range(2)]
+    z = np.zeros_like(theta)
+    ref = learn.ppo_update(theta, z, z.copy(), 0, 1e-3, bt, perms, D, hid, n_epochs=2, n_minibatches=3)
+    one = learn.ppo_update_union(theta, z, z.copy(), 0, 1e-3, [bt], [perms], D, hid, n_epochs=2, n_minibatches=3)
+    assert np.array_equal(ref[0], one[0]) and ref[3] == one[3] and ref[4] == one[4]
+    two = learn.ppo_update_union(theta, z, z.copy(), 0, 1e-3, [bt, bt], [perms, perms], D, hid, n_epochs=2,
+                                 n_minibatches=3)
+    # the duplicated union normalises with ddof = 1 over 2B samples instead of B: its std is smaller by
+    # sqrt(2(B-1)/(2B-1)), so the two updates agree only to that O(1/B) difference
+    assert two[3] == ref[3] and np.allclose(two[0], ref[0], rtol=0, atol=5e-4)
+    A, _ = learn.gae(bt["r"], bt["V"], bt["V_T"], bt["b"], bt["term"], bt["timeout"])
+    a = A.reshape(-1)
+    s1, s2 = np.std(a, ddof=1), np.std(np.concatenate([a, a]), ddof=1)
+    assert abs(s2 / s1 - np.sqrt(2.0 * (a.size - 1) / (2 * a.size - 1))) < 1e-12
