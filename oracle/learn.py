@@ -64,8 +64,31 @@ def round_bf16(x):
     return b.astype(np.uint32).view(np.float32).astype(np.float64).reshape(np.shape(x))
 
 
-def _q(x, quant):
-    return round_bf16(x) if quant == "bf16" else x
+def round_tf32(x):
+    """Round-to-nearest-even to TF32 (10 explicit mantissa bits) of the fp32 rounding of x, as fp64."""
+    b = np.ascontiguousarray(np.asarray(x, np.float64).astype(np.float32)).view(np.uint32).astype(np.uint64)
+    b = (b + 0xFFF + ((b >> 13) & 1)) & 0xFFFFE000
+    return b.astype(np.uint32).view(np.float32).astype(np.float64).reshape(np.shape(x))
+
+
+def round_fp32(x):
+    return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+
+_ROUND = {"bf16": round_bf16, "tf32": round_tf32, "fp32": round_fp32}
+
+
+def _q(x, quant, point=None):
+    """Rounding of a GEMM operand at one of the GPU path's rounding points (SURVEY §8(c).1 diagnostic switch).
+    quant: None (exact fp64), "bf16" / "tf32" / "fp32" (every point), or "<format>@<point>" (that point only);
+    points: "w" forward weights, "h" stored activations (incl. the input rows), "dz" stored pre-activation
+    gradients, "wb" weights of the input-gradient products."""
+    if quant is None:
+        return x
+    fmt, _, only = quant.partition("@")
+    if only and point != only:
+        return x
+    return _ROUND[fmt](x)
 
 
 def elu(x):
@@ -75,11 +98,11 @@ def elu(x):
 def mlp_forward(p: dict, x: np.ndarray, net: str, quant=None):
     """Returns output and the list of layer inputs/outputs needed by the backward pass.
     quant='bf16' rounds the hidden-layer weights and the stored activations to bf16 (GPU rounding points)."""
-    x = _q(x, quant)
+    x = _q(x, quant, "h")
     acts = [x]
     h = x
     for l in range(1, 4):
-        h = _q(elu(h @ _q(p[f"{net}W{l}"], quant).T + p[f"{net}b{l}"]), quant)
+        h = _q(elu(h @ _q(p[f"{net}W{l}"], quant, "w").T + p[f"{net}b{l}"]), quant, "h")
         acts.append(h)
     y = h @ p[f"{net}W4"].T + p[f"{net}b4"]
     return y, acts
@@ -95,9 +118,9 @@ def mlp_backward(p: dict, acts, dy: np.ndarray, net: str, grads: dict, quant=Non
         grads[f"{net}W{l}"] = g.T @ a_in
         grads[f"{net}b{l}"] = g.sum(axis=0)
         if l > 1:
-            g = g @ (p[f"{net}W{l}"] if l == 4 else _q(p[f"{net}W{l}"], quant))
+            g = g @ (p[f"{net}W{l}"] if l == 4 else _q(p[f"{net}W{l}"], quant, "wb"))
             out = acts[l - 1]
-            g = _q(g * np.where(out > 0, 1.0, out + 1.0), quant)
+            g = _q(g * np.where(out > 0, 1.0, out + 1.0), quant, "dz")
 
 
 def logp_gauss(a, mu, logstd):

@@ -264,4 +264,8 @@ def test_nonfinite_advantage_skips_its_minibatches_on_gpu_and_oracle():
         k = int(np.nonzero(perms[e] == b_flat)[0][0]) // M
         assert st_q[e * K + k].get("skipped")
     assert abs(sc["alpha"] - a_q) <= 1e-6 * a_q
-    assert rel(th, th_q) <= 1e-3
+    with np.errstate(invalid="ignore"):
+        th_x, *_ = learn.ppo_update(theta.astype(np.float64), z, z.copy(), 0, 1e-3, bo, perms, cfg.obs_dim, cfg.hidden)
+    d_q, d_x, gap = rel(th, th_q), rel(th, th_x), rel(th_q, th_x)
+    print(f"skip test drift: vs bf16-point oracle {d_q:.3e}, vs fp64 {d_x:.3e} (gap {gap:.3e})")
+    assert d_x <= gap + 1e-3                              # DESIGN R28
