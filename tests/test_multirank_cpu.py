@@ -121,3 +121,39 @@ def test_bench_reference_arm_under_torchrun():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _lib_worker(rank, world, port, out_dir):
+    """One rank of the product's multi-process setup on CPU: the library is loaded, rank 0 draws the NCCL
+    unique id through lg_nccl_unique_id and the process group (gloo here, as torch.distributed carries it on a
+    GPU box) delivers it to every rank; each rank validates its own (rank, world) config through the C ABI."""
+    sys.path.insert(0, ROOT)
+    from paper_2109_11978_b200 import lg
+    from paper_2109_11978_b200.context import Config
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        st, raw = lg.lg_nccl_unique_id()
+        assert st == 0
+        uid = torch.frombuffer(bytearray(raw), dtype=torch.uint8).clone()
+    dist.broadcast(uid, 0)
+    st, sizes = lg.lg_required_sizes(Config.make(n_envs=64, n_steps=4, rank=rank, world_size=world).to_c())
+    bad, _ = lg.lg_required_sizes(Config.make(n_envs=64, n_steps=4, rank=world, world_size=world).to_c())
+    np.savez(os.path.join(out_dir, f"lib{rank}.npz"), uid=uid.numpy(), st=st, bad=bad, sizes=np.array(sizes))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_library_setup(tmp_path):
+    from paper_2109_11978_b200 import build
+    build.build()
+    port = _free_port()
+    mp.spawn(_lib_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r0, r1 = (np.load(tmp_path / f"lib{r}.npz") for r in (0, 1))
+    assert np.array_equal(r0["uid"], r1["uid"]) and r0["uid"].any()    # every rank holds rank 0's id
+    assert int(r0["st"]) == 0 and int(r1["st"]) == 0                   # LG_OK for rank 0 and rank 1 of 2
+    assert int(r0["bad"]) == 2 and int(r1["bad"]) == 2                 # rank >= world: LG_ERR_RANGE
+    assert np.array_equal(r0["sizes"], r1["sizes"])                    # identical per-rank layouts
+    from paper_2109_11978_b200 import lg
+    assert lg._lib.lg_group_create(None, 2, None) == 1                  # LG_ERR_INVALID_ARG
