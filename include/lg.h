@@ -58,6 +58,10 @@ typedef enum {
 /* implementation switch (diagnostics/parity): policy_act uses the per-layer GEMM + head kernels instead of the
  * fused rollout-policy kernel (same results bit for bit; only the 512-256-128 MLP has a fused kernel) */
 #define LG_F_UNFUSED_POLICY 256u
+/* implementation switch (diagnostics/parity): the update runs layer 3 and the PPO loss head as two kernels (forward
+ * GEMM + warp-per-row loss head) instead of the loss epilogue fused into the layer-3 GEMM (dZ3 and every gradient
+ * but the head / log-std ones are the same bits; those are the same sums in another order) */
+#define LG_F_UNFUSED_LOSS 512u
 
 #define LG_NUM_BUFFERS 20
 /* Buffer slots for lg_required_sizes / lg_create. Layouts are DESIGN.md §4. */

@@ -263,6 +263,7 @@ struct lg_ctx {
   GemmArgs l1_upd, l2, l3, l1_boot, l2_boot, l3_boot, l1_vt, dx3, dx2, dw3, dw2, dw1;
   GemmArgs l2r, l3r;        // layers 2, 3 for M <= n_envs rows (rollout): narrower tiles (bn2r, bn3r)
   GemmArgs l1_upd_b1, dw1_b1;  // layer-1 forward and weight gradient on gathered set 1 (l1_upd / dw1: set 0)
+  GemmArgs l3loss;          // update layer 3 with the PPO loss head in its epilogue (EPI 4; le set per minibatch)
   int bn2r = 0, bn3r = 0;
   int bn1u = 0, bn2u = 0, bn3u = 0, bnx3 = 0, bnx2 = 0;  // update GEMMs (minibatch rows; narrower when M is small)
   CUtensorMap tmW2f[2], tmW3f[2];  // the fused rollout policy's W2 / W3 maps (its fixed boxes, not the update's)
@@ -506,6 +507,18 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   set_fwd_common(g2, d.Mmb, d.H1, d.H0, bn2, 2); g2.ldo = 2 * d.H1;
   set_fwd_common(g3, d.Mmb, d.H2, d.H1, bn3, 2); g3.ldo = 2 * d.H2;
   g3.ws = 1;
+  {  // layer 3 + loss head (EPI 4): 128-wide tiles (a whole head input row per tile), output dZ3
+    GemmArgs& gl = ctx->l3loss;
+    memset(&gl, 0, sizeof(gl));
+    for (int z = 0; z < 2; ++z) {
+      gl.tmA[z] = g3.tmA[z];
+      ok &= make_tmap_bf16(&gl.tmB[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, 128);
+      cmap(&gl.tmC[z], dZ3 + z * d.H2, d.H2, 2 * d.H2);
+      gl.bias[z] = b3 + z * d.H2;
+    }
+    set_fwd_common(gl, d.Mmb, d.H2, d.H1, 128, 2);
+    gl.ldo = 2 * d.H2;
+  }
   for (int z = 0; z < 2; ++z) {
     ok &= make_tmap_bf16(&ctx->tmW2f[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, bn_for(d.H1));
     ok &= make_tmap_bf16(&ctx->tmW3f[z], W3 + (size_t)z * d.H2 * d.H1, d.H2, d.H1, d.H1, bn_for(d.H2));
@@ -1027,6 +1040,12 @@ lg_status storage_compute_gae(lg_ctx* ctx, float* adv, float* ret) {
 
 // gradient of one minibatch (rows already gathered into the ACTIV minibatch arrays)
 static GatherArgs gather_args(lg_ctx* ctx, int b);
+static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm);
+// the loss epilogue fused into layer 3 (EPI 4): its weight-stationary schedule keeps W3 (H1 x 128 bf16 per net)
+// resident, which fits for H1 <= 256
+static bool fused_loss_ok(const lg_ctx* ctx) {
+  return ctx->d.H1 <= 256 && ctx->d.H2 <= 128 && !(ctx->cfg.flags & LG_F_UNFUSED_LOSS);
+}
 
 // One minibatch's gradient on gathered set b. With next_perm, the gather of the next minibatch (into set
 // 1 - b) is launched on st right after dX2, beside the last weight-gradient GEMM on st2.
@@ -1038,8 +1057,43 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   void* K = ctx->buf[LG_BUF_WORK];
   float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
   GemmArgs l1 = b ? ctx->l1_upd_b1 : ctx->l1_upd;
-  lg_status s = forward_rows(ctx, l1, ctx->bn1u, d.Mmb);
-  if (s != LG_OK) return s;
+  lg_status s;
+  HeadReduceArgs hr;
+  hr.HP = L.HP; hr.H2 = d.H2;
+  hr.part = at<float>(K, L.k_lpart); hr.spart = at<double>(K, L.k_spart); hr.grad = grad;
+  hr.off_W4a = ctx->cn.W4[0]; hr.off_b4a = ctx->cn.b4[0]; hr.off_W4c = ctx->cn.W4[1]; hr.off_b4c = ctx->cn.b4[1];
+  hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
+  if (fused_loss_ok(ctx)) {
+    // layers 1, 2, then layer 3 with the PPO loss head in its epilogue (H3 stays on chip; output dZ3)
+    g_gemm_cat = LG_PROF_GEMM_FWD;
+    l1.M = d.Mmb;
+    GemmArgs g2 = ctx->l2;
+    g2.M = d.Mmb;
+    if ((s = gemm(ctx, GEMM_FWD, l1, ctx->bn1u, 1)) != LG_OK) return s;
+    if ((s = gemm(ctx, GEMM_FWD, g2, ctx->bn2u, 2)) != LG_OK) return s;
+    GemmArgs gl = ctx->l3loss;
+    gl.M = d.Mmb;
+    LossEpi& le = gl.le;
+    le.W4a = at<float>(W, L.w_W4a); le.b4a = at<float>(W, L.w_b4a); le.W4c = at<float>(W, L.w_W4c);
+    le.b4c = at<float>(W, L.w_b4c); le.logstd = at<float>(W, L.w_ls); le.logstd_old = at<float>(W, L.w_lso);
+    le.act = at<float>(A, b ? L.b_act : L.a_act); le.mu_old = at<float>(A, b ? L.b_mu : L.a_mu);
+    le.logp_old = at<float>(A, b ? L.b_logp : L.a_logp);
+    le.V_old = at<float>(A, b ? L.b_V : L.a_V); le.adv = at<float>(A, b ? L.b_adv : L.a_adv);
+    le.ret = at<float>(A, b ? L.b_ret : L.a_ret);
+    le.clip = ctx->cfg.clip; le.vclip = ctx->cfg.vclip; le.vf_coef = ctx->cfg.vf_coef; le.invM = 1.0f / (float)d.Mmb;
+    le.H2 = d.H2; le.payload = ctx->payload; le.part = at<float>(K, L.k_lpart); le.spart = at<double>(K, L.k_spart); le.HP = L.HP;
+    int grid = 0;
+    {
+      Scope sc_(ctx, LG_PROF_LOSS);
+      cudaError_t e = launch_gemm_loss(gl, &grid, ctx->st);
+      if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm_loss: %s", cudaGetErrorString(e));
+    }
+    hr.nblk = grid;
+    { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
+    CKL();
+    return backward_chain(ctx, b, next_perm);
+  }
+  if ((s = forward_rows(ctx, l1, ctx->bn1u, d.Mmb)) != LG_OK) return s;
   LossArgs la;
   la.nd = NetDims{d.D, d.Dp, d.H0, d.H1, d.H2};
   la.M = d.Mmb;
@@ -1058,14 +1112,19 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   la.HP = L.HP;
   { Scope sc_(ctx, LG_PROF_LOSS); launch_loss_heads(la, ctx->st); }
   CKL();
-  HeadReduceArgs hr;
-  hr.nblk = loss_blocks(d.Mmb); hr.HP = L.HP; hr.H2 = d.H2;
-  hr.part = la.part; hr.spart = la.spart; hr.grad = grad;
-  hr.off_W4a = ctx->cn.W4[0]; hr.off_b4a = ctx->cn.b4[0]; hr.off_W4c = ctx->cn.W4[1]; hr.off_b4c = ctx->cn.b4[1];
-  hr.off_logstd = ctx->cn.logstd; hr.ent_coef = ctx->cfg.ent_coef; hr.payload = ctx->payload; hr.M = d.Mmb;
+  hr.nblk = loss_blocks(d.Mmb);
   // (measured: on the dW stream instead, the reduction delays dW3 -> dW1 by more than it saves here)
   { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
   CKL();
+  return backward_chain(ctx, b, next_perm);
+}
+
+// dZ3 -> dX3, dX2 (st) beside dW3, dW2, dW1 (st2); with next_perm the next minibatch's gather
+static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm) {
+  const Dims& d = ctx->d;
+  const Layout& L = ctx->L;
+  float* grad = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
+  lg_status s;
   // the weight-gradient chain runs on st2 beside the dX chain; the profiled pass (lg_profile, timing each
   // category) keeps everything on st so that every kernel's measured duration is its own
   cudaStream_t sdw = ctx->prof ? ctx->st : ctx->st2;

@@ -190,6 +190,52 @@ __device__ __forceinline__ float sample_action(const Rng& rng, uint32_t g, uint3
   return sample_action_b(rng.block((uint32_t)(j >> 2), g, ev, TAG_ACTION), j, mu, ls);
 }
 
+// ------------------------------------------------------------------ PPO loss of one sample
+// Shared by the two loss-head kernels (k_loss_heads, and the layer-3 GEMM's loss epilogue), so the per-row
+// quantities that feed dZ3 -- dL/dlogp and dL/dV -- are the same expressions (the same bits) on both paths.
+// Clipped surrogate: returns dL/dlogp = -(A or 0) ratio / M; sv = the row's surrogate term.
+__device__ __forceinline__ float ppo_dlogp(float ratio, float adv, float clip, float invM, float& sv, bool& clipped) {
+  const float s1 = ratio * adv;
+  const float rc = fminf(fmaxf(ratio, 1.0f - clip), 1.0f + clip);
+  const float s2 = rc * adv;
+  const bool take1 = s1 <= s2;
+  const bool inside = ratio >= 1.0f - clip && ratio <= 1.0f + clip;
+  sv = take1 ? s1 : s2;
+  clipped = fabsf(ratio - 1.0f) > clip;
+  return -(take1 ? adv : (inside ? adv : 0.0f)) * invM * ratio;
+}
+// PPO2 clipped value loss (reading R14): returns dL/dV; vv = the row's value-loss term
+__device__ __forceinline__ float ppo_dvalue(float V, float Vo, float ret, float vclip, float vf_coef, float invM,
+                                            float& vv) {
+  const float vc = Vo + fminf(fmaxf(V - Vo, -vclip), vclip);
+  const float e1 = (V - ret) * (V - ret), e2 = (vc - ret) * (vc - ret);
+  const bool take_u = e1 >= e2;
+  const bool vin = fabsf(V - Vo) <= vclip;
+  vv = take_u ? e1 : e2;
+  return vf_coef * (take_u ? 2.0f * (V - ret) : (vin ? 2.0f * (vc - ret) : 0.0f)) * invM;
+}
+// analytic KL(pi_old || pi) of one action dimension (reading R15): klc = the mu-independent part
+__device__ __forceinline__ float kl_const(float ls, float lso, float iv) {
+  return ls - lso + expf(2.0f * lso) * (0.5f * iv) - 0.5f;
+}
+__device__ __forceinline__ float kl_term(float klc, float dm, float iv) { return klc + dm * dm * (0.5f * iv); }
+// d(-logp)/d(log sigma_j) factor of one dimension, times dL/dlogp
+__device__ __forceinline__ float gls_term(float dLdlp, float d, float iv) { return dLdlp * (d * d * iv - 1.0f); }
+// the 12-dimension sum of the warp-per-row kernels' dim_sum (term j on lane 2j, butterfly offsets 16..1),
+// evaluated by one thread in the same addition order
+__device__ __forceinline__ float dim_sum12(const float* t) {
+  float e8[8];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) e8[m] = t[m] + t[m + 8];
+#pragma unroll
+  for (int m = 4; m < 8; ++m) e8[m] = t[m] + 0.0f;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) e8[m] = e8[m] + e8[m + 4];
+  e8[0] = e8[0] + e8[2];
+  e8[1] = e8[1] + e8[3];
+  return (e8[0] + e8[1]) + 0.0f;
+}
+
 // ------------------------------------------------------------------ programmatic dependent launch
 // Kernels launched with launch_pdl (kernels.h) let their dependent grid start launching as soon as all their
 // CTAs are running (pdl_trigger), and block in pdl_wait until the preceding grid has completed and its memory

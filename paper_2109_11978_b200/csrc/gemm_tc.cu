@@ -138,6 +138,14 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 16 consecutive fp32 columns of this thread's TMEM lane (no wait)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 
 // ---- CTA-pair (tcgen05 cta_group::2) helpers
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -195,8 +203,83 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// issued by one thread; the three weight parts in turn, each over the two 64-column blocks in K steps of 16
+// (w4 = the atoms of build_w4_atoms)
+__device__ __forceinline__ void head_mma(uint32_t d1, uint32_t a3, uint32_t w4) {
+  constexpr uint32_t id = idesc_bf16(128, 16, false, false);
+  int n = 0;
+#pragma unroll
+  for (int part = 0; part < 3; ++part)
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+      for (int k = 0; k < 4; ++k, ++n)
+        tc_mma(d1, sdesc(a3 + kb * 16384u + 32u * k, 0u, 1024u), sdesc(w4 + part * 4096u + kb * 2048u + 32u * k, 0u, 1024u),
+               id, n > 0 ? 1u : 0u);
+}
+
 constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
+
+// ------------------------------------------------------------------ the policy / value heads on the tensor core
+// Shared by the rollout policy (k_policy_fused) and the update's loss epilogue (EPI 4) so both produce the same
+// mu and V bits (the first minibatch's probability ratio is exactly 1):
+//   D1[row][j] = sum_c H3[row][c] W4[j][c]   (M = 128 rows, N = 16 head outputs, K = 128 H3 columns)
+// A = H3 as two K-major SW128 blocks of 64 columns 16 KB apart (the layer activation layout); B = W4 of one net
+// as three bf16 parts whose sum is the fp32 weight exactly (split3_bf16), [16 rows j][128 columns] in two
+// 64-column SW128 atoms 2 KB apart (rows >= 12, or >= 1 for the critic, and columns >= H2 are zero). The same
+// atoms are the MN-major B (N = column, K = j) of the head-input gradient dH3 = dmu W4 (LBO 2 KB).
+__device__ __forceinline__ uint16_t bf16_bits(float x) {
+  const __nv_bfloat16 b = __float2bfloat16_rn(x);
+  return *reinterpret_cast<const uint16_t*>(&b);
+}
+// fp32 x = p0 + p1 + p2 exactly, each part a bf16 (8 significant bits): RNE to bf16, then the exact fp32 residual
+__device__ __forceinline__ void split3_bf16(float x, uint16_t* p) {
+  p[0] = bf16_bits(x);
+  const float r1 = x - __uint_as_float((uint32_t)p[0] << 16);
+  p[1] = bf16_bits(r1);
+  p[2] = bf16_bits(r1 - __uint_as_float((uint32_t)p[1] << 16));
+}
+constexpr int W4_PART = 4096;  // bytes of one part of the head-weight atoms
+__device__ __forceinline__ void build_w4_atoms(uint8_t* w4, const float* W4a, const float* W4c, int H2, int z, int t0,
+                                               int nt) {
+  for (int k = t0; k < 16 * 128; k += nt) {  // element (j, c): atom c / 64, row j, 16-B chunk (c % 64) / 8 ^ (j & 7)
+    const int j = k >> 7, c = k & 127;
+    float v = 0.0f;
+    if (c < H2) v = z == 0 ? (j < 12 ? __ldg(W4a + j * H2 + c) : 0.0f) : (j == 0 ? __ldg(W4c + c) : 0.0f);
+    uint16_t pt[3];
+    split3_bf16(v, pt);
+    const int off = (c >> 6) * 2048 + j * 128 + ((((c & 63) >> 3) ^ (j & 7)) << 4) + 2 * (c & 7);
+#pragma unroll
+    for (int u = 0; u < 3; ++u) *reinterpret_cast<uint16_t*>(w4 + u * W4_PART + off) = pt[u];
+  }
+}
+
+// EPI 4 (loss epilogue) shared-memory carve-up (offsets from a 1024-B aligned base):
+//  A3     the tile's H3 [128 rows][128] bf16 as two K-major SW128 blocks of 64 columns: A of the head MMA (K-major,
+//         M = row, K = column), MN-major A (M = column, K = row) of the head-weight gradient, and afterwards the
+//         staging buffer of the dZ3 TMA stores (its 32-row x 64-column sub-tiles are SW128 store boxes)
+//  DMU    dmu (actor) / dV (critic) per row as three bf16 parts (split3_bf16: their sum is the fp32 value), 128-B
+//         rows (columns 0..15 used, the rest zero): K-major A (M = row, K = head output) of dH3 = dmu W4, MN-major B
+//         (N = head output, K = row) of dW4
+//  W4     the net's head weights as build_w4_atoms lays them out (three parts)
+//  REC    per-row records [128][36] fp32 (dmu[12], dV, dlogstd terms[12], pad, fp64 statistics[5])
+//  CST    per-dimension constants (log sigma, sigma^-2, KL constant, b4a); BIAS b3 of the CTA's net
+namespace le {
+constexpr int A3 = 0;
+constexpr int DMU = A3 + 32768;     // three parts, 16 KB apart
+constexpr int W4 = DMU + 3 * 16384;  // three parts, 4 KB apart
+constexpr int REC = W4 + 3 * 4096;
+constexpr int REC_LD = 36;
+constexpr int CST = REC + 128 * REC_LD * 4;
+constexpr int BIAS = CST + 48 * 4;
+constexpr int BYTES = BIAS + 128 * 4;
+// TMEM columns: the layer-3 accumulators use [0, 256)
+constexpr int TM_D2 = 256;  // dH3 [row][128]
+constexpr int TM_D3 = 384;  // dW4 accumulator [column][16], across the CTA's tiles
+constexpr int TM_D1 = 400;  // head outputs [row][16]
+static_assert(REC % 8 == 0 && BYTES % 16 == 0 && W4 % 1024 == 0, "loss epilogue smem alignment");
+}  // namespace le
 
 template <int BN, int EPI, bool PAIR = false, int WSKB = 0>
 struct GemmCfg {
@@ -205,17 +288,18 @@ struct GemmCfg {
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // a CTA of a pair holds half of B
   static constexpr int ONES_BYTES = EPI == 3 ? 16 * 128 : 0;  // 16 rows x 64 bf16 of 1.0 (bias column)
   static constexpr int EPI_BUF = 4096;         // one 32 x 128-B staging sub-tile
-  static constexpr int EPI_NBUF = (EPI == 3 || WSKB) ? 1 : 2;
+  static constexpr int EPI_NBUF = EPI == 4 ? 0 : ((EPI == 3 || WSKB) ? 1 : 2);  // EPI 4 stages dZ3 in its own smem
   static constexpr int BIAS_BYTES = EPI == 0 ? EPI_WARPS * 128 * 4 : 0;
+  static constexpr int LOSS_BYTES = EPI == 4 ? le::BYTES : 0;
   static constexpr int BRES = WSKB * B_BYTES;  // weight-stationary: the resident column block of B
-  static constexpr int FIXED = 1024 + ONES_BYTES + EPI_WARPS * EPI_NBUF * EPI_BUF + BIAS_BYTES + 512 + BRES;
+  static constexpr int FIXED = 1024 + ONES_BYTES + EPI_WARPS * EPI_NBUF * EPI_BUF + BIAS_BYTES + LOSS_BYTES + 512 + BRES;
   static constexpr int STAGE_BYTES = WSKB ? A_BYTES : A_BYTES + B_BYTES;
   static constexpr int STAGES_FIT = (232448 - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int ACC_COLS = ((BN + (EPI == 3 ? 16 : 0)) + 31) / 32 * 32;
   static constexpr int ACC_STAGES = 2 * ACC_COLS <= 512 ? 2 : 1;
   static constexpr int TMEM_NEED = ACC_STAGES * ACC_COLS;
-  static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
+  static constexpr int TMEM_COLS = EPI == 4 ? 512 : TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
   static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
   static_assert(STAGES >= 2, "operand ring");
 };
@@ -288,6 +372,339 @@ __device__ __forceinline__ TileCoord decode(const GemmArgs& a, int t, int m_tile
   return c;
 }
 
+// ------------------------------------------------------------------ EPI 4: the PPO loss head in the epilogue
+// Layer 3 of the update (tile = 128 rows x 128 columns of one net: the CTA serves one net, z = 0 actor, 1 critic)
+// ends the forward pass and starts the backward one in the same epilogue; H3 never goes to
+// HBM. Per tile:
+//  1. H3 = bf16(ELU(acc + b3)) into smem (A3; thread (row, h) writes columns 64h .. 64h+63).
+//  2. one thread issues the head MMA (head_mma: mu - b4a or V - b4c, the rollout kernel's instruction sequence, so
+//     the first minibatch's probability ratio is exactly 1); every thread reads its row's 16 outputs.
+//  3. per row (both threads): log-probability (dim_sum12), ratio, clipped surrogate / value loss (the shared
+//     ppo_dlogp / ppo_dvalue), KL; dmu_j = dL/dlogp (a_j - mu_j) / sigma_j^2, or dV -> smem as three bf16 parts
+//     (split3_bf16: exact), so the tensor core sees the fp32 operands of the two-kernel path.
+//  4. one thread issues dH3 = dmu W4 (K = 16; part products of order <= 2) into TMEM and dW4 += H3^T dmu (K = the
+//     tile's 128 rows, three dmu parts) into a TMEM accumulator that lives across the CTA's tiles;
+//     meanwhile each warp sums its per-row record columns (head biases, log-std, loss statistics) over the rows.
+//  5. dZ3 = dH3 * ELU'(H3) -> bf16 over H3 in A3 -> TMA stores.
+// At the end the CTA writes its partial row (k_loss_heads layout) to le.part / le.spart; k_reduce_heads sums the
+// rows in CTA order (deterministic). Ownership: dW4 = the D3 accumulator, TMEM lane c read by warps 4..7; record
+// column col < 25 (dmu_j -> db4a, dV -> db4c, dlogstd terms; fp64 statistics surrogate, value loss, KL, clip
+// count, non-finite rows) by lane 0 of epilogue warp col % 8.
+constexpr float SIX_LN_2PI_F = 11.027262398456072f;
+__device__ __forceinline__ float elu_grad_out(float h) { return h > 0.0f ? 1.0f : h + 1.0f; }
+__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long loss_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define LOSS_STAMP(k)                                                                                          \
+  do {                                                                                                         \
+    if (L.dbg && et == 0) L.dbg[((size_t)blockIdx.x * 8 + (local - 1 < 7 ? local - 1 : 7)) * 8 + (k)] = loss_gtimer(); \
+  } while (0)
+
+template <typename C, typename TileAt, typename Skip>
+__device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileAt tile_at, Skip skip, uint32_t tmem,
+                                              uint64_t* tfull, uint64_t* tempty, uint64_t* lmma, uint8_t* sLoss,
+                                              int z) {
+  const LossEpi& L = args.le;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = warp - 4, q = e & 3, h = e >> 2;
+  const int et = threadIdx.x - 128;
+  uint8_t* sA3 = sLoss + le::A3;
+  uint8_t* sD = sLoss + le::DMU;
+  float* sRec = reinterpret_cast<float*>(sLoss + le::REC);
+  float* sCst = reinterpret_cast<float*>(sLoss + le::CST);  // ls[12] | sigma^-2[12] | KL constant[12] | b4a[12]
+  float* sBias = reinterpret_cast<float*>(sLoss + le::BIAS);
+  const int H2 = L.H2;
+  // ---- once per CTA: the net's head weights (three bf16 parts), constants, b3, zeroed operands / records
+  build_w4_atoms(sLoss + le::W4, L.W4a, L.W4c, H2, z, et, 256);
+  for (int k = et; k < 3 * 16384 / 16; k += 256) reinterpret_cast<uint4*>(sD)[k] = make_uint4(0u, 0u, 0u, 0u);
+  for (int k = et; k < 128 * le::REC_LD; k += 256) sRec[k] = 0.0f;  // columns a net never writes stay zero
+  if (et < 12) {
+    const float ls = __ldg(L.logstd + et), lso = __ldg(L.logstd_old + et);
+    const float iv = expf(-2.0f * ls);
+    sCst[et] = ls;
+    sCst[12 + et] = iv;
+    sCst[24 + et] = kl_const(ls, lso, iv);
+    sCst[36 + et] = __ldg(L.b4a + et);
+  }
+  if (et < 128) sBias[et] = et < args.N ? __ldg(args.bias[z] + et) : 0.0f;
+  // the first payload writer of the minibatch clears the non-finite counter (the previous minibatch's Adam has
+  // consumed it: this kernel runs after that minibatch's layers 1, 2)
+  if (blockIdx.x == 0 && et == 0 && L.payload) L.payload[4] = 0.0f;
+  const float b4c = __ldg(L.b4c);
+  // record-column sums (lane 0 of warp e owns float columns e, e + 8, e + 16, e + 24 (< 25) and fp64 statistic
+  // e (< 5))
+  float xf[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  double xd = 0.0;
+  fence_async_smem();
+  bar_epi();
+  const uint32_t tD1 = tmem + le::TM_D1, tD2 = tmem + le::TM_D2, tD3 = tmem + le::TM_D3;
+  constexpr uint32_t id2 = idesc_bf16(128, 128, false, true);  // dH3 [row][col] = dmu [row][j] . W4 [j][col]
+  constexpr uint32_t id3 = idesc_bf16(128, 16, true, true);    // dW4 [col][j] += H3^T [col][row] . dmu [row][j]
+  const int r = q * 32 + lane;
+  const uint32_t lrow = (uint32_t)(q * 32) << 16;
+  // 16-B chunk ch (columns 8ch .. 8ch+7) of this thread's 64 columns of row r in A3 (block h, swizzled by row)
+  auto a3_chunk = [&](int ch) { return sA3 + h * 16384 + r * 128 + ((ch ^ (r & 7)) << 4); };
+  int local = 0;
+  TileCoord tc;
+  for (int it = 0; tile_at(it, tc); ++it) {
+    if (skip(tc)) continue;
+    const int acc = local % C::ACC_STAGES;
+    const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
+    const bool first = local == 0;
+    ++local;
+    const int row = tc.m0 + r;
+    const bool valid = row < M;
+    // row inputs (independent of the accumulator: their loads overlap the waits below)
+    float in_a[12], in_m[12];
+    float lpo = 0.0f, adv = 0.0f, Vo = 0.0f, ret = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) in_a[j] = in_m[j] = 0.0f;
+    if (valid) {
+      if (z == 0) {
+        const float4* pa = reinterpret_cast<const float4*>(L.act + (size_t)row * 12);
+        const float4* pm = reinterpret_cast<const float4*>(L.mu_old + (size_t)row * 12);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const float4 va = __ldg(pa + k), vm = __ldg(pm + k);
+          in_a[4 * k] = va.x; in_a[4 * k + 1] = va.y; in_a[4 * k + 2] = va.z; in_a[4 * k + 3] = va.w;
+          in_m[4 * k] = vm.x; in_m[4 * k + 1] = vm.y; in_m[4 * k + 2] = vm.z; in_m[4 * k + 3] = vm.w;
+        }
+        lpo = __ldg(L.logp_old + row);
+        adv = __ldg(L.adv + row);
+      } else {
+        Vo = __ldg(L.V_old + row);
+        ret = __ldg(L.ret + row);
+      }
+    }
+    LOSS_STAMP(0);
+    if (lane == 0) bulk_wait_read0();  // this warp's previous dZ3 store has read its A3 sub-tile
+    __syncwarp();
+    bar_epi();                         // every warp's: A3 is free
+    LOSS_STAMP(1);
+    mbar_wait(&tfull[acc], aph);
+    __syncwarp();
+    tc_fence_after();
+    LOSS_STAMP(2);
+    // (1) H3 = bf16(ELU(acc + b3)) of columns 64h .. 64h+63 into A3
+    {
+      const uint32_t tb = tmem + acc * C::ACC_COLS + lrow + 64 * h;
+      uint32_t a32[2][32];
+      tmem_ld32_nowait(tb, a32[0]);
+      tmem_ld32_nowait(tb + 32, a32[1]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = 8 * ch + 2 * k;
+          const float2 b2 = *reinterpret_cast<const float2*>(sBias + 64 * h + c);
+          const __nv_bfloat162 p = __floats2bfloat162_rn(elu_fast(__uint_as_float(a32[c >> 5][c & 31]) + b2.x),
+                                                         elu_fast(__uint_as_float(a32[c >> 5][(c & 31) + 1]) + b2.y));
+          w[k] = *reinterpret_cast<const uint32_t*>(&p);
+        }
+        *reinterpret_cast<uint4*>(a3_chunk(ch)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();  // the accumulator stage is free once read: the next tile's layer-3 MMAs may start
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[acc]);
+    bar_epi();
+    // (2) the head MMA
+    if (et == 0) {
+      tc_fence_after();
+      head_mma(tD1, smem_u32(sA3), smem_u32(sLoss + le::W4));
+      tc_commit(lmma);
+    }
+    mbar_wait(lmma, 0u);  // two commits per tile: the head MMA completes phase 0, the gradient MMAs phase 1
+    __syncwarp();
+    tc_fence_after();
+    uint32_t d1[16];
+    tmem_ld16_nowait(tD1 + lrow, d1);
+    tmem_wait_ld();
+    LOSS_STAMP(3);
+    // (3) the row's loss terms; dmu / dV (parts 0, 2 by the thread of h = 0, part 1 by h = 1) and the row record
+    float* rec = sRec + r * le::REC_LD;
+    double* rd = reinterpret_cast<double*>(rec + 26);
+    float dq[12];
+    if (z == 0) {
+      float mu[12], t[12];
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        mu[j] = __fadd_rn(__uint_as_float(d1[j]), sCst[36 + j]);
+        t[j] = logp_term(in_a[j], mu[j], sCst[j]);
+      }
+      const float lp = __fsub_rn(-dim_sum12(t), SIX_LN_2PI_F);
+      const float ratio = expf(lp - lpo);
+      float svf = 0.0f;
+      bool clipped = false;
+      const float dLdlp = valid ? ppo_dlogp(ratio, adv, L.clip, L.invM, svf, clipped) : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        const float d = in_a[j] - mu[j];
+        dq[j] = dLdlp * d * sCst[12 + j];
+        const float dm = in_m[j] - mu[j];
+        t[j] = kl_term(sCst[24 + j], dm, sCst[12 + j]);
+        if (h == 0) {
+          rec[j] = dq[j];
+          rec[13 + j] = valid ? gls_term(dLdlp, d, sCst[12 + j]) : 0.0f;
+        }
+      }
+      const float kl = dim_sum12(t);
+      if (h == 0) {
+        const double sv = valid ? (double)svf : 0.0, kv = valid ? (double)kl : 0.0;
+        rd[0] = sv;
+        rd[2] = kv;
+        rd[3] = valid && clipped ? 1.0 : 0.0;
+        rd[4] = (isfinite(sv) && isfinite(kv)) ? 0.0 : 1.0;
+      }
+    } else {
+      const float V = __fadd_rn(__uint_as_float(d1[0]), b4c);
+      float vvf = 0.0f;
+      const float dV = valid ? ppo_dvalue(V, Vo, ret, L.vclip, L.vf_coef, L.invM, vvf) : 0.0f;
+      dq[0] = dV;
+#pragma unroll
+      for (int j = 1; j < 12; ++j) dq[j] = 0.0f;
+      if (h == 0) {
+        rec[12] = dV;
+        rd[1] = valid ? (double)vvf : 0.0;
+        rd[4] = isfinite(rd[1]) ? 0.0 : 1.0;
+      }
+    }
+    {  // row r of each DMU part: 16 bf16 (j < 12 used) = 16-B chunks 0, 1 of the 128-B row, swizzled by r & 7
+      uint32_t w[3][8];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        uint16_t p0[3], p1[3];
+        split3_bf16(dq[2 * k], p0);
+        split3_bf16(dq[2 * k + 1], p1);
+#pragma unroll
+        for (int u = 0; u < 3; ++u) w[u][k] = (uint32_t)p0[u] | ((uint32_t)p1[u] << 16);
+      }
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        if ((u == 1) != (h == 1)) continue;
+        w[u][6] = w[u][7] = 0u;
+        uint8_t* drow = sD + u * 16384 + r * 128;
+        *reinterpret_cast<uint4*>(drow + ((0 ^ (r & 7)) << 4)) = make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
+        *reinterpret_cast<uint4*>(drow + ((1 ^ (r & 7)) << 4)) = make_uint4(w[u][4], w[u][5], w[u][6], w[u][7]);
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    LOSS_STAMP(4);
+    bar_epi();
+    // (4) the head-gradient MMAs (one thread); meanwhile each warp sums its record columns over the tile's rows
+    // (lane l: rows l, l + 32, l + 64, l + 96 in order, then a fixed butterfly)
+    if (et == 0) {
+      tc_fence_after();
+      // dH3: the part products of order <= 2 (00, 01, 10, 02, 20, 11); the dropped ones are below 2^-24 relative
+      constexpr int PA[6] = {0, 0, 1, 0, 2, 1}, PB[6] = {0, 1, 0, 2, 0, 1};
+#pragma unroll
+      for (int t = 0; t < 6; ++t)
+        tc_mma(tD2, sdesc(smem_u32(sD) + PA[t] * 16384u, 0u, 1024u),
+               sdesc(smem_u32(sLoss + le::W4) + PB[t] * 4096u, 2048u, 1024u), id2, t > 0 ? 1u : 0u);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {  // K = the tile's 128 rows in steps of 16 (2 KB of 128-B rows)
+        const uint64_t a3 = sdesc(smem_u32(sA3) + ks * 2048u, 16384u, 1024u);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+          tc_mma(tD3, a3, sdesc(smem_u32(sD) + u * 16384u + ks * 2048u, 16384u, 1024u), id3,
+                 (first && ks == 0 && u == 0) ? 0u : 1u);
+      }
+      tc_commit(lmma);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int col = e + 8 * k;
+      if (col < 25) {
+        float v = sRec[lane * le::REC_LD + col];
+        v = v + sRec[(lane + 32) * le::REC_LD + col];
+        v = v + sRec[(lane + 64) * le::REC_LD + col];
+        v = v + sRec[(lane + 96) * le::REC_LD + col];
+        v = warp_sum(v);
+        xf[k] = xf[k] + v;
+      }
+    }
+    if (e < 5) {
+      const double* d0 = reinterpret_cast<const double*>(sRec + 26) + e;
+      double v = d0[lane * (le::REC_LD / 2)];
+      v += d0[(lane + 32) * (le::REC_LD / 2)];
+      v += d0[(lane + 64) * (le::REC_LD / 2)];
+      v += d0[(lane + 96) * (le::REC_LD / 2)];
+      xd += warp_sum_d(v);
+    }
+    LOSS_STAMP(5);
+    mbar_wait(lmma, 1u);
+    __syncwarp();
+    tc_fence_after();
+    LOSS_STAMP(6);
+    // (5) dZ3 = dH3 * ELU'(H3) of columns 64h .. 64h+63 -> bf16 over the H3 values in A3 (the MMAs have read
+    // them): sub-tile (q, h) of the dZ3 stores is A3 + h * 16 KB + q * 4 KB
+    {
+      uint32_t a32[2][32];
+      tmem_ld32_nowait(tD2 + lrow + 64 * h, a32[0]);
+      tmem_ld32_nowait(tD2 + lrow + 64 * h + 32, a32[1]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        uint4* p = reinterpret_cast<uint4*>(a3_chunk(ch));
+        const uint4 hv4 = *p;
+        const uint32_t hw[4] = {hv4.x, hv4.y, hv4.z, hv4.w};
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = 8 * ch + 2 * k;
+          const float g0 = __uint_as_float(a32[c >> 5][c & 31]) * elu_grad_out(__uint_as_float(hw[k] << 16));
+          const float g1 = __uint_as_float(a32[c >> 5][(c & 31) + 1]) * elu_grad_out(__uint_as_float(hw[k] & 0xFFFF0000u));
+          const __nv_bfloat162 pk = __floats2bfloat162_rn(g0, g1);
+          w[k] = *reinterpret_cast<const uint32_t*>(&pk);
+        }
+        *p = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    fence_async_smem();
+    __syncwarp();
+    LOSS_STAMP(7);
+    if (lane == 0 && tc.n0 + 64 * h < args.N) {
+      tma_store_2d(&args.tmC[z], sA3 + h * 16384 + q * 4096, tc.n0 + 64 * h, tc.m0 + q * 32);
+      bulk_commit();
+    }
+    tc_fence_before();  // this tile's TMEM reads (D1, D2) precede the next tile's MMAs into them
+  }
+  // the CTA's partial row (k_loss_heads layout: W4a [12][H2] | b4a [12] | W4c [H2] | b4c | logstd [12])
+  float* out = L.part + (size_t)blockIdx.x * L.HP;
+  if (h == 0) {  // dW4: TMEM lane c of the D3 accumulator (zero when the CTA had no tile)
+    const int c = q * 32 + lane;
+    uint32_t d3[16];
+    tc_fence_after();
+    tmem_ld16_nowait(tD3 + lrow, d3);
+    tmem_wait_ld();
+    if (c < H2) {
+#pragma unroll
+      for (int j = 0; j < 12; ++j) out[j * H2 + c] = (local > 0 && z == 0) ? __uint_as_float(d3[j]) : 0.0f;
+      out[12 * H2 + 12 + c] = (local > 0 && z == 1) ? __uint_as_float(d3[0]) : 0.0f;
+    }
+  }
+  if (lane == 0) {  // record column col -> b4a (0..11), b4c (12), log-std (13..24: d/dlogstd, entropy added later)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int col = e + 8 * k;
+      if (col < 12) out[12 * H2 + col] = xf[k];
+      else if (col == 12) out[13 * H2 + 12] = xf[k];
+      else if (col < 25) out[13 * H2 + 13 + (col - 13)] = xf[k];
+    }
+    if (e < 5) L.spart[(size_t)blockIdx.x * 8 + e] = xd;
+  }
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
+}
+
 // PAIR: a cluster of 2 CTAs computes 256-row tiles with tcgen05.mma.cta_group::2 -- each CTA loads its own
 // 128 rows of A and half of B (so each SM receives 2/3 of the operand bytes of a 128 x BN tile), both CTAs'
 // loads complete on the leader's full barrier, the leader issues the MMAs and multicasts its commits, and the
@@ -307,12 +724,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   uint8_t* sEpi = sB + (WSKB ? C::BRES : C::STAGES * C::B_BYTES);
   uint8_t* sOnes = sEpi + EPI_WARPS * C::EPI_NBUF * C::EPI_BUF;
   float* sBias = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES + C::BIAS_BYTES);
+  uint8_t* sLoss = sOnes + C::ONES_BYTES + C::BIAS_BYTES;  // EPI 4
+  uint64_t* full = reinterpret_cast<uint64_t*>(sLoss + C::LOSS_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;  // WSKB: the resident B slice has landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint64_t* lmma = bfull + 1;    // EPI 4: the epilogue's head-gradient MMAs of a tile have completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmma + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
@@ -329,14 +748,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     if (PAIR) c.m0 = 2 * c.m0 + (int)rank * 128;
     return c;
   };
-  // weight-stationary schedule: slice = cid % nsl (fixed column block of B), row tiles mi, mi + cps, ...
+  // weight-stationary schedule: slice = cid % nsl (fixed column block of B), row tiles mi, mi + cps, ...; with
+  // ws_split and two slices (the loss epilogue: actor rows cost more than critic rows) CTAs [0, ws_split) serve
+  // slice 0 and the rest slice 1, each taking every (slice CTA count)-th row tile
   const int nsl = args.n_tiles * args.nz;
   const int cps = WSKB ? (int)gridDim.x / nsl : 1;
-  const int wslice = WSKB ? cid % nsl : 0;
+  const bool split2 = WSKB && args.ws_split > 0 && nsl == 2;
+  const int wslice = WSKB ? (split2 ? (cid < args.ws_split ? 0 : 1) : cid % nsl) : 0;
+  const int wfirst = split2 ? (wslice ? cid - args.ws_split : cid) : cid / nsl;
+  const int wstride = split2 ? (wslice ? (int)gridDim.x - args.ws_split : args.ws_split) : cps;
   // the it-th tile of this CTA (false when there is none)
   auto tile_at = [&](int it, TileCoord& c) -> bool {
     if (WSKB) {
-      const int m = cid / nsl + it * cps;
+      const int m = wfirst + it * wstride;
       if (m >= m_tiles) return false;
       c.z = wslice / args.n_tiles; c.ntile = wslice - c.z * args.n_tiles; c.n0 = c.ntile * BN; c.split = 0;
       c.m0 = m * 128;
@@ -348,17 +772,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     return true;
   };
   auto skip = [&](const TileCoord& c) { return (PAIR ? c.m0 - (int)rank * 128 : c.m0) >= M; };
+  bool has_tiles = true;
   if (!PAIR) {  // CTA-uniform early exit when none of this CTA's tiles has rows (device-sized M, e.g. no time-outs)
     bool any = false;
     TileCoord c0;
     for (int it = 0; !any && tile_at(it, c0); ++it) any = !skip(c0);
-    if (!any) return;
+    if (!any && EPI != 4) return;  // (the loss epilogue still writes this CTA's -- zero -- partial row)
+    has_tiles = any;
   }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], (PAIR ? 2 : 1) * EPI_WARPS); }
     mbar_init(bfull, 1);
+    mbar_init(lmma, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (EPI == 3) {  // 16 x 64 bf16 ones (any swizzle of a constant tile is the same tile)
@@ -389,7 +816,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      if (WSKB) {  // the slice's B column block, once (kb_total <= WSKB k-blocks, checked by the host)
+      if (WSKB && has_tiles) {  // the slice's B column block, once (kb_total <= WSKB k-blocks, checked by the host)
         TileCoord c0;
         tile_at(0, c0);
         const CUtensorMap* tmB = &args.tmB[c0.z];
@@ -470,7 +897,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      if (WSKB) {
+      if (WSKB && has_tiles) {
         mbar_wait(bfull, 0);
         tc_fence_after();
       }
@@ -515,6 +942,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
       }
     }
     __syncwarp();
+  } else if (warp >= 4 && EPI == 4) {
+    // ---------------------------------------------------------------- loss epilogue
+    loss_epilogue<C>(args, M, tile_at, skip, tmem, tfull, tempty, lmma, sLoss, wslice);
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
     const int e = warp - 4, q = e & 3, h = e >> 2;
@@ -1275,10 +1705,11 @@ constexpr int STAGE = 256 * BK * 2;    // one 256-row weight chunk (32 KB)
 constexpr int NSTAGE = 2;
 constexpr int OFF_RING = R1_BYTES;
 constexpr int OFF_BIAS = OFF_RING + NSTAGE * STAGE;           // b1 (512) | b2 (256) | b3 (128) fp32
-constexpr int OFF_HW = OFF_BIAS + (H0 + H1 + H2) * 4;          // head weights [13][128] fp32
-constexpr int OFF_XCH = OFF_HW + 13 * H2 * 4;                   // [128 rows][2][13] partial sums per thread
+constexpr int OFF_W4 = OFF_BIAS + 4096;                         // the net's head weights, build_w4_atoms (3 parts)
+constexpr int OFF_XCH = OFF_W4 + 3 * W4_PART;                   // [128 rows][2][13] log-density terms
 constexpr int OFF_BAR = OFF_XCH + 128 * 26 * 4;
-constexpr int SMEM = 1024 + OFF_BAR + 16 * 8;
+constexpr int SMEM = 1024 + OFF_BAR + 24 * 8;
+static_assert(OFF_W4 % 1024 == 0 && (H0 + H1 + H2) * 4 <= 4096, "fused policy smem layout");
 }  // namespace fp
 
 // bf16 pack of 32 fp32 values after bias + ELU, written into a K-major SW128 A block (row r, columns c..c+31
@@ -1317,16 +1748,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   float* sB1 = reinterpret_cast<float*>(smem + fp::OFF_BIAS);
   float* sB2 = sB1 + fp::H0;
   float* sB3 = sB2 + fp::H1;
-  float* sHW = reinterpret_cast<float*>(smem + fp::OFF_HW);
+  uint8_t* sW4 = smem + fp::OFF_W4;  // build_w4_atoms
   float* sX = reinterpret_cast<float*>(smem + fp::OFF_XCH);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + fp::OFF_BAR);
   uint64_t* xfull = bars + 0;
   uint64_t* full = bars + 1;           // [4]
   uint64_t* empty = bars + 5;          // [4]
-  uint64_t* tfull = bars + 9;          // [3]
-  uint64_t* h1ready = bars + 12;
-  uint64_t* h2ready = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* tfull = bars + 9;          // [4]: layers 1, 2, 3, heads
+  uint64_t* h1ready = bars + 13;
+  uint64_t* h2ready = bars + 14;
+  uint64_t* h3ready = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   // weight-chunk slots: 0, 1 = the ring; 2, 3 = R1 blocks 4-5 and 6-7, free while layer 1 runs (the
   // observation tile occupies blocks 0..kb1-1 <= 3, H1 is written only after every layer-1 MMA completed),
   // so layer 1 streams W1 four chunks deep; layers 2 and 3 use the ring
@@ -1340,9 +1772,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   if (threadIdx.x == 0) {
     mbar_init(xfull, 1);
     for (int s2 = 0; s2 < 4; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
-    for (int s2 = 0; s2 < 3; ++s2) mbar_init(&tfull[s2], 1);
+    for (int s2 = 0; s2 < 4; ++s2) mbar_init(&tfull[s2], 1);
     mbar_init(h1ready, EPI_WARPS);
     mbar_init(h2ready, EPI_WARPS);
+    mbar_init(h3ready, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -1435,6 +1868,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
         release(sl);
       }
       tc_commit(&tfull[2]);
+      // the heads: H3 (bf16, in R1 blocks 0, 1) . W4^T into TMEM columns [384, 400)
+      mbar_wait(h3ready, 0);
+      tc_fence_after();
+      head_mma(tmem + 384, smem_u32(R1), smem_u32(sW4));
+      tc_commit(&tfull[3]);
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -1442,23 +1880,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     const int e = warp - 4, q = e & 3, h = e >> 2;
     const int r = q * 32 + lane;  // TMEM lane = tile row
     const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
-    // biases and head weights are staged here, while the producer and the MMA warp run layer 1: 16-B cp.async
-    // chunks, all in flight at once (a load-then-store loop serialised ~10 global latencies per thread)
+    // biases (16-B cp.async chunks, all in flight at once) and the net's head weights (three bf16 parts) are
+    // staged here, while the producer and the MMA warp run layer 1
     {
       const int et = threadIdx.x - 128, nt = EPI_WARPS * 32;
-      constexpr int C1 = fp::H0 / 4, C2 = C1 + fp::H1 / 4, C3 = C2 + fp::H2 / 4, C4 = C3 + 12 * fp::H2 / 4,
-                    C5 = C4 + fp::H2 / 4;
-      for (int k = et; k < C5; k += nt) {
+      constexpr int C1 = fp::H0 / 4, C2 = C1 + fp::H1 / 4, C3 = C2 + fp::H2 / 4;
+      for (int k = et; k < C3; k += nt) {
         const float* src;
         float* dst;
         if (k < C1) { src = a.b1 + z * fp::H0 + 4 * k; dst = sB1 + 4 * k; }
         else if (k < C2) { src = a.b2 + z * fp::H1 + 4 * (k - C1); dst = sB2 + 4 * (k - C1); }
-        else if (k < C3) { src = a.b3 + z * fp::H2 + 4 * (k - C2); dst = sB3 + 4 * (k - C2); }
-        else if (k < C4) { src = a.W4a + 4 * (k - C3); dst = sHW + 4 * (k - C3); }
-        else { src = a.W4c + 4 * (k - C4); dst = sHW + 12 * fp::H2 + 4 * (k - C4); }
+        else { src = a.b3 + z * fp::H2 + 4 * (k - C2); dst = sB3 + 4 * (k - C2); }
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
+      build_w4_atoms(sW4, a.W4a, a.W4c, fp::H2, z, et, nt);
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
     }
@@ -1494,71 +1930,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     __syncwarp();
     if (lane == 0) mbar_arrive(h2ready);
     if (threadIdx.x == 128) FP_STAMP(5);
-    // layer 3 -> H3 (as stored by the unfused path: bf16-rounded) -> heads. The thread of parity h forms the
-    // partial sums of the warp-per-row head (head_fwd_warp) for the lanes l = 2i + h and combines them in that
-    // butterfly's order (pairs by lane bits 4, 3, 2, 1); the last level (bit 0) adds the two threads' sums.
+    // layer 3 -> H3 (bf16, as the unfused path stores it) into R1 blocks 0, 1 (H2 is dead once tfull[2] fired)
+    // -> the head MMA (head_mma: the loss epilogue's instruction sequence) -> mu - b4a / V - b4c in TMEM
     mbar_wait(&tfull[2], 0);
     __syncwarp();
     tc_fence_after();
     if (threadIdx.x == 128) FP_STAMP(6);
-    const int nval = z == 0 ? 12 : 1;
-    float tot[12];
-#pragma unroll
-    for (int j = 0; j < 12; ++j) tot[j] = 0.0f;
-    {
-      // this thread's 16 lanes l = 2i + h: columns 4l .. 4l+3 of H3, bf16-rounded as the unfused path stores it
-      float hv[64];
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {  // 32-column chunk cc = lanes 8cc .. 8cc+7
-        uint32_t acc[32];
-        tmem_ld32_nowait(tb + 256 + 32 * cc, acc);
-        tmem_wait_ld();
-#pragma unroll
-        for (int li = 0; li < 4; ++li)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int l = 8 * cc + 2 * li + h;
-            const uint32_t av = h ? acc[8 * li + 4 + u] : acc[8 * li + u];
-            const float x = elu_fast(__uint_as_float(av) + sB3[4 * l + u]);
-            hv[4 * (4 * cc + li) + u] = __bfloat162float(__float2bfloat16_rn(x));
-          }
-      }
-#pragma unroll
-      for (int j = 0; j < 12; ++j) {
-        if (j < nval) {
-          const float* wrow = sHW + (z == 0 ? j : 12) * fp::H2;
-          float pl[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float4 w = *reinterpret_cast<const float4*>(wrow + 4 * (2 * i + h));  // one broadcast LDS.128
-            float s2 = __fmul_rn(w.x, hv[4 * i]);
-            s2 = fmaf(w.y, hv[4 * i + 1], s2);
-            s2 = fmaf(w.z, hv[4 * i + 2], s2);
-            pl[i] = fmaf(w.w, hv[4 * i + 3], s2);
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) pl[i] = pl[i] + pl[i + 8];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) pl[i] = pl[i] + pl[i + 4];
-#pragma unroll
-          for (int i = 0; i < 2; ++i) pl[i] = pl[i] + pl[i + 2];
-          tot[j] = pl[0] + pl[1];
-        }
-      }
+    for (int c = h * 64; c < h * 64 + 64; c += 32) {
+      uint32_t acc[32];
+      tmem_ld32_nowait(tb + 256 + c, acc);
+      tmem_wait_ld();
+      store_act_block(R1, r, c, acc, sB3 + c);
     }
-    // exchange the two threads' sums (the butterfly's last level adds them: a + b == b + a), then the two
-    // threads of a row split the action dimensions: h = 0 takes j < 6 (ACTION Philox blocks 0, 1), h = 1 takes
-    // j >= 6 (blocks 1, 2); their log-density terms meet again in smem for the fixed-order sum.
+    fence_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(h3ready);
+    mbar_wait(&tfull[3], 0);
+    __syncwarp();
+    tc_fence_after();
+    uint32_t d1[16];
+    tmem_ld16_nowait(tb + 384, d1);
+    tmem_wait_ld();
+    const int nval = z == 0 ? 12 : 1;
+    (void)nval;
+    // the two threads of a row split the action dimensions: h = 0 takes j < 6 (ACTION Philox blocks 0, 1),
+    // h = 1 takes j >= 6 (blocks 1, 2); their log-density terms meet in smem for the fixed-order sum.
     if (threadIdx.x == 128) FP_STAMP(7);
     const int hs = (warp - 4) >> 2;
-    float* xrow = sX + r * 26;  // [2][13]: the two threads' partial sums
-#pragma unroll
-    for (int j = 0; j < 12; ++j) if (j < nval) xrow[hs * 13 + j] = tot[j];
-    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
+    float* xrow = sX + r * 26;
     const int row = m0 + r;
     if (z == 1) {
       if (hs == 0 && row < a.N) {
-        const float V = __fadd_rn(tot[0] + xrow[13], __ldg(a.b4c));
+        const float V = __fadd_rn(__uint_as_float(d1[0]), __ldg(a.b4c));
         a.value[row] = V;
         if (a.u_value) a.u_value[row] = V;
       }
@@ -1574,9 +1978,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
 #pragma unroll
         for (int jj = 0; jj < 6; ++jj) {
           const int j = 6 * hs + jj;
-          const float other = xrow[(1 - hs) * 13 + j];
-          const float tj = hs == 0 ? tot[jj] : tot[6 + jj];  // constant indices: tot[] stays in registers
-          const float mu = __fadd_rn(tj + other, __ldg(a.b4a + j));
+          const float dj = __uint_as_float(hs == 0 ? d1[jj] : d1[6 + jj]);  // constant indices: d1[] stays in registers
+          const float mu = __fadd_rn(dj, __ldg(a.b4a + j));
           const float ls = __ldg(a.logstd + j);
           const bool first = (j >> 2) == (hs == 0 ? 0 : 1);
           const float act = a.deterministic ? mu : sample_action_b(first ? blk0 : blk1, j, mu, ls);
@@ -1587,7 +1990,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
           if (a.u_mu) a.u_mu[(size_t)row * 12 + j] = mu;
         }
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));  // all sums read before the terms overwrite them
 #pragma unroll
       for (int jj = 0; jj < 6; ++jj) trow[6 * hs + jj] = tm[jj];
       asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
@@ -1807,6 +2209,38 @@ cudaError_t launch_gemm_dw(int bn, const GemmArgs& a, const DwOut& o, int S, cud
     case 256: return launch_dw_bn<256>(a, o, S, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// EPI 4: the update's layer 3 + PPO loss head. Weight-stationary (each CTA keeps its net's W3, <= 4 k-blocks);
+// the grid covers min(m_tiles, #SMs / 2) CTAs per net, split between the nets by the epilogue cost of their rows
+// (an actor row does 12 head outputs, its KL and 12 x 128 head-gradient products; a critic row one) --
+// LG_LOSS_ACTOR_FRAC overrides the share (measurement only). Every CTA owns at least one tile.
+int gemm_loss_grid(const GemmArgs& a) {
+  const int m_tiles = (a.M + 127) / 128;
+  return 2 * std::min(m_tiles, g_dw_max_ctas() / 2);
+}
+cudaError_t launch_gemm_loss(const GemmArgs& a0, int* grid_out, cudaStream_t st) {
+  using C = GemmCfg<128, 4, false, 4>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<128, false, false, 4, false, 4>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  static const double frac = [] { const char* e = getenv("LG_LOSS_ACTOR_FRAC"); return e ? atof(e) : 0.65; }();
+  GemmArgs a = a0;
+  a.m_tiles = (a.M + 127) / 128;
+  a.nz = 2; a.n_tiles = 1; a.n_splits = 1; a.kb_per_split = a.kb_total;
+  if (a.kb_total < 1 || a.kb_total > 4 || a.N > 128 || a.le.H2 != a.N || a.M_dev) return cudaErrorInvalidValue;
+  const int grid = gemm_loss_grid(a);
+  int split = (int)std::lround(frac * grid);
+  split = std::max(split, grid - a.m_tiles);
+  split = std::min(split, a.m_tiles);
+  split = std::max(1, std::min(grid - 1, split));
+  a.ws_split = split;
+  if (grid_out) *grid_out = grid;
+  return launch_pdl(k_gemm_tc<128, false, false, 4, false, 4>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, st, a);
 }
 
 cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, cudaStream_t st) {

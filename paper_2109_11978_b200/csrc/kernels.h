@@ -74,6 +74,22 @@ void launch_action_eps(int N, int rank, uint32_t s0, uint32_t s1, const DevScala
 // ------------------------------------------------------------------ tcgen05 GEMM
 enum GemmKind { GEMM_FWD = 0, GEMM_DX = 1, GEMM_DW = 2 };
 
+// EPI 4 (layer-3 forward of the update): the PPO loss head fused into the epilogue: per row the
+// actor / critic heads, the clipped surrogate, value loss, KL, dmu / dV -> dZ3 (the GEMM's bf16 output), and
+// per-CTA partials of the head / log-std gradients and loss statistics (k_reduce_heads sums them).
+struct LossEpi {
+  const float* W4a; const float* b4a; const float* W4c; const float* b4c;
+  const float* logstd; const float* logstd_old;
+  const float* act; const float* mu_old; const float* logp_old; const float* V_old; const float* adv; const float* ret;
+  float clip, vclip, vf_coef, invM;
+  int H2;                    // real head input width (<= 128; the tile is 128 wide)
+  float* payload;            // the non-finite counter payload[4] is cleared by CTA 0 (first writer of the minibatch)
+  float* part;               // [gridDim.x][HP] CTA partials (k_loss_heads layout)
+  double* spart;             // [gridDim.x][8] fp64 statistics
+  int HP;
+  unsigned long long* dbg;   // diagnostics only (tools/gemm_probe loss): per-CTA, per-tile phase timestamps, else null
+};
+
 struct GemmArgs {
   CUtensorMap tmA[2];
   CUtensorMap tmB[2];
@@ -95,11 +111,17 @@ struct GemmArgs {
   CUtensorMap tmBp[2];       // pair + K-major B: B with a box of BN/2 rows (each CTA loads half of the tile's B)
   int ws;                    // forward / input-gradient GEMMs: weight-stationary schedule (each CTA keeps one column
                              // block of B resident in shared memory and streams only A), when the block fits
+  int ws_split;              // weight-stationary with two slices: CTAs [0, ws_split) serve slice 0 (0 = alternate)
+  LossEpi le;                // EPI 4 only
 };
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
 bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows);
 cudaError_t launch_gemm(GemmKind kind, int bn, const GemmArgs& a, cudaStream_t st);
+// the update's layer-3 forward with the PPO loss head in its epilogue (EPI 4; a.le): 128-wide tiles, weight-stationary
+// (H1 <= 256), CTAs split between the actor and critic slices; returns the grid size (rows of le.part) in *grid
+cudaError_t launch_gemm_loss(const GemmArgs& a, int* grid, cudaStream_t st);
+int gemm_loss_grid(const GemmArgs& a);
 
 struct DwOut {                 // canonical destinations of a weight-gradient GEMM (see k_gemm_dw)
   float* grad;

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(LOSS_WARPS * 32, 1) k_loss_heads(LossArgs a) {
   const float ls = j < 12 ? __ldg(a.logstd + j) : 0.0f;
   const float lso = j < 12 ? __ldg(a.logstd_old + j) : 0.0f;
   const float iv = expf(-2.0f * ls);
-  const float klc = ls - lso + expf(2.0f * lso) * (0.5f * iv) - 0.5f;  // KL terms independent of mu
+  const float klc = kl_const(ls, lso, iv);  // KL terms independent of mu
   const float invM = 1.0f / (float)a.M;
   float gWa[12][4], gWc[4];
 #pragma unroll
@@ -228,30 +228,23 @@ __global__ void __launch_bounds__(LOSS_WARPS * 32, 1) k_loss_heads(LossArgs a) {
     const float lp = logp_warp(act, tot, ls, lane);
     // clipped surrogate (§2.2 / DESIGN.md §3.11); every lane evaluates the row scalars
     const float ratio = expf(lp - lpo);
-    const float s1 = ratio * adv;
-    const float rc = fminf(fmaxf(ratio, 1.0f - a.clip), 1.0f + a.clip);
-    const float s2 = rc * adv;
-    const bool take1 = s1 <= s2;
-    const bool inside = ratio >= 1.0f - a.clip && ratio <= 1.0f + a.clip;
-    const float dLdlp = -(take1 ? adv : (inside ? adv : 0.0f)) * invM * ratio;
-    const float vc = Vo + fminf(fmaxf(V - Vo, -a.vclip), a.vclip);
-    const float e1 = (V - ret) * (V - ret), e2 = (vc - ret) * (vc - ret);
-    const bool take_u = e1 >= e2;
-    const bool vin = fabsf(V - Vo) <= a.vclip;
-    const float dV = a.vf_coef * (take_u ? 2.0f * (V - ret) : (vin ? 2.0f * (vc - ret) : 0.0f)) * invM;
+    float svf, vvf;
+    bool clipped;
+    const float dLdlp = ppo_dlogp(ratio, adv, a.clip, invM, svf, clipped);
+    const float dV = ppo_dvalue(V, Vo, ret, a.vclip, a.vf_coef, invM, vvf);
     const float d = act - tot;
     const float dmu = dLdlp * d * iv;
     const float dm = muo - tot;
-    const float kl = dim_sum(klc + dm * dm * (0.5f * iv), lane);
+    const float kl = dim_sum(kl_term(klc, dm, iv), lane);
     if (dl) {
       gb = gb + dmu;
-      gls = gls + dLdlp * (d * d * iv - 1.0f);
+      gls = gls + gls_term(dLdlp, d, iv);
     }
     if (lane == 0) {
       gbv = gbv + dV;
-      const double sv = (double)(take1 ? s1 : s2), vv = (double)(take_u ? e1 : e2), kv = (double)kl;
+      const double sv = (double)svf, vv = (double)vvf, kv = (double)kl;
       st0 += sv; st1 += vv; st2 += kv;
-      st3 += fabsf(ratio - 1.0f) > a.clip ? 1.0 : 0.0;
+      st3 += clipped ? 1.0 : 0.0;
       st4 += (isfinite(sv) && isfinite(vv) && isfinite(kv)) ? 0.0 : 1.0;
     }
     // dH3 = W4a^T dmu (actor), dV w4c (critic); dZ3 = dH3 * ELU'(H3); dW4 += dY h

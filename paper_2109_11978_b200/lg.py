@@ -17,6 +17,7 @@ BUF = dict(HEIGHTFIELD=0, STATE=1, OBS=2, ACT=3, MU=4, LOGP=5, VALUE=6, REWARD=7
            VALUE_T=12, THETA=13, ADAM_M=14, ADAM_V=15, GRAD=16, WEIGHTS=17, ACTIV=18, WORK=19)
 F_CURRICULUM, F_NOISE, F_PUSH, F_BOOTSTRAP, F_DETERMINISTIC = 1, 2, 4, 8, 32
 F_UNFUSED_POLICY = 256  # diagnostics: per-layer rollout policy instead of the fused kernel (bit-identical)
+F_UNFUSED_LOSS = 512  # diagnostics: layer-3 GEMM + separate loss-head kernel instead of the fused loss epilogue
 STATUS = {0: "LG_OK", 1: "LG_ERR_INVALID_ARG", 2: "LG_ERR_RANGE", 3: "LG_ERR_SHAPE", 4: "LG_ERR_STATE",
           5: "LG_ERR_CUDA", 6: "LG_ERR_NCCL", 7: "LG_ERR_UNSUPPORTED"}
 

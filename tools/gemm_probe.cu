@@ -10,6 +10,7 @@
 #include <cmath>
 #include <algorithm>
 #include <vector>
+#include <string>
 
 #include "../paper_2109_11978_b200/csrc/kernels.h"
 
@@ -132,6 +133,75 @@ static void probe_dx(int M, int N, int K, int bn, cudaStream_t st, bool once = f
     printf("dx M=%d N=%d K=%d bn=%d probe=%d  %8.2f us  %7.1f TFLOP/s\n", M, N, K, bn, probe, us, fl / us * 1e-6);
   }
   CK(cudaFree(dZ)); CK(cudaFree(W)); CK(cudaFree(H)); CK(cudaFree(Y));
+}
+
+// update layer 3 + fused PPO loss head (EPI 4): time it and print per-phase timestamps (tile 0 of the CTA with
+// the latest finish, and averages over CTAs) -- phases: 0 tile start, 1 A3 free, 2 accumulator ready, 3 head sums,
+// 4 loss terms, 5 MMA issued / small sums done, 6 MMAs complete, 7 dZ3 staged
+static void probe_loss(int M, float frac, cudaStream_t st) {
+  const int H1 = 256, H2 = 128;
+  __nv_bfloat16 *H2a, *W3, *dZ3;
+  float *b3, *W4a, *b4a, *W4c, *b4c, *ls, *lso, *act, *muo, *lpo, *Vo, *adv, *ret, *part, *payload;
+  double* spart;
+  unsigned long long* dbg;
+  CK(cudaMalloc(&H2a, (size_t)M * 2 * H1 * 2)); fill(H2a, (size_t)M * 2 * H1);
+  CK(cudaMalloc(&W3, (size_t)2 * H2 * H1 * 2)); fill(W3, (size_t)2 * H2 * H1);
+  CK(cudaMalloc(&dZ3, (size_t)M * 2 * H2 * 2));
+  auto fz = [&](float** p, size_t n, float v) {
+    CK(cudaMalloc(p, n * 4));
+    std::vector<float> h(n);
+    uint32_t s = 777u + (uint32_t)n;
+    for (size_t i = 0; i < n; ++i) { s = s * 1664525u + 1013904223u; h[i] = v * (((s >> 9) & 1023) / 512.0f - 1.0f); }
+    CK(cudaMemcpy(*p, h.data(), n * 4, cudaMemcpyHostToDevice));
+  };
+  fz(&b3, 2 * H2, 0.1f); fz(&W4a, 12 * H2, 0.1f); fz(&b4a, 12, 0.1f); fz(&W4c, H2, 0.1f); fz(&b4c, 1, 0.1f);
+  fz(&ls, 12, 0.1f); fz(&lso, 12, 0.1f); fz(&act, (size_t)M * 12, 1.0f); fz(&muo, (size_t)M * 12, 1.0f);
+  fz(&lpo, M, 5.0f); fz(&Vo, M, 1.0f); fz(&adv, M, 1.0f); fz(&ret, M, 1.0f);
+  CK(cudaMalloc(&part, (size_t)148 * (13 * H2 + 28) * 4));
+  CK(cudaMalloc(&spart, (size_t)148 * 8 * 8));
+  CK(cudaMalloc(&payload, 64));
+  CK(cudaMalloc(&dbg, (size_t)148 * 64 * 8));
+  CK(cudaMemset(dbg, 0, (size_t)148 * 64 * 8));
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  for (int z = 0; z < 2; ++z) {
+    make_tmap_bf16(&g.tmA[z], H2a + z * H1, M, H1, 2 * H1, 128);
+    make_tmap_bf16(&g.tmB[z], W3 + (size_t)z * H2 * H1, H2, H1, H1, 128);
+    make_tmap_bf16(&g.tmC[z], dZ3 + z * H2, M, H2, 2 * H2, 32);
+    g.bias[z] = b3 + z * H2;
+  }
+  g.M = M; g.N = H2; g.kb_total = H1 / 64; g.kb_per_split = g.kb_total; g.n_tiles = 1; g.n_splits = 1;
+  LossEpi& le = g.le;
+  le.W4a = W4a; le.b4a = b4a; le.W4c = W4c; le.b4c = b4c; le.logstd = ls; le.logstd_old = lso;
+  le.act = act; le.mu_old = muo; le.logp_old = lpo; le.V_old = Vo; le.adv = adv; le.ret = ret;
+  le.clip = 0.2f; le.vclip = 0.2f; le.vf_coef = 1.0f; le.invM = 1.0f / M; le.H2 = H2; le.payload = payload;
+  le.part = part; le.spart = spart; le.HP = (13 * H2 + 25 + 3) / 4 * 4;
+  if (frac > 0) setenv("LG_LOSS_ACTOR_FRAC", std::to_string(frac).c_str(), 1);
+  int grid = 0;
+  float us = time_us([&] { CK(launch_gemm_loss(g, &grid, st)); }, st);
+  printf("loss M=%d grid=%d  %8.2f us\n", M, grid, us);
+  le.dbg = dbg;
+  CK(launch_gemm_loss(g, &grid, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> h((size_t)148 * 64);
+  CK(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+  unsigned long long t0 = ~0ull, tend = 0;
+  int slow = 0;
+  for (int b = 0; b < grid; ++b) {
+    if (h[b * 64] && h[b * 64] < t0) t0 = h[b * 64];
+    for (int k = 0; k < 64; ++k)
+      if (h[b * 64 + k] > tend) { tend = h[b * 64 + k]; slow = b; }
+  }
+  printf("first stamp -> last stamp %.2f us; slowest CTA %d\n", (tend - t0) * 1e-3, slow);
+  for (int b : {0, grid / 2, slow, grid - 1}) {
+    printf("CTA %3d:", b);
+    for (int t = 0; t < 8; ++t) {
+      if (!h[(b * 8 + t) * 8]) break;
+      printf(" |t%d", t);
+      for (int k = 0; k < 8; ++k) printf(" %.2f", (h[(b * 8 + t) * 8 + k] - t0) * 1e-3);
+    }
+    printf("\n");
+  }
 }
 
 // weight gradient: dW[N_out][N_in] = dZ[K][N_out]^T X[K][N_in], split-K over G clusters of S per tile
@@ -553,6 +623,10 @@ int main(int argc, char** argv) {
   if (!strcmp(which, "onedx") && argc >= 6) {
     g_do_flush = false;
     probe_dx(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), st, true);
+    return 0;
+  }
+  if (!strcmp(which, "loss")) {  // loss M [actor_frac]
+    probe_loss(atoi(argv[2]), argc > 3 ? (float)atof(argv[3]) : 0.0f, st);
     return 0;
   }
   if (!strcmp(which, "roll")) {  // rollout-size forward GEMMs (M = 4096 envs) at different tile widths
