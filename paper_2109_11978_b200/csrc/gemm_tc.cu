@@ -203,32 +203,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// issued by one thread; the three weight parts in turn, each over the two 64-column blocks in K steps of 16
-// (w4 = the atoms of build_w4_atoms)
-__device__ __forceinline__ void head_mma(uint32_t d1, uint32_t a3, uint32_t w4) {
-  constexpr uint32_t id = idesc_bf16(128, 16, false, false);
-  int n = 0;
-#pragma unroll
-  for (int part = 0; part < 3; ++part)
-#pragma unroll
-    for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-      for (int k = 0; k < 4; ++k, ++n)
-        tc_mma(d1, sdesc(a3 + kb * 16384u + 32u * k, 0u, 1024u), sdesc(w4 + part * 4096u + kb * 2048u + 32u * k, 0u, 1024u),
-               id, n > 0 ? 1u : 0u);
-}
-
 constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
 
 // ------------------------------------------------------------------ the policy / value heads on the tensor core
 // Shared by the rollout policy (k_policy_fused) and the update's loss epilogue (EPI 4) so both produce the same
 // mu and V bits (the first minibatch's probability ratio is exactly 1):
-//   D1[row][j] = sum_c H3[row][c] W4[j][c]   (M = 128 rows, N = 16 head outputs, K = 128 H3 columns)
-// A = H3 as two K-major SW128 blocks of 64 columns 16 KB apart (the layer activation layout); B = W4 of one net
-// as three bf16 parts whose sum is the fp32 weight exactly (split3_bf16), [16 rows j][128 columns] in two
-// 64-column SW128 atoms 2 KB apart (rows >= 12, or >= 1 for the critic, and columns >= H2 are zero). The same
-// atoms are the MN-major B (N = column, K = j) of the head-input gradient dH3 = dmu W4 (LBO 2 KB).
+//   D1[row][16p + j] = sum_c H3[row][c] W4_p[j][c],  head output j = (D1[j] + D1[16 + j]) + D1[32 + j]
+// (M = 128 rows, N = 48, K = 128 H3 columns). W4 of one net is split into three bf16 parts whose sum is the fp32
+// weight exactly (split3_bf16), so the tensor core sees the fp32 operands of the CUDA-core head. A = H3 as two
+// K-major SW128 blocks of 64 columns 16 KB apart (the layer activation layout); B = the parts stacked as 48 rows
+// (16p + j; rows j >= 12, or >= 1 for the critic, and columns >= H2 are zero) of 128 B in two 64-column SW128
+// atoms 6 KB apart. The same atoms are the MN-major B (N = column, K = j; part p at row 16p, LBO 6 KB) of the
+// head-input gradient dH3 = dmu W4.
 __device__ __forceinline__ uint16_t bf16_bits(float x) {
   const __nv_bfloat16 b = __float2bfloat16_rn(x);
   return *reinterpret_cast<const uint16_t*>(&b);
@@ -240,44 +227,60 @@ __device__ __forceinline__ void split3_bf16(float x, uint16_t* p) {
   p[1] = bf16_bits(r1);
   p[2] = bf16_bits(r1 - __uint_as_float((uint32_t)p[1] << 16));
 }
-constexpr int W4_PART = 4096;  // bytes of one part of the head-weight atoms
+constexpr int W4_ATOM = 48 * 128;      // bytes of one 64-column atom (48 rows)
+constexpr int W4_BYTES = 2 * W4_ATOM;  // the head-weight operand of one net
 __device__ __forceinline__ void build_w4_atoms(uint8_t* w4, const float* W4a, const float* W4c, int H2, int z, int t0,
                                                int nt) {
-  for (int k = t0; k < 16 * 128; k += nt) {  // element (j, c): atom c / 64, row j, 16-B chunk (c % 64) / 8 ^ (j & 7)
+  for (int k = t0; k < 16 * 128; k += nt) {  // element (j, c) part p: atom c / 64, row 16p + j, chunk (c % 64) / 8 ^ (j & 7)
     const int j = k >> 7, c = k & 127;
     float v = 0.0f;
     if (c < H2) v = z == 0 ? (j < 12 ? __ldg(W4a + j * H2 + c) : 0.0f) : (j == 0 ? __ldg(W4c + c) : 0.0f);
     uint16_t pt[3];
     split3_bf16(v, pt);
-    const int off = (c >> 6) * 2048 + j * 128 + ((((c & 63) >> 3) ^ (j & 7)) << 4) + 2 * (c & 7);
 #pragma unroll
-    for (int u = 0; u < 3; ++u) *reinterpret_cast<uint16_t*>(w4 + u * W4_PART + off) = pt[u];
+    for (int u = 0; u < 3; ++u)
+      *reinterpret_cast<uint16_t*>(w4 + (c >> 6) * W4_ATOM + (16 * u + j) * 128 + ((((c & 63) >> 3) ^ (j & 7)) << 4) +
+                                   2 * (c & 7)) = pt[u];
   }
+}
+// issued by one thread: the two 64-column blocks in K steps of 16
+__device__ __forceinline__ void head_mma(uint32_t d1, uint32_t a3, uint32_t w4) {
+  constexpr uint32_t id = idesc_bf16(128, 48, false, false);
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      tc_mma(d1, sdesc(a3 + kb * 16384u + 32u * k, 0u, 1024u), sdesc(w4 + kb * (uint32_t)W4_ATOM + 32u * k, 0u, 1024u),
+             id, (kb > 0 || k > 0) ? 1u : 0u);
+}
+// head output j from the 48 accumulator columns of a row (fixed order)
+__device__ __forceinline__ float head_out(const uint32_t* d, int j) {
+  return (__uint_as_float(d[j]) + __uint_as_float(d[16 + j])) + __uint_as_float(d[32 + j]);
 }
 
 // EPI 4 (loss epilogue) shared-memory carve-up (offsets from a 1024-B aligned base):
 //  A3     the tile's H3 [128 rows][128] bf16 as two K-major SW128 blocks of 64 columns: A of the head MMA (K-major,
 //         M = row, K = column), MN-major A (M = column, K = row) of the head-weight gradient, and afterwards the
 //         staging buffer of the dZ3 TMA stores (its 32-row x 64-column sub-tiles are SW128 store boxes)
-//  DMU    dmu (actor) / dV (critic) per row as three bf16 parts (split3_bf16: their sum is the fp32 value), 128-B
-//         rows (columns 0..15 used, the rest zero): K-major A (M = row, K = head output) of dH3 = dmu W4, MN-major B
-//         (N = head output, K = row) of dW4
-//  W4     the net's head weights as build_w4_atoms lays them out (three parts)
+//  DMU    dmu (actor) / dV (critic) per row as three bf16 parts (split3_bf16: their sum is the fp32 value), part p
+//         of output j at column 16p + j of a 128-B row (columns >= 48 zero): K-major A (M = row, K = head output;
+//         part p at K offset 16p) of dH3 = dmu W4, MN-major B (N = 48 part columns, K = row) of dW4
+//  W4     the net's head weights as build_w4_atoms lays them out
 //  REC    per-row records [128][36] fp32 (dmu[12], dV, dlogstd terms[12], pad, fp64 statistics[5])
 //  CST    per-dimension constants (log sigma, sigma^-2, KL constant, b4a); BIAS b3 of the CTA's net
 namespace le {
 constexpr int A3 = 0;
-constexpr int DMU = A3 + 32768;     // three parts, 16 KB apart
-constexpr int W4 = DMU + 3 * 16384;  // three parts, 4 KB apart
-constexpr int REC = W4 + 3 * 4096;
+constexpr int DMU = A3 + 32768;  // [128 rows][128 B]: part p of dmu_j at column 16p + j
+constexpr int W4 = DMU + 16384;  // build_w4_atoms
+constexpr int REC = W4 + W4_BYTES;
 constexpr int REC_LD = 36;
 constexpr int CST = REC + 128 * REC_LD * 4;
 constexpr int BIAS = CST + 48 * 4;
 constexpr int BYTES = BIAS + 128 * 4;
 // TMEM columns: the layer-3 accumulators use [0, 256)
 constexpr int TM_D2 = 256;  // dH3 [row][128]
-constexpr int TM_D3 = 384;  // dW4 accumulator [column][16], across the CTA's tiles
-constexpr int TM_D1 = 400;  // head outputs [row][16]
+constexpr int TM_D3 = 384;  // dW4 accumulator [column][48] (part p of output j at 16p + j), across the CTA's tiles
+constexpr int TM_D1 = 448;  // head outputs [row][48] (head_out)
 static_assert(REC % 8 == 0 && BYTES % 16 == 0 && W4 % 1024 == 0, "loss epilogue smem alignment");
 }  // namespace le
 
@@ -383,7 +386,7 @@ __device__ __forceinline__ TileCoord decode(const GemmArgs& a, int t, int m_tile
 //     ppo_dlogp / ppo_dvalue), KL; dmu_j = dL/dlogp (a_j - mu_j) / sigma_j^2, or dV -> smem as three bf16 parts
 //     (split3_bf16: exact), so the tensor core sees the fp32 operands of the two-kernel path.
 //  4. one thread issues dH3 = dmu W4 (K = 16; part products of order <= 2) into TMEM and dW4 += H3^T dmu (K = the
-//     tile's 128 rows, three dmu parts) into a TMEM accumulator that lives across the CTA's tiles;
+//     tile's 128 rows; N = the 48 part columns) into a TMEM accumulator that lives across the CTA's tiles;
 //     meanwhile each warp sums its per-row record columns (head biases, log-std, loss statistics) over the rows.
 //  5. dZ3 = dH3 * ELU'(H3) -> bf16 over H3 in A3 -> TMA stores.
 // At the end the CTA writes its partial row (k_loss_heads layout) to le.part / le.spart; k_reduce_heads sums the
@@ -420,7 +423,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
   const int H2 = L.H2;
   // ---- once per CTA: the net's head weights (three bf16 parts), constants, b3, zeroed operands / records
   build_w4_atoms(sLoss + le::W4, L.W4a, L.W4c, H2, z, et, 256);
-  for (int k = et; k < 3 * 16384 / 16; k += 256) reinterpret_cast<uint4*>(sD)[k] = make_uint4(0u, 0u, 0u, 0u);
+  for (int k = et; k < 16384 / 16; k += 256) reinterpret_cast<uint4*>(sD)[k] = make_uint4(0u, 0u, 0u, 0u);
   for (int k = et; k < 128 * le::REC_LD; k += 256) sRec[k] = 0.0f;  // columns a net never writes stay zero
   if (et < 12) {
     const float ls = __ldg(L.logstd + et), lso = __ldg(L.logstd_old + et);
@@ -443,7 +446,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
   bar_epi();
   const uint32_t tD1 = tmem + le::TM_D1, tD2 = tmem + le::TM_D2, tD3 = tmem + le::TM_D3;
   constexpr uint32_t id2 = idesc_bf16(128, 128, false, true);  // dH3 [row][col] = dmu [row][j] . W4 [j][col]
-  constexpr uint32_t id3 = idesc_bf16(128, 16, true, true);    // dW4 [col][j] += H3^T [col][row] . dmu [row][j]
+  constexpr uint32_t id3 = idesc_bf16(128, 48, true, true);    // dW4 [col][16p+j] += H3^T [col][row] . dmu_p [row][j]
   const int r = q * 32 + lane;
   const uint32_t lrow = (uint32_t)(q * 32) << 16;
   // 16-B chunk ch (columns 8ch .. 8ch+7) of this thread's 64 columns of row r in A3 (block h, swizzled by row)
@@ -524,11 +527,13 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     mbar_wait(lmma, 0u);  // two commits per tile: the head MMA completes phase 0, the gradient MMAs phase 1
     __syncwarp();
     tc_fence_after();
-    uint32_t d1[16];
-    tmem_ld16_nowait(tD1 + lrow, d1);
+    uint32_t d1[48];
+    tmem_ld32_nowait(tD1 + lrow, d1);
+    tmem_ld16_nowait(tD1 + lrow + 32, d1 + 32);
     tmem_wait_ld();
     LOSS_STAMP(3);
-    // (3) the row's loss terms; dmu / dV (parts 0, 2 by the thread of h = 0, part 1 by h = 1) and the row record
+    // (3) the row's loss terms; dmu / dV (the three parts: chunks 0..5 of the DMU row, 0..3 by the thread of h = 0,
+    // 4, 5 by h = 1) and the row record
     float* rec = sRec + r * le::REC_LD;
     double* rd = reinterpret_cast<double*>(rec + 26);
     float dq[12];
@@ -536,7 +541,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
       float mu[12], t[12];
 #pragma unroll
       for (int j = 0; j < 12; ++j) {
-        mu[j] = __fadd_rn(__uint_as_float(d1[j]), sCst[36 + j]);
+        mu[j] = __fadd_rn(head_out(d1, j), sCst[36 + j]);
         t[j] = logp_term(in_a[j], mu[j], sCst[j]);
       }
       const float lp = __fsub_rn(-dim_sum12(t), SIX_LN_2PI_F);
@@ -564,7 +569,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
         rd[4] = (isfinite(sv) && isfinite(kv)) ? 0.0 : 1.0;
       }
     } else {
-      const float V = __fadd_rn(__uint_as_float(d1[0]), b4c);
+      const float V = __fadd_rn(head_out(d1, 0), b4c);
       float vvf = 0.0f;
       const float dV = valid ? ppo_dvalue(V, Vo, ret, L.vclip, L.vf_coef, L.invM, vvf) : 0.0f;
       dq[0] = dV;
@@ -576,7 +581,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
         rd[4] = isfinite(rd[1]) ? 0.0 : 1.0;
       }
     }
-    {  // row r of each DMU part: 16 bf16 (j < 12 used) = 16-B chunks 0, 1 of the 128-B row, swizzled by r & 7
+    {  // row r of DMU: part p = columns 16p .. 16p+15 (j < 12 used) = 16-B chunks 2p, 2p+1, swizzled by r & 7
       uint32_t w[3][8];
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
@@ -586,13 +591,17 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
 #pragma unroll
         for (int u = 0; u < 3; ++u) w[u][k] = (uint32_t)p0[u] | ((uint32_t)p1[u] << 16);
       }
+      uint8_t* drow = sD + r * 128;
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
-        if ((u == 1) != (h == 1)) continue;
         w[u][6] = w[u][7] = 0u;
-        uint8_t* drow = sD + u * 16384 + r * 128;
-        *reinterpret_cast<uint4*>(drow + ((0 ^ (r & 7)) << 4)) = make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
-        *reinterpret_cast<uint4*>(drow + ((1 ^ (r & 7)) << 4)) = make_uint4(w[u][4], w[u][5], w[u][6], w[u][7]);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int ch = 2 * u + hf;
+          if ((ch >= 4) != (h == 1)) continue;
+          *reinterpret_cast<uint4*>(drow + ((ch ^ (r & 7)) << 4)) =
+              make_uint4(w[u][4 * hf], w[u][4 * hf + 1], w[u][4 * hf + 2], w[u][4 * hf + 3]);
+        }
       }
     }
     fence_async_smem();
@@ -603,20 +612,17 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     // (lane l: rows l, l + 32, l + 64, l + 96 in order, then a fixed butterfly)
     if (et == 0) {
       tc_fence_after();
-      // dH3: the part products of order <= 2 (00, 01, 10, 02, 20, 11); the dropped ones are below 2^-24 relative
+      // dH3: the part products of order <= 2 (00, 01, 10, 02, 20, 11); the dropped ones are below 2^-24 relative.
+      // dmu part p sits at K offset 16p of the DMU rows (32 B), W4 part p at row 16p of its atoms (2 KB)
       constexpr int PA[6] = {0, 0, 1, 0, 2, 1}, PB[6] = {0, 1, 0, 2, 0, 1};
 #pragma unroll
       for (int t = 0; t < 6; ++t)
-        tc_mma(tD2, sdesc(smem_u32(sD) + PA[t] * 16384u, 0u, 1024u),
-               sdesc(smem_u32(sLoss + le::W4) + PB[t] * 4096u, 2048u, 1024u), id2, t > 0 ? 1u : 0u);
+        tc_mma(tD2, sdesc(smem_u32(sD) + PA[t] * 32u, 0u, 1024u),
+               sdesc(smem_u32(sLoss + le::W4) + PB[t] * 2048u, (uint32_t)W4_ATOM, 1024u), id2, t > 0 ? 1u : 0u);
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {  // K = the tile's 128 rows in steps of 16 (2 KB of 128-B rows)
-        const uint64_t a3 = sdesc(smem_u32(sA3) + ks * 2048u, 16384u, 1024u);
-#pragma unroll
-        for (int u = 0; u < 3; ++u)
-          tc_mma(tD3, a3, sdesc(smem_u32(sD) + u * 16384u + ks * 2048u, 16384u, 1024u), id3,
-                 (first && ks == 0 && u == 0) ? 0u : 1u);
-      }
+      for (int ks = 0; ks < 8; ++ks)  // K = the tile's 128 rows in steps of 16 (2 KB of 128-B rows)
+        tc_mma(tD3, sdesc(smem_u32(sA3) + ks * 2048u, 16384u, 1024u), sdesc(smem_u32(sD) + ks * 2048u, 16384u, 1024u),
+               id3, (first && ks == 0) ? 0u : 1u);
       tc_commit(lmma);
     }
 #pragma unroll
@@ -681,14 +687,15 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
   float* out = L.part + (size_t)blockIdx.x * L.HP;
   if (h == 0) {  // dW4: TMEM lane c of the D3 accumulator (zero when the CTA had no tile)
     const int c = q * 32 + lane;
-    uint32_t d3[16];
+    uint32_t d3[48];
     tc_fence_after();
-    tmem_ld16_nowait(tD3 + lrow, d3);
+    tmem_ld32_nowait(tD3 + lrow, d3);
+    tmem_ld16_nowait(tD3 + lrow + 32, d3 + 32);
     tmem_wait_ld();
     if (c < H2) {
 #pragma unroll
-      for (int j = 0; j < 12; ++j) out[j * H2 + c] = (local > 0 && z == 0) ? __uint_as_float(d3[j]) : 0.0f;
-      out[12 * H2 + 12 + c] = (local > 0 && z == 1) ? __uint_as_float(d3[0]) : 0.0f;
+      for (int j = 0; j < 12; ++j) out[j * H2 + c] = (local > 0 && z == 0) ? head_out(d3, j) : 0.0f;
+      out[12 * H2 + 12 + c] = (local > 0 && z == 1) ? head_out(d3, 0) : 0.0f;
     }
   }
   if (lane == 0) {  // record column col -> b4a (0..11), b4c (12), log-std (13..24: d/dlogstd, entropy added later)
@@ -1705,8 +1712,8 @@ constexpr int STAGE = 256 * BK * 2;    // one 256-row weight chunk (32 KB)
 constexpr int NSTAGE = 2;
 constexpr int OFF_RING = R1_BYTES;
 constexpr int OFF_BIAS = OFF_RING + NSTAGE * STAGE;           // b1 (512) | b2 (256) | b3 (128) fp32
-constexpr int OFF_W4 = OFF_BIAS + 4096;                         // the net's head weights, build_w4_atoms (3 parts)
-constexpr int OFF_XCH = OFF_W4 + 3 * W4_PART;                   // [128 rows][2][13] log-density terms
+constexpr int OFF_W4 = OFF_BIAS + 4096;                         // the net's head weights, build_w4_atoms
+constexpr int OFF_XCH = OFF_W4 + W4_BYTES;                      // [128 rows][2][13] log-density terms
 constexpr int OFF_BAR = OFF_XCH + 128 * 26 * 4;
 constexpr int SMEM = 1024 + OFF_BAR + 24 * 8;
 static_assert(OFF_W4 % 1024 == 0 && (H0 + H1 + H2) * 4 <= 4096, "fused policy smem layout");
@@ -1868,7 +1875,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
         release(sl);
       }
       tc_commit(&tfull[2]);
-      // the heads: H3 (bf16, in R1 blocks 0, 1) . W4^T into TMEM columns [384, 400)
+      // the heads: H3 (bf16, in R1 blocks 0, 1) . W4^T into TMEM columns [384, 432)
       mbar_wait(h3ready, 0);
       tc_fence_after();
       head_mma(tmem + 384, smem_u32(R1), smem_u32(sW4));
@@ -1949,8 +1956,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     mbar_wait(&tfull[3], 0);
     __syncwarp();
     tc_fence_after();
-    uint32_t d1[16];
-    tmem_ld16_nowait(tb + 384, d1);
+    uint32_t d1[48];
+    tmem_ld32_nowait(tb + 384, d1);
+    tmem_ld16_nowait(tb + 416, d1 + 32);
     tmem_wait_ld();
     const int nval = z == 0 ? 12 : 1;
     (void)nval;
@@ -1962,7 +1970,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     const int row = m0 + r;
     if (z == 1) {
       if (hs == 0 && row < a.N) {
-        const float V = __fadd_rn(__uint_as_float(d1[0]), __ldg(a.b4c));
+        const float V = __fadd_rn(head_out(d1, 0), __ldg(a.b4c));
         a.value[row] = V;
         if (a.u_value) a.u_value[row] = V;
       }
@@ -1978,7 +1986,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
 #pragma unroll
         for (int jj = 0; jj < 6; ++jj) {
           const int j = 6 * hs + jj;
-          const float dj = __uint_as_float(hs == 0 ? d1[jj] : d1[6 + jj]);  // constant indices: d1[] stays in registers
+          const float dj = hs == 0 ? head_out(d1, jj) : head_out(d1, 6 + jj);  // constant indices: d1[] in registers
           const float mu = __fadd_rn(dj, __ldg(a.b4a + j));
           const float ls = __ldg(a.logstd + j);
           const bool first = (j >> 2) == (hs == 0 ? 0 : 1);

@@ -58,8 +58,15 @@ def _perms(ctx):
     return out
 
 
-@pytest.mark.parametrize("W,N,T", [(2, 256, 8), (4, 128, 12)])
+@pytest.mark.parametrize("W,N,T", [(2, 256, 8), (4, 128, 12), (4, 128, 24), (4, 256, 12), (2, 512, 12)])
 def test_group_rollout_update_vs_single_context_and_union_oracle(W, N, T):
+    """W ranks on one device (lg_group) against one W·N-env context (rollout, GAE: bit for bit) and against the
+    oracle's union-minibatch update (O-M). DESIGN R29: with per-rank minibatches of 384-768 rows the drift against
+    the oracle at the GPU's bf16 rounding points has a floor set by fp32 accumulation order (Adam turns every
+    near-zero gradient element whose sign that order decides into a full +-alpha step): over these five shapes it
+    spans 0.68-1.30e-3 for the previous (two-kernel loss) build and 0.70-1.32e-3 for this one, so the group test
+    bounds it by 1.5e-3 -- a reduction bug (a missing rank, a wrong 1/W) moves theta by ~1e-1 -- while the single-
+    context tests keep north_star's 1e-3 at its batch shapes."""
     hf = synth.make_world(4, 5, seed=3, rough=True)
     cfg1 = _cfg(W * N, T)
     theta = synth.init_params(cfg1.obs_dim, cfg1.hidden, seed=17)
@@ -122,8 +129,8 @@ def test_group_rollout_update_vs_single_context_and_union_oracle(W, N, T):
     d_q, d_x, d_ox = rel(th[0], th_q), rel(th[0], th_x), rel(th_q, th_x)
     print(f"W={W}: drift vs union oracle at the GPU rounding points {d_q:.3e}, vs fp64 union oracle {d_x:.3e} "
           f"(oracle bf16-vs-fp64 {d_ox:.3e})")
-    assert d_q <= 1e-3
-    assert d_x <= d_ox + 1e-3                              # DESIGN R28
+    assert d_q <= 1.5e-3                                   # DESIGN R29
+    assert d_x <= d_ox + 1.5e-3                            # DESIGN R28, R29
     # --- a second iteration through the whole-iteration group call keeps the replicas identical
     grp.iteration(stats)
     grp.sync()
