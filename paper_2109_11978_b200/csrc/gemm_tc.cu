@@ -266,15 +266,15 @@ __device__ __forceinline__ float head_out(const uint32_t* d, int j) {
 //         of output j at column 16p + j of a 128-B row (columns >= 48 zero): K-major A (M = row, K = head output;
 //         part p at K offset 16p) of dH3 = dmu W4, MN-major B (N = 48 part columns, K = row) of dW4
 //  W4     the net's head weights as build_w4_atoms lays them out
-//  REC    per-row records [128][36] fp32 (dmu[12], dV, dlogstd terms[12], pad, fp64 statistics[5])
+//  REC    per-row records, column-major: [25][128] fp32 (dmu[12], dV, dlogstd terms[12]), [5][128] fp64 statistics
 //  CST    per-dimension constants (log sigma, sigma^-2, KL constant, b4a); BIAS b3 of the CTA's net
 namespace le {
 constexpr int A3 = 0;
 constexpr int DMU = A3 + 32768;  // [128 rows][128 B]: part p of dmu_j at column 16p + j
 constexpr int W4 = DMU + 16384;  // build_w4_atoms
 constexpr int REC = W4 + W4_BYTES;
-constexpr int REC_LD = 36;
-constexpr int CST = REC + 128 * REC_LD * 4;
+constexpr int REC_NF = 25, REC_ND = 5;           // column-major: [25][128] fp32, then [5][128] fp64
+constexpr int CST = REC + 128 * (REC_NF * 4 + REC_ND * 8);
 constexpr int BIAS = CST + 48 * 4;
 constexpr int BYTES = BIAS + 128 * 4;
 // TMEM columns: the layer-3 accumulators use [0, 256)
@@ -404,8 +404,45 @@ __device__ __forceinline__ unsigned long long loss_gtimer() {
 }
 #define LOSS_STAMP(k)                                                                                          \
   do {                                                                                                         \
-    if (L.dbg && et == 0) L.dbg[((size_t)blockIdx.x * 8 + (local - 1 < 7 ? local - 1 : 7)) * 8 + (k)] = loss_gtimer(); \
+    if (L.dbg && et == 0) L.dbg[((size_t)blockIdx.x * 8 + (local - 1 < 7 ? local - 1 : 7)) * 16 + (k)] = loss_gtimer(); \
   } while (0)
+
+// warp 3, one thread: per tile, the head MMA once the epilogue has staged H3 (lmma[2]), the gradient MMAs once it
+// has staged dmu (lmma[3]); completions on lmma[0] / lmma[1]. (Issued from a converged control warp the
+// descriptors stay on the uniform datapath; from an epilogue thread each MMA paid ~6 register-to-uniform moves.)
+template <typename C, typename TileAt, typename Skip>
+__device__ __forceinline__ void loss_mma(TileAt tile_at, Skip skip, uint32_t tmem, uint64_t* lmma, uint8_t* sLoss) {
+  const uint32_t tD1 = tmem + le::TM_D1, tD2 = tmem + le::TM_D2, tD3 = tmem + le::TM_D3;
+  constexpr uint32_t id2 = idesc_bf16(128, 128, false, true);  // dH3 [row][col] = dmu [row][j] . W4 [j][col]
+  constexpr uint32_t id3 = idesc_bf16(128, 48, true, true);    // dW4 [col][16p+j] += H3^T [col][row] . dmu_p [row][j]
+  const uint32_t a3 = smem_u32(sLoss + le::A3), dmu = smem_u32(sLoss + le::DMU), w4 = smem_u32(sLoss + le::W4);
+  int local = 0;
+  TileCoord tc;
+  for (int it = 0; tile_at(it, tc); ++it) {
+    if (skip(tc)) continue;
+    const uint32_t ph = (uint32_t)(local & 1);
+    const bool first = local == 0;
+    ++local;
+    mbar_wait(&lmma[2], ph);
+    tc_fence_after();
+    head_mma(tD1, a3, w4);
+    tc_commit(&lmma[0]);
+    mbar_wait(&lmma[3], ph);
+    tc_fence_after();
+    // dH3: the part products of order <= 2 (00, 01, 10, 02, 20, 11); the dropped ones are below 2^-24 relative.
+    // dmu part p sits at K offset 16p of the DMU rows (32 B), W4 part p at row 16p of its atoms (2 KB)
+    constexpr int PA[6] = {0, 0, 1, 0, 2, 1}, PB[6] = {0, 1, 0, 2, 0, 1};
+#pragma unroll
+    for (int t = 0; t < 6; ++t)
+      tc_mma(tD2, sdesc(dmu + PA[t] * 32u, 0u, 1024u), sdesc(w4 + PB[t] * 2048u, (uint32_t)W4_ATOM, 1024u), id2,
+             t > 0 ? 1u : 0u);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)  // K = the tile's 128 rows in steps of 16 (2 KB of 128-B rows)
+      tc_mma(tD3, sdesc(a3 + ks * 2048u, 16384u, 1024u), sdesc(dmu + ks * 2048u, 16384u, 1024u), id3,
+             (first && ks == 0) ? 0u : 1u);
+    tc_commit(&lmma[1]);
+  }
+}
 
 template <typename C, typename TileAt, typename Skip>
 __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileAt tile_at, Skip skip, uint32_t tmem,
@@ -424,7 +461,8 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
   // ---- once per CTA: the net's head weights (three bf16 parts), constants, b3, zeroed operands / records
   build_w4_atoms(sLoss + le::W4, L.W4a, L.W4c, H2, z, et, 256);
   for (int k = et; k < 16384 / 16; k += 256) reinterpret_cast<uint4*>(sD)[k] = make_uint4(0u, 0u, 0u, 0u);
-  for (int k = et; k < 128 * le::REC_LD; k += 256) sRec[k] = 0.0f;  // columns a net never writes stay zero
+  for (int k = et; k < 128 * (le::REC_NF + 2 * le::REC_ND); k += 256) sRec[k] = 0.0f;  // columns a net never writes stay zero
+  double* sRecD = reinterpret_cast<double*>(sRec + 128 * le::REC_NF);
   if (et < 12) {
     const float ls = __ldg(L.logstd + et), lso = __ldg(L.logstd_old + et);
     const float iv = expf(-2.0f * ls);
@@ -457,7 +495,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     if (skip(tc)) continue;
     const int acc = local % C::ACC_STAGES;
     const uint32_t aph = (uint32_t)((local / C::ACC_STAGES) & 1);
-    const bool first = local == 0;
+    const uint32_t mph = (uint32_t)(local & 1);  // lmma[0], lmma[1] complete once per tile
     ++local;
     const int row = tc.m0 + r;
     const bool valid = row < M;
@@ -516,15 +554,12 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     fence_async_smem();
     tc_fence_before();  // the accumulator stage is free once read: the next tile's layer-3 MMAs may start
     __syncwarp();
-    if (lane == 0) mbar_arrive(&tempty[acc]);
-    bar_epi();
-    // (2) the head MMA
-    if (et == 0) {
-      tc_fence_after();
-      head_mma(tD1, smem_u32(sA3), smem_u32(sLoss + le::W4));
-      tc_commit(lmma);
+    if (lane == 0) {
+      mbar_arrive(&tempty[acc]);
+      mbar_arrive(&lmma[2]);  // H3 staged: warp 3 issues the head MMA
     }
-    mbar_wait(lmma, 0u);  // two commits per tile: the head MMA completes phase 0, the gradient MMAs phase 1
+    // (2) the head MMA
+    mbar_wait(&lmma[0], mph);
     __syncwarp();
     tc_fence_after();
     uint32_t d1[48];
@@ -534,8 +569,8 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     LOSS_STAMP(3);
     // (3) the row's loss terms; dmu / dV (the three parts: chunks 0..5 of the DMU row, 0..3 by the thread of h = 0,
     // 4, 5 by h = 1) and the row record
-    float* rec = sRec + r * le::REC_LD;
-    double* rd = reinterpret_cast<double*>(rec + 26);
+    float* rec = sRec + r;     // column col at rec[col * 128]
+    double* rd = sRecD + r;    // statistic k at rd[k * 128]
     float dq[12];
     if (z == 0) {
       float mu[12], t[12];
@@ -556,17 +591,17 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
         const float dm = in_m[j] - mu[j];
         t[j] = kl_term(sCst[24 + j], dm, sCst[12 + j]);
         if (h == 0) {
-          rec[j] = dq[j];
-          rec[13 + j] = valid ? gls_term(dLdlp, d, sCst[12 + j]) : 0.0f;
+          rec[j * 128] = dq[j];
+          rec[(13 + j) * 128] = valid ? gls_term(dLdlp, d, sCst[12 + j]) : 0.0f;
         }
       }
       const float kl = dim_sum12(t);
       if (h == 0) {
         const double sv = valid ? (double)svf : 0.0, kv = valid ? (double)kl : 0.0;
         rd[0] = sv;
-        rd[2] = kv;
-        rd[3] = valid && clipped ? 1.0 : 0.0;
-        rd[4] = (isfinite(sv) && isfinite(kv)) ? 0.0 : 1.0;
+        rd[2 * 128] = kv;
+        rd[3 * 128] = valid && clipped ? 1.0 : 0.0;
+        rd[4 * 128] = (isfinite(sv) && isfinite(kv)) ? 0.0 : 1.0;
       }
     } else {
       const float V = __fadd_rn(head_out(d1, 0), b4c);
@@ -576,9 +611,10 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
 #pragma unroll
       for (int j = 1; j < 12; ++j) dq[j] = 0.0f;
       if (h == 0) {
-        rec[12] = dV;
-        rd[1] = valid ? (double)vvf : 0.0;
-        rd[4] = isfinite(rd[1]) ? 0.0 : 1.0;
+        const double vv = valid ? (double)vvf : 0.0;
+        rec[12 * 128] = dV;
+        rd[128] = vv;
+        rd[4 * 128] = isfinite(vv) ? 0.0 : 1.0;
       }
     }
     {  // row r of DMU: part p = columns 16p .. 16p+15 (j < 12 used) = 16-B chunks 2p, 2p+1, swizzled by r & 7
@@ -606,47 +642,32 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     }
     fence_async_smem();
     tc_fence_before();
+    __syncwarp();
     LOSS_STAMP(4);
-    bar_epi();
-    // (4) the head-gradient MMAs (one thread); meanwhile each warp sums its record columns over the tile's rows
-    // (lane l: rows l, l + 32, l + 64, l + 96 in order, then a fixed butterfly)
-    if (et == 0) {
-      tc_fence_after();
-      // dH3: the part products of order <= 2 (00, 01, 10, 02, 20, 11); the dropped ones are below 2^-24 relative.
-      // dmu part p sits at K offset 16p of the DMU rows (32 B), W4 part p at row 16p of its atoms (2 KB)
-      constexpr int PA[6] = {0, 0, 1, 0, 2, 1}, PB[6] = {0, 1, 0, 2, 0, 1};
-#pragma unroll
-      for (int t = 0; t < 6; ++t)
-        tc_mma(tD2, sdesc(smem_u32(sD) + PA[t] * 32u, 0u, 1024u),
-               sdesc(smem_u32(sLoss + le::W4) + PB[t] * 2048u, (uint32_t)W4_ATOM, 1024u), id2, t > 0 ? 1u : 0u);
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)  // K = the tile's 128 rows in steps of 16 (2 KB of 128-B rows)
-        tc_mma(tD3, sdesc(smem_u32(sA3) + ks * 2048u, 16384u, 1024u), sdesc(smem_u32(sD) + ks * 2048u, 16384u, 1024u),
-               id3, (first && ks == 0) ? 0u : 1u);
-      tc_commit(lmma);
-    }
+    if (lane == 0) mbar_arrive(&lmma[3]);  // dmu staged: warp 3 issues the gradient MMAs
+    // (4) meanwhile each warp sums its record columns over the tile's rows: every lane keeps its rows' partial sums
+    // (rows l, l + 32, l + 64, l + 96 of every tile, in order) and the warp adds its lanes once at the end
+    bar_epi();                             // every row's record is written
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int col = e + 8 * k;
       if (col < 25) {
-        float v = sRec[lane * le::REC_LD + col];
-        v = v + sRec[(lane + 32) * le::REC_LD + col];
-        v = v + sRec[(lane + 64) * le::REC_LD + col];
-        v = v + sRec[(lane + 96) * le::REC_LD + col];
-        v = warp_sum(v);
-        xf[k] = xf[k] + v;
+        const float* cp = sRec + col * 128 + lane;
+        xf[k] = xf[k] + cp[0];
+        xf[k] = xf[k] + cp[32];
+        xf[k] = xf[k] + cp[64];
+        xf[k] = xf[k] + cp[96];
       }
     }
     if (e < 5) {
-      const double* d0 = reinterpret_cast<const double*>(sRec + 26) + e;
-      double v = d0[lane * (le::REC_LD / 2)];
-      v += d0[(lane + 32) * (le::REC_LD / 2)];
-      v += d0[(lane + 64) * (le::REC_LD / 2)];
-      v += d0[(lane + 96) * (le::REC_LD / 2)];
-      xd += warp_sum_d(v);
+      const double* d0 = sRecD + e * 128 + lane;
+      xd += d0[0];
+      xd += d0[32];
+      xd += d0[64];
+      xd += d0[96];
     }
     LOSS_STAMP(5);
-    mbar_wait(lmma, 1u);
+    mbar_wait(&lmma[1], mph);
     __syncwarp();
     tc_fence_after();
     LOSS_STAMP(6);
@@ -698,6 +719,9 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
       out[12 * H2 + 12 + c] = (local > 0 && z == 1) ? head_out(d3, 0) : 0.0f;
     }
   }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) xf[k] = warp_sum(xf[k]);  // (fixed butterfly, the same order on every lane)
+  xd = warp_sum_d(xd);
   if (lane == 0) {  // record column col -> b4a (0..11), b4c (12), log-std (13..24: d/dlogstd, entropy added later)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -737,8 +761,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;  // WSKB: the resident B slice has landed
-  uint64_t* lmma = bfull + 1;    // EPI 4: the epilogue's head-gradient MMAs of a tile have completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmma + 1);
+  uint64_t* lmma = bfull + 1;    // EPI 4: [0] head MMA done, [1] gradient MMAs done, [2] H3 staged, [3] dmu staged
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lmma + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
@@ -792,7 +816,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], (PAIR ? 2 : 1) * EPI_WARPS); }
     mbar_init(bfull, 1);
-    mbar_init(lmma, 1);
+    mbar_init(&lmma[0], 1);
+    mbar_init(&lmma[1], 1);
+    mbar_init(&lmma[2], EPI_WARPS);
+    mbar_init(&lmma[3], EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (EPI == 3) {  // 16 x 64 bf16 ones (any swizzle of a constant tile is the same tile)
@@ -948,6 +975,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
         else tc_commit(&tfull[acc]);
       }
     }
+    __syncwarp();
+  } else if (warp == 3 && EPI == 4) {
+    // ---------------------------------------------------------------- loss epilogue's MMA issuer
+    if (lane == 0) loss_mma<C>(tile_at, skip, tmem, lmma, sLoss);
     __syncwarp();
   } else if (warp >= 4 && EPI == 4) {
     // ---------------------------------------------------------------- loss epilogue

@@ -136,8 +136,8 @@ static void probe_dx(int M, int N, int K, int bn, cudaStream_t st, bool once = f
 }
 
 // update layer 3 + fused PPO loss head (EPI 4): time it and print per-phase timestamps (tile 0 of the CTA with
-// the latest finish, and averages over CTAs) -- phases: 0 tile start, 1 A3 free, 2 accumulator ready, 3 head sums,
-// 4 loss terms, 5 MMA issued / small sums done, 6 MMAs complete, 7 dZ3 staged
+// the latest finish) -- phases: 0 tile start, 1 A3 free, 2 accumulator ready, 3 head outputs read, 4 loss terms,
+// 5 small sums done, 6 gradient MMAs complete, 7 dZ3 staged, 8 gradient MMAs issued, 9 after the loss barrier
 static void probe_loss(int M, float frac, cudaStream_t st) {
   const int H1 = 256, H2 = 128;
   __nv_bfloat16 *H2a, *W3, *dZ3;
@@ -160,8 +160,8 @@ static void probe_loss(int M, float frac, cudaStream_t st) {
   CK(cudaMalloc(&part, (size_t)148 * (13 * H2 + 28) * 4));
   CK(cudaMalloc(&spart, (size_t)148 * 8 * 8));
   CK(cudaMalloc(&payload, 64));
-  CK(cudaMalloc(&dbg, (size_t)148 * 64 * 8));
-  CK(cudaMemset(dbg, 0, (size_t)148 * 64 * 8));
+  CK(cudaMalloc(&dbg, (size_t)148 * 128 * 8));
+  CK(cudaMemset(dbg, 0, (size_t)148 * 128 * 8));
   GemmArgs g;
   memset(&g, 0, sizeof(g));
   for (int z = 0; z < 2; ++z) {
@@ -183,22 +183,22 @@ static void probe_loss(int M, float frac, cudaStream_t st) {
   le.dbg = dbg;
   CK(launch_gemm_loss(g, &grid, st));
   CK(cudaStreamSynchronize(st));
-  std::vector<unsigned long long> h((size_t)148 * 64);
+  std::vector<unsigned long long> h((size_t)148 * 128);
   CK(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
   unsigned long long t0 = ~0ull, tend = 0;
   int slow = 0;
   for (int b = 0; b < grid; ++b) {
-    if (h[b * 64] && h[b * 64] < t0) t0 = h[b * 64];
-    for (int k = 0; k < 64; ++k)
-      if (h[b * 64 + k] > tend) { tend = h[b * 64 + k]; slow = b; }
+    if (h[b * 128] && h[b * 128] < t0) t0 = h[b * 128];
+    for (int k = 0; k < 128; ++k)
+      if (h[b * 128 + k] > tend) { tend = h[b * 128 + k]; slow = b; }
   }
   printf("first stamp -> last stamp %.2f us; slowest CTA %d\n", (tend - t0) * 1e-3, slow);
   for (int b : {0, grid / 2, slow, grid - 1}) {
     printf("CTA %3d:", b);
     for (int t = 0; t < 8; ++t) {
-      if (!h[(b * 8 + t) * 8]) break;
+      if (!h[(b * 8 + t) * 16]) break;
       printf(" |t%d", t);
-      for (int k = 0; k < 8; ++k) printf(" %.2f", (h[(b * 8 + t) * 8 + k] - t0) * 1e-3);
+      for (int k = 0; k < 10; ++k) printf(" %.2f", (h[(b * 8 + t) * 16 + k] - t0) * 1e-3);
     }
     printf("\n");
   }
