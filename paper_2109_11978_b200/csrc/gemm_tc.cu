@@ -1257,18 +1257,17 @@ __device__ __forceinline__ void dw_partial_barrier_reduce(const GemmArgs& args, 
     DW_STAMP(6);
     return;
   }
-  // partial -> L2 buffer [tile][split][128][RLD]: one bulk async copy (the TMA engine streams the whole
-  // 128 x RLD fp32 tile from shared memory)
+  // partial -> L2 buffer [tile][split][128][RLD]: every thread copies 16-B chunks (coalesced, L2-only stores).
+  // (One bulk async copy of the whole 128 x RLD tile by one thread streamed at ~25 B/clk per SM: 5-6 us of a
+  // ~23 us launch; the all-thread copy runs near the SM's store rate.)
   float* part_me = out.part + ((size_t)tile * S + split) * 128 * RLD;
-  fence_async_smem();  // this thread's smem writes -> visible to the async proxy
   __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(part_me), "r"(smem_u32(red)),
-                 "r"((uint32_t)(128 * RLD * 4))
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+  {
+    const float4* src = reinterpret_cast<const float4*>(red);
+    float4* dst = reinterpret_cast<float4*>(part_me);
+    constexpr int NV = 128 * RLD / 4;
+#pragma unroll 4
+    for (int k = threadIdx.x; k < NV; k += blockDim.x) __stcg(dst + k, src[k]);
   }
   __threadfence();
   __syncthreads();

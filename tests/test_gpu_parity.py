@@ -360,6 +360,51 @@ def test_deterministic_policy_takes_the_mean_action():
     assert np.max(np.abs(mus[0] - mus[1])) <= 1e-4 * np.sqrt(np.mean(mus[0].astype(np.float64) ** 2))
 
 
+def test_traversability_evaluation_vs_oracle():
+    """NEXT-4 (P:119 Fig. caption): tools/evaluate.py's protocol -- robots spawned at the centre of every
+    tile of a generated world (3 levels x 5 terrain kinds), command (0.75, U[-0.1, 0.1], 0), deterministic policy
+    a = mu, no noise / pushes / curriculum -- replayed on the oracle environment with the GPU's actions: every
+    robot's first outcome (tile exit before base contact / crash / neither) and its step are the same, the final
+    environment state is bit-exact, and every step's actions equal the oracle MLP's mean on the same bf16
+    observation rows within the bf16 tolerance."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "evaluate", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "evaluate.py"))
+    ev = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ev)
+    L, E, steps, seed = 3, 4, 150, 5
+    ctx, hf, cmd = ev.setup(L, E, steps, seed)
+    C = len(ev.KINDS)
+    N = L * C * E
+    env = oracle.Env(N, hf, L, C, seed=seed, flags=0)
+    env.reset()
+    k = np.arange(N) // E
+    env.state["level"] = k // C
+    env.state["col"] = k % C
+    env.reset(init=False)
+    env.state["cmd"] = cmd
+    assert gpu_state(ctx).tobytes() == env.state.tobytes()
+    out, stp, acts = ev.run(ctx, steps, record=True)
+    theta = synth.init_params(ctx.cfg.obs_dim if hasattr(ctx.cfg, "obs_dim") else 235, (512, 256, 128), seed=seed)
+    p = learn.unpack(theta.astype(np.float64), 235, (512, 256, 128))
+    obs = ctx.obs.float().cpu().numpy()[:, :, :235]
+    o_out = np.zeros(N, np.int8)
+    o_stp = np.full(N, -1, np.int32)
+    for t in range(steps):
+        mu_o, _ = learn.mlp_forward(p, obs[t], "a")
+        assert_bf16_close(acts[t], mu_o, f"mu t={t}")
+        _, _, te, _, _, _ = env.step(acts[t])
+        crashed = (te != 0) & (o_out == 0)
+        crossed = (env.state["crossed"] != 0) & (o_out == 0) & ~crashed
+        o_out[crashed] = -1
+        o_out[crossed] = 1
+        o_stp[crashed | crossed] = t + 1
+    assert np.array_equal(out, o_out) and np.array_equal(stp, o_stp)
+    assert gpu_state(ctx).tobytes() == env.state.tobytes()
+    assert (o_out != 0).any()                          # the replay decides outcomes (crashes at least)
+
+
 # ------------------------------------------------------------------ GAE (fp32 vs fp64 oracle)
 def _rollout(ctx, cfg):
     ctx.reset()
