@@ -81,6 +81,17 @@ int bn_fit(int bn, int n, int m_rows, int nz) {
   return bn;
 }
 int bn_small(int n, int m_rows, int nz) { return bn_fit(bn_for(n), n, m_rows, nz); }
+// schedule of the update's layer-2 forward GEMM (LG_L2_MODE): 0 tile order (W2 re-streamed per tile), 1 weight-
+// stationary 128-wide column blocks, 2 CTA pairs (256-row tiles, each CTA streams half of W2's tile; the default:
+// measured on one box 4.555 / 4.583 / 4.657 ms per C3 iteration for 2 / 0 / 1)
+bool reduce_side() {  // LG_REDUCE_SIDE=0 keeps k_reduce_heads on the main stream (measurement)
+  static const bool v = [] { const char* e = getenv("LG_REDUCE_SIDE"); return !(e && e[0] == '0'); }();
+  return v;
+}
+int l2_mode() {
+  static const int m = [] { const char* e = getenv("LG_L2_MODE"); return e ? atoi(e) : 2; }();
+  return m;
+}
 
 struct DwPlan {
   int rows, N, bn, n_tiles, m_tiles, kb_total, tiles, S, kb_per_split, pair;
@@ -252,6 +263,9 @@ struct lg_ctx {
   // events, captured as graph edges)
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork[3] = {nullptr, nullptr, nullptr}, ev_join = nullptr;
+  // third stream: the head-gradient reduction (k_reduce_heads) beside dX3 (it feeds only Adam / the collective)
+  cudaStream_t st3 = nullptr;
+  cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
   lg_status err = LG_OK;
   std::string msg;
   int world = 1;
@@ -264,6 +278,8 @@ struct lg_ctx {
   GemmArgs l2r, l3r;        // layers 2, 3 for M <= n_envs rows (rollout): narrower tiles (bn2r, bn3r)
   GemmArgs l1_upd_b1, dw1_b1;  // layer-1 forward and weight gradient on gathered set 1 (l1_upd / dw1: set 0)
   GemmArgs l3loss;          // update layer 3 with the PPO loss head in its epilogue (EPI 4; le set per minibatch)
+  GemmArgs l2u;             // update layer 2 (minibatch rows), in the schedule of l2_mode()
+  int bn2x = 0;             // its tile width
   int bn2r = 0, bn3r = 0;
   int bn1u = 0, bn2u = 0, bn3u = 0, bnx3 = 0, bnx2 = 0;  // update GEMMs (minibatch rows; narrower when M is small)
   CUtensorMap tmW2f[2], tmW3f[2];  // the fused rollout policy's W2 / W3 maps (its fixed boxes, not the update's)
@@ -278,6 +294,8 @@ struct lg_ctx {
   // profiling (lg_profile): event pairs around launches
   struct PP { int cat, a, b; };
   bool prof = false, capturing = false;
+  // single-rank ppo_update: dW1 stores only its split partials and Adam sums them (AdamDw1); set by run_update
+  bool dw1_partial = false;
   std::vector<cudaEvent_t> ev;
   std::vector<PP> pairs, gpairs;
   size_t evn = 0;
@@ -426,6 +444,9 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     bool ok2 = cudaStreamCreateWithPriority(&ctx->st2, cudaStreamNonBlocking, prio) == cudaSuccess;
     for (int k = 0; k < 3; ++k) ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_fork[k], cudaEventDisableTiming) == cudaSuccess;
     ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaStreamCreateWithPriority(&ctx->st3, cudaStreamNonBlocking, prio) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_fork3, cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_join3, cudaEventDisableTiming) == cudaSuccess;
     if (!ok2) {
       delete ctx;
       return LG_ERR_CUDA;
@@ -505,6 +526,23 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     g3.bias[z] = b3 + z * d.H2;
   }
   set_fwd_common(g2, d.Mmb, d.H1, d.H0, bn2, 2); g2.ldo = 2 * d.H1;
+  {  // the update's layer 2: B (W2 of a net, H1 x H0) is re-streamed for every row tile unless it stays resident
+    GemmArgs& u2 = ctx->l2u;
+    u2 = g2;
+    ctx->bn2x = bn2;
+    const int mode = l2_mode();
+    if (mode == 1 && d.H0 / 64 <= 8) {  // weight-stationary 128-wide column blocks (128 x H0 bf16 <= 128 KB resident)
+      ctx->bn2x = 128;
+      for (int z = 0; z < 2; ++z)
+        ok &= make_tmap_bf16(&u2.tmB[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, 128);
+      set_fwd_common(u2, d.Mmb, d.H1, d.H0, 128, 2);
+      u2.ws = 1;
+    } else if (mode == 2 && bn2 >= 128) {  // CTA pairs: 256-row tiles, each CTA streams half of the tile's B
+      u2.pair = 1;
+      for (int z = 0; z < 2; ++z)
+        ok &= make_tmap_bf16(&u2.tmBp[z], W2 + (size_t)z * d.H1 * d.H0, d.H1, d.H0, d.H0, bn2 / 2);
+    }
+  }
   set_fwd_common(g3, d.Mmb, d.H2, d.H1, bn3, 2); g3.ldo = 2 * d.H2;
   g3.ws = 1;
   {  // layer 3 + loss head (EPI 4): 128-wide tiles (a whole head input row per tile), output dZ3
@@ -675,6 +713,9 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
 lg_status lg_destroy(lg_ctx* ctx) {
   if (!ctx) return LG_ERR_INVALID_ARG;
   if (ctx->st2) { cudaStreamSynchronize(ctx->st2); cudaStreamDestroy(ctx->st2); }
+  if (ctx->st3) { cudaStreamSynchronize(ctx->st3); cudaStreamDestroy(ctx->st3); }
+  if (ctx->ev_fork3) cudaEventDestroy(ctx->ev_fork3);
+  if (ctx->ev_join3) cudaEventDestroy(ctx->ev_join3);
   for (int k = 0; k < 3; ++k) if (ctx->ev_fork[k]) cudaEventDestroy(ctx->ev_fork[k]);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
@@ -762,11 +803,11 @@ static lg_status forward_rows(lg_ctx* ctx, GemmArgs& l1, int bn1, int M, int cat
   g_gemm_cat = cat;
   l1.M = M;
   const bool small = M <= d.N;
-  GemmArgs g2 = small ? ctx->l2r : ctx->l2, g3 = small ? ctx->l3r : ctx->l3;
+  GemmArgs g2 = small ? ctx->l2r : ctx->l2u, g3 = small ? ctx->l3r : ctx->l3;
   g2.M = M; g3.M = M;
   lg_status s;
   if ((s = gemm(ctx, GEMM_FWD, l1, bn1, 1)) != LG_OK) return s;
-  if ((s = gemm(ctx, GEMM_FWD, g2, small ? ctx->bn2r : ctx->bn2u, 2)) != LG_OK) return s;
+  if ((s = gemm(ctx, GEMM_FWD, g2, small ? ctx->bn2r : ctx->bn2x, 2)) != LG_OK) return s;
   if ((s = gemm(ctx, GEMM_FWD, g3, small ? ctx->bn3r : ctx->bn3u, 2)) != LG_OK) return s;
   return LG_OK;
 }
@@ -1043,6 +1084,12 @@ static GatherArgs gather_args(lg_ctx* ctx, int b);
 static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm);
 // the loss epilogue fused into layer 3 (EPI 4): its weight-stationary schedule keeps W3 (H1 x 128 bf16 per net)
 // resident, which fits for H1 <= 256
+// the layer-1 weight gradient leaves its split-K reduction to Adam (single-rank ppo_update, S > 1 splits):
+// no grid barrier and no reduction pass on the critical path; the multi-rank collective needs the reduced gradient
+static bool dw1_partial_ok(const lg_ctx* ctx) {
+  static const bool off = [] { const char* e = getenv("LG_DW1_PARTIAL"); return e && e[0] == '0'; }();
+  return !off && ctx->dw1_partial && ctx->world == 1 && !ctx->group && ctx->L.dw1.S > 1;
+}
 static bool fused_loss_ok(const lg_ctx* ctx) {
   return ctx->d.H1 <= 256 && ctx->d.H2 <= 128 && !(ctx->cfg.flags & LG_F_UNFUSED_LOSS);
 }
@@ -1067,10 +1114,10 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
     // layers 1, 2, then layer 3 with the PPO loss head in its epilogue (H3 stays on chip; output dZ3)
     g_gemm_cat = LG_PROF_GEMM_FWD;
     l1.M = d.Mmb;
-    GemmArgs g2 = ctx->l2;
+    GemmArgs g2 = ctx->l2u;
     g2.M = d.Mmb;
     if ((s = gemm(ctx, GEMM_FWD, l1, ctx->bn1u, 1)) != LG_OK) return s;
-    if ((s = gemm(ctx, GEMM_FWD, g2, ctx->bn2u, 2)) != LG_OK) return s;
+    if ((s = gemm(ctx, GEMM_FWD, g2, ctx->bn2x, 2)) != LG_OK) return s;
     GemmArgs gl = ctx->l3loss;
     gl.M = d.Mmb;
     LossEpi& le = gl.le;
@@ -1089,9 +1136,20 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
       if (e != cudaSuccess) return fail(ctx, LG_ERR_CUDA, "gemm_loss: %s", cudaGetErrorString(e));
     }
     hr.nblk = grid;
-    { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
+    // the head-gradient / statistics reduction feeds only Adam (and the collective): on the third stream beside
+    // dX3 (the profiled pass keeps it on st so its duration is its own)
+    const bool side = !ctx->prof && reduce_side();
+    cudaStream_t sr = side ? ctx->st3 : ctx->st;
+    if (side) {
+      CK(cudaEventRecord(ctx->ev_fork3, ctx->st));
+      CK(cudaStreamWaitEvent(ctx->st3, ctx->ev_fork3, 0));
+    }
+    { Scope sc_(ctx, LG_PROF_REDUCE, sr); launch_reduce_heads(hr, sr); }
     CKL();
-    return backward_chain(ctx, b, next_perm);
+    if (side) CK(cudaEventRecord(ctx->ev_join3, ctx->st3));
+    s = backward_chain(ctx, b, next_perm);
+    if (s == LG_OK && side) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join3, 0));
+    return s;
   }
   if ((s = forward_rows(ctx, l1, ctx->bn1u, d.Mmb)) != LG_OK) return s;
   LossArgs la;
@@ -1129,9 +1187,11 @@ static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm) {
   // category) keeps everything on st so that every kernel's measured duration is its own
   cudaStream_t sdw = ctx->prof ? ctx->st : ctx->st2;
   auto dw = [&](const GemmArgs& g, const DwPlan& p, size_t koff, int cols, const long long* woff,
-                const long long* boff, int row_split) -> lg_status {
+                const long long* boff, int row_split, bool partial = false) -> lg_status {
     DwOut o;
     memset(&o, 0, sizeof(o));
+    o.partial_only = partial ? 1 : 0;
+    o.part_bound = 3.4028234663852886e38f / (float)p.S;
     o.G = 1;
     o.part = at<float>(ctx->buf[LG_BUF_WORK], koff);
     o.cnt = at<int>(ctx->buf[LG_BUF_WORK], koff + p.part_bytes);
@@ -1168,7 +1228,9 @@ static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm) {
   if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
   if ((s = fork(2)) != LG_OK) return s;
-  if ((s = dw(b ? ctx->dw1_b1 : ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0)) != LG_OK) return s;
+  if ((s = dw(b ? ctx->dw1_b1 : ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0, dw1_partial_ok(ctx))) !=
+      LG_OK)
+    return s;
   if (next_perm) {  // the next minibatch's gather (set 1 - b) runs beside dW1
     GatherArgs g = gather_args(ctx, 1 - b);
     g.perm = next_perm;
@@ -1238,6 +1300,7 @@ lg_status ppo_minibatch_grad(lg_ctx* ctx, const int32_t* idx, int32_t M_mb) {
 
 static AdamArgs adam_args(lg_ctx* ctx) {
   AdamArgs aa;
+  memset(&aa, 0, sizeof(aa));
   aa.sh = ctx->shadow;
   aa.theta = reinterpret_cast<float*>(ctx->buf[LG_BUF_THETA]);
   aa.m = reinterpret_cast<float*>(ctx->buf[LG_BUF_ADAM_M]);
@@ -1246,6 +1309,13 @@ static AdamArgs adam_args(lg_ctx* ctx) {
   aa.b1 = ctx->cfg.adam_b1; aa.b2 = ctx->cfg.adam_b2; aa.eps = ctx->cfg.adam_eps;
   aa.inv_world = 1.0f / (float)ctx->world;
   aa.sc = ctx->sc;
+  if (dw1_partial_ok(ctx)) {
+    const Layout& L = ctx->L;
+    AdamDw1& p = aa.dw1;
+    p.part = at<float>(ctx->buf[LG_BUF_WORK], L.k_dw1);
+    p.S = L.dw1.S; p.rld = L.dw1.bn + 20; p.bn = L.dw1.bn; p.n_tiles = L.dw1.n_tiles; p.H0 = ctx->d.H0; p.D = ctx->d.D;
+    p.w_off[0] = ctx->cn.W1[0]; p.w_off[1] = ctx->cn.W1[1]; p.b_off[0] = ctx->cn.b1[0]; p.b_off[1] = ctx->cn.b1[1];
+  }
   return aa;
 }
 static uint32_t* perm_of(lg_ctx* ctx) { return at<uint32_t>(ctx->buf[LG_BUF_WORK], ctx->L.k_perm); }
@@ -1319,6 +1389,11 @@ static lg_status update_end(lg_ctx* ctx, lg_update_stats* stats) {
 }
 static lg_status run_update(lg_ctx* const* cs, int n, lg_update_stats* const* stats) {
   lg_status s;
+  struct Flag {  // dw1_partial for the duration of the update (ppo_minibatch_grad keeps the reduced gradient)
+    lg_ctx* const* cs; int n;
+    Flag(lg_ctx* const* c, int k) : cs(c), n(k) { for (int r = 0; r < n; ++r) cs[r]->dw1_partial = true; }
+    ~Flag() { for (int r = 0; r < n; ++r) cs[r]->dw1_partial = false; }
+  } flag(cs, n);
   for (int r = 0; r < n; ++r) if ((s = update_begin(cs[r])) != LG_OK) return s;
   const int n_mb = cs[0]->d.E * cs[0]->d.K;
   for (int k = 0; k < n_mb; ++k) {

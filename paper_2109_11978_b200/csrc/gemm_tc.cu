@@ -1266,8 +1266,21 @@ __device__ __forceinline__ void dw_partial_barrier_reduce(const GemmArgs& args, 
     const float4* src = reinterpret_cast<const float4*>(red);
     float4* dst = reinterpret_cast<float4*>(part_me);
     constexpr int NV = 128 * RLD / 4;
+    const float bound = out.part_bound;
 #pragma unroll 4
-    for (int k = threadIdx.x; k < NV; k += blockDim.x) __stcg(dst + k, src[k]);
+    for (int k = threadIdx.x; k < NV; k += blockDim.x) {
+      const float4 w = src[k];
+      __stcg(dst + k, w);
+      // partial_only: the consumer (Adam) cannot see the reduced gradient before it applies the step, so the
+      // non-finite rule is taken on the partials (|x| < FLT_MAX / S keeps the S-term sum finite)
+      if (out.partial_only)
+        bad |= !(fabsf(w.x) < bound && fabsf(w.y) < bound && fabsf(w.z) < bound && fabsf(w.w) < bound);
+    }
+  }
+  if (out.partial_only) {
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(out.payload + 4, 1.0f);
+    DW_STAMP(6);
+    return;
   }
   __threadfence();
   __syncthreads();

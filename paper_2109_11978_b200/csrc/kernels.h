@@ -134,6 +134,9 @@ struct DwOut {                 // canonical destinations of a weight-gradient GE
   int* cnt;                    // grid barrier: cnt[0] arrivals (back to 0 at each release), cnt[1] generation
   unsigned long long* dbg;     // diagnostics only (tools/gemm_probe): per-CTA phase timestamps, else null
   int dbg_mode;                // diagnostics only: 1 = skip the reduction, 2 = loads only, 3 = stores only
+  int partial_only;            // store the split partials and stop (Adam sums them: AdamArgs::dw1)
+  float part_bound;            // partial_only: a partial element with |x| >= part_bound (or NaN) counts as non-finite
+                               // (FLT_MAX / S: the S-term sum in Adam cannot overflow)
 };
 // split-K over S CTAs per output tile in one cooperative wave (S * tiles <= #SMs), deterministic reduction
 // of the S fp32 partials through L2 by the whole grid
@@ -287,11 +290,22 @@ struct ShadowArgs {
 };
 constexpr int ADAM_BLOCK_ELEMS = 512;  // k_adam: 256 threads x 2 elements, every block inside one segment
 
+// the layer-1 weight gradient as k_gemm_dw's split partials [tile][S][128][rld] (W1 row R = z H0 + r, column c):
+// Adam sums the S splits in split order 0..S-1 --
+// the reduction k_gemm_dw would have done, the same bits -- instead of reading grad (single-rank update only)
+struct AdamDw1 {
+  const float* part;         // null: W1 / b1 come from grad like every other tensor
+  int S, rld, bn, n_tiles, H0;  // tile t = (R / 128) * n_tiles + c / bn holds columns [bn t', bn t' + bn); bias at
+                                 // column bn of the c = 0 tile
+  long long w_off[2], b_off[2];
+  int D;
+};
 struct AdamArgs {
   ShadowArgs sh;
   float* theta; float* m; float* v; const float* grad;
   float b1, b2, eps, inv_world;
   DevScalars* sc;
+  AdamDw1 dw1;
 };
 void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc,
                  cudaStream_t st);

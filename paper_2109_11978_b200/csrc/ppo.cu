@@ -671,11 +671,53 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payloa
   const int l0 = (bid - a.sh.blk0[sg]) * ADAM_BLOCK_ELEMS + threadIdx.x;
   // this thread's elements are loaded first, so their latency overlaps the Alg. 1 / bias-correction scalars
   float g[ADAM_PER_THREAD], mo[ADAM_PER_THREAD], vo[ADAM_PER_THREAD], tho[ADAM_PER_THREAD];
+  // W1 / b1 of a net from the layer-1 weight gradient's split partials (AdamDw1), summed in split order
+  const AdamDw1& P1 = a.dw1;
+  int zw = -1, zb = -1;
+  if (P1.part) {
+    for (int z = 0; z < 2; ++z) {
+      if (G.off == P1.w_off[z]) zw = z;
+      if (G.off == P1.b_off[z]) zb = z;
+    }
+  }
 #pragma unroll
   for (int u = 0; u < ADAM_PER_THREAD; ++u) {
     const int l = l0 + u * 256;
     const long long i = G.off + l;
-    if (l < n) { g[u] = a.grad[i]; mo[u] = a.m[i]; vo[u] = a.v[i]; tho[u] = a.theta[i]; }
+    if (l < n) {
+      mo[u] = a.m[i]; vo[u] = a.v[i]; tho[u] = a.theta[i];
+      if (zw < 0 && zb < 0) {
+        g[u] = a.grad[i];
+      } else {
+        int R, nt, col;
+        if (zw >= 0) {
+          const int r = l / P1.D, c = l - r * P1.D;
+          R = zw * P1.H0 + r;
+          nt = c / P1.bn;
+          col = c - nt * P1.bn;
+        } else {
+          R = zb * P1.H0 + l;
+          nt = 0;
+          col = P1.bn;
+        }
+        const int tile = (R >> 7) * P1.n_tiles + nt;
+        const float* p = P1.part + ((size_t)tile * P1.S * 128 + (R & 127)) * P1.rld + col;
+        const size_t sstride = (size_t)128 * P1.rld;
+        float acc = 0.0f;
+        // six loads of a pass in flight, then the split-order sum (a wider pass doubled the kernel's registers
+        // and halved the occupancy of every Adam / gather block)
+#pragma unroll 1
+        for (int s0 = 0; s0 < P1.S; s0 += 6) {
+          float w[6];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) w[q] = s0 + q < P1.S ? __ldcg(p + (size_t)(s0 + q) * sstride) : 0.0f;
+#pragma unroll
+          for (int q = 0; q < 6; ++q)
+            if (s0 + q < P1.S) acc = (s0 + q == 0) ? w[0] : acc + w[q];
+        }
+        g[u] = acc;
+      }
+    }
   }
   if (threadIdx.x == 0) {
     DevScalars* sc = a.sc;

@@ -607,6 +607,35 @@ def test_ppo_update_parameter_drift_vs_oracle(scan, rough):
         assert d <= 1e-3, k
 
 
+def test_update_with_adam_summing_dw1_partials_is_bit_identical():
+    """Single-rank ppo_update lets the layer-1 weight-gradient GEMM store only its split-K partials and Adam sum
+    them in split order (no grid barrier / reduction pass on the critical path): the same sum as the GEMM's own
+    reduction, so θ after a full 5 x 4 update is bit-identical to LG_DW1_PARTIAL=0 (run in a second process: the
+    switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import synth\n"
+        "from paper_2109_11978_b200.context import Config, Context\n"
+        "cfg = Config.make(n_envs=512, n_steps=24, scan_nx=17, scan_ny=11, n_levels=4, n_cols=5, flags=15, seed=4)\n"
+        "ctx = Context(cfg, synth.make_world(4, 5, seed=3, rough=True))\n"
+        "ctx.params_set(synth.init_params(cfg.obs_dim, cfg.hidden, seed=4))\n"
+        "ctx.reset()\n"
+        "for _ in range(2): ctx.iteration()\n"
+        "ctx.sync()\n"
+        "sys.stdout.buffer.write(ctx.theta.cpu().numpy().tobytes())\n") % root
+    outs = []
+    for v in ("1", "0"):
+        env = dict(os.environ, LG_DW1_PARTIAL=v)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stderr.decode()[-2000:]
+        outs.append(r.stdout)
+    assert len(outs[0]) > 0 and outs[0] == outs[1]
+
+
 # ------------------------------------------------------------------ whole iteration, graph replay
 @pytest.mark.parametrize("n_envs,T,levels,cols", [(256, 8, 4, 5), (4096, 24, 10, 20), (16384, 50, 10, 20)])
 def test_iteration_graph_replay_matches_eager(n_envs, T, levels, cols):
