@@ -1084,11 +1084,17 @@ static GatherArgs gather_args(lg_ctx* ctx, int b);
 static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm);
 // the loss epilogue fused into layer 3 (EPI 4): its weight-stationary schedule keeps W3 (H1 x 128 bf16 per net)
 // resident, which fits for H1 <= 256
-// the layer-1 weight gradient leaves its split-K reduction to Adam (single-rank ppo_update, S > 1 splits):
-// no grid barrier and no reduction pass on the critical path; the multi-rank collective needs the reduced gradient
+// the weight gradients leave their split-K reduction to Adam (single-rank ppo_update, S > 1 splits): no grid
+// barrier and no reduction pass (dW1's is on the critical path); the multi-rank collective needs reduced gradients
 static bool dw1_partial_ok(const lg_ctx* ctx) {
   static const bool off = [] { const char* e = getenv("LG_DW1_PARTIAL"); return e && e[0] == '0'; }();
   return !off && ctx->dw1_partial && ctx->world == 1 && !ctx->group && ctx->L.dw1.S > 1;
+}
+// the same for the background layers 2 and 3 (LG_DW23_PARTIAL=0 switches it off; same-box A/B on C3: 4.38 ms with,
+// 4.48 ms without -- Adam reads 16 MB more, the two background launches lose their barrier and reduction)
+static bool dw23_partial_ok(const lg_ctx* ctx, const DwPlan& p) {
+  static const bool off = [] { const char* e = getenv("LG_DW23_PARTIAL"); return e && e[0] == '0'; }();
+  return !off && ctx->dw1_partial && ctx->world == 1 && !ctx->group && p.S > 1;
 }
 static bool fused_loss_ok(const lg_ctx* ctx) {
   return ctx->d.H1 <= 256 && ctx->d.H2 <= 128 && !(ctx->cfg.flags & LG_F_UNFUSED_LOSS);
@@ -1216,7 +1222,7 @@ static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm) {
   // launch order inside a layer (measured, same box): dW3 before dX3, dX2 before dW2 (-0.3 %)
   // layer 3
   if ((s = fork(0)) != LG_OK) return s;
-  if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0)) != LG_OK) return s;
+  if ((s = dw(ctx->dw3, L.dw3, L.k_dw3, d.H1, ctx->cn.W3, ctx->cn.b3, 0, dw23_partial_ok(ctx, L.dw3))) != LG_OK) return s;
   GemmArgs x3 = ctx->dx3;
   x3.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x3, ctx->bnx3, 2)) != LG_OK) return s;
@@ -1225,7 +1231,7 @@ static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm) {
   GemmArgs x2 = ctx->dx2;
   x2.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x2, ctx->bnx2, 2)) != LG_OK) return s;
-  if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0)) != LG_OK) return s;
+  if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0, dw23_partial_ok(ctx, L.dw2))) != LG_OK) return s;
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
   if ((s = fork(2)) != LG_OK) return s;
   if ((s = dw(b ? ctx->dw1_b1 : ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0, dw1_partial_ok(ctx))) !=
@@ -1309,13 +1315,18 @@ static AdamArgs adam_args(lg_ctx* ctx) {
   aa.b1 = ctx->cfg.adam_b1; aa.b2 = ctx->cfg.adam_b2; aa.eps = ctx->cfg.adam_eps;
   aa.inv_world = 1.0f / (float)ctx->world;
   aa.sc = ctx->sc;
-  if (dw1_partial_ok(ctx)) {
-    const Layout& L = ctx->L;
-    AdamDw1& p = aa.dw1;
-    p.part = at<float>(ctx->buf[LG_BUF_WORK], L.k_dw1);
-    p.S = L.dw1.S; p.rld = L.dw1.bn + 20; p.bn = L.dw1.bn; p.n_tiles = L.dw1.n_tiles; p.H0 = ctx->d.H0; p.D = ctx->d.D;
-    p.w_off[0] = ctx->cn.W1[0]; p.w_off[1] = ctx->cn.W1[1]; p.b_off[0] = ctx->cn.b1[0]; p.b_off[1] = ctx->cn.b1[1];
-  }
+  const Layout& L = ctx->L;
+  auto part = [&](AdamPart& p, const DwPlan& pl, size_t koff, int m_tiles_z, int row_split, int cols,
+                  const long long* w, const long long* b) {
+    p.part = at<float>(ctx->buf[LG_BUF_WORK], koff);
+    p.S = pl.S; p.rld = pl.bn + 20; p.bn = pl.bn; p.n_tiles = pl.n_tiles; p.m_tiles = m_tiles_z;
+    p.row_split = row_split; p.cols = cols;
+    p.w_off[0] = w[0]; p.w_off[1] = w[1]; p.b_off[0] = b[0]; p.b_off[1] = b[1];
+  };
+  const Dims& d = ctx->d;
+  if (dw1_partial_ok(ctx)) part(aa.part[0], L.dw1, L.k_dw1, L.dw1.m_tiles, d.H0, d.D, ctx->cn.W1, ctx->cn.b1);
+  if (dw23_partial_ok(ctx, L.dw2)) part(aa.part[1], L.dw2, L.k_dw2, L.dw2.m_tiles, 0, d.H0, ctx->cn.W2, ctx->cn.b2);
+  if (dw23_partial_ok(ctx, L.dw3)) part(aa.part[2], L.dw3, L.k_dw3, L.dw3.m_tiles, 0, d.H1, ctx->cn.W3, ctx->cn.b3);
   return aa;
 }
 static uint32_t* perm_of(lg_ctx* ctx) { return at<uint32_t>(ctx->buf[LG_BUF_WORK], ctx->L.k_perm); }

@@ -290,22 +290,22 @@ struct ShadowArgs {
 };
 constexpr int ADAM_BLOCK_ELEMS = 512;  // k_adam: 256 threads x 2 elements, every block inside one segment
 
-// the layer-1 weight gradient as k_gemm_dw's split partials [tile][S][128][rld] (W1 row R = z H0 + r, column c):
-// Adam sums the S splits in split order 0..S-1 --
-// the reduction k_gemm_dw would have done, the same bits -- instead of reading grad (single-rank update only)
-struct AdamDw1 {
-  const float* part;         // null: W1 / b1 come from grad like every other tensor
-  int S, rld, bn, n_tiles, H0;  // tile t = (R / 128) * n_tiles + c / bn holds columns [bn t', bn t' + bn); bias at
-                                 // column bn of the c = 0 tile
+// a layer's weight gradient as k_gemm_dw's split partials [tile][S][128][rld]: Adam sums the S splits of an element
+// in split order 0..S-1 -- the reduction k_gemm_dw would have done, the same bits -- instead of reading grad
+// (single-rank update only). Element (net z, row r, column c) lives in output row tile mt = (z row_split + r) / 128
+// when the nets share one GEMM (layer 1, row_split = H0), else mt = z m_tiles + r / 128; tile = mt n_tiles + c / bn;
+// the bias at column bn of the c = 0 tile
+struct AdamPart {
+  const float* part;         // null: the layer's W / b come from grad like every other tensor
+  int S, rld, bn, n_tiles, m_tiles, row_split, cols;
   long long w_off[2], b_off[2];
-  int D;
 };
 struct AdamArgs {
   ShadowArgs sh;
   float* theta; float* m; float* v; const float* grad;
   float b1, b2, eps, inv_world;
   DevScalars* sc;
-  AdamDw1 dw1;
+  AdamPart part[3];          // layers 1, 2, 3
 };
 void launch_adam(const AdamArgs& a, const float* payload, float kl_target, int world, int m, float* acc,
                  cudaStream_t st);

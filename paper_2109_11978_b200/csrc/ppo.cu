@@ -671,13 +671,17 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payloa
   const int l0 = (bid - a.sh.blk0[sg]) * ADAM_BLOCK_ELEMS + threadIdx.x;
   // this thread's elements are loaded first, so their latency overlaps the Alg. 1 / bias-correction scalars
   float g[ADAM_PER_THREAD], mo[ADAM_PER_THREAD], vo[ADAM_PER_THREAD], tho[ADAM_PER_THREAD];
-  // W1 / b1 of a net from the layer-1 weight gradient's split partials (AdamDw1), summed in split order
-  const AdamDw1& P1 = a.dw1;
-  int zw = -1, zb = -1;
-  if (P1.part) {
+  // a weight / bias tensor whose gradient is still in its GEMM's split partials (AdamPart): summed here in split
+  // order. The segment is block-uniform, so is its layer / net / kind.
+  const AdamPart* PP = nullptr;
+  int pz = 0;
+  bool pbias = false;
+  for (int li = 0; li < 3; ++li) {
+    const AdamPart& q = a.part[li];
+    if (!q.part) continue;
     for (int z = 0; z < 2; ++z) {
-      if (G.off == P1.w_off[z]) zw = z;
-      if (G.off == P1.b_off[z]) zb = z;
+      if (G.off == q.w_off[z]) { PP = &q; pz = z; pbias = false; }
+      if (G.off == q.b_off[z]) { PP = &q; pz = z; pbias = true; }
     }
   }
 #pragma unroll
@@ -686,34 +690,35 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payloa
     const long long i = G.off + l;
     if (l < n) {
       mo[u] = a.m[i]; vo[u] = a.v[i]; tho[u] = a.theta[i];
-      if (zw < 0 && zb < 0) {
+      if (!PP) {
         g[u] = a.grad[i];
       } else {
-        int R, nt, col;
-        if (zw >= 0) {
-          const int r = l / P1.D, c = l - r * P1.D;
-          R = zw * P1.H0 + r;
-          nt = c / P1.bn;
-          col = c - nt * P1.bn;
+        int r, nt, col;
+        if (!pbias) {
+          r = l / PP->cols;
+          const int c = l - r * PP->cols;
+          nt = c / PP->bn;
+          col = c - nt * PP->bn;
         } else {
-          R = zb * P1.H0 + l;
+          r = l;
           nt = 0;
-          col = P1.bn;
+          col = PP->bn;
         }
-        const int tile = (R >> 7) * P1.n_tiles + nt;
-        const float* p = P1.part + ((size_t)tile * P1.S * 128 + (R & 127)) * P1.rld + col;
-        const size_t sstride = (size_t)128 * P1.rld;
+        const int R = PP->row_split ? pz * PP->row_split + r : r;
+        const int mt = PP->row_split ? (R >> 7) : pz * PP->m_tiles + (R >> 7);
+        const float* p = PP->part + ((size_t)(mt * PP->n_tiles + nt) * PP->S * 128 + (R & 127)) * PP->rld + col;
+        const size_t sstride = (size_t)128 * PP->rld;
         float acc = 0.0f;
         // six loads of a pass in flight, then the split-order sum (a wider pass doubled the kernel's registers
         // and halved the occupancy of every Adam / gather block)
 #pragma unroll 1
-        for (int s0 = 0; s0 < P1.S; s0 += 6) {
+        for (int s0 = 0; s0 < PP->S; s0 += 6) {
           float w[6];
 #pragma unroll
-          for (int q = 0; q < 6; ++q) w[q] = s0 + q < P1.S ? __ldcg(p + (size_t)(s0 + q) * sstride) : 0.0f;
+          for (int q = 0; q < 6; ++q) w[q] = s0 + q < PP->S ? __ldcg(p + (size_t)(s0 + q) * sstride) : 0.0f;
 #pragma unroll
           for (int q = 0; q < 6; ++q)
-            if (s0 + q < P1.S) acc = (s0 + q == 0) ? w[0] : acc + w[q];
+            if (s0 + q < PP->S) acc = (s0 + q == 0) ? w[0] : acc + w[q];
         }
         g[u] = acc;
       }

@@ -607,11 +607,11 @@ def test_ppo_update_parameter_drift_vs_oracle(scan, rough):
         assert d <= 1e-3, k
 
 
-def test_update_with_adam_summing_dw1_partials_is_bit_identical():
-    """Single-rank ppo_update lets the layer-1 weight-gradient GEMM store only its split-K partials and Adam sum
-    them in split order (no grid barrier / reduction pass on the critical path): the same sum as the GEMM's own
-    reduction, so θ after a full 5 x 4 update is bit-identical to LG_DW1_PARTIAL=0 (run in a second process: the
-    switch is read once per process)."""
+def test_update_with_adam_summing_dw_partials_is_bit_identical():
+    """Single-rank ppo_update lets the weight-gradient GEMMs store only their split-K partials and Adam sum them
+    in split order (no grid barrier / reduction pass): the same sums as the GEMMs' own reductions, so θ after two
+    iterations is bit-identical with every reduction in the GEMMs (LG_DW1_PARTIAL=0 LG_DW23_PARTIAL=0) and with
+    only layer 1's in Adam (separate processes: the switches are read once per process)."""
     import os
     import subprocess
     import sys
@@ -628,12 +628,12 @@ def test_update_with_adam_summing_dw1_partials_is_bit_identical():
         "ctx.sync()\n"
         "sys.stdout.buffer.write(ctx.theta.cpu().numpy().tobytes())\n") % root
     outs = []
-    for v in ("1", "0"):
-        env = dict(os.environ, LG_DW1_PARTIAL=v)
+    for v1, v23 in (("1", "1"), ("0", "0"), ("1", "0")):  # default (all in Adam), all in the GEMMs, layer 1 only
+        env = dict(os.environ, LG_DW1_PARTIAL=v1, LG_DW23_PARTIAL=v23)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, env=env, timeout=300)
         assert r.returncode == 0, r.stderr.decode()[-2000:]
         outs.append(r.stdout)
-    assert len(outs[0]) > 0 and outs[0] == outs[1]
+    assert len(outs[0]) > 0 and outs[0] == outs[1] == outs[2]
 
 
 # ------------------------------------------------------------------ whole iteration, graph replay
