@@ -1409,6 +1409,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   static_assert(128 * RLD * 4 <= C::STAGES * (C::A_BYTES + C::B_BYTES), "reduction buffer must fit the ring");
 
   DW_STAMP(0);
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = gridDim.x;  // splits per tile
   const int tile = blockIdx.y;
@@ -1435,6 +1436,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw(const __grid_consta
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   DW_STAMP(1);
+  pdl_wait();  // (partial_only launches use PDL: the prologue above overlapped the predecessor)
   const int kb0 = (int)split * args.kb_per_split;
   const int nkb = max(0, min(args.kb_per_split, args.kb_total - kb0));
   const CUtensorMap* tmA = &args.tmA[tc.z];
@@ -1574,6 +1576,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw2(const __grid_const
   static_assert(128 * RLD * 4 <= C::STAGES * (C::A_BYTES + C::B_BYTES), "reduction buffer must fit the ring");
 
   DW_STAMP(0);
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int S = gridDim.x / 2;  // splits per pair tile
@@ -1607,6 +1610,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw2(const __grid_const
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   DW_STAMP(1);
+  pdl_wait();  // (partial_only launches use PDL: the prologue above overlapped the predecessor)
   const int kb0 = split * args.kb_per_split;
   const int nkb = max(0, min(args.kb_per_split, args.kb_total - kb0));
   const CUtensorMap* tmA = &args.tmA[z];
@@ -1705,6 +1709,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_dw2(const __grid_const
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
 
+// launch of a weight-gradient GEMM that stores only its partials (no grid barrier): 0 cooperative (the default:
+// the whole wave starts together), 1 plain, 2 programmatic dependent launch (LG_DW_PARTIAL_LAUNCH, measurement;
+// same-box C3: PDL 4.72 ms vs cooperative 4.38 ms -- early-resident CTAs hold SMs the critical dX kernels need)
+static int dw_partial_launch() {
+  static const int m = [] { const char* e = getenv("LG_DW_PARTIAL_LAUNCH"); return e ? atoi(e) : 0; }();
+  return m;
+}
 template <int BN>
 static cudaError_t launch_dw2_bn(const GemmArgs& a, const DwOut& o, int S, cudaStream_t st) {
   using C = Dw2Cfg<BN>;
@@ -1725,10 +1736,15 @@ static cudaError_t launch_dw2_bn(const GemmArgs& a, const DwOut& o, int S, cudaS
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
-  attr[1].val.cooperative = 1;
+  if (o.partial_only && dw_partial_launch() != 0) {  // no grid barrier: plain (1) or PDL (2) cluster launch
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+  } else {
+    attr[1].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+    attr[1].val.cooperative = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = (o.partial_only && dw_partial_launch() == 1) ? 1 : 2;
   return cudaLaunchKernelEx(&cfg, k_gemm_dw2<BN>, a, o);
 }
 
@@ -2236,10 +2252,15 @@ static cudaError_t launch_dw_bn(const GemmArgs& a, const DwOut& o, int S, cudaSt
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
-  attr[0].val.cooperative = 1;
+  if (o.partial_only && dw_partial_launch() != 0) {  // no grid barrier: plain (1) or PDL (2) launch
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (o.partial_only && dw_partial_launch() == 1) ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, k_gemm_dw<BN, KMAJ>, a, o);
 }
 
