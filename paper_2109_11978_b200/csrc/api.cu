@@ -266,6 +266,11 @@ struct lg_ctx {
   // third stream: the head-gradient reduction (k_reduce_heads) beside dX3 (it feeds only Adam / the collective)
   cudaStream_t st3 = nullptr;
   cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
+  // multi-rank (NCCL): the gradient allreduce in two buckets -- layers 2-4 + heads on st4 as soon as dW2 and the
+  // head reduction are done (overlapping dW1), layer 1 + the loss statistics on st after dW1
+  cudaStream_t st4 = nullptr;
+  cudaEvent_t ev_dw2 = nullptr, ev_heads = nullptr, ev_comm = nullptr;
+  bool early_sent = false;  // this minibatch's early bucket is on st4
   lg_status err = LG_OK;
   std::string msg;
   int world = 1;
@@ -294,8 +299,9 @@ struct lg_ctx {
   // profiling (lg_profile): event pairs around launches
   struct PP { int cat, a, b; };
   bool prof = false, capturing = false;
-  // single-rank ppo_update: dW1 stores only its split partials and Adam sums them (AdamDw1); set by run_update
-  bool dw1_partial = false;
+  // inside ppo_update (run_update): single-rank updates let Adam sum the weight-gradient partials (AdamPart),
+  // NCCL ranks send the early gradient bucket beside dW1; ppo_minibatch_grad keeps the plain reduced gradient
+  bool in_update = false;
   std::vector<cudaEvent_t> ev;
   std::vector<PP> pairs, gpairs;
   size_t evn = 0;
@@ -447,6 +453,10 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     ok2 = ok2 && cudaStreamCreateWithPriority(&ctx->st3, cudaStreamNonBlocking, prio) == cudaSuccess;
     ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_fork3, cudaEventDisableTiming) == cudaSuccess;
     ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_join3, cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaStreamCreateWithPriority(&ctx->st4, cudaStreamNonBlocking, prio) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_dw2, cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_heads, cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_comm, cudaEventDisableTiming) == cudaSuccess;
     if (!ok2) {
       delete ctx;
       return LG_ERR_CUDA;
@@ -716,6 +726,8 @@ lg_status lg_destroy(lg_ctx* ctx) {
   if (ctx->st3) { cudaStreamSynchronize(ctx->st3); cudaStreamDestroy(ctx->st3); }
   if (ctx->ev_fork3) cudaEventDestroy(ctx->ev_fork3);
   if (ctx->ev_join3) cudaEventDestroy(ctx->ev_join3);
+  if (ctx->st4) { cudaStreamSynchronize(ctx->st4); cudaStreamDestroy(ctx->st4); }
+  for (cudaEvent_t e : {ctx->ev_dw2, ctx->ev_heads, ctx->ev_comm}) if (e) cudaEventDestroy(e);
   for (int k = 0; k < 3; ++k) if (ctx->ev_fork[k]) cudaEventDestroy(ctx->ev_fork[k]);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
@@ -952,6 +964,49 @@ static void* coll_ptr(lg_ctx* ctx, CollSel sel) {
   if (sel == COLL_GAE_VAR) return tot + 1;
   return ctx->buf[LG_BUF_GRAD];
 }
+// The [grad ‖ payload] vector of a minibatch in two buckets: early = the parameters of layers 2-4,
+// the heads and log-std of both nets (final once dW2 and the head reduction are done), late = layer 1 of both nets
+// (dW1) and the 16-float statistics payload. Canonical order per net: W1 b1 W2 b2 W3 b3 W4 b4, log-std last, so the
+// buckets are two ranges each (+ the payload); together they cover [0, P + 16) exactly once.
+struct Range { long long off, len; };
+static int grad_bucket(const lg_ctx* ctx, bool early, Range* r) {
+  const Canon& c = ctx->cn;
+  const long long P = ctx->d.P;
+  if (early) {
+    r[0] = {c.W2[0], c.W1[1] - c.W2[0]};
+    r[1] = {c.W2[1], P - c.W2[1]};
+    return 2;
+  }
+  r[0] = {c.W1[0], c.W2[0] - c.W1[0]};
+  r[1] = {c.W1[1], c.W2[1] - c.W1[1]};
+  r[2] = {P, 16};
+  return 3;
+}
+static lg_status nccl_ranges(lg_ctx* ctx, bool early, cudaStream_t st) {
+  Range r[3];
+  const int k = grad_bucket(ctx, early, r);
+  float* g = reinterpret_cast<float*>(ctx->buf[LG_BUF_GRAD]);
+  CKN(ncclGroupStart());
+  for (int i = 0; i < k; ++i) CKN(ncclAllReduce(g + r[i].off, g + r[i].off, (size_t)r[i].len, ncclFloat32, ncclSum, ctx->comm, st));
+  CKN(ncclGroupEnd());
+  return LG_OK;
+}
+// NCCL ranks: the early bucket on st4 once dW2 (st2) and the head reduction (ev_heads) are done -- beside dW1
+static lg_status send_early_bucket(lg_ctx* ctx) {
+  ctx->early_sent = false;
+  if (!ctx->in_update || ctx->world == 1 || !ctx->comm || ctx->group) return LG_OK;
+  CK(cudaEventRecord(ctx->ev_dw2, ctx->prof ? ctx->st : ctx->st2));
+  CK(cudaStreamWaitEvent(ctx->st4, ctx->ev_dw2, 0));
+  CK(cudaStreamWaitEvent(ctx->st4, ctx->ev_heads, 0));
+  {
+    Scope sc_(ctx, LG_PROF_COMM, ctx->st4);
+    lg_status s = nccl_ranges(ctx, true, ctx->st4);
+    if (s != LG_OK) return s;
+  }
+  CK(cudaEventRecord(ctx->ev_comm, ctx->st4));
+  ctx->early_sent = true;
+  return LG_OK;
+}
 static lg_status collective(lg_ctx* const* cs, int n, CollSel sel) {
   lg_ctx* ctx = cs[0];
   const bool dbl = sel != COLL_GRAD;
@@ -961,18 +1016,38 @@ static lg_status collective(lg_ctx* const* cs, int n, CollSel sel) {
     if (!ctx->comm) return fail(ctx, LG_ERR_STATE, "world_size %d without a communicator (lg_set_nccl)", ctx->world);
     void* p = coll_ptr(ctx, sel);
     Scope sc_(ctx, LG_PROF_COMM);
+    if (sel == COLL_GRAD && ctx->early_sent) {  // layers 2-4 went on st4 beside dW1: join it, then layer 1 + stats
+      CK(cudaStreamWaitEvent(ctx->st, ctx->ev_comm, 0));
+      ctx->early_sent = false;
+      return nccl_ranges(ctx, false, ctx->st);
+    }
     CKN(ncclAllReduce(p, p, count, dbl ? ncclFloat64 : ncclFloat32, ncclSum, ctx->comm, ctx->st));
     return LG_OK;
   }
+  // the ranks of an lg_group on one device: a rank-ordered sum kernel per range (the gradient in the NCCL path's
+  // bucket ranges, so the group tests cover the partition)
   GroupSumArgs g;
   memset(&g, 0, sizeof(g));
   g.n = n;
-  g.count = (long long)count;
   g.is_double = dbl ? 1 : 0;
-  for (int r = 0; r < n; ++r) g.p[r] = coll_ptr(cs[r], sel);
   Scope sc_(ctx, LG_PROF_COMM);
-  launch_group_sum(g, ctx->st);
-  CKL();
+  if (dbl) {
+    g.count = (long long)count;
+    for (int r = 0; r < n; ++r) g.p[r] = coll_ptr(cs[r], sel);
+    launch_group_sum(g, ctx->st);
+    CKL();
+    return LG_OK;
+  }
+  for (int early = 1; early >= 0; --early) {
+    Range rg[3];
+    const int k = grad_bucket(ctx, early != 0, rg);
+    for (int i = 0; i < k; ++i) {
+      g.count = rg[i].len;
+      for (int r = 0; r < n; ++r) g.p[r] = reinterpret_cast<float*>(coll_ptr(cs[r], sel)) + rg[i].off;
+      launch_group_sum(g, ctx->st);
+      CKL();
+    }
+  }
   return LG_OK;
 }
 
@@ -1088,13 +1163,13 @@ static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm);
 // barrier and no reduction pass (dW1's is on the critical path); the multi-rank collective needs reduced gradients
 static bool dw1_partial_ok(const lg_ctx* ctx) {
   static const bool off = [] { const char* e = getenv("LG_DW1_PARTIAL"); return e && e[0] == '0'; }();
-  return !off && ctx->dw1_partial && ctx->world == 1 && !ctx->group && ctx->L.dw1.S > 1;
+  return !off && ctx->in_update && ctx->world == 1 && !ctx->group && ctx->L.dw1.S > 1;
 }
 // the same for the background layers 2 and 3 (LG_DW23_PARTIAL=0 switches it off; same-box A/B on C3: 4.38 ms with,
 // 4.48 ms without -- Adam reads 16 MB more, the two background launches lose their barrier and reduction)
 static bool dw23_partial_ok(const lg_ctx* ctx, const DwPlan& p) {
   static const bool off = [] { const char* e = getenv("LG_DW23_PARTIAL"); return e && e[0] == '0'; }();
-  return !off && ctx->dw1_partial && ctx->world == 1 && !ctx->group && p.S > 1;
+  return !off && ctx->in_update && ctx->world == 1 && !ctx->group && p.S > 1;
 }
 static bool fused_loss_ok(const lg_ctx* ctx) {
   return ctx->d.H1 <= 256 && ctx->d.H2 <= 128 && !(ctx->cfg.flags & LG_F_UNFUSED_LOSS);
@@ -1152,6 +1227,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
     }
     { Scope sc_(ctx, LG_PROF_REDUCE, sr); launch_reduce_heads(hr, sr); }
     CKL();
+    CK(cudaEventRecord(ctx->ev_heads, sr));
     if (side) CK(cudaEventRecord(ctx->ev_join3, ctx->st3));
     s = backward_chain(ctx, b, next_perm);
     if (s == LG_OK && side) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_join3, 0));
@@ -1180,6 +1256,7 @@ static lg_status minibatch_gradient(lg_ctx* ctx, int b, const uint32_t* next_per
   // (measured: on the dW stream instead, the reduction delays dW3 -> dW1 by more than it saves here)
   { Scope sc_(ctx, LG_PROF_REDUCE); launch_reduce_heads(hr, ctx->st); }
   CKL();
+  CK(cudaEventRecord(ctx->ev_heads, ctx->st));
   return backward_chain(ctx, b, next_perm);
 }
 
@@ -1232,6 +1309,7 @@ static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm) {
   x2.M = d.Mmb;
   if ((s = gemm(ctx, GEMM_DX, x2, ctx->bnx2, 2)) != LG_OK) return s;
   if ((s = dw(ctx->dw2, L.dw2, L.k_dw2, d.H0, ctx->cn.W2, ctx->cn.b2, 0, dw23_partial_ok(ctx, L.dw2))) != LG_OK) return s;
+  if ((s = send_early_bucket(ctx)) != LG_OK) return s;  // NCCL ranks: layers 2-4 + heads beside dW1
   // layer 1 (both nets in one GEMM: rows [0,H0) actor, [H0,2H0) critic); only the first D columns are θ
   if ((s = fork(2)) != LG_OK) return s;
   if ((s = dw(b ? ctx->dw1_b1 : ctx->dw1, L.dw1, L.k_dw1, d.D, ctx->cn.W1, ctx->cn.b1, d.H0, dw1_partial_ok(ctx))) !=
@@ -1400,10 +1478,10 @@ static lg_status update_end(lg_ctx* ctx, lg_update_stats* stats) {
 }
 static lg_status run_update(lg_ctx* const* cs, int n, lg_update_stats* const* stats) {
   lg_status s;
-  struct Flag {  // dw1_partial for the duration of the update (ppo_minibatch_grad keeps the reduced gradient)
+  struct Flag {  // in_update for the duration of the update (ppo_minibatch_grad keeps the reduced gradient)
     lg_ctx* const* cs; int n;
-    Flag(lg_ctx* const* c, int k) : cs(c), n(k) { for (int r = 0; r < n; ++r) cs[r]->dw1_partial = true; }
-    ~Flag() { for (int r = 0; r < n; ++r) cs[r]->dw1_partial = false; }
+    Flag(lg_ctx* const* c, int k) : cs(c), n(k) { for (int r = 0; r < n; ++r) cs[r]->in_update = true; }
+    ~Flag() { for (int r = 0; r < n; ++r) cs[r]->in_update = false; }
   } flag(cs, n);
   for (int r = 0; r < n; ++r) if ((s = update_begin(cs[r])) != LG_OK) return s;
   const int n_mb = cs[0]->d.E * cs[0]->d.K;
