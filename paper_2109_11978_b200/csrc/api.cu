@@ -121,10 +121,11 @@ static DwPlan dw_plan_bn(int rows, int N, int K, int nz, int bn, bool background
   p.pair = 0;
   // one wave of <= 148 CTAs (background: <= 98), and >= 8 (background: 32) k-blocks per CTA (the fp32
   // partial costs ~3 k-blocks of traffic)
-  // (LG_DW_BG_CTAS / LG_DW_BG_SPLITS override the background plan: measurement only)
+  // (LG_DW_BG_CTAS / LG_DW_BG_SPLITS override the background plan, LG_DW1_CTAS the critical one: measurement only)
   static const int bg_ctas = [] { const char* e = getenv("LG_DW_BG_CTAS"); return e ? atoi(e) : 98; }();
   static const int BG_SPLITS = [] { const char* e = getenv("LG_DW_BG_SPLITS"); return e ? atoi(e) : 12; }();
-  const int max_ctas = background ? bg_ctas : 148;
+  static const int crit_ctas = [] { const char* e = getenv("LG_DW1_CTAS"); return e ? atoi(e) : 148; }();
+  const int max_ctas = background ? bg_ctas : crit_ctas;
   int S = std::max(1, std::min(std::max(1, p.kb_total / 8), max_ctas / std::max(1, p.tiles)));
   if (background) S = std::min(S, BG_SPLITS);
   p.kb_per_split = (p.kb_total + S - 1) / S;

@@ -229,19 +229,34 @@ __device__ __forceinline__ void split3_bf16(float x, uint16_t* p) {
 }
 constexpr int W4_ATOM = 48 * 128;      // bytes of one 64-column atom (48 rows)
 constexpr int W4_BYTES = 2 * W4_ATOM;  // the head-weight operand of one net
-__device__ __forceinline__ void build_w4_atoms(uint8_t* w4, const float* W4a, const float* W4c, int H2, int z, int t0,
-                                               int nt) {
-  for (int k = t0; k < 16 * 128; k += nt) {  // element (j, c) part p: atom c / 64, row 16p + j, chunk (c % 64) / 8 ^ (j & 7)
-    const int j = k >> 7, c = k & 127;
-    float v = 0.0f;
-    if (c < H2) v = z == 0 ? (j < 12 ? __ldg(W4a + j * H2 + c) : 0.0f) : (j == 0 ? __ldg(W4c + c) : 0.0f);
+// element (j, c) part p: atom c / 64, row 16p + j, chunk (c % 64) / 8 ^ (j & 7). In two phases so that a caller's
+// other prologue loads share one round trip: w4_load (elements t0 + i * nt, i < 8: nt >= 256 threads), w4_store.
+__device__ __forceinline__ void w4_load(float* v, const float* W4a, const float* W4c, int H2, int z, int t0, int nt) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int k = t0 + i * nt, j = k >> 7, c = k & 127;
+    v[i] = 0.0f;
+    if (k < 16 * 128 && c < H2) v[i] = z == 0 ? (j < 12 ? __ldg(W4a + j * H2 + c) : 0.0f) : (j == 0 ? __ldg(W4c + c) : 0.0f);
+  }
+}
+__device__ __forceinline__ void w4_store(uint8_t* w4, const float* v, int t0, int nt) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int k = t0 + i * nt, j = k >> 7, c = k & 127;
+    if (k >= 16 * 128) break;
     uint16_t pt[3];
-    split3_bf16(v, pt);
+    split3_bf16(v[i], pt);
 #pragma unroll
     for (int u = 0; u < 3; ++u)
       *reinterpret_cast<uint16_t*>(w4 + (c >> 6) * W4_ATOM + (16 * u + j) * 128 + ((((c & 63) >> 3) ^ (j & 7)) << 4) +
                                    2 * (c & 7)) = pt[u];
   }
+}
+__device__ __forceinline__ void build_w4_atoms(uint8_t* w4, const float* W4a, const float* W4c, int H2, int z, int t0,
+                                               int nt) {
+  float v[8];
+  w4_load(v, W4a, W4c, H2, z, t0, nt);
+  w4_store(w4, v, t0, nt);
 }
 // issued by one thread: the two 64-column blocks in K steps of 16
 __device__ __forceinline__ void head_mma(uint32_t d1, uint32_t a3, uint32_t w4) {
@@ -458,24 +473,34 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
   float* sCst = reinterpret_cast<float*>(sLoss + le::CST);  // ls[12] | sigma^-2[12] | KL constant[12] | b4a[12]
   float* sBias = reinterpret_cast<float*>(sLoss + le::BIAS);
   const int H2 = L.H2;
-  // ---- once per CTA: the net's head weights (three bf16 parts), constants, b3, zeroed operands / records
-  build_w4_atoms(sLoss + le::W4, L.W4a, L.W4c, H2, z, et, 256);
+  if (L.dbg && et == 0) L.dbg[(size_t)blockIdx.x * 128 + 8] = loss_gtimer();  // (diagnostics: epilogue entry)
+  // ---- once per CTA: the net's head weights (three bf16 parts), constants, b3, zeroed operands / records; every
+  // global load of the prologue is issued first (one round trip instead of one per step)
+  float w4v[8];
+  w4_load(w4v, L.W4a, L.W4c, H2, z, et, 256);
+  float ls = 0.0f, lso = 0.0f, b4a = 0.0f, b3 = 0.0f;
+  if (et < 12) {
+    ls = __ldg(L.logstd + et);
+    lso = __ldg(L.logstd_old + et);
+    b4a = __ldg(L.b4a + et);
+  }
+  if (et < args.N && et < 128) b3 = __ldg(args.bias[z] + et);
+  const float b4c = __ldg(L.b4c);
   for (int k = et; k < 16384 / 16; k += 256) reinterpret_cast<uint4*>(sD)[k] = make_uint4(0u, 0u, 0u, 0u);
   for (int k = et; k < 128 * (le::REC_NF + 2 * le::REC_ND); k += 256) sRec[k] = 0.0f;  // columns a net never writes stay zero
   double* sRecD = reinterpret_cast<double*>(sRec + 128 * le::REC_NF);
+  w4_store(sLoss + le::W4, w4v, et, 256);
   if (et < 12) {
-    const float ls = __ldg(L.logstd + et), lso = __ldg(L.logstd_old + et);
     const float iv = expf(-2.0f * ls);
     sCst[et] = ls;
     sCst[12 + et] = iv;
     sCst[24 + et] = kl_const(ls, lso, iv);
-    sCst[36 + et] = __ldg(L.b4a + et);
+    sCst[36 + et] = b4a;
   }
-  if (et < 128) sBias[et] = et < args.N ? __ldg(args.bias[z] + et) : 0.0f;
+  if (et < 128) sBias[et] = b3;
   // the first payload writer of the minibatch clears the non-finite counter (the previous minibatch's Adam has
   // consumed it: this kernel runs after that minibatch's layers 1, 2)
   if (blockIdx.x == 0 && et == 0 && L.payload) L.payload[4] = 0.0f;
-  const float b4c = __ldg(L.b4c);
   // record-column sums (lane 0 of warp e owns float columns e, e + 8, e + 16, e + 24 (< 25) and fp64 statistic
   // e (< 5))
   float xf[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -732,6 +757,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     }
     if (e < 5) L.spart[(size_t)blockIdx.x * 8 + e] = xd;
   }
+  if (L.dbg && et == 0) L.dbg[(size_t)blockIdx.x * 128 + 9] = loss_gtimer();  // (diagnostics: epilogue exit)
   if (lane == 0) bulk_wait_all();
   __syncwarp();
 }
@@ -1820,15 +1846,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   uint64_t* xfull = bars + 0;
   uint64_t* full = bars + 1;           // [4]
   uint64_t* empty = bars + 5;          // [4]
-  uint64_t* tfull = bars + 9;          // [4]: layers 1, 2, 3, heads
-  uint64_t* h1ready = bars + 13;
-  uint64_t* h2ready = bars + 14;
-  uint64_t* h3ready = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  // weight-chunk slots: 0, 1 = the ring; 2, 3 = R1 blocks 4-5 and 6-7, free while layer 1 runs (the
-  // observation tile occupies blocks 0..kb1-1 <= 3, H1 is written only after every layer-1 MMA completed),
-  // so layer 1 streams W1 four chunks deep; layers 2 and 3 use the ring
+  uint64_t* tfull = bars + 9;          // [5]: layer 1 columns 0-255, 256-511, layer 2, layer 3, heads
+  uint64_t* h1ready = bars + 14;       // [2]: H1 columns 0-255 / 256-511 staged
+  uint64_t* h2ready = bars + 16;       // [4]: H2 k-block kb staged
+  uint64_t* h3ready = bars + 20;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  // The layers overlap: the H1 epilogue of columns 0-255 runs beside the layer-1 MMAs of columns 256-511, layer 2
+  // starts on k-blocks 0-3 once columns 0-255 are staged (beside the epilogue of 256-511), and layer 3 takes each
+  // H2 k-block as soon as it is staged. R1 blocks: the observation tile occupies 0..kb1-1 (<= 3) until layer 1 is
+  // done, so H1 columns 0-255 go to blocks 4-7 and columns 256-511 to blocks 0-3 (layer 2 reads k-block kb from
+  // block (kb + 4) % 8: the same MMAs in the same order, bit-identical). Weight-chunk slots: 0, 1 = the ring;
+  // 2, 3 = R1 blocks 4-5 and 6-7, free until H1 columns 0-255 are staged: W1's first half streams four chunks deep
   auto slot_ptr = [&](int sl) { return sl < 2 ? ring + sl * fp::STAGE : R1 + (4 + 2 * (sl - 2)) * fp::ABLK; };
+  auto w1_slot = [&](int g) { return g < 4 ? (g & 3) : (g & 1); };  // chunk g of W1 (g < 4: columns 0-255)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = a.z0 + (int)blockIdx.y;
@@ -1838,9 +1868,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
   if (threadIdx.x == 0) {
     mbar_init(xfull, 1);
     for (int s2 = 0; s2 < 4; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
-    for (int s2 = 0; s2 < 4; ++s2) mbar_init(&tfull[s2], 1);
-    mbar_init(h1ready, EPI_WARPS);
-    mbar_init(h2ready, EPI_WARPS);
+    for (int s2 = 0; s2 < 5; ++s2) mbar_init(&tfull[s2], 1);
+    for (int s2 = 0; s2 < 2; ++s2) mbar_init(&h1ready[s2], EPI_WARPS);
+    for (int s2 = 0; s2 < 4; ++s2) mbar_init(&h2ready[s2], EPI_WARPS);
     mbar_init(h3ready, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1869,7 +1899,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
       };
       int g = 0;
       for (int nh = 0; nh < 2; ++nh)
-        for (int kb = 0; kb < a.kb1; ++kb, ++g) load(g & 3, &a.tmW1, kb * fp::BK, z * fp::H0 + nh * 256, fp::STAGE);
+        for (int kb = 0; kb < a.kb1; ++kb, ++g) load(w1_slot(nh * 4 + kb), &a.tmW1, kb * fp::BK, z * fp::H0 + nh * 256, fp::STAGE);
       int rr = 0;
       for (int kb = 0; kb < fp::H0 / fp::BK; ++kb, ++rr) load(rr & 1, &a.tmW2[z], kb * fp::BK, 0, fp::STAGE);
       for (int kb = 0; kb < fp::H1 / fp::BK; ++kb, ++rr) load(rr & 1, &a.tmW3[z], kb * fp::BK, 0, fp::STAGE / 2);
@@ -1893,10 +1923,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
       mbar_wait(xfull, 0);
       tc_fence_after();
       // layer 1: two 256-column halves of this net's 512 outputs, K = kb1 blocks of the observation
-      int g = 0;
-      for (int nh = 0; nh < 2; ++nh)
-        for (int kb = 0; kb < a.kb1; ++kb, ++g) {
-          const int sl = g & 3;
+      for (int nh = 0; nh < 2; ++nh) {
+        for (int kb = 0; kb < a.kb1; ++kb) {
+          const int sl = w1_slot(nh * 4 + kb);
           const uint32_t b0 = take(sl);
           const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
 #pragma unroll
@@ -1905,25 +1934,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
                    (kb > 0 || k > 0) ? 1u : 0u);
           release(sl);
         }
-      tc_commit(&tfull[0]);
-      // layer 2: A = H1 (8 blocks in R1), N = 256 into TMEM columns [0, 256)
-      mbar_wait(h1ready, 0);
-      tc_fence_after();
+        tc_commit(&tfull[nh]);
+      }
+      // layer 2: A = H1 (k-block kb in R1 block (kb + 4) % 8), N = 256 into TMEM columns [0, 256) -- free once
+      // H1 columns 0-255 are read (h1ready[0]); k-blocks 4-7 wait for columns 256-511 (h1ready[1])
       int rr = 0;
       for (int kb = 0; kb < fp::H0 / fp::BK; ++kb, ++rr) {
+        if (kb == 0 || kb == 4) {
+          mbar_wait(&h1ready[kb >> 2], 0);
+          tc_fence_after();
+        }
         const int sl = rr & 1;
         const uint32_t b0 = take(sl);
-        const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
+        const uint32_t a0 = smem_u32(R1 + ((kb + 4) & 7) * fp::ABLK);
 #pragma unroll
         for (int k = 0; k < fp::BK / 16; ++k)
           tc_mma(tmem, sdesc(a0 + k * 32u, 0u, 1024u), sdesc(b0 + k * 32u, 0u, 1024u), id256, (kb > 0 || k > 0) ? 1u : 0u);
         release(sl);
       }
-      tc_commit(&tfull[1]);
-      // layer 3: A = H2 (4 blocks in R1), N = 128 into TMEM columns [256, 384)
-      mbar_wait(h2ready, 0);
-      tc_fence_after();
+      tc_commit(&tfull[2]);
+      // layer 3: A = H2 (4 blocks in R1, each as soon as it is staged), N = 128 into TMEM columns [256, 384)
       for (int kb = 0; kb < fp::H1 / fp::BK; ++kb, ++rr) {
+        mbar_wait(&h2ready[kb], 0);
+        tc_fence_after();
         const int sl = rr & 1;
         const uint32_t b0 = take(sl);
         const uint32_t a0 = smem_u32(R1 + kb * fp::ABLK);
@@ -1933,12 +1966,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
                  (kb > 0 || k > 0) ? 1u : 0u);
         release(sl);
       }
-      tc_commit(&tfull[2]);
+      tc_commit(&tfull[3]);
       // the heads: H3 (bf16, in R1 blocks 0, 1) . W4^T into TMEM columns [384, 432)
       mbar_wait(h3ready, 0);
       tc_fence_after();
       head_mma(tmem + 384, smem_u32(R1), smem_u32(sW4));
-      tc_commit(&tfull[3]);
+      tc_commit(&tfull[4]);
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -1964,41 +1997,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
     }
-    // layer 1 -> H1 (bias + ELU, bf16) into R1 (the observation tile there is dead once tfull[0] fired)
-    mbar_wait(&tfull[0], 0);
-    __syncwarp();
-    tc_fence_after();
-    if (threadIdx.x == 128) FP_STAMP(2);
-    for (int c = h * 256; c < h * 256 + 256; c += 32) {
-      uint32_t acc[32];
-      tmem_ld32_nowait(tb + c, acc);
-      tmem_wait_ld();
-      store_act_block(R1, r, c, acc, sB1 + c);
+    // layer 1 -> H1 (bias + ELU, bf16): columns 0-255 into R1 blocks 4-7 as soon as their MMAs are done (beside
+    // the MMAs of columns 256-511), then columns 256-511 into blocks 0-3 (the observation tile is dead by then);
+    // each half: thread (q, h) takes columns 128h .. 128h+127 of it
+    for (int nh = 0; nh < 2; ++nh) {
+      mbar_wait(&tfull[nh], 0);
+      __syncwarp();
+      tc_fence_after();
+      if (threadIdx.x == 128) FP_STAMP(2 + nh);
+      uint8_t* dst = nh == 0 ? R1 + 4 * fp::ABLK : R1 - 4 * fp::ABLK;  // block (c >> 6) + 4 or - 4
+      for (int c = nh * 256 + h * 128; c < nh * 256 + h * 128 + 128; c += 32) {
+        uint32_t acc[32];
+        tmem_ld32_nowait(tb + c, acc);
+        tmem_wait_ld();
+        store_act_block(dst, r, c, acc, sB1 + c);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&h1ready[nh]);
     }
-    fence_async_smem();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(h1ready);
-    if (threadIdx.x == 128) FP_STAMP(3);
-    // layer 2 -> H2 into R1 (H1 is dead once tfull[1] fired)
-    mbar_wait(&tfull[1], 0);
+    // layer 2 -> H2 into R1 blocks 0-3 (H1 is dead once tfull[2] fired), one k-block at a time for layer 3:
+    // thread (q, h) takes columns 64kb + 32h .. +31 of block kb
+    mbar_wait(&tfull[2], 0);
     __syncwarp();
     tc_fence_after();
     if (threadIdx.x == 128) FP_STAMP(4);
-    for (int c = h * 128; c < h * 128 + 128; c += 32) {
+    for (int kb = 0; kb < fp::H1 / fp::BK; ++kb) {
+      const int c = 64 * kb + 32 * h;
       uint32_t acc[32];
       tmem_ld32_nowait(tb + c, acc);
       tmem_wait_ld();
       store_act_block(R1, r, c, acc, sB2 + c);
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&h2ready[kb]);
     }
-    fence_async_smem();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(h2ready);
     if (threadIdx.x == 128) FP_STAMP(5);
-    // layer 3 -> H3 (bf16, as the unfused path stores it) into R1 blocks 0, 1 (H2 is dead once tfull[2] fired)
+    // layer 3 -> H3 (bf16, as the unfused path stores it) into R1 blocks 0, 1 (H2 is dead once tfull[3] fired)
     // -> the head MMA (head_mma: the loss epilogue's instruction sequence) -> mu - b4a / V - b4c in TMEM
-    mbar_wait(&tfull[2], 0);
+    mbar_wait(&tfull[3], 0);
     __syncwarp();
     tc_fence_after();
     if (threadIdx.x == 128) FP_STAMP(6);
@@ -2012,7 +2051,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(h3ready);
-    mbar_wait(&tfull[3], 0);
+    mbar_wait(&tfull[4], 0);
     __syncwarp();
     tc_fence_after();
     uint32_t d1[48];
@@ -2300,16 +2339,29 @@ cudaError_t launch_gemm_loss(const GemmArgs& a0, int* grid_out, cudaStream_t st)
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  static const double frac = [] { const char* e = getenv("LG_LOSS_ACTOR_FRAC"); return e ? atof(e) : 0.65; }();
+  static const double frac = [] { const char* e = getenv("LG_LOSS_ACTOR_FRAC"); return e ? atof(e) : -1.0; }();
   GemmArgs a = a0;
   a.m_tiles = (a.M + 127) / 128;
   a.nz = 2; a.n_tiles = 1; a.n_splits = 1; a.kb_per_split = a.kb_total;
   if (a.kb_total < 1 || a.kb_total > 4 || a.N > 128 || a.le.H2 != a.N || a.M_dev) return cudaErrorInvalidValue;
   const int grid = gemm_loss_grid(a);
-  int split = (int)std::lround(frac * grid);
-  split = std::max(split, grid - a.m_tiles);
-  split = std::min(split, a.m_tiles);
-  split = std::max(1, std::min(grid - 1, split));
+  const int lo = std::max(1, grid - a.m_tiles), hi = std::min(a.m_tiles, grid - 1);
+  int split;
+  if (frac > 0) {
+    split = std::max(lo, std::min(hi, (int)std::lround(frac * grid)));
+  } else {
+    // the busiest CTA's tiles x per-tile cost (tools/gemm_probe loss stamps: an actor tile ~5.0 us, a critic tile
+    // ~4.1 us); ties go to the split that balances the nets' average load (C3: 64..84 actor CTAs of 148 all give
+    // 3 tiles per CTA; same-box A/B 4.32 ms against 4.37 with the previous fixed 65 % actor share)
+    constexpr double CA = 1.22, CC = 1.0;
+    double best = 1e30, bal = 1e30;
+    split = lo;
+    for (int s = lo; s <= hi; ++s) {
+      const double ta = CA * ((a.m_tiles + s - 1) / s), tc = CC * ((a.m_tiles + grid - s - 1) / (grid - s));
+      const double mx = std::max(ta, tc), b = std::fabs(CA * a.m_tiles / s - CC * a.m_tiles / (grid - s));
+      if (mx < best - 1e-9 || (mx < best + 1e-9 && b < bal)) { best = mx; bal = b; split = s; }
+    }
+  }
   a.ws_split = split;
   if (grid_out) *grid_out = grid;
   return launch_pdl(k_gemm_tc<128, false, false, 4, false, 4>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, st, a);

@@ -188,17 +188,17 @@ static void probe_loss(int M, float frac, cudaStream_t st) {
   unsigned long long t0 = ~0ull, tend = 0;
   int slow = 0;
   for (int b = 0; b < grid; ++b) {
-    if (h[b * 128] && h[b * 128] < t0) t0 = h[b * 128];
+    if (h[b * 128 + 8] && h[b * 128 + 8] < t0) t0 = h[b * 128 + 8];
     for (int k = 0; k < 128; ++k)
       if (h[b * 128 + k] > tend) { tend = h[b * 128 + k]; slow = b; }
   }
   printf("first stamp -> last stamp %.2f us; slowest CTA %d\n", (tend - t0) * 1e-3, slow);
   for (int b : {0, grid / 2, slow, grid - 1}) {
-    printf("CTA %3d:", b);
+    printf("CTA %3d: entry %.2f exit %.2f", b, (h[b * 128 + 8] - t0) * 1e-3, (h[b * 128 + 9] - t0) * 1e-3);
     for (int t = 0; t < 8; ++t) {
       if (!h[(b * 8 + t) * 16]) break;
       printf(" |t%d", t);
-      for (int k = 0; k < 10; ++k) printf(" %.2f", (h[(b * 8 + t) * 16 + k] - t0) * 1e-3);
+      for (int k = 0; k < 8; ++k) printf(" %.2f", (h[(b * 8 + t) * 16 + k] - t0) * 1e-3);
     }
     printf("\n");
   }
