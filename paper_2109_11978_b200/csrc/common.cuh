@@ -170,10 +170,11 @@ __device__ __forceinline__ float h_bilinear(const World& w, float x, float y) {
 // Written with explicit roundings so every kernel that evaluates them (rollout heads, fused rollout policy,
 // loss head) produces the same bits regardless of the translation unit's contraction choices.
 // log-density term of one action dimension: 0.5 z^2 + log sigma, z = (a - mu) / sigma
-__device__ __forceinline__ float logp_term(float a, float mu, float ls) {
-  const float z = __fmul_rn(__fsub_rn(a, mu), expf(-ls));
+__device__ __forceinline__ float logp_term_e(float a, float mu, float einv, float ls) {  // einv = expf(-ls)
+  const float z = __fmul_rn(__fsub_rn(a, mu), einv);
   return __fadd_rn(__fmul_rn(__fmul_rn(0.5f, z), z), ls);
 }
+__device__ __forceinline__ float logp_term(float a, float mu, float ls) { return logp_term_e(a, mu, expf(-ls), ls); }
 // action of dimension j from the ACTION Philox block j/4 of env g at event ev: a = mu + sigma * eps,
 // eps = Box-Muller pair (2k, 2k+1), k = j/2 (cos for even j, sin for odd j)
 __device__ __forceinline__ float sample_action_b(const U4& b, int j, float mu, float ls) {  // b = block j/4

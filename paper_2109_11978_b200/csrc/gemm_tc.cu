@@ -282,7 +282,7 @@ __device__ __forceinline__ float head_out(const uint32_t* d, int j) {
 //         part p at K offset 16p) of dH3 = dmu W4, MN-major B (N = 48 part columns, K = row) of dW4
 //  W4     the net's head weights as build_w4_atoms lays them out
 //  REC    per-row records, column-major: [25][128] fp32 (dmu[12], dV, dlogstd terms[12]), [5][128] fp64 statistics
-//  CST    per-dimension constants (log sigma, sigma^-2, KL constant, b4a); BIAS b3 of the CTA's net
+//  CST    per-dimension constants (log sigma, sigma^-2, KL constant, b4a, e^-log sigma); BIAS b3 of the CTA's net
 namespace le {
 constexpr int A3 = 0;
 constexpr int DMU = A3 + 32768;  // [128 rows][128 B]: part p of dmu_j at column 16p + j
@@ -290,7 +290,7 @@ constexpr int W4 = DMU + 16384;  // build_w4_atoms
 constexpr int REC = W4 + W4_BYTES;
 constexpr int REC_NF = 25, REC_ND = 5;           // column-major: [25][128] fp32, then [5][128] fp64
 constexpr int CST = REC + 128 * (REC_NF * 4 + REC_ND * 8);
-constexpr int BIAS = CST + 48 * 4;
+constexpr int BIAS = CST + 64 * 4;
 constexpr int BYTES = BIAS + 128 * 4;
 // TMEM columns: the layer-3 accumulators use [0, 256)
 constexpr int TM_D2 = 256;  // dH3 [row][128]
@@ -470,7 +470,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
   uint8_t* sA3 = sLoss + le::A3;
   uint8_t* sD = sLoss + le::DMU;
   float* sRec = reinterpret_cast<float*>(sLoss + le::REC);
-  float* sCst = reinterpret_cast<float*>(sLoss + le::CST);  // ls[12] | sigma^-2[12] | KL constant[12] | b4a[12]
+  float* sCst = reinterpret_cast<float*>(sLoss + le::CST);  // ls | sigma^-2 | KL constant | b4a | e^-ls ([12] each)
   float* sBias = reinterpret_cast<float*>(sLoss + le::BIAS);
   const int H2 = L.H2;
   if (L.dbg && et == 0) L.dbg[(size_t)blockIdx.x * 128 + 8] = loss_gtimer();  // (diagnostics: epilogue entry)
@@ -496,6 +496,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
     sCst[12 + et] = iv;
     sCst[24 + et] = kl_const(ls, lso, iv);
     sCst[36 + et] = b4a;
+    sCst[48 + et] = expf(-ls);  // the per-dimension factor of logp_term, once per CTA (same bits as per row)
   }
   if (et < 128) sBias[et] = b3;
   // the first payload writer of the minibatch clears the non-finite counter (the previous minibatch's Adam has
@@ -602,7 +603,7 @@ __device__ __forceinline__ void loss_epilogue(const GemmArgs& args, int M, TileA
 #pragma unroll
       for (int j = 0; j < 12; ++j) {
         mu[j] = __fadd_rn(head_out(d1, j), sCst[36 + j]);
-        t[j] = logp_term(in_a[j], mu[j], sCst[j]);
+        t[j] = logp_term_e(in_a[j], mu[j], sCst[48 + j], sCst[j]);
       }
       const float lp = __fsub_rn(-dim_sum12(t), SIX_LN_2PI_F);
       const float ratio = expf(lp - lpo);
