@@ -660,6 +660,9 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
   ep.hf = reinterpret_cast<const float*>(ctx->buf[LG_BUF_HEIGHTFIELD]);
   ep.R = d.R_hf; ep.C = d.C_hf; ep.inv_cell = cfg->inv_cell;
   ep.N = d.N; ep.rank = cfg->rank; ep.n_levels = d.L; ep.n_cols = d.C; ep.scan_nx = d.nx; ep.scan_ny = d.ny;
+  // exact when k * (ny_magic * ny - 2^20) < 2^20: k < nx * ny <= 464 and the excess is < ny <= 464 (lg_create's
+  // 512-wide observation row bound)
+  ep.ny_magic = d.ny > 0 ? ((1u << 20) + (uint32_t)d.ny - 1u) / (uint32_t)d.ny : 0u;
   ep.obs_dim = d.D; ep.obs_stride = d.Dp; ep.flags = cfg->flags;
   ep.seed_lo = (uint32_t)(cfg->seed & 0xFFFFFFFFu); ep.seed_hi = (uint32_t)(cfg->seed >> 32);
   ep.state = reinterpret_cast<uint32_t*>(ctx->buf[LG_BUF_STATE]);

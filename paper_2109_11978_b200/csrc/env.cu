@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(64 * OBS_ROWS_PER_BLOCK) k_env_obs(EnvParams P
     World W{P.hf, P.R, P.C, P.inv_cell};
     const float px = o->px, py = o->py, pz = o->pz, c = o->c, sn = o->s;
     const int k0 = e0 - 48;
-    int ix = k0 / P.scan_ny, iy = k0 - ix * P.scan_ny;
+    int ix = (int)(((uint32_t)k0 * P.ny_magic) >> 20), iy = k0 - ix * P.scan_ny;  // k0 / ny, exact (host check)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (e0 + j < D) {
@@ -253,16 +253,19 @@ __global__ void __launch_bounds__(64 * OBS_ROWS_PER_BLOCK) k_env_obs(EnvParams P
     Rng rng{P.seed_lo, P.seed_hi};
     const uint32_t wbase = o->word0 + 4u * (uint32_t)gq;
     const U4 nb0 = rng.block(wbase >> 2, o->g, ev, TAG_OBS);
-    U4 nb1 = nb0;
-    if (wbase & 3u) nb1 = rng.block((wbase >> 2) + 1, o->g, ev, TAG_OBS);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (sc[j] != 0.0f) {
-        const uint32_t w = wbase + (uint32_t)j;
-        const uint32_t word = ((w >> 2) == (wbase >> 2)) ? pick(nb0, w) : pick(nb1, w);
-        v[j] = v[j] + usym(sc[j], word);
-      }
+    // words wbase .. wbase+3 = the 4-word window at offset wbase % 4 of [nb0 | nb1] (the offset is the row's,
+    // so uniform across the warp)
+    uint32_t wd[4] = {nb0.x, nb0.y, nb0.z, nb0.w};
+    const uint32_t sh = wbase & 3u;
+    if (sh) {
+      const U4 nb1 = rng.block((wbase >> 2) + 1, o->g, ev, TAG_OBS);
+      if (sh == 1) { wd[0] = nb0.y; wd[1] = nb0.z; wd[2] = nb0.w; wd[3] = nb1.x; }
+      else if (sh == 2) { wd[0] = nb0.z; wd[1] = nb0.w; wd[2] = nb1.x; wd[3] = nb1.y; }
+      else { wd[0] = nb0.w; wd[1] = nb1.x; wd[2] = nb1.y; wd[3] = nb1.z; }
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (sc[j] != 0.0f) v[j] = v[j] + usym(sc[j], wd[j]);
   }
   if (df) {
 #pragma unroll

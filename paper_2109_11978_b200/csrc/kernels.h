@@ -40,6 +40,7 @@ struct EnvParams {
   int R, C;
   float inv_cell;
   int N, rank, n_levels, n_cols, scan_nx, scan_ny, obs_dim, obs_stride;
+  uint32_t ny_magic;         // ceil(2^20 / scan_ny): k / scan_ny = (k * ny_magic) >> 20 for the scan indices
   uint32_t flags, seed_lo, seed_hi;
   uint32_t* state;           // SoA [66][N]
   DevScalars* scalars;
