@@ -656,6 +656,7 @@ __device__ __forceinline__ void write_shadow(const ShadowArgs& sh, long long i, 
 // Grid: the parameter segments (ShadowArgs, one per weight / bias tensor) each get ceil(n / 512) blocks, so a
 // block's 512 elements lie in one segment: its canonical range and its bf16 / fp32 GEMM shadow are found once.
 constexpr int ADAM_PER_THREAD = ADAM_BLOCK_ELEMS / 256;
+constexpr int ADAM_W = 6;  // split partials per element and pass
 __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payload, float kl_target, int world, int m,
                                           float* acc, int bid) {
   __shared__ float s_step, s_ibc2;
@@ -684,43 +685,68 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a, const float* payloa
       if (G.off == q.b_off[z]) { PP = &q; pz = z; pbias = true; }
     }
   }
+  // the state first (its latency overlaps the partial sums), then the gradient: the canonical vector, or the sum
+  // of the GEMM's split partials in split order (AdamPart) -- both elements' loads of a pass in flight together
+  // (2 x ADAM_W at once), addresses stepped by one split stride, no per-load predicate. Same-box A/B per C3
+  // iteration against one element's six loads at a time: ADAM_W = 2 / 3 / 4 / 6 / 8 / 9 / 12: -0.7 / -1.1 / -1.3 /
+  // -1.6 / -1.3 / -1.5 / -1.4 % (48 registers in every variant)
 #pragma unroll
   for (int u = 0; u < ADAM_PER_THREAD; ++u) {
     const int l = l0 + u * 256;
     const long long i = G.off + l;
+    g[u] = 0.0f;
     if (l < n) {
       mo[u] = a.m[i]; vo[u] = a.v[i]; tho[u] = a.theta[i];
-      if (!PP) {
-        g[u] = a.grad[i];
+      if (!PP) g[u] = a.grad[i];
+    }
+  }
+  if (PP) {
+    const float* p[ADAM_PER_THREAD];
+    bool ok[ADAM_PER_THREAD];
+#pragma unroll
+    for (int u = 0; u < ADAM_PER_THREAD; ++u) {
+      const int l = l0 + u * 256;
+      ok[u] = l < n;
+      int r, nt, col;
+      if (!pbias) {
+        r = l / PP->cols;
+        const int c = l - r * PP->cols;
+        nt = c / PP->bn;
+        col = c - nt * PP->bn;
       } else {
-        int r, nt, col;
-        if (!pbias) {
-          r = l / PP->cols;
-          const int c = l - r * PP->cols;
-          nt = c / PP->bn;
-          col = c - nt * PP->bn;
-        } else {
-          r = l;
-          nt = 0;
-          col = PP->bn;
-        }
-        const int R = PP->row_split ? pz * PP->row_split + r : r;
-        const int mt = PP->row_split ? (R >> 7) : pz * PP->m_tiles + (R >> 7);
-        const float* p = PP->part + ((size_t)(mt * PP->n_tiles + nt) * PP->S * 128 + (R & 127)) * PP->rld + col;
-        const size_t sstride = (size_t)128 * PP->rld;
-        float acc = 0.0f;
-        // six loads of a pass in flight, then the split-order sum (a wider pass doubled the kernel's registers
-        // and halved the occupancy of every Adam / gather block)
+        r = l;
+        nt = 0;
+        col = PP->bn;
+      }
+      const int R = PP->row_split ? pz * PP->row_split + r : r;
+      const int mt = PP->row_split ? (R >> 7) : pz * PP->m_tiles + (R >> 7);
+      p[u] = ok[u] ? PP->part + ((size_t)(mt * PP->n_tiles + nt) * PP->S * 128 + (R & 127)) * PP->rld + col : PP->part;
+    }
+    const size_t ss = (size_t)128 * PP->rld;
+    const int S = PP->S;
+    int s0 = 0;
 #pragma unroll 1
-        for (int s0 = 0; s0 < PP->S; s0 += 6) {
-          float w[6];
+    for (; s0 + ADAM_W <= S; s0 += ADAM_W) {
+      float w[ADAM_PER_THREAD][ADAM_W];
 #pragma unroll
-          for (int q = 0; q < 6; ++q) w[q] = s0 + q < PP->S ? __ldcg(p + (size_t)(s0 + q) * sstride) : 0.0f;
+      for (int u = 0; u < ADAM_PER_THREAD; ++u)
 #pragma unroll
-          for (int q = 0; q < 6; ++q)
-            if (s0 + q < PP->S) acc = (s0 + q == 0) ? w[0] : acc + w[q];
-        }
-        g[u] = acc;
+        for (int q = 0; q < ADAM_W; ++q) w[u][q] = __ldcg(p[u] + q * ss);
+#pragma unroll
+      for (int u = 0; u < ADAM_PER_THREAD; ++u) {
+        g[u] = s0 == 0 ? w[u][0] : g[u] + w[u][0];
+#pragma unroll
+        for (int q = 1; q < ADAM_W; ++q) g[u] = g[u] + w[u][q];
+        p[u] += ADAM_W * ss;
+      }
+    }
+#pragma unroll 1
+    for (; s0 < S; ++s0) {
+#pragma unroll
+      for (int u = 0; u < ADAM_PER_THREAD; ++u) {
+        const float w = __ldcg(p[u]);
+        g[u] = s0 == 0 ? w : g[u] + w;
+        p[u] += ss;
       }
     }
   }
