@@ -578,8 +578,7 @@ __device__ __forceinline__ void gather_body(const GatherArgs& a, int bid) {
   uint4 v[GATHER_ROWS][2];
 #pragma unroll
   for (int k = 0; k < GATHER_ROWS; ++k) {
-    const uint32_t t = b[k] / (uint32_t)a.N, i = b[k] - t * (uint32_t)a.N;
-    const uint4* src = reinterpret_cast<const uint4*>(a.obs + ((size_t)t * a.N + i) * a.Dp);
+    const uint4* src = reinterpret_cast<const uint4*>(a.obs + (size_t)b[k] * a.Dp);  // sample b = t N + i: row b of OBS
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = lane + 32 * h;
