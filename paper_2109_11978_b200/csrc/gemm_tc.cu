@@ -1027,7 +1027,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
       const int row = tc.m0 + q * 32 + lane;
       // work that does not depend on the accumulator, done while the MMA runs
       uint32_t av[32];
-      if (EPI == 0 && active) {
+      if (EPI == 0 && active && (!WSKB || local == 1)) {  // (weight-stationary: one column block per CTA, once)
         const float* bias = args.bias[tc.z];
         for (int i = lane; i < WCOLS; i += 32) {
           const int n = tc.n0 + h * WCOLS + i;
