@@ -306,7 +306,11 @@ struct GemmCfg {
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // a CTA of a pair holds half of B
   static constexpr int ONES_BYTES = EPI == 3 ? 16 * 128 : 0;  // 16 rows x 64 bf16 of 1.0 (bias column)
   static constexpr int EPI_BUF = 4096;         // one 32 x 128-B staging sub-tile
-  static constexpr int EPI_NBUF = EPI == 4 ? 0 : ((EPI == 3 || WSKB) ? 1 : 2);  // EPI 4 stages dZ3 in its own smem
+  // staging buffers per epilogue warp: EPI 4 stages dZ3 in its own smem; weight-stationary forward GEMMs have room
+  // for one (their resident B takes the rest); the weight-stationary dX2 takes two and stages its saved activation
+  // by coalesced cp.async like the other dX GEMMs (A ring 4 -> 2 stages; same-box A/B -0.3 % per C3 iteration
+  // against one buffer with the activation loaded per row into registers and prefetched into L2)
+  static constexpr int EPI_NBUF = EPI == 4 ? 0 : ((EPI == 3 || (WSKB && EPI != 2)) ? 1 : 2);
   static constexpr int BIAS_BYTES = EPI == 0 ? EPI_WARPS * 128 * 4 : 0;
   static constexpr int LOSS_BYTES = EPI == 4 ? le::BYTES : 0;
   static constexpr int BRES = WSKB * B_BYTES;  // weight-stationary: the resident column block of B
@@ -1058,6 +1062,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
               if (nbn + j / 2 < args.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + j));
           }
         }
+      }
+      if (EPI == 2 && !AUX_STAGED && active) {
         const int nb = tc.n0 + h * WCOLS;
         const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nb);
         if (row < M && nb + 64 <= args.N) {  // whole 64-column chunk in range (the common case)
