@@ -324,6 +324,7 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = EPI == 4 ? 512 : TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
   static constexpr int SMEM = FIXED + STAGES * STAGE_BYTES;
   static_assert(STAGES >= 2, "operand ring");
+  static_assert(EPI != 2 || EPI_NBUF == 2, "input-gradient epilogues stage the saved activation");
 };
 
 // ELU(x) = x > 0 ? x : e^x - 1, with e^x = 2^(x log2 e) from ex2.approx.ftz (one MUFU op, no subnormal
@@ -1047,23 +1048,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
                   args.N, lane);
       }
       if (EPI == 2 && !AUX_STAGED && active) {
-        // the saved activation of this thread's row in the CTA's next tile: into L2 now (its DRAM latency was
-        // the epilogue's main stall), read into registers one chunk ahead when that tile comes
-        // (one tile ahead: same-box A/B -0.9 % per C3 iteration; two or three tiles ahead +0.3 / +1.1 %)
-        TileCoord tn;
-        int itn = it + 1;
-        while (tile_at(itn, tn) && skip(tn)) ++itn;
-        if (tile_at(itn, tn)) {
-          const int rn = tn.m0 + q * 32 + lane, nbn = tn.n0 + h * WCOLS;
-          if (rn < M) {
-            const char* pa = reinterpret_cast<const char*>(args.aux[tn.z] + (size_t)rn * args.ld_aux + nbn);
-#pragma unroll
-            for (int j = 0; j < WCOLS * 2; j += 128)
-              if (nbn + j / 2 < args.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + j));
-          }
-        }
-      }
-      if (EPI == 2 && !AUX_STAGED && active) {
         const int nb = tc.n0 + h * WCOLS;
         const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nb);
         if (row < M && nb + 64 <= args.N) {  // whole 64-column chunk in range (the common case)
@@ -1154,23 +1138,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm_tc(const __grid_consta
                 const float g1 = __uint_as_float(rr[kk + 1]) * fminf(h1 + 1.0f, 1.0f);
                 __nv_bfloat162 o = __floats2bfloat162_rn(g0, g1);
                 pk[k / 2] = *reinterpret_cast<uint32_t*>(&o);
-              }
-            }
-            if (EPI == 2 && !AUX_STAGED && c + 64 < (h + 1) * WCOLS) {  // prefetch the next chunk's saved activation
-              const int nn = nb + 64;
-              const uint4* a4 = reinterpret_cast<const uint4*>(args.aux[tc.z] + (size_t)row * args.ld_aux + nn);
-              if (row < M && nn + 64 <= args.N) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  const uint4 u = __ldg(a4 + j);
-                  av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
-                }
-              } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  uint4 u = (row < M && nn + 8 * j < args.N) ? a4[j] : make_uint4(0, 0, 0, 0);
-                  av[4 * j] = u.x; av[4 * j + 1] = u.y; av[4 * j + 2] = u.z; av[4 * j + 3] = u.w;
-                }
               }
             }
             uint8_t* buf = mybuf + (C::EPI_NBUF == 2 ? (nst & 1) * C::EPI_BUF : 0);
