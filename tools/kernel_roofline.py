@@ -74,15 +74,19 @@ def main(rep, rnd="r01"):
     labels = [""] * len(out)
     for i, e in enumerate(out):
         if e["name"].startswith("k_gather"):
-            order = ["L1", "L2", "L3", None, None, "dW3", "dX3", "dX2", "dW2", "dW1"]
+            # launch order of a minibatch: layer 1, layer 2, layer 3 + the PPO loss epilogue (one kernel), the head
+            # reduction (side stream), dW3, dX3, dX2, dW2, dW1, then Adam + the next gather
+            order = ["L1", "L2", "L3", None, "dW3", "dX3", "dX2", "dW2", "dW1"]
             for k, lab in enumerate(order, start=1):
                 if i + k < len(out) and lab:
                     labels[i + k] = lab
             break
     # GEMMs before the minibatch: the time-out bootstrap critic chain (V(o_T) runs in the fused policy kernel)
-    for i, e in enumerate(out):
+    first_gather = next((i for i, e in enumerate(out) if e["name"].startswith("k_gather")), len(out))
+    for i, e in enumerate(out[:first_gather]):
         if e["name"].startswith("k_gemm_tc") and not labels[i]:
             labels[i] = "boot"
+    out, labels = out[:first_gather + 11], labels[:first_gather + 11]  # one minibatch (its Adam + next gather)
     print(f"# {rnd}: per-kernel roofline fractions (`ncu --set full --clock-control none`, one launch of each kernel)\n")
     print(f"Peaks: bf16 dense {tc_peak:.0f} TFLOP/s sustained, HBM {hbm_peak:.0f} GB/s ({src}). Durations are ncu's "
           "serialised, cold-cache launch times (shares agree with the bench's in-graph times; absolutes are higher).\n")
@@ -101,7 +105,7 @@ def main(rep, rnd="r01"):
             bound, achs, frac = "tensor", f"{ach:.0f} TFLOP/s", ach / tc_peak
         else:
             bound, achs, frac = "hbm", f"{gbs:.0f} GB/s", gbs / hbm_peak
-        role = {"L1": "forward layer 1 (both nets)", "L2": "forward layer 2", "L3": "forward layer 3",
+        role = {"L1": "forward layer 1 (both nets)", "L2": "forward layer 2", "L3": "forward layer 3 + PPO loss epilogue",
                 "dW3": "weight grad layer 3", "dX3": "input grad layer 3", "dW2": "weight grad layer 2",
                 "dX2": "input grad layer 2", "dW1": "weight grad layer 1", "cL1": "critic L1 on o_T",
                 "cL2": "critic L2 on o_T", "cL3": "critic L3 on o_T",
