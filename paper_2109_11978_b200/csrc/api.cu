@@ -272,6 +272,10 @@ struct lg_ctx {
   cudaStream_t st4 = nullptr;
   cudaEvent_t ev_dw2 = nullptr, ev_heads = nullptr, ev_comm = nullptr;
   bool early_sent = false;  // this minibatch's early bucket is on st4
+  // the iteration's shuffles (k_perm: they depend only on the iteration counter) on st3 beside the rollout, whose
+  // policy kernel leaves most SMs idle; the update waits for ev_perm instead of launching them
+  cudaEvent_t ev_pfork = nullptr, ev_perm = nullptr;
+  bool perm_early = false;
   lg_status err = LG_OK;
   std::string msg;
   int world = 1;
@@ -458,6 +462,8 @@ lg_status lg_create(const lg_config* cfg, void* const buffers_h[LG_NUM_BUFFERS],
     ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_dw2, cudaEventDisableTiming) == cudaSuccess;
     ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_heads, cudaEventDisableTiming) == cudaSuccess;
     ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_comm, cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_pfork, cudaEventDisableTiming) == cudaSuccess;
+    ok2 = ok2 && cudaEventCreateWithFlags(&ctx->ev_perm, cudaEventDisableTiming) == cudaSuccess;
     if (!ok2) {
       delete ctx;
       return LG_ERR_CUDA;
@@ -729,6 +735,8 @@ lg_status lg_destroy(lg_ctx* ctx) {
   if (ctx->st2) { cudaStreamSynchronize(ctx->st2); cudaStreamDestroy(ctx->st2); }
   if (ctx->st3) { cudaStreamSynchronize(ctx->st3); cudaStreamDestroy(ctx->st3); }
   if (ctx->ev_fork3) cudaEventDestroy(ctx->ev_fork3);
+  if (ctx->ev_pfork) cudaEventDestroy(ctx->ev_pfork);
+  if (ctx->ev_perm) cudaEventDestroy(ctx->ev_perm);
   if (ctx->ev_join3) cudaEventDestroy(ctx->ev_join3);
   if (ctx->st4) { cudaStreamSynchronize(ctx->st4); cudaStreamDestroy(ctx->st4); }
   for (cudaEvent_t e : {ctx->ev_dw2, ctx->ev_heads, ctx->ev_comm}) if (e) cudaEventDestroy(e);
@@ -1421,18 +1429,28 @@ static bool gather_prefetch() {  // LG_GATHER_PREFETCH=1: next gather beside dW1
   return v;
 }
 
+// the Feistel permutations of all E epochs of the iteration (P:272 shuffled minibatches), one launch
+static lg_status launch_perms(lg_ctx* ctx, cudaStream_t st) {
+  const Dims& d = ctx->d;
+  PermArgs pa;
+  pa.B = (uint32_t)d.B; pa.E = d.E; pa.epoch = 0; pa.rank = ctx->cfg.rank;
+  pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
+  pa.sc = ctx->sc; pa.perm = perm_of(ctx); pa.n_epochs = d.E;
+  { Scope sc_(ctx, LG_PROF_GATHER, st); launch_perm(pa, st); }
+  CKL();
+  return LG_OK;
+}
 // ppo_update, per rank: Alg. 1 / Adam scalars of the iteration, the E shuffles, the first minibatch's gather
 static lg_status update_begin(lg_ctx* ctx) {
   const Dims& d = ctx->d;
   { Scope sc_(ctx, LG_PROF_MISC); iter_begin(ctx); }
   CKL();
-  {  // the Feistel permutations of all E epochs (P:272 shuffled minibatches), one launch
-    PermArgs pa;
-    pa.B = (uint32_t)d.B; pa.E = d.E; pa.epoch = 0; pa.rank = ctx->cfg.rank;
-    pa.seed_lo = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu); pa.seed_hi = (uint32_t)(ctx->cfg.seed >> 32);
-    pa.sc = ctx->sc; pa.perm = perm_of(ctx); pa.n_epochs = d.E;
-    { Scope sc_(ctx, LG_PROF_GATHER); launch_perm(pa, ctx->st); }
-    CKL();
+  if (ctx->perm_early) {  // computed beside the rollout (run_iteration)
+    CK(cudaStreamWaitEvent(ctx->st, ctx->ev_perm, 0));
+    ctx->perm_early = false;
+  } else {  // the Feistel permutations of all E epochs (P:272 shuffled minibatches), one launch
+    lg_status s = launch_perms(ctx, ctx->st);
+    if (s != LG_OK) return s;
   }
   {  // the first minibatch's gather (later ones ride in the Adam launch, or beside dW1 with prefetch)
     GatherArgs g = gather_args(ctx, 0);
@@ -1560,6 +1578,14 @@ lg_status lg_broadcast_params(lg_ctx* ctx) {
 // ------------------------------------------------------------------ whole iteration
 static lg_status run_iteration(lg_ctx* ctx, lg_update_stats* stats) {
   lg_status s;
+  static const bool perm_early = [] { const char* e = getenv("LG_PERM_EARLY"); return !(e && e[0] == '0'); }();
+  if (perm_early && !ctx->prof) {  // the shuffles depend only on the iteration counter: beside the rollout
+    CK(cudaEventRecord(ctx->ev_pfork, ctx->st));
+    CK(cudaStreamWaitEvent(ctx->st3, ctx->ev_pfork, 0));
+    if ((s = launch_perms(ctx, ctx->st3)) != LG_OK) return s;
+    CK(cudaEventRecord(ctx->ev_perm, ctx->st3));
+    ctx->perm_early = true;
+  }
   for (int t = 0; t < ctx->d.T; ++t) {
     if ((s = policy_act(ctx, t, nullptr, nullptr, nullptr, nullptr)) != LG_OK) return s;
     if ((s = env_step_obs_reward(ctx, t, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) != LG_OK) return s;
