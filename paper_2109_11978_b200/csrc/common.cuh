@@ -177,7 +177,8 @@ __device__ __forceinline__ float logp_term_e(float a, float mu, float einv, floa
 __device__ __forceinline__ float logp_term(float a, float mu, float ls) { return logp_term_e(a, mu, expf(-ls), ls); }
 // action of dimension j from the ACTION Philox block j/4 of env g at event ev: a = mu + sigma * eps,
 // eps = Box-Muller pair (2k, 2k+1), k = j/2 (cos for even j, sin for odd j)
-__device__ __forceinline__ float sample_action_b(const U4& b, int j, float mu, float ls) {  // b = block j/4
+// sigma * eps of that sample (independent of mu: the rollout policy computes it before its layers finish)
+__device__ __forceinline__ float action_noise_b(const U4& b, int j, float ls) {  // b = block j/4
   const int k2 = (j & ~1) & 3;
   const uint32_t w0 = pick(b, (uint32_t)k2), w1 = pick(b, (uint32_t)k2 + 1u);
   const float u1 = (float)((w0 >> 8) + 1u) * 0x1p-24f;
@@ -185,7 +186,10 @@ __device__ __forceinline__ float sample_action_b(const U4& b, int j, float mu, f
   const float rr = sqrtf(-2.0f * log_poly(u1));
   float sn, cs;
   sincos_poly(0x1.921fb6p2f * u2, sn, cs);
-  return __fadd_rn(mu, __fmul_rn(expf(ls), __fmul_rn(rr, (j & 1) ? sn : cs)));
+  return __fmul_rn(expf(ls), __fmul_rn(rr, (j & 1) ? sn : cs));
+}
+__device__ __forceinline__ float sample_action_b(const U4& b, int j, float mu, float ls) {  // b = block j/4
+  return __fadd_rn(mu, action_noise_b(b, j, ls));
 }
 __device__ __forceinline__ float sample_action(const Rng& rng, uint32_t g, uint32_t ev, int j, float mu, float ls) {
   return sample_action_b(rng.block((uint32_t)(j >> 2), g, ev, TAG_ACTION), j, mu, ls);

@@ -1986,6 +1986,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32));
     }
+    // the actor's per-row sampling terms do not depend on the layers: sigma * eps (ACTION Philox), e^-log sigma,
+    // log sigma and b4a of this thread's six action dimensions, computed while layer 1 runs (the same operations
+    // as sample_action_b / logp_term: the same bits)
+    const int hs = (warp - 4) >> 2;
+    float pre_se[6], pre_ei[6], pre_ls[6], pre_b4[6];
+#pragma unroll
+    for (int jj = 0; jj < 6; ++jj) pre_se[jj] = pre_ei[jj] = pre_ls[jj] = pre_b4[jj] = 0.0f;
+    if (z == 0 && m0 + r < a.N) {
+      Rng rng{a.seed_lo, a.seed_hi};
+      const uint32_t gid = (uint32_t)(a.rank * a.N + m0 + r);
+      const uint32_t ev = a.scalars->s_base + (uint32_t)a.t + 1u;
+      const U4 blk0 = rng.block((uint32_t)(hs == 0 ? 0 : 1), gid, ev, TAG_ACTION);
+      const U4 blk1 = rng.block((uint32_t)(hs == 0 ? 1 : 2), gid, ev, TAG_ACTION);
+#pragma unroll
+      for (int jj = 0; jj < 6; ++jj) {
+        const int j = 6 * hs + jj;
+        pre_ls[jj] = __ldg(a.logstd + j);
+        pre_b4[jj] = __ldg(a.b4a + j);
+        pre_ei[jj] = expf(-pre_ls[jj]);
+        const bool first = (j >> 2) == (hs == 0 ? 0 : 1);
+        pre_se[jj] = action_noise_b(first ? blk0 : blk1, j, pre_ls[jj]);
+      }
+    }
     // layer 1 -> H1 (bias + ELU, bf16): columns 0-255 into R1 blocks 4-7 as soon as their MMAs are done (beside
     // the MMAs of columns 256-511), then columns 256-511 into blocks 0-3 (the observation tile is dead by then);
     // each half: thread (q, h) takes columns 128h .. 128h+127 of it
@@ -2052,7 +2075,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
     // the two threads of a row split the action dimensions: h = 0 takes j < 6 (ACTION Philox blocks 0, 1),
     // h = 1 takes j >= 6 (blocks 1, 2); their log-density terms meet in smem for the fixed-order sum.
     if (threadIdx.x == 128) FP_STAMP(7);
-    const int hs = (warp - 4) >> 2;
     float* xrow = sX + r * 26;
     const int row = m0 + r;
     if (z == 1) {
@@ -2065,20 +2087,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_policy_fused(const __grid_c
       float* trow = xrow;  // reused for the 12 log-density terms after the sums are consumed
       float tm[6];
       if (row < a.N) {
-        Rng rng{a.seed_lo, a.seed_hi};
-        const uint32_t gid = (uint32_t)(a.rank * a.N + row);
-        const uint32_t ev = a.scalars->s_base + (uint32_t)a.t + 1u;
-        const U4 blk0 = rng.block((uint32_t)(hs == 0 ? 0 : 1), gid, ev, TAG_ACTION);
-        const U4 blk1 = rng.block((uint32_t)(hs == 0 ? 1 : 2), gid, ev, TAG_ACTION);
 #pragma unroll
         for (int jj = 0; jj < 6; ++jj) {
           const int j = 6 * hs + jj;
           const float dj = hs == 0 ? head_out(d1, jj) : head_out(d1, 6 + jj);  // constant indices: d1[] in registers
-          const float mu = __fadd_rn(dj, __ldg(a.b4a + j));
-          const float ls = __ldg(a.logstd + j);
-          const bool first = (j >> 2) == (hs == 0 ? 0 : 1);
-          const float act = a.deterministic ? mu : sample_action_b(first ? blk0 : blk1, j, mu, ls);
-          tm[jj] = logp_term(act, mu, ls);
+          const float mu = __fadd_rn(dj, pre_b4[jj]);
+          const float act = a.deterministic ? mu : __fadd_rn(mu, pre_se[jj]);
+          tm[jj] = logp_term_e(act, mu, pre_ei[jj], pre_ls[jj]);
           a.act[(size_t)row * 12 + j] = act;
           a.mu[(size_t)row * 12 + j] = mu;
           if (a.u_act) a.u_act[(size_t)row * 12 + j] = act;
