@@ -16,8 +16,10 @@
  * (S:184-186); FK straight leg and yaw equivariance; settling to m·g
  * (S:204); reward examples; observation examples; curriculum examples
  * and exhaustive L=3 sequences; Feistel bijection.
- * The multi-step transition trajectory itself is "parity unpinned" beyond those invariants: it is
- * pinned only by DESIGN.md §3.5, which both sides implement.
+ * Multi-step transition: pinned in flight by the closed forms of its integrator over 80 substeps (free fall,
+ * torque-free spin about a principal axis, a PD-driven joint: test_flight_trajectory_closed_forms) and in contact
+ * by the settling equilibrium. Between those, a contact-rich trajectory is "parity unpinned": it is fixed
+ * only by DESIGN.md §3.5, which both sides implement (the GPU is bit-exact to it).
  */
 #include <math.h>
 #include <stdint.h>

@@ -439,6 +439,46 @@ def test_pd_joint_through_the_transition_kp80():
         assert np.all(tau_o[others] == 0.0) and np.all(qdd_o[others] == 0.0)
 
 
+def test_flight_trajectory_closed_forms():
+    """The multi-step transition over 20 policy steps = 80 semi-implicit Euler substeps of a robot
+    in flight (no contact), against the closed forms of that integrator, evaluated in fp64 here:
+    base free fall v_z(n) = -g dt n, p_z(n) = p_z(0) - g dt² n(n+1)/2 (velocity first, then position with the new
+    velocity); torque-free spin about the principal z axis (ω × Iω = 0, so ω stays exactly constant) with the
+    first-order quaternion step q + (dt/2) q⊗ω followed by normalisation, which turns the heading by exactly
+    2 atan(ω dt / 2) per substep; and one PD-driven joint following the scalar recurrence of S:181 (R24's Kp = 80)
+    while the others stay at q* -- the joints are decoupled from the base without contact forces."""
+    env = _env()
+    env.reset()
+    _place(env, 0, 5.0)
+    w, th0, dt, g = 2.0, 0.3, 0.005, 9.81
+    env.state["w"][0] = (0.0, 0.0, w)
+    env.state["quat"][0] = (math.cos(th0 / 2), 0.0, 0.0, math.sin(th0 / 2))
+    j, qs = 1, 0.1
+    a = np.zeros(12, np.float32)
+    a[j] = np.float32(2.0 * qs)
+    q, qd = 0.0, 0.0
+    for step in range(1, 21):
+        tau_o, qdd_o, _, crash, nc, fz = env.transition_single(0, a)
+        assert crash == 0 and fz == 0.0
+        for _ in range(4):
+            tau = max(-80.0, min(80.0, 80.0 * (qs - q) - 2.0 * qd))
+            qd += dt * ((tau - 0.5 * qd) / 0.25)
+            q += dt * qd
+        n = 4 * step
+        st = env.state[0]
+        assert abs(st["v"][2] - (-g * dt * n)) < 2e-5
+        assert abs(st["p"][2] - (5.0 - g * dt * dt * n * (n + 1) / 2)) < 2e-5
+        assert st["p"][0] == 4.0 and st["p"][1] == 4.0 and st["v"][0] == 0.0 and st["v"][1] == 0.0
+        assert tuple(st["w"]) == (0.0, 0.0, np.float32(w))
+        th = th0 + 2.0 * n * math.atan(w * dt / 2.0)
+        qt = st["quat"].astype(np.float64)
+        assert qt[1] == 0.0 and qt[2] == 0.0
+        assert abs(qt[0] - math.cos(th / 2)) < 1e-6 and abs(qt[3] - math.sin(th / 2)) < 1e-6
+        assert abs((st["q"][j] - QDEF[j]) - q) < 1e-6 and abs(st["qd"][j] - qd) < 1e-5
+        others = [k for k in range(12) if k != j]
+        assert np.all(st["q"][others] == QDEF[others]) and np.all(st["qd"][others] == 0.0)
+
+
 def _ramp_world(a, b, levels=2, cols=2):
     """Heightfield of a plane: node (i, j) -- at the cell centre ((i+1/2)·0.1, (j+1/2)·0.1) -- holds a·i + b·j."""
     i = np.arange(80 * levels, dtype=np.float64)[:, None]
