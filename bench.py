@@ -250,6 +250,10 @@ def main():
     ctx = Context(cfg, hf)
     theta = synth.init_params(cfg.obs_dim, cfg.hidden, seed=1234)
     ctx.params_set(theta)
+    if world == 1 and os.environ.get("LG_NCCL_LOOPBACK") == "1":  # diagnostic: the multi-rank path on one GPU
+        st, b = lg.lg_nccl_unique_id()
+        lg.check(st, what="lg_nccl_unique_id")
+        ctx._ck(lg.lg_set_nccl(ctx.ctx, bytes(b)), "lg_set_nccl")
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:

@@ -976,6 +976,15 @@ static void* coll_ptr(lg_ctx* ctx, CollSel sel) {
   if (sel == COLL_GAE_VAR) return tot + 1;
   return ctx->buf[LG_BUF_GRAD];
 }
+// whether the update takes the multi-rank path (the collectives, reduced weight gradients): world > 1, or a
+// single rank with a one-rank NCCL communicator (LG_NCCL_LOOPBACK=1: a diagnostic that runs the NCCL path --
+// collectives captured in the iteration graph, the bucket streams, the dW grid reduction -- on one GPU, where
+// every allreduce is the identity)
+static bool nccl_loopback() {
+  static const bool v = [] { const char* e = getenv("LG_NCCL_LOOPBACK"); return e && e[0] == '1'; }();
+  return v;
+}
+static bool multi_rank(const lg_ctx* ctx) { return ctx->world > 1 || (ctx->comm != nullptr && nccl_loopback()); }
 // The [grad ‖ payload] vector of a minibatch in two buckets: early = the parameters of layers 2-4,
 // the heads and log-std of both nets (final once dW2 and the head reduction are done), late = layer 1 of both nets
 // (dW1) and the 16-float statistics payload. Canonical order per net: W1 b1 W2 b2 W3 b3 W4 b4, log-std last, so the
@@ -1006,7 +1015,7 @@ static lg_status nccl_ranges(lg_ctx* ctx, bool early, cudaStream_t st) {
 // NCCL ranks: the early bucket on st4 once dW2 (st2) and the head reduction (ev_heads) are done -- beside dW1
 static lg_status send_early_bucket(lg_ctx* ctx) {
   ctx->early_sent = false;
-  if (!ctx->in_update || ctx->world == 1 || !ctx->comm || ctx->group) return LG_OK;
+  if (!ctx->in_update || !multi_rank(ctx) || !ctx->comm || ctx->group) return LG_OK;
   CK(cudaEventRecord(ctx->ev_dw2, ctx->prof ? ctx->st : ctx->st2));
   CK(cudaStreamWaitEvent(ctx->st4, ctx->ev_dw2, 0));
   CK(cudaStreamWaitEvent(ctx->st4, ctx->ev_heads, 0));
@@ -1024,7 +1033,7 @@ static lg_status collective(lg_ctx* const* cs, int n, CollSel sel) {
   const bool dbl = sel != COLL_GRAD;
   const size_t count = dbl ? 1 : (size_t)ctx->d.P + 16;
   if (n == 1) {
-    if (ctx->world == 1) return LG_OK;
+    if (!multi_rank(ctx)) return LG_OK;
     if (!ctx->comm) return fail(ctx, LG_ERR_STATE, "world_size %d without a communicator (lg_set_nccl)", ctx->world);
     void* p = coll_ptr(ctx, sel);
     Scope sc_(ctx, LG_PROF_COMM);
@@ -1175,13 +1184,13 @@ static lg_status backward_chain(lg_ctx* ctx, int b, const uint32_t* next_perm);
 // barrier and no reduction pass (dW1's is on the critical path); the multi-rank collective needs reduced gradients
 static bool dw1_partial_ok(const lg_ctx* ctx) {
   static const bool off = [] { const char* e = getenv("LG_DW1_PARTIAL"); return e && e[0] == '0'; }();
-  return !off && ctx->in_update && ctx->world == 1 && !ctx->group && ctx->L.dw1.S > 1;
+  return !off && ctx->in_update && !multi_rank(ctx) && !ctx->group && ctx->L.dw1.S > 1;
 }
 // the same for the background layers 2 and 3 (LG_DW23_PARTIAL=0 switches it off; same-box A/B on C3: 4.38 ms with,
 // 4.48 ms without -- Adam reads 16 MB more, the two background launches lose their barrier and reduction)
 static bool dw23_partial_ok(const lg_ctx* ctx, const DwPlan& p) {
   static const bool off = [] { const char* e = getenv("LG_DW23_PARTIAL"); return e && e[0] == '0'; }();
-  return !off && ctx->in_update && ctx->world == 1 && !ctx->group && p.S > 1;
+  return !off && ctx->in_update && !multi_rank(ctx) && !ctx->group && p.S > 1;
 }
 static bool fused_loss_ok(const lg_ctx* ctx) {
   return ctx->d.H1 <= 256 && ctx->d.H2 <= 128 && !(ctx->cfg.flags & LG_F_UNFUSED_LOSS);
@@ -1561,7 +1570,7 @@ lg_status lg_set_nccl(lg_ctx* ctx, const uint8_t id_h[128]) {
   GUARD();
   if (!id_h) return fail(ctx, LG_ERR_INVALID_ARG, "null id");
   if (ctx->group) return fail(ctx, LG_ERR_STATE, "lg_set_nccl: the context is a rank of an lg_group");
-  if (ctx->world <= 1) return LG_OK;
+  if (ctx->world <= 1 && !nccl_loopback()) return LG_OK;
   ncclUniqueId id;
   memcpy(&id, id_h, 128);
   CKN(ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->cfg.rank));
@@ -1570,7 +1579,7 @@ lg_status lg_set_nccl(lg_ctx* ctx, const uint8_t id_h[128]) {
 
 lg_status lg_broadcast_params(lg_ctx* ctx) {
   GUARD();
-  if (ctx->world > 1 && ctx->comm)
+  if (multi_rank(ctx) && ctx->comm)
     CKN(ncclBroadcast(ctx->buf[LG_BUF_THETA], ctx->buf[LG_BUF_THETA], (size_t)ctx->d.P, ncclFloat32, 0, ctx->comm, ctx->st));
   return lg_params_sync(ctx);
 }

@@ -276,3 +276,42 @@ def test_nonfinite_advantage_skips_its_minibatches_on_gpu_and_oracle():
     d_q, d_x, gap = rel(th, th_q), rel(th, th_x), rel(th_q, th_x)
     print(f"skip test drift: vs bf16-point oracle {d_q:.3e}, vs fp64 {d_x:.3e} (gap {gap:.3e})")
     assert d_x <= gap + 1e-3                              # DESIGN R28
+
+@pytest.mark.gpu
+def test_nccl_path_on_one_gpu_loopback():
+    """The NCCL path on one GPU (LG_NCCL_LOOPBACK=1: a one-rank communicator from lg_nccl_unique_id /
+    lg_set_nccl, lg_broadcast_params, and every world > 1 branch of the update): the advantage-statistics and
+    per-minibatch gradient allreduces captured in the iteration graph (early bucket on the fourth stream beside
+    dW1, late bucket after it), the weight gradients reduced by the dW grids instead of by Adam. A one-rank
+    allreduce is the identity and the grid reduction sums the partials in Adam's order, so θ after two graph
+    iterations is bit-identical to the single-rank path (separate processes: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import os, sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import synth\n"
+        "from paper_2109_11978_b200 import lg\n"
+        "from paper_2109_11978_b200.context import Config, Context\n"
+        "cfg = Config.make(n_envs=512, n_steps=24, scan_nx=17, scan_ny=11, n_levels=4, n_cols=5, flags=15, seed=4)\n"
+        "ctx = Context(cfg, synth.make_world(4, 5, seed=3, rough=True))\n"
+        "ctx.params_set(synth.init_params(cfg.obs_dim, cfg.hidden, seed=4))\n"
+        "if os.environ.get('LG_NCCL_LOOPBACK') == '1':\n"
+        "    st, b = lg.lg_nccl_unique_id()\n"
+        "    lg.check(st, what='lg_nccl_unique_id')\n"
+        "    ctx._ck(lg.lg_set_nccl(ctx.ctx, bytes(b)), 'lg_set_nccl')\n"
+        "    ctx._ck(lg.lg_broadcast_params(ctx.ctx), 'lg_broadcast_params')\n"
+        "ctx.reset()\n"
+        "ctx.capture()\n"
+        "for _ in range(2): ctx.replay()\n"
+        "ctx.sync()\n"
+        "sys.stdout.buffer.write(ctx.theta.cpu().numpy().tobytes())\n") % root
+    outs = []
+    for v in ("0", "1"):
+        env = dict(os.environ, LG_NCCL_LOOPBACK=v, NCCL_DEBUG="WARN")
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stderr.decode()[-2000:]
+        outs.append(r.stdout)
+    n = len(outs[0])  # (θ bytes; anything NCCL writes to stdout would precede them)
+    assert n > 0 and len(outs[1]) >= n and outs[1][-n:] == outs[0]
